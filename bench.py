@@ -1,0 +1,422 @@
+"""RBGP4 SDMM benchmark (BASELINE.json metric: effective TFLOP/s = 2*nnz*N / time).
+
+Workload (BASELINE.json configs[1]): the 512-output-channel convolutions of
+VGG19-CIFAR lowered to SDMM via a materialised im2col, batch 256 per GPU,
+at 87.5 % RBGP4 sparsity (the dyadic grid point nearest the "90 %" of the
+config; SURVEY hard part 6):
+
+    conv9      (M, K, N) = (512, 2304, 4096)
+    conv10-12  (512, 4608, 4096)   <- dominant kernel (3 launches per step)
+    conv13-16  (512, 4608, 1024)
+
+A "step" is one pass of those eight products over one batch (im2col'd
+activations resident in HBM as bf16, W in the succinct device format),
+computed by the tcgen05 bf16 kernel with fp32 accumulation and bf16
+outputs.  The eight inputs total 170 MB > the 126 MB L2, so each step
+streams its operands from HBM (no explicit flush).  Multi-GPU runs shard the
+batch (one process per GPU, weak scaling, no collective on the hot path).
+
+`--impl reference` times the reference's CPU algorithm (the pinned C port of
+kronsparse._tile_worker in oracle/, all host threads) on a bounded column
+sample of the same workload, in the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RBGP4 SDMM effective TFLOP/s (2*nnz*N)"
+UNIT = "TFLOP/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--sparsity", type=float, default=0.875)
+    ap.add_argument("--batch", type=int, default=256, help="images per GPU")
+    ap.add_argument("--compute", default="bf16", choices=["bf16", "tf32", "ffma", "exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------- workload
+def build_layers(sparsity: float, batch: int):
+    import paper_2006_13486_b200 as ks
+    from paper_2006_13486_b200 import workloads as wl
+
+    layers = []
+    for cfg in wl.vgg19_cifar_512(sparsity, batch=batch):
+        chain = wl.build_chain(cfg)
+        rng = ks.make_rng(np.random.SeedSequence([cfg.seed, 1]).generate_state(1)[0])
+        w = ks.init_random(chain, rng, precision="f32")
+        params = ks.tiling_for_chain(chain, tn=cfg.tn, rn=cfg.rn, bn=cfg.bn)
+        g_o, _, g_i, _ = chain.graphs
+        layers.append(dict(cfg=cfg, chain=chain, w=w, params=params, rng=rng,
+                           m=w.rows, k=w.cols, n=cfg.n_cols, nnz=w.nnz,
+                           flops=2 * w.nnz * cfg.n_cols,
+                           adj_ints=g_o.num_left * len(g_o.adjacency[0])
+                           + g_i.num_left * len(g_i.adjacency[0])))
+    return layers
+
+
+def algorithmic_bytes(layer, s_in: int, s_out: int) -> int:
+    """Compulsory traffic: W values + index maps + I + O, once."""
+    return (layer["nnz"] * s_in + 4 * layer["adj_ints"] + layer["k"] * layer["n"] * s_in
+            + layer["m"] * layer["n"] * s_out)
+
+
+def make_input(layer, dtype_np=np.float32):
+    """I = uniform(-1, 1, (K, N)) on the layer's Philox stream (bench.py:138-140)."""
+    return layer["rng"].uniform(-1.0, 1.0, size=(layer["k"], layer["n"])).astype(dtype_np)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peak_hbm():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    try:
+        with open(TRAFFIC_PATH) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_sample(layers, seconds: float, threads: int, cols: int = 128):
+    """Reference algorithm (oracle C port of _tile_worker, f32) on a column slice.
+
+    Work is linear in N and tiles are independent (reference sdmm.py:167), so
+    a `cols`-wide slice of every layer is a faithful sample of the workload.
+    Returns (TFLOP/s, description, repetitions).
+    """
+    import oracle
+    oracle.build()
+    samples = []
+    for layer in layers:
+        inp = make_input(dict(layer, n=cols, rng=np.random.default_rng(1)))
+        samples.append((layer, inp))
+    flops = sum(2 * lay["nnz"] * cols for lay, _ in samples)
+    # one warm pass, then repeat until the time budget is used
+    for lay, inp in samples:
+        oracle.tiled(lay["w"], inp, lay["params"], threads=threads)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        for lay, inp in samples:
+            oracle.tiled(lay["w"], inp, lay["params"], threads=threads)
+        reps += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    desc = (f"all 8 layers, first {cols} of N columns each (linear in N), f32 exact-order "
+            f"C port of kronsparse._tile_worker, {reps} reps in {dt:.1f}s")
+    return flops * reps / dt / 1e12, desc, reps
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    layers = build_layers(args.sparsity, args.batch)
+    import oracle
+    oracle.build()
+    cols = 64
+    samples = [(lay, make_input(dict(lay, n=cols, rng=np.random.default_rng(1)))) for lay in layers]
+    flops = sum(2 * lay["nnz"] * cols for lay, _ in samples)
+
+    def step():
+        for lay, inp in samples:
+            oracle.tiled(lay["w"], inp, lay["params"], threads=threads)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = flops * args.steps / dt / 1e12
+    sample = (f"8 VGG19 512-ch layers at {args.sparsity * 100:g}% , first {cols} columns of each "
+              f"(work linear in N); f32 exact-order C port of kronsparse._tile_worker")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference bench recipe)",
+        "config": workload_config(args, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def workload_config(args, world):
+    return {"workload": f"vgg19-cifar-512ch-convs-im2col-sp{args.sparsity * 100:g}",
+            "layers": "conv9-16 (M,K,N)=(512,2304|4608,256*HW)",
+            "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+            "sparsity": args.sparsity, "factorisation": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1)",
+            "compute": args.compute, "parallelism": f"batch-shard x{world}",
+            "l2": "inputs (170 MB bf16) larger than L2 (126 MB); no explicit flush"}
+
+
+# ----------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    import paper_2006_13486_b200 as ks
+    from paper_2006_13486_b200 import _native
+    from paper_2006_13486_b200.device import device_format
+    from paper_2006_13486_b200.sdmm import launch_sdmm
+
+    compute = args.compute
+    tc = compute in ("bf16", "tf32")
+    op_dt = torch.bfloat16 if compute == "bf16" else torch.float32
+    out_dt = torch.bfloat16 if compute == "bf16" else torch.float32
+    s_in = 2 if compute == "bf16" else 4
+    s_out = s_in
+
+    layers = build_layers(args.sparsity, args.batch)
+    # every rank gets its own batch shard: same W (replicated), distinct inputs
+    for lay in layers:
+        lay["rng"] = ks.make_rng(np.random.SeedSequence([lay["cfg"].seed, 1, rank]).generate_state(1)[0])
+    host_in, dev_in, dev_out, fmts = [], [], [], []
+    for lay in layers:
+        x32 = torch.from_numpy(make_input(lay))
+        xh = x32.to(op_dt).pin_memory()
+        host_in.append(xh)
+        dev_in.append(xh.to(dev))
+        dev_out.append(torch.empty((lay["m"], lay["n"]), dtype=out_dt, device=dev))
+        fmts.append(device_format(lay["w"], dev, op_dt))
+    torch.cuda.synchronize()
+
+    # one CUDA graph per layer: the launch is captured once, replays cost ~us
+    stream = torch.cuda.Stream(device=dev)
+    graphs = []
+    with torch.cuda.stream(stream):
+        for fmt, x, o in zip(fmts, dev_in, dev_out):
+            launch_sdmm(fmt, compute, x, o, dev)  # eager warm-up (sets kernel attributes)
+        stream.synchronize()
+        for fmt, x, o in zip(fmts, dev_in, dev_out):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                launch_sdmm(fmt, compute, x, o, dev)
+            graphs.append(g)
+    torch.cuda.synchronize()
+
+    flops_step = sum(lay["flops"] for lay in layers)
+    dom = [i for i, lay in enumerate(layers) if lay["k"] == 4608 and lay["n"] == 16 * args.batch]
+    n_ev = args.steps * len(dom)
+    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+
+    def step(record=None):
+        for i, g in enumerate(graphs):
+            if record is not None and i in dom:
+                ev_s[record[0]].record(stream)
+                g.replay()
+                ev_e[record[0]].record(stream)
+                record[0] += 1
+            else:
+                g.replay()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    time.sleep(0.3)  # sampler warm-up (first samples land before the timed region)
+    _native.reset_launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        t_start.record(stream)
+        cursor = [0]
+        for _ in range(args.steps):
+            step(cursor)
+        t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = flops_step * world / (ms_per_step * 1e-3) / 1e12
+    dom_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
+    dom_avg_ms = statistics.mean(dom_ms) if dom_ms else float("nan")
+    launches_in_region = len(graphs) * args.steps  # graph replays of our kernels
+
+    # roofline of the dominant kernel (HBM-bound at this shape)
+    dom_layer = layers[dom[0]]
+    bytes_launch = algorithmic_bytes(dom_layer, s_in, s_out)
+    peak, peak_src = load_peak_hbm()
+    achieved = bytes_launch / (dom_avg_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": load_traffic(),
+                "kernel": f"tc_kernel<bf16> conv10-12 (M,K,N)=({dom_layer['m']},{dom_layer['k']},"
+                          f"{dom_layer['n']})", "algorithmic_bytes_per_launch": bytes_launch,
+                "avg_launch_us": dom_avg_ms * 1e3, "peak_source": peak_src,
+                "tflops_eff": dom_layer["flops"] / (dom_avg_ms * 1e-3) / 1e12}
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            outs = []
+            for lay, xh in zip(layers, host_in):
+                o, _ = ks.rbgp4mm(lay["w"], xh, lay["params"], compute=compute)
+                outs.append(o)
+            return outs
+        e2e_step()
+        torch.cuda.synchronize()
+        reps = max(3, min(20, args.steps // 10))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": flops_step * world / e2e_s / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in host_in)),
+               "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in dev_out)),
+               "ms_per_step": e2e_s * 1e3,
+               "path": "paper_2006_13486_b200.rbgp4mm(w, pinned host bf16 tensor, params, "
+                       "compute='bf16') per layer"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        v, desc, _ = cpu_sample(layers, args.cpu_seconds, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if compute == "bf16" else "f32",
+            "data": "synthetic (reference bench recipe: Philox masks/values, U(-1,1) inputs)",
+            "config": workload_config(args, world),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_in_region, "clocks": clocks,
+        }))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,134 @@
+/*
+ * rbgp4.h -- C ABI of the B200 RBGP4 sparse x dense product O = W_s x I.
+ *
+ * Plain pointers and sizes only (no torch, no CUDA types: `stream` is a
+ * cudaStream_t passed as void*).  All pointers except `desc` are DEVICE
+ * pointers on the current CUDA device.  Every entry point returns 0 on
+ * success and a negative RBGP4_E* code on failure; the thread-local
+ * rbgp4_last_error() then holds a one-line message.  Launches are
+ * stream-ordered and asynchronous; nothing here synchronises the device.
+ *
+ * Reference interfaces replaced (reference = kronsparse, /root/reference/pkg/src):
+ *   rbgp4_sdmm        <- kronsparse.sdmm._tile_worker(values, adj_o, adj_i, inp, out,
+ *                        tm, tk, tn, rm, rk, bm, bk, rn, bn, n_ui, n_vi, d_i,
+ *                        start, stride)                       sdmm.py:148-205 (args 268-273)
+ *   rbgp4_chain_sdmm  <- kronsparse.sdmm._csr_rows(indptr, indices, values, inp, out)
+ *                        as called by sdmm_reference             sdmm.py:297-330
+ *                        (general K-factor chains; columns enumerated in
+ *                        closed form as in rcubs.neighbors, rcubs.py:57-76)
+ *   rbgp4_csr_sdmm    <- kronsparse.sdmm._csr_rows on a raw CsrMatrix   sdmm.py:297-330
+ *   rbgp4_cast        <- the `.astype(...)` conversions the reference applies
+ *                        to operands (bench.py:138-140), on device
+ */
+#ifndef RBGP4_H_
+#define RBGP4_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RBGP4_ABI_VERSION 1
+
+/* status codes */
+#define RBGP4_OK 0
+#define RBGP4_EINVAL (-1)      /* inconsistent descriptor / unsupported shape */
+#define RBGP4_EUNSUPPORTED (-2) /* compute mode not available for this shape  */
+#define RBGP4_ECUDA (-3)       /* CUDA runtime / launch failure               */
+#define RBGP4_EWORKSPACE (-4)  /* workspace missing or too small              */
+
+/* element types */
+#define RBGP4_F32 0
+#define RBGP4_F64 1
+#define RBGP4_BF16 2
+
+/* compute modes of rbgp4_sdmm */
+#define RBGP4_COMPUTE_EXACT 0 /* SIMT, reference rounding: bit-identical to rbgp4mm  */
+#define RBGP4_COMPUTE_FFMA 1  /* SIMT, same order, fused multiply-add (f32 / f64)    */
+#define RBGP4_COMPUTE_TF32 2  /* tcgen05 kind::tf32, f32 operands, fp32 accumulate   */
+#define RBGP4_COMPUTE_BF16 3  /* tcgen05 kind::f16 (bf16), fp32 accumulate           */
+
+/*
+ * Four-factor chain (g_o, g_r, g_i, g_b) with g_r = K_{rm,rk} and
+ * g_b = K_{bm,bk} complete.  W is rows x cols with
+ *   rows = u_o*rm*u_i*bm,   cols = v_o*rk*v_i*bk,
+ *   row_nnz = d_o*rk*d_i*bk;
+ * `values` is the (rows, row_nnz) row-major array of RcubsMatrix.values
+ * (sorted-column order, rcubs.py:1-12), adj_o is (u_o, d_o) and adj_i is
+ * (u_i, d_i), int32 row-major with ascending rows (graphs.py:87-96).
+ * I is cols x n_cols with row stride ld_in; O is rows x n_cols with row
+ * stride ld_out (elements).  O is fully overwritten (no accumulation).
+ */
+typedef struct rbgp4_desc {
+    int64_t rows, cols, n_cols;
+    int64_t ld_in, ld_out;
+    int32_t u_o, v_o, d_o;
+    int32_t rm, rk;
+    int32_t u_i, v_i, d_i;
+    int32_t bm, bk;
+} rbgp4_desc;
+
+/*
+ * O = W x I.  `in_dtype` is the element type of values and I
+ * (F32/F64 for EXACT and FFMA, F32 for TF32, BF16 for BF16); `out_dtype`
+ * is F32/F64 (= in_dtype) for the SIMT modes and F32 or BF16 for the
+ * tensor-core modes.  `workspace` may be NULL when
+ * rbgp4_workspace_size() returns 0.
+ */
+int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
+               const void *values, const int32_t *adj_o, const int32_t *adj_i,
+               const void *inp, void *out, void *workspace, size_t workspace_bytes,
+               void *stream);
+
+/* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
+size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
+
+/* 1 if rbgp4_sdmm supports (desc, compute, in_dtype, out_dtype), else 0;
+ * the reason for a 0 is left in rbgp4_last_error(). */
+int rbgp4_sdmm_supported(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype);
+
+/*
+ * General K-factor chain, reference rounding of sdmm_reference:
+ * out[u, n] = fl(... fl(fl(v_0 x_0) + fl(v_1 x_1)) ...) over u's nonzeros in
+ * ascending column order.  Factor f has left/right sizes num_left[f],
+ * num_right[f], left degree degree[f] and its (num_left[f], degree[f])
+ * int32 adjacency at adjacency + adj_offset[f].  Host arrays: num_left,
+ * num_right, degree, adj_offset (k entries each).  Device: adjacency,
+ * values (rows, row_nnz), inp (cols, ld_in), out (rows, ld_out).
+ */
+int rbgp4_chain_sdmm(int k, const int32_t *num_left, const int32_t *num_right,
+                     const int32_t *degree, const int64_t *adj_offset,
+                     const int32_t *adjacency, int dtype, const void *values,
+                     const void *inp, void *out, int64_t n_cols, int64_t ld_in,
+                     int64_t ld_out, void *stream);
+
+/*
+ * Raw CSR triple (sdmm_reference on a CsrMatrix): same rounding, explicit
+ * int64 indptr (rows+1) and int32 column indices, all device pointers.
+ */
+int rbgp4_csr_sdmm(int64_t rows, const int64_t *indptr, const int32_t *indices, int dtype,
+                   const void *values, const void *inp, void *out, int64_t n_cols,
+                   int64_t ld_in, int64_t ld_out, void *stream);
+
+/* dst[i] = (dst_dtype) src[i] for n elements (F32<->BF16, F64->BF16, F64<->F32). */
+int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t n,
+               void *stream);
+
+/* Thread-local description of the last failure on this thread. */
+const char *rbgp4_last_error(void);
+
+/* RBGP4_ABI_VERSION of the loaded library. */
+int rbgp4_abi_version(void);
+
+/* Number of kernels this thread has launched through the ABI (for the
+ * benchmark's gpu_launches accounting); reset with rbgp4_reset_launch_count. */
+int64_t rbgp4_launch_count(void);
+void rbgp4_reset_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RBGP4_H_ */

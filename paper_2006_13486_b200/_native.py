@@ -1,0 +1,91 @@
+"""ctypes binding of the in-tree C-ABI library `librbgp4_b200.so`.
+
+The product path has no fallback: if the library is missing or cannot be
+loaded, every call raises :class:`DeviceError`.  Device memory and streams
+come from PyTorch (plumbing only); the arithmetic is in the library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DeviceError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b200.so")
+
+F32, F64, BF16 = 0, 1, 2
+COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
+EXPORTED = (
+    "rbgp4_sdmm", "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
+    "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
+    "rbgp4_reset_launch_count",
+)
+
+
+class Desc(ctypes.Structure):
+    """Mirror of `rbgp4_desc` (include/rbgp4.h)."""
+
+    _fields_ = [
+        ("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("n_cols", ctypes.c_int64),
+        ("ld_in", ctypes.c_int64), ("ld_out", ctypes.c_int64),
+        ("u_o", ctypes.c_int32), ("v_o", ctypes.c_int32), ("d_o", ctypes.c_int32),
+        ("rm", ctypes.c_int32), ("rk", ctypes.c_int32),
+        ("u_i", ctypes.c_int32), ("v_i", ctypes.c_int32), ("d_i", ctypes.c_int32),
+        ("bm", ctypes.c_int32), ("bk", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the library, raising DeviceError if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"CUDA extension not built ({LIB_PATH} missing); run "
+            "`python -m paper_2006_13486_b200.build` -- there is no CPU fallback"
+        )
+    try:
+        h = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise DeviceError(f"cannot load {LIB_PATH}: {exc}") from exc
+    vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+    h.rbgp4_sdmm.argtypes = [ctypes.POINTER(Desc), i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]
+    h.rbgp4_sdmm.restype = i32
+    h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
+    h.rbgp4_workspace_size.restype = sz
+    h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]
+    h.rbgp4_sdmm_supported.restype = i32
+    h.rbgp4_chain_sdmm.argtypes = [i32, vp, vp, vp, vp, vp, i32, vp, vp, vp, i64, i64, i64, vp]
+    h.rbgp4_chain_sdmm.restype = i32
+    h.rbgp4_csr_sdmm.argtypes = [i64, vp, vp, i32, vp, vp, vp, i64, i64, i64, vp]
+    h.rbgp4_csr_sdmm.restype = i32
+    h.rbgp4_cast.argtypes = [i32, i32, vp, vp, i64, vp]
+    h.rbgp4_cast.restype = i32
+    h.rbgp4_last_error.restype = ctypes.c_char_p
+    h.rbgp4_abi_version.restype = i32
+    h.rbgp4_launch_count.restype = i64
+    h.rbgp4_reset_launch_count.restype = None
+    _lib = h
+    return h
+
+
+def last_error() -> str:
+    return lib().rbgp4_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise DeviceError(f"{what} failed (code {rc}): {last_error()}")
+
+
+def launch_count() -> int:
+    return int(lib().rbgp4_launch_count())
+
+
+def reset_launch_count() -> None:
+    lib().rbgp4_reset_launch_count()

@@ -1,0 +1,343 @@
+// sdmm_simt.cu -- K1: SIMT RBGP4 product with the reference's accumulation order.
+//
+// Replaces kronsparse.sdmm._tile_worker (reference sdmm.py:148-205).  One CTA
+// owns one (tm x tnc) output tile: tile-row tbm of W and a tnc-wide column
+// block of I/O.  It walks only g_o's adjacency row (d_o of v_o W tiles; the
+// others are structurally zero and skipped), staging per step
+//   W tile  values[tbm*tm : +tm, s*d_t : +d_t]      (compressed, dense)
+//   I tile  I[adj_o[tbm][s]*tk : +tk, n0 : n0+tnc]
+// into a 2-stage cp.async ring in shared memory.  Within the tile the rows
+// fall into u_i repetition groups of g = rm*bm rows sharing one set of d_t I
+// rows; a per-group row table (computed once per CTA) turns each W column j
+// into its I row, so the gather is an indexed shared-memory read.
+//
+// Each thread owns NCH chunks of RT rows (same group) x 4 columns.  For every
+// output element the arithmetic is exactly the reference's:
+//   acc = 0;  for s: { c = 0;  for j in d_t: c = c + w*x;  acc = acc + c; }
+// EXACT=true rounds every multiply and add separately (__fmul_rn/__fadd_rn,
+// never contracted) and is bit-identical to the reference for any tiling;
+// EXACT=false uses FFMA in the same order (rel. error ~1e-7, 2x issue rate).
+#include "common.cuh"
+
+namespace rbgp4 {
+namespace {
+
+struct SimtParams {
+    int64_t rows, n_cols, ld_in, ld_out, row_nnz;
+    int32_t d_o, tm, tk, rm, rk, bm, bk, u_i, v_i, d_i, d_t, g;
+    int32_t tnc, cthreads, wstride, istride;
+    int32_t vec_in, vec_out;  // 16-byte paths legal for I loads / O stores
+};
+
+constexpr int kThreads = 256;
+
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <> __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+template <> __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+template <typename T> __device__ __forceinline__ T fma_rn(T a, T b, T c);
+template <> __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+template <> __device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int n = valid ? 16 : 0;  // zero-fill past the edge
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+template <int B>
+__device__ __forceinline__ void cp_async_small(void *smem, const void *gmem, bool valid) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    int n = valid ? B : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem), "n"(B), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <typename T>
+__device__ __forceinline__ void load4(const T *p, T (&x)[4]) {
+    if constexpr (sizeof(T) == 4) {
+        float4 v = *reinterpret_cast<const float4 *>(p);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    } else {
+        double2 a = reinterpret_cast<const double2 *>(p)[0];
+        double2 b = reinterpret_cast<const double2 *>(p)[1];
+        x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+    }
+}
+
+// Stage step s of tile-row tbm into one ring slot.
+template <typename T>
+__device__ __forceinline__ void stage(const SimtParams &p, const T *__restrict__ values,
+                                      const T *__restrict__ inp, int64_t tbm, int64_t oind,
+                                      int64_t n0, int s, T *ws, T *is) {
+    const int tid = threadIdx.x;
+    // compressed W tile: tm rows x d_t contiguous values (scalar copies, odd stride)
+    const T *wsrc = values + tbm * p.tm * p.row_nnz + int64_t(s) * p.d_t;
+    for (int e = tid; e < p.tm * p.d_t; e += kThreads) {
+        int r = e / p.d_t, j = e - r * p.d_t;
+        cp_async_small<sizeof(T)>(ws + r * p.wstride + j, wsrc + r * p.row_nnz + j, true);
+    }
+    // I tile: tk rows x tnc columns, zero-filled beyond n_cols
+    const T *isrc = inp + oind * p.tk * p.ld_in + n0;
+    if (p.vec_in) {
+        constexpr int V = 16 / sizeof(T);
+        const int chunks = p.tnc / V;
+        for (int e = tid; e < p.tk * chunks; e += kThreads) {
+            int r = e / chunks, c = (e - r * chunks) * V;
+            bool ok = n0 + c < p.n_cols;  // n_cols % V == 0 on this path
+            cp_async16(is + r * p.istride + c, ok ? isrc + r * p.ld_in + c : isrc, ok);
+        }
+    } else {
+        for (int e = tid; e < p.tk * p.tnc; e += kThreads) {
+            int r = e / p.tnc, c = e - r * p.tnc;
+            bool ok = n0 + c < p.n_cols;
+            cp_async_small<sizeof(T)>(is + r * p.istride + c, ok ? isrc + r * p.ld_in + c : isrc, ok);
+        }
+    }
+}
+
+template <typename T, bool EXACT, int RT, int NCH>
+__global__ void __launch_bounds__(kThreads)
+simt_kernel(const SimtParams p, const T *__restrict__ values, const int32_t *__restrict__ adj_o,
+            const int32_t *__restrict__ adj_i, const T *__restrict__ inp, T *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t n0 = int64_t(blockIdx.x) * p.tnc;
+    const int64_t tbm = blockIdx.y;
+    const int tid = threadIdx.x;
+
+    // smem: [W ring x2][I ring x2][row table]
+    T *wring = reinterpret_cast<T *>(smem_raw);
+    T *iring = wring + 2 * p.tm * p.wstride;
+    int32_t *rowidx = reinterpret_cast<int32_t *>(iring + 2 * p.tk * p.istride);
+    const int wslot = p.tm * p.wstride, islot = p.tk * p.istride;
+
+    // I row of W column j for group ui: (rk*v_i + adj_i[ui][ink])*bk + k,
+    // with j = (rk*d_i + ink)*bk + k  (reference sdmm.py:183-184)
+    for (int e = tid; e < p.u_i * p.d_t; e += kThreads) {
+        int ui = e / p.d_t, j = e - ui * p.d_t;
+        int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
+        rowidx[e] = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;
+    }
+
+    const int tc = tid % p.cthreads;
+    const int rthread = tid / p.cthreads;
+    const int rthreads = kThreads / p.cthreads;
+    const int nchunks = p.tm / RT;
+
+    // rows owned by this thread: chunk q covers group slots [rc*RT, rc*RT+RT)
+    int urow[NCH][RT];
+    int ugrp[NCH];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        int rc = rthread + q * rthreads;
+        int slot = (rc < nchunks ? rc : 0) * RT;
+        int ui = slot / p.g, within = slot - ui * p.g;
+        ugrp[q] = ui;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            int w = within + i, rm = w / p.bm, m = w - rm * p.bm;
+            urow[q][i] = (rm * p.u_i + ui) * p.bm + m;
+        }
+    }
+
+    T acc[NCH][RT][4];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[q][i][e] = T(0);
+
+    const int32_t *orow = adj_o + tbm * p.d_o;
+    stage<T>(p, values, inp, tbm, orow[0], n0, 0, wring, iring);
+    cp_async_commit();
+
+    for (int s = 0; s < p.d_o; ++s) {
+        if (s + 1 < p.d_o) {
+            const int b = (s + 1) & 1;
+            stage<T>(p, values, inp, tbm, orow[s + 1], n0, s + 1, wring + b * wslot,
+                     iring + b * islot);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const T *ws = wring + (s & 1) * wslot;
+        const T *is = iring + (s & 1) * islot + tc * 4;
+#pragma unroll
+        for (int q = 0; q < NCH; ++q) {
+            if (rthread + q * rthreads >= nchunks) break;
+            const int32_t *ridx = rowidx + ugrp[q] * p.d_t;
+            T c[RT][4];
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) c[i][e] = T(0);
+            const T *wrow[RT];
+#pragma unroll
+            for (int i = 0; i < RT; ++i) wrow[i] = ws + urow[q][i] * p.wstride;
+#pragma unroll 4
+            for (int j = 0; j < p.d_t; ++j) {
+                T x[4];
+                load4<T>(is + ridx[j] * p.istride, x);
+#pragma unroll
+                for (int i = 0; i < RT; ++i) {
+                    const T w = wrow[i][j];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if constexpr (EXACT) c[i][e] = add_rn(c[i][e], mul_rn(w, x[e]));
+                        else c[i][e] = fma_rn(w, x[e], c[i][e]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < RT; ++i)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[q][i][e] = add_rn(acc[q][i][e], c[i][e]);
+        }
+        __syncthreads();
+    }
+
+    // epilogue: each thread writes RT rows x 4 consecutive columns per chunk
+    const int64_t col = n0 + tc * 4;
+#pragma unroll
+    for (int q = 0; q < NCH; ++q) {
+        if (rthread + q * rthreads >= nchunks) break;
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+            T *dst = out + (tbm * p.tm + urow[q][i]) * p.ld_out + col;
+            if (p.vec_out && col + 3 < p.n_cols) {
+                if constexpr (sizeof(T) == 4) {
+                    *reinterpret_cast<float4 *>(dst) =
+                        make_float4(acc[q][i][0], acc[q][i][1], acc[q][i][2], acc[q][i][3]);
+                } else {
+                    reinterpret_cast<double2 *>(dst)[0] = make_double2(acc[q][i][0], acc[q][i][1]);
+                    reinterpret_cast<double2 *>(dst)[1] = make_double2(acc[q][i][2], acc[q][i][3]);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (col + e < p.n_cols) dst[e] = acc[q][i][e];
+            }
+        }
+    }
+}
+
+struct SimtPlan {
+    int rt, nch, cthreads;
+    size_t smem;
+};
+
+template <typename T>
+size_t smem_bytes(const ChainDims &c, int cthreads) {
+    int tnc = 4 * cthreads;
+    int wstride = c.d_t | 1;
+    size_t ring = 2 * (size_t(c.tm) * wstride + size_t(c.tk) * tnc) * sizeof(T);
+    ring = (ring + 15) & ~size_t(15);
+    return ring + size_t(c.u_i) * c.d_t * sizeof(int32_t);
+}
+
+template <typename T>
+int plan_simt(const ChainDims &c, SimtPlan *plan) {
+    int rt = (c.g % 4 == 0) ? 4 : (c.g % 2 == 0) ? 2 : 1;
+    const int max_regs_chunks = sizeof(T) == 4 ? 16 : 8;  // NCH*RT bound (register budget)
+    const size_t smem_cap = 227 * 1024;
+    for (int cthreads : {32, 16, 8}) {
+        int rthreads = kThreads / cthreads;
+        int chunks = c.tm / rt;
+        int nch = 1;
+        while (nch * rthreads < chunks) nch *= 2;
+        if (nch > 8 || nch * rt > max_regs_chunks) continue;
+        size_t sm = smem_bytes<T>(c, cthreads);
+        if (sm > smem_cap) continue;
+        // do not waste columns on narrow inputs
+        if (cthreads > 8 && 4 * cthreads >= 2 * c.n_cols) continue;
+        *plan = {rt, nch, cthreads, sm};
+        return 1;
+    }
+    set_error("SIMT path: tile %dx%d (d_t=%d, u_i=%d) exceeds register/shared-memory budget",
+              c.tm, c.tk, c.d_t, c.u_i);
+    return 0;
+}
+
+template <typename T, bool EXACT, int RT, int NCH>
+int launch_one(const ChainDims &c, const SimtPlan &pl, const T *values, const int32_t *adj_o,
+               const int32_t *adj_i, const T *inp, T *out, cudaStream_t stream) {
+    SimtParams p{};
+    p.rows = c.rows; p.n_cols = c.n_cols; p.ld_in = c.ld_in; p.ld_out = c.ld_out;
+    p.row_nnz = c.row_nnz; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.rm = c.rm; p.rk = c.rk;
+    p.bm = c.bm; p.bk = c.bk; p.u_i = c.u_i; p.v_i = c.v_i; p.d_i = c.d_i; p.d_t = c.d_t;
+    p.g = c.g; p.cthreads = pl.cthreads; p.tnc = 4 * pl.cthreads;
+    p.wstride = c.d_t | 1; p.istride = p.tnc;
+    constexpr int V = 16 / sizeof(T);
+    p.vec_in = (c.ld_in % V == 0) && (c.n_cols % V == 0) &&
+               (reinterpret_cast<uintptr_t>(inp) % 16 == 0);
+    p.vec_out = (c.ld_out % V == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    auto kern = simt_kernel<T, EXACT, RT, NCH>;
+    if (pl.smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(pl.smem));
+        if (e != cudaSuccess) {
+            set_error("cudaFuncSetAttribute(simt): %s", cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+    }
+    dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm));
+    kern<<<grid, kThreads, pl.smem, stream>>>(p, values, adj_o, adj_i, inp, out);
+    RBGP4_CHECK_LAUNCH("simt_kernel launch");
+    return RBGP4_OK;
+}
+
+template <typename T, bool EXACT>
+int dispatch(const ChainDims &c, const SimtPlan &pl, const void *values, const int32_t *adj_o,
+             const int32_t *adj_i, const void *inp, void *out, cudaStream_t s) {
+    auto v = static_cast<const T *>(values);
+    auto x = static_cast<const T *>(inp);
+    auto o = static_cast<T *>(out);
+#define RBGP4_SIMT_CASE(RT_, NCH_)                                                        \
+    if (pl.rt == RT_ && pl.nch == NCH_)                                                   \
+        return launch_one<T, EXACT, RT_, NCH_>(c, pl, v, adj_o, adj_i, x, o, s);
+    RBGP4_SIMT_CASE(1, 1) RBGP4_SIMT_CASE(1, 2) RBGP4_SIMT_CASE(1, 4) RBGP4_SIMT_CASE(1, 8)
+    RBGP4_SIMT_CASE(2, 1) RBGP4_SIMT_CASE(2, 2) RBGP4_SIMT_CASE(2, 4)
+    if constexpr (sizeof(T) == 4) {
+        RBGP4_SIMT_CASE(2, 8) RBGP4_SIMT_CASE(4, 1) RBGP4_SIMT_CASE(4, 2) RBGP4_SIMT_CASE(4, 4)
+    } else {
+        RBGP4_SIMT_CASE(4, 1) RBGP4_SIMT_CASE(4, 2)
+    }
+#undef RBGP4_SIMT_CASE
+    set_error("SIMT path: no kernel instance for RT=%d NCH=%d", pl.rt, pl.nch);
+    return RBGP4_EUNSUPPORTED;
+}
+
+}  // namespace
+
+int simt_supported(const ChainDims &c, int dtype) {
+    SimtPlan pl;
+    return dtype == RBGP4_F64 ? plan_simt<double>(c, &pl) : plan_simt<float>(c, &pl);
+}
+
+int launch_simt(const ChainDims &c, int compute, int dtype, const void *values,
+                const int32_t *adj_o, const int32_t *adj_i, const void *inp, void *out,
+                cudaStream_t stream) {
+    if (c.n_cols == 0 || c.rows == 0) return RBGP4_OK;
+    SimtPlan pl;
+    const bool exact = compute == RBGP4_COMPUTE_EXACT;
+    if (dtype == RBGP4_F32) {
+        if (!plan_simt<float>(c, &pl)) return RBGP4_EUNSUPPORTED;
+        return exact ? dispatch<float, true>(c, pl, values, adj_o, adj_i, inp, out, stream)
+                     : dispatch<float, false>(c, pl, values, adj_o, adj_i, inp, out, stream);
+    }
+    if (dtype == RBGP4_F64) {
+        if (!plan_simt<double>(c, &pl)) return RBGP4_EUNSUPPORTED;
+        return exact ? dispatch<double, true>(c, pl, values, adj_o, adj_i, inp, out, stream)
+                     : dispatch<double, false>(c, pl, values, adj_o, adj_i, inp, out, stream);
+    }
+    set_error("SIMT path supports f32/f64 operands, got dtype %d", dtype);
+    return RBGP4_EINVAL;
+}
+
+}  // namespace rbgp4

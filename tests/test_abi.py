@@ -1,0 +1,99 @@
+"""The C-ABI library loads on a CPU-only box and exports the declared surface.
+
+No kernel is launched here: only descriptor validation and planning, which
+are host code inside the library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2006_13486_b200 import _native
+from paper_2006_13486_b200.device import chain_fields
+from paper_2006_13486_b200.sdmm import make_desc
+from paper_2006_13486_b200 import workloads as wl
+
+from conftest import ROOT
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "rbgp4.h")).read()
+    return sorted(set(re.findall(r"\b(rbgp4_[a-z_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert set(declared_functions()) == set(_native.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.rbgp4_abi_version() == 1
+
+
+def test_desc_struct_layout():
+    # two int64 groups (5) + ten int32 fields -> 80 bytes, no padding surprises
+    assert ctypes.sizeof(_native.Desc) == 5 * 8 + 10 * 4
+
+
+def _desc(cfg, n=None):
+    chain = wl.build_chain(cfg)
+    n = cfg.n_cols if n is None else n
+    return make_desc(chain_fields(chain), n, n, n)
+
+
+def test_supported_matrix():
+    lib = _native.lib()
+    d = _desc(wl.C1A)
+    exact, ffma = _native.COMPUTE["exact"], _native.COMPUTE["ffma"]
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), exact, _native.F32, _native.F32) == 1
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), ffma, _native.F64, _native.F64) == 1
+    # SIMT output type must equal the operand type
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), exact, _native.F32, _native.F64) == 0
+    assert "same type" in _native.last_error()
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), 9, _native.F32, _native.F32) == 0
+    assert lib.rbgp4_workspace_size(ctypes.byref(d), exact, _native.F32) == 0
+
+
+def test_inconsistent_descriptor_rejected():
+    lib = _native.lib()
+    d = _desc(wl.C1A)
+    d.rows += 1
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), 0, _native.F32, _native.F32) == 0
+    assert "disagrees" in _native.last_error()
+    rc = lib.rbgp4_sdmm(ctypes.byref(d), 0, 0, 0, None, None, None, None, None, None, 0, None)
+    assert rc == -1
+
+
+def test_leading_dimension_rejected():
+    lib = _native.lib()
+    d = _desc(wl.C1A)
+    d.ld_in = d.n_cols - 1
+    assert lib.rbgp4_sdmm_supported(ctypes.byref(d), 0, _native.F32, _native.F32) == 0
+    assert "leading" in _native.last_error()
+
+
+def test_chain_kernel_argument_checks():
+    lib = _native.lib()
+    one = (ctypes.c_int32 * 1)(4)
+    off = (ctypes.c_int64 * 1)(0)
+    rc = lib.rbgp4_chain_sdmm(0, one, one, one, off, None, 0, None, None, None, 8, 8, 8, None)
+    assert rc == -1 and "chain length" in _native.last_error()
+    rc = lib.rbgp4_chain_sdmm(1, one, one, one, off, None, 7, None, None, None, 8, 8, 8, None)
+    assert rc == -1
+
+
+def test_product_path_fails_loudly_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    import paper_2006_13486_b200 as ks
+    chain, w, inp = wl.make_operands(wl.C1A)
+    with pytest.raises(ks.DeviceError):
+        ks.rbgp4mm(w, inp, ks.tiling_for_chain(chain))

@@ -1,0 +1,146 @@
+"""CUDA path vs the reference (golden hashes) and vs the pinned CPU oracle.
+
+Bar (BASELINE north star):
+  * compute="exact"  -> bit-identical to the reference rbgp4mm (f32 and f64)
+  * sdmm_reference   -> bit-identical to the reference sdmm_reference
+  * compute="ffma"   -> max-rel <= 1e-5 (f32) / 1e-12 (f64) vs the f64 oracle
+  * tf32 / bf16      -> rel-L2 <= 1e-2 vs the f64 oracle
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2006_13486_b200 as ks
+from paper_2006_13486_b200 import _native
+from paper_2006_13486_b200 import workloads as wl
+
+from conftest import case_config, corpus_chain, corpus_inputs, ring_graph, sha16
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def f64_oracle(w, inp):
+    w64 = ks.RcubsMatrix(w.chain, np.asarray(w.values, dtype=np.float64))
+    return oracle.reference_product(w64, np.asarray(inp, dtype=np.float64), threads=8)
+
+
+def test_device_and_library_present():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    assert _native.lib().rbgp4_abi_version() == 1
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_cases_exact_bit_identical(golden, precision):
+    for cid, entry in golden["cases"].items():
+        cfg = case_config(entry, precision, cid)
+        chain, w, inp = wl.make_operands(cfg)
+        p = ks.tiling_for_chain(chain, tn=cfg.tn, rn=cfg.rn, bn=cfg.bn, workers=4)
+        out, rep = ks.rbgp4mm(w, inp, p)
+        assert out.dtype == w.dtype and out.shape == (w.rows, cfg.n_cols)
+        assert sha16(out) == entry[precision]["rbgp4mm"], cid
+        assert rep.to_dict() == entry[precision]["report"], cid
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_cases_sdmm_reference_bit_identical(golden, precision):
+    for cid, entry in golden["cases"].items():
+        chain, w, inp = wl.make_operands(case_config(entry, precision, cid))
+        assert sha16(ks.sdmm_reference(w, inp)) == entry[precision]["sdmm_reference"], cid
+        assert sha16(ks.sdmm_reference(w.to_unstructured(), inp)) == \
+            entry[precision]["sdmm_reference"], cid
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64"])
+def test_corpus_exact_bit_identical(golden, precision):
+    for rec in golden["corpus"]:
+        chain = corpus_chain(rec)
+        w, inp = corpus_inputs(rec, chain, precision)
+        p = ks.tiling_for_chain(chain, tn=rec["tn"], rn=rec["rn"], bn=rec["bn"])
+        out, rep = ks.rbgp4mm(w, inp, p)
+        assert sha16(out) == rec[precision]["rbgp4mm"], rec
+        assert rep.fma_count == rec[precision]["fma_count"]
+        assert rep.steps_skipped_per_tile == rec[precision]["steps_skipped_per_tile"]
+
+
+@pytest.mark.parametrize("precision,tol", [("f32", 1e-5), ("f64", 1e-12)])
+def test_corpus_ffma_within_tolerance(golden, precision, tol):
+    worst = 0.0
+    for rec in golden["corpus"]:
+        chain = corpus_chain(rec)
+        w, inp = corpus_inputs(rec, chain, precision)
+        p = ks.tiling_for_chain(chain, tn=rec["tn"], rn=rec["rn"], bn=rec["bn"])
+        out, _ = ks.rbgp4mm(w, inp, p, compute="ffma")
+        worst = max(worst, oracle.max_rel(out, f64_oracle(w, inp)))
+    assert worst <= tol, worst
+
+
+def test_identity_passthrough_bit_exact():
+    chain = ks.RbgpChain((ring_graph(4, d=1), ks.complete_graph(1, 1), ks.complete_graph(1, 1),
+                          ks.complete_graph(1, 1)))
+    w = ks.RcubsMatrix(chain, np.ones((4, 1)))
+    inp = np.random.default_rng(0).standard_normal((4, 8))
+    out, rep = ks.rbgp4mm(w, inp, ks.tiling_for_chain(chain, tn=8, rn=1, bn=8, workers=2))
+    assert np.array_equal(out, inp) and rep.steps_per_tile == 1
+
+
+def test_ragged_and_strided_columns():
+    """N not a multiple of 4, odd leading dimensions, column sub-views."""
+    chain, w, _ = wl.make_operands(wl.C1A)
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    rng = np.random.default_rng(3)
+    for n in (1, 3, 5, 130):
+        inp = rng.uniform(-1, 1, (w.cols, n)).astype(np.float32)
+        out, _ = ks.rbgp4mm(w, inp, p)
+        assert np.array_equal(out, oracle.tiled(w, inp, p)), n
+    big = torch.from_numpy(rng.uniform(-1, 1, (w.cols, 301)).astype(np.float32)).cuda()
+    view = big[:, 7:7 + 129]  # ld_in = 301, unaligned base
+    out, _ = ks.rbgp4mm(w, view, p)
+    assert out.is_cuda
+    ref = oracle.tiled(w, view.cpu().numpy(), p)
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+def test_zero_columns():
+    chain, w, _ = wl.make_operands(wl.C1A)
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    out, rep = ks.rbgp4mm(w, np.zeros((w.cols, 0), np.float32), p)
+    assert out.shape == (w.rows, 0) and rep.fma_count == 0
+
+
+def test_torch_tensors_stay_on_device_and_out_param():
+    chain, w, inp = wl.make_operands(wl.C1A)
+    p = ks.tiling_for_chain(chain)
+    x = torch.from_numpy(inp).cuda()
+    res = torch.empty((w.rows, inp.shape[1]), device="cuda", dtype=torch.float32)
+    out, _ = ks.rbgp4mm(w, x, p, out=res)
+    assert out is res
+    assert sha16(res.cpu().numpy()) == "9fe440861f6f8868"
+    pinned = torch.from_numpy(inp).pin_memory()
+    host, _ = ks.rbgp4mm(w, pinned, p)
+    assert not host.is_cuda and sha16(host.numpy()) == "9fe440861f6f8868"
+
+
+def test_general_chain_reference_on_gpu():
+    rng = np.random.default_rng(11)
+    chain = ks.RbgpChain((ring_graph(8, 3), ks.complete_graph(2, 2), ring_graph(4, 2)))
+    w = ks.init_random(chain, 4, precision="f32")
+    inp = rng.uniform(-1, 1, (w.cols, 77)).astype(np.float32)
+    got = ks.sdmm_reference(w, inp)
+    assert np.array_equal(got, oracle.reference_product(w, inp))
+
+
+@pytest.mark.parametrize("compute,tol", [("tf32", 1e-2), ("bf16", 1e-2)])
+def test_tensor_core_modes(golden, compute, tol):
+    lib = _native.lib()
+    for cid in ("c1b", "vgg-c10-875", "vgg-c10-tc", "t2-o50-i50"):
+        entry = golden["cases"][cid]
+        chain, w, inp = wl.make_operands(case_config(entry, "f32", cid))
+        p = ks.tiling_for_chain(chain, tn=entry["tn"], rn=entry["rn"], bn=entry["bn"])
+        out, _ = ks.rbgp4mm(w, inp, p, compute=compute)
+        err = oracle.rel_l2(out, f64_oracle(w, inp))
+        assert err <= tol, (cid, compute, err)
