@@ -169,7 +169,10 @@ def load_traffic():
 
 
 # ----------------------------------------------------------------- CPU legs
-def cpu_sample(layers, seconds: float, threads: int, cols: int = 128):
+CPU_SAMPLE_COLS = 512  # 4 column tiles of the reference tn=128 -> 16 tiles per layer
+
+
+def cpu_sample(layers, seconds: float, threads: int, cols: int = CPU_SAMPLE_COLS):
     """Reference algorithm (oracle C port of _tile_worker, f32) on a column slice.
 
     Work is linear in N and tiles are independent (reference sdmm.py:167), so
@@ -207,7 +210,7 @@ def run_reference(args):
     layers = build_layers(args.sparsity, args.batch)
     import oracle
     oracle.build()
-    cols = 64
+    cols = CPU_SAMPLE_COLS
     samples = [(lay, make_input(dict(lay, n=cols, rng=np.random.default_rng(1)))) for lay in layers]
     flops = sum(2 * lay["nnz"] * cols for lay, _ in samples)
 
@@ -222,8 +225,9 @@ def run_reference(args):
         step()
     dt = time.perf_counter() - t0
     value = flops * args.steps / dt / 1e12
-    sample = (f"8 VGG19 512-ch layers at {args.sparsity * 100:g}% , first {cols} columns of each "
-              f"(work linear in N); f32 exact-order C port of kronsparse._tile_worker")
+    sample = (f"8 VGG19 512-ch layers at {args.sparsity * 100:g}%, first {cols} columns of each "
+              f"(tn=128 tiles, work linear in N); f32 exact-order C port of "
+              f"kronsparse._tile_worker on {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,

@@ -18,11 +18,13 @@
 //   D          += A * B   with tk*E/32 tcgen05.mma (M=128, N=TN, K=32 bytes),
 //               fp32 accumulation in TMEM (TN columns).
 //
-// Warp roles (192 threads):  warps 0-3 densify A and run the epilogue
+// Warp roles (224 threads):  warps 0-3 densify A and run the epilogue
 // (tcgen05.ld 32x32b -> registers -> 16-byte global stores; warp w owns TMEM
-// lanes 32w..32w+31 = output rows);  warp 4 lane 0 issues the TMA loads;
-// warp 5 allocates TMEM and lane 0 issues the MMAs.  An NS-stage mbarrier
-// ring links them:  full_b (TMA tx bytes), full_a (128 densify arrivals),
+// lanes 32w..32w+31 = output rows);  warp 4 lane 0 issues the I-slab TMA
+// loads; warp 6 lane 0 the compressed-W TMA loads (separate rings so the I
+// stream never waits on densify progress); warp 5 allocates TMEM and lane 0
+// issues the MMAs.  An NS-stage mbarrier
+// ring links them:  full_b (TMA tx bytes), full_a (4 densify-warp arrivals),
 // empty (tcgen05.commit), tmem_full (last commit).
 //
 // Roofline: bound by HBM for the VGG/WRN layer shapes (compressed W + I +
@@ -33,12 +35,25 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cstring>
 #include <mutex>
 
 namespace rbgp4 {
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;
+
+// Debug trace (RBGP4_TC_DEBUG bit 8): CTA 0 stamps clock64 at every role hand-off.
+// Layout: [event][step], event = 0 B issued, 1 W issued, 2 densify start, 3 densify end,
+// 4 MMA start, 5 MMA end; [6][0] setup done, [6][1] epilogue start, [6][2] epilogue end;
+// 7 MMA saw full_b, 8 densify saw full_w (per W stage).
+constexpr int kTraceSteps = 512;
+__device__ unsigned long long g_trace[10][kTraceSteps];
+__device__ __forceinline__ void trace(const int debug, int ev, int step) {
+    if ((debug & 8) && blockIdx.x == 0 && blockIdx.y == 0 && step < kTraceSteps)
+        g_trace[ev][step] = clock64();
+}
 constexpr int kBlockM = 128;
 
 struct TcParams {
@@ -46,9 +61,15 @@ struct TcParams {
     int32_t tm, tk, d_o, d_t, u_i, v_i, d_i, rk, bm, bk;
     int32_t tn;              // MMA N (columns per CTA), multiple of 16, <= 256
     int32_t rows_valid;      // 128, or 64 when tm == 64 (upper half of A is zero)
-    int32_t stages;
+    int32_t na, nb, nw;      // ring depths: dense A tiles, I slabs, compressed W tiles
+    int32_t w_tma;           // compressed W tiles staged by TMA (else read by the densify warps)
+    int32_t ws;              // steps per W stage (one TMA box carries ws consecutive W tiles)
+    int32_t i3d;             // one 3-D TMA per I slab (all column atoms) instead of one per atom
     int32_t a_swz;           // K-major swizzle span of A in bytes: 32 / 64 / 128
-    int32_t a_stage_bytes, b_stage_bytes;
+    int32_t a_stage_bytes, b_stage_bytes, w_stage_bytes;
+    int32_t debug;           // ablation bits (RBGP4_TC_DEBUG): 1 no densify, 2 no MMA, 4 no epilogue
+    int32_t ksplit, sps;     // split-K: CTAs per output tile (one cluster) and steps per slice
+    int32_t adj_smem;        // g_i adjacency staged in shared memory for the table build
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -65,8 +86,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef RBGP4_MBAR_POLL
+#define RBGP4_MBAR_POLL 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
+#if RBGP4_MBAR_POLL
+    // pure polling: test_wait never suspends the thread
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr), "r"(parity) : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -74,6 +108,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(addr), "r"(parity) : "memory");
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
                                             int32_t x, int32_t y) {
@@ -81,6 +116,31 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+template <typename E>
+__device__ __forceinline__ void sts_elem(uint32_t addr, E v) {
+    if constexpr (sizeof(E) == 2) sts16(addr, *reinterpret_cast<uint16_t *>(&v));
+    else sts32(addr, *reinterpret_cast<uint32_t *>(&v));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int32_t x, int32_t y, int32_t z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() {
@@ -147,89 +207,144 @@ __device__ __forceinline__ uint32_t swz(uint32_t off, int span) {
 // ---------------------------------------------------------------- the kernel
 template <typename E, bool OUT_BF16>
 __global__ void __launch_bounds__(kThreads, 1)
-tc_kernel(const __grid_constant__ CUtensorMap imap, const TcParams p, const E *__restrict__ values,
-          const int32_t *__restrict__ adj_o, const int32_t *__restrict__ adj_i,
-          void *__restrict__ out) {
+tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
+          const TcParams p, const E *__restrict__ values, const int32_t *__restrict__ adj_o,
+          const int32_t *__restrict__ adj_i, void *__restrict__ out, float *__restrict__ wsp) {
     constexpr bool kTF32 = sizeof(E) == 4;
     constexpr int kElt = sizeof(E);
     extern __shared__ unsigned char smem_raw[];
-    // 1024-byte aligned carve-up: [A stages][B stages][aoff table][barriers][tmem ptr]
+    // 1024-byte aligned carve-up:
+    //   [A ring: na x 128 x tk dense]  [B ring: nb x tk x tn]  [W ring: nw x rows x d_t]
+    //   [aoff table 128 x d_t u16]  [barriers]  [tmem ptr]
     unsigned char *base = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char *a_buf = base;
-    unsigned char *b_buf = a_buf + p.stages * p.a_stage_bytes;
+    unsigned char *b_buf = a_buf + p.na * p.a_stage_bytes;
+    unsigned char *w_buf = b_buf + p.nb * p.b_stage_bytes;
     // aoff[j * 128 + r]: byte offset (inside an A stage) of nonzero j of CTA row r
-    uint16_t *aoff = reinterpret_cast<uint16_t *>(b_buf + p.stages * p.b_stage_bytes);
+    uint16_t *aoff = reinterpret_cast<uint16_t *>(w_buf + p.nw * p.w_stage_bytes);
+    int32_t *adj_s = reinterpret_cast<int32_t *>(
+        (reinterpret_cast<uintptr_t>(aoff + kBlockM * p.d_t) + 15) & ~uintptr_t(15));
     uint64_t *bars = reinterpret_cast<uint64_t *>(
-        (reinterpret_cast<uintptr_t>(aoff + kBlockM * p.d_t) + 7) & ~uintptr_t(7));
-    uint64_t *full_b = bars, *full_a = bars + p.stages, *empty = bars + 2 * p.stages;
-    uint64_t *tmem_full = bars + 3 * p.stages;
+        (reinterpret_cast<uintptr_t>(adj_s + (p.adj_smem ? p.u_i * p.d_i : 0)) + 7) & ~uintptr_t(7));
+    uint64_t *full_b = bars, *empty_b = full_b + p.nb;
+    uint64_t *full_a = empty_b + p.nb, *empty_a = full_a + p.na;
+    uint64_t *full_w = empty_a + p.na, *empty_w = full_w + p.nw;
+    uint64_t *tmem_full = empty_w + p.nw;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) trace(p.debug, 6, 3);
     const int64_t n0 = int64_t(blockIdx.x) * p.tn;
     const int64_t m0 = int64_t(blockIdx.y) * p.rows_valid;  // first W row of this CTA
     const int64_t tbm = m0 / p.tm;
     const int row_in_tile0 = int(m0 - tbm * p.tm);
+    // split-K: this CTA runs steps [s_begin, s_begin + nsteps) of the tile-row
+    const int kslice = blockIdx.z;
+    const int s_begin = kslice * p.sps;
+    const int nsteps = min(p.d_o, s_begin + p.sps) - s_begin;
 
-    // ---- one-time setup: zero A stages, scatter-offset table, barriers, TMEM.
-    // The in-tile pattern is the same for every step, so the (row, j) -> A
-    // position map is computed once here and the per-step densify is a pure
-    // table-driven scatter (reference index map: sdmm.py:183-186).
-    {
-        uint4 z = make_uint4(0, 0, 0, 0);
-        uint4 *a4 = reinterpret_cast<uint4 *>(a_buf);
-        for (int i = threadIdx.x; i < p.stages * p.a_stage_bytes / 16; i += kThreads) a4[i] = z;
-        for (int e = threadIdx.x; e < kBlockM * p.d_t; e += kThreads) {
-            const int j = e / kBlockM, r = e - j * kBlockM;
-            const int u_loc = row_in_tile0 + r;
-            const int ui = (u_loc / p.bm) % p.u_i;
-            const int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
-            const int kcol = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;  // local K index
-            const uint32_t kb = uint32_t(kcol) * kElt;
-            aoff[e] = uint16_t((kb / p.a_swz) * (kBlockM * p.a_swz) +
-                               swz(uint32_t(r) * p.a_swz + (kb % p.a_swz), p.a_swz));
-        }
-    }
-    if (warp == 4 && lane == 0) {
-        for (int s = 0; s < p.stages; ++s) {
-            mbar_init(&full_b[s], 1);
-            mbar_init(&full_a[s], kBlockM);
-            mbar_init(&empty[s], 1);
-        }
-        mbar_init(tmem_full, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
-    }
+    // TMEM first: the allocation latency overlaps the table build below
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
                      "r"(uint32_t(p.tn < 32 ? 32 : p.tn)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (lane == 0) trace(p.debug, 6, 5);
+    }
+    // ---- one-time setup: zero the A ring, scatter-offset table, barriers, TMEM.
+    // The in-tile pattern is the same for every step, so the (row, j) -> A
+    // position map is computed once here and the per-step densify is a pure
+    // table-driven scatter (reference index map: sdmm.py:183-186).  Zeros
+    // written now are never overwritten: every step fills the same positions.
+    {
+        uint4 z = make_uint4(0, 0, 0, 0);
+        uint4 *a4 = reinterpret_cast<uint4 *>(a_buf);
+        for (int i = threadIdx.x; i < p.na * p.a_stage_bytes / 16; i += kThreads) a4[i] = z;
+        const int32_t *adj = adj_i;
+        if (p.adj_smem && threadIdx.x < kBlockM) {
+            // one coalesced copy instead of d_t dependent global loads per row; only the
+            // four table-building warps synchronise on it (named barrier 1)
+            for (int i = threadIdx.x; i < p.u_i * p.d_i; i += kBlockM) adj_s[i] = adj_i[i];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            adj = adj_s;
+        }
+        if (threadIdx.x < kBlockM) {
+            // thread r owns CTA row r: walk j = ((rk*d_i + ink)*bk + k) with counters
+            const int r = threadIdx.x;
+            const int ui = ((row_in_tile0 + r) / p.bm) % p.u_i;
+            const int32_t *arow = adj + ui * p.d_i;
+            const int sh = p.a_swz == 128 ? 7 : p.a_swz == 64 ? 6 : 5;  // log2(swizzle span)
+            const uint32_t rbase = uint32_t(r) << sh;
+            int k = 0, ink = 0, rk = 0;
+            int kbase = arow[0] * p.bk;  // (rk*v_i + adj_i[ui][ink])*bk
+            for (int j = 0; j < p.d_t; ++j) {
+                const uint32_t kb = uint32_t(kbase + k) * kElt;  // byte offset along K
+                aoff[j * kBlockM + r] =
+                    uint16_t(((kb >> sh) << (sh + 7)) + swz(rbase + (kb & (p.a_swz - 1)), p.a_swz));
+                if (++k == p.bk) {
+                    k = 0;
+                    if (++ink == p.d_i) { ink = 0; ++rk; }
+                    if (rk < p.rk) kbase = (rk * p.v_i + arow[ink]) * p.bk;
+                }
+            }
+        }
+    }
+    if (threadIdx.x == 0) trace(p.debug, 6, 4);
+    if (warp == 4 && lane == 0) {
+        for (int i = 0; i < p.nb; ++i) { mbar_init(&full_b[i], 1); mbar_init(&empty_b[i], 1); }
+        for (int i = 0; i < p.na; ++i) { mbar_init(&full_a[i], 4); mbar_init(&empty_a[i], 1); }
+        for (int i = 0; i < p.nw; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
+        if (p.w_tma)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     }
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_d = *tmem_slot;
-    const int32_t *orow = adj_o + tbm * p.d_o;
+    const int32_t *orow = adj_o + tbm * p.d_o + s_begin;
+    if (threadIdx.x == 0) trace(p.debug, 6, 0);
 
     if (warp == 4) {
-        // ================= TMA producer: I slabs =================
+        // ================= TMA producer: I slabs (runs ahead by the B ring depth) ==========
         if (lane == 0) {
             const int atoms = p.tn * kElt / 128;           // 128-byte MN atoms per slab
             const int atom_cols = 128 / kElt;
             const uint32_t atom_bytes = uint32_t(p.tk) * 128;
-            for (int s = 0; s < p.d_o; ++s) {
-                const int st = s % p.stages;
-                const uint32_t ph = (s / p.stages) & 1;
-                mbar_wait(&empty[st], ph ^ 1);
+            for (int s = 0; s < nsteps; ++s) {
+                const int st = s % p.nb;
+                const uint32_t ph = (s / p.nb) & 1;
+                mbar_wait(&empty_b[st], ph ^ 1);
                 mbar_expect_tx(&full_b[st], uint32_t(p.b_stage_bytes));
                 const int32_t krow = orow[s] * p.tk;
                 unsigned char *dst = b_buf + st * p.b_stage_bytes;
-                for (int a = 0; a < atoms; ++a)
-                    tma_load_2d(dst + a * atom_bytes, &imap, &full_b[st],
-                                int32_t(n0) + a * atom_cols, krow);
+                if (p.i3d) {
+                    // one instruction for the whole slab: (atom cols, K rows, atoms) box
+                    tma_load_3d(dst, &imap, &full_b[st], 0, krow, int32_t(n0) / atom_cols);
+                } else {
+                    for (int a = 0; a < atoms; ++a)
+                        tma_load_2d(dst + a * atom_bytes, &imap, &full_b[st],
+                                    int32_t(n0) + a * atom_cols, krow);
+                }
+                trace(p.debug, 0, s);
+            }
+        }
+    } else if (warp == 6) {
+        // ================= TMA producer: compressed W tiles (own ring, own pace) ============
+        if (lane == 0 && p.w_tma) {
+            const int wstages = (nsteps + p.ws - 1) / p.ws;
+            for (int g = 0; g < wstages; ++g) {
+                const int st = g % p.nw;
+                const uint32_t ph = (g / p.nw) & 1;
+                mbar_wait(&empty_w[st], ph ^ 1);
+                mbar_expect_tx(&full_w[st], uint32_t(p.w_stage_bytes));
+                tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st],
+                            (s_begin + g * p.ws) * p.d_t, int32_t(m0));
+                trace(p.debug, 1, g);
             }
         }
     } else if (warp == 5) {
@@ -239,29 +354,45 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const TcParams p, const E *_
             const uint32_t fmt = kTF32 ? 2u : 1u;
             const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
                                    (uint32_t(p.tn >> 3) << 17) | (uint32_t(kBlockM >> 4) << 24);
-            const uint32_t a_layout = swizzle_layout_code(p.a_swz);
             const int ksteps = p.tk * kElt / 32;
-            for (int s = 0; s < p.d_o; ++s) {
-                const int st = s % p.stages;
-                const uint32_t ph = (s / p.stages) & 1;
-                mbar_wait(&full_b[st], ph);
-                mbar_wait(&full_a[st], ph);
+            // Descriptors are built once; per stage / K-step only the 14-bit start-address
+            // field (16-byte units, low word) moves, so the issue loop is pure adds.
+            const uint64_t a_desc0 =
+                smem_desc(smem_u32(a_buf), 0, 8 * p.a_swz, swizzle_layout_code(p.a_swz));
+            // MN-major B: bf16 -> SWIZZLE_128B (8-row K groups, SBO 1024);
+            // tf32 -> SWIZZLE_128B_BASE32B (32 B chunks, 4-row K groups, SBO 512)
+            const uint64_t b_desc0 = kTF32 ? smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 512, 1u)
+                                           : smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 1024, 2u);
+            const uint32_t a_stage16 = uint32_t(p.a_stage_bytes) >> 4;
+            const uint32_t b_stage16 = uint32_t(p.b_stage_bytes) >> 4;
+            const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
+            const uint32_t a_jump16 = uint32_t(kBlockM - 1) * a_span16;        // next K atom
+            const uint32_t b_step16 = uint32_t(32 / kElt) * 128 / 16;           // 32/E K-rows
+            for (int s = 0; s < nsteps; ++s) {
+                const int sb = s % p.nb, sa = s % p.na;
+                mbar_wait(&full_b[sb], (s / p.nb) & 1);
+                trace(p.debug, 7, s);
+                mbar_wait(&full_a[sa], (s / p.na) & 1);
                 tc_fence_after();
-                const uint32_t a0 = smem_u32(a_buf + st * p.a_stage_bytes);
-                const uint32_t b0 = smem_u32(b_buf + st * p.b_stage_bytes);
+                trace(p.debug, 4, s);
+                uint64_t ad = a_desc0 + uint64_t(sa) * a_stage16;
+                uint64_t bd = b_desc0 + uint64_t(sb) * b_stage16;
+                uint32_t in_atom = 0;
                 for (int kk = 0; kk < ksteps; ++kk) {
-                    const uint32_t kb = uint32_t(kk) * 32;  // byte offset along K
-                    const uint32_t a_addr =
-                        a0 + (kb / p.a_swz) * (kBlockM * p.a_swz) + (kb % p.a_swz);
-                    const uint64_t ad = smem_desc(a_addr, 0, 8 * p.a_swz, a_layout);
-                    const uint32_t b_addr = b0 + (kb / kElt) * 128;  // 32/E K-rows of 128 B
-                    // MN-major B: bf16 -> SWIZZLE_128B (8-row K groups, SBO 1024);
-                    // tf32 -> SWIZZLE_128B_BASE32B (32 B chunks, 4-row K groups, SBO 512)
-                    const uint64_t bd = kTF32 ? smem_desc(b_addr, uint32_t(p.tk) * 128, 512, 1u)
-                                              : smem_desc(b_addr, uint32_t(p.tk) * 128, 1024, 2u);
-                    tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                    if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                    ad += 2;  // 32 bytes along K inside the swizzle atom
+                    in_atom += 2;
+                    if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
+                    bd += b_step16;
                 }
-                tc_commit(&empty[st]);
+                if ((p.debug & 34) == 34) {  // ablation: no MMAs issued, release slots directly
+                    mbar_arrive(&empty_b[sb]);
+                    mbar_arrive(&empty_a[sa]);
+                } else {
+                    tc_commit(&empty_b[sb]);
+                    tc_commit(&empty_a[sa]);
+                }
+                trace(p.debug, 5, s);
             }
             tc_commit(tmem_full);
         }
@@ -269,52 +400,144 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const TcParams p, const E *_
         // ================= densify (warps 0-3), then epilogue =================
         const int t = threadIdx.x;  // 0..127: this thread densifies CTA row t
         const bool active = t < p.rows_valid;
+        constexpr int V = 16 / kElt;          // elements per 16-byte chunk
+        constexpr int kRegNnz = 64;           // d_t handled from registers up to this
         const E *vrow = values + (m0 + t) * p.row_nnz;
-        constexpr int V = 16 / kElt;  // elements per 16-byte load
-        const bool vec = (p.d_t % V == 0) && (p.row_nnz % V == 0) &&
-                         (reinterpret_cast<uintptr_t>(values) % 16 == 0);
-        for (int s = 0; s < p.d_o; ++s) {
-            const int st = s % p.stages;
-            const uint32_t ph = (s / p.stages) & 1;
-            mbar_wait(&empty[st], ph ^ 1);
-            unsigned char *a = a_buf + st * p.a_stage_bytes;
-            if (active) {
-                const E *vs = vrow + int64_t(s) * p.d_t;
-                if (vec) {
+        // this row's scatter offsets never change: keep them in registers (2 per reg)
+        uint32_t offp[kRegNnz / 2];
+        const bool reg_path = p.w_tma && p.d_t <= kRegNnz;
+#pragma unroll
+        for (int i = 0; i < kRegNnz / 2; ++i) {
+            const int j = 2 * i;
+            uint32_t lo = j < p.d_t ? aoff[j * kBlockM + t] : 0u;
+            uint32_t hi = j + 1 < p.d_t ? aoff[(j + 1) * kBlockM + t] : 0u;
+            offp[i] = lo | (hi << 16);
+        }
+        const uint32_t wrow = smem_u32(w_buf) + uint32_t(t * p.ws * p.d_t * kElt);
+        for (int s = 0; s < nsteps; ++s) {
+            const int sa = s % p.na;
+            const int wg = s / p.ws, wsub = s - wg * p.ws;  // W stage and slot inside it
+            if (p.w_tma && wsub == 0) {
+                mbar_wait(&full_w[wg % p.nw], (wg / p.nw) & 1);
+                if (t == 0) trace(p.debug, 8, wg);
+            }
+            mbar_wait(&empty_a[sa], ((s / p.na) & 1) ^ 1);
+            if (t == 0) trace(p.debug, 2, s);
+            const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
+            if (active && !(p.debug & 1)) {
+                if (reg_path) {
+                    // compressed row t of this step (TMA-staged): 16-byte shared loads,
+                    // all issued before the scatter so their latency overlaps
+                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
+                                         uint32_t(wsub * p.d_t * kElt);
+                    uint4 q[kRegNnz / V];
+#pragma unroll
+                    for (int c = 0; c < kRegNnz / V; ++c)
+                        if (c * V < p.d_t) q[c] = lds128(src + 16 * c);
+#pragma unroll
+                    for (int c = 0; c < kRegNnz / V; ++c) {
+                        if (c * V < p.d_t) {
+                            const E *qe = reinterpret_cast<const E *>(&q[c]);
+#pragma unroll
+                            for (int v = 0; v < V; ++v) {
+                                const int j = c * V + v;
+                                const uint32_t o = (offp[j / 2] >> (16 * (j & 1))) & 0xFFFFu;
+                                sts_elem<E>(a + o, qe[v]);
+                            }
+                        }
+                    }
+                } else if (p.w_tma) {
+                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
+                                         uint32_t(wsub * p.d_t * kElt);
                     for (int j = 0; j < p.d_t; j += V) {
-                        uint4 q = __ldg(reinterpret_cast<const uint4 *>(vs + j));
+                        uint4 q = lds128(src + j * kElt);
                         const E *qe = reinterpret_cast<const E *>(&q);
 #pragma unroll
-                        for (int v = 0; v < V; ++v)
-                            *reinterpret_cast<E *>(a + aoff[(j + v) * kBlockM + t]) = qe[v];
+                        for (int v = 0; v < V; ++v) sts_elem<E>(a + aoff[(j + v) * kBlockM + t], qe[v]);
                     }
                 } else {
-                    for (int j = 0; j < p.d_t; ++j)
-                        *reinterpret_cast<E *>(a + aoff[j * kBlockM + t]) = vs[j];
+                    const E *vs = vrow + int64_t(s_begin + s) * p.d_t;
+                    for (int j = 0; j < p.d_t; ++j) sts_elem<E>(a + aoff[j * kBlockM + t], vs[j]);
                 }
             }
+            // make the generic-proxy stores visible to the tensor core, then one
+            // release-arrive per warp (full_a counts 4 warps)
             fence_async_smem();
-            mbar_arrive(&full_a[st]);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&full_a[sa]);
+                if (p.w_tma && (wsub == p.ws - 1 || s == nsteps - 1)) mbar_arrive(&empty_w[wg % p.nw]);
+            }
+            if (t == 0) trace(p.debug, 3, s);
         }
-        // ---- epilogue: TMEM -> registers -> global
+        // ---- epilogue phase 1: wait for the accumulator; split-K slices > 0 park
+        // their fp32 partial tile in the workspace (L2-resident) for the leader
         mbar_wait(tmem_full, 0);
         tc_fence_after();
+        if (threadIdx.x == 0) trace(p.debug, 6, 1);
+        if (kslice > 0) {
+            const int row = warp * 32 + lane;
+            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
+            float *dst = wsp + (int64_t(kslice - 1) * (int64_t(gridDim.y) * p.rows_valid) + m0 + row) *
+                                   p.n_cols;
+            for (int c = 0; c < p.tn; c += 32) {
+                uint32_t r[32];
+                TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                const int64_t col = n0 + c;
+                if (row >= p.rows_valid || col >= p.n_cols) continue;
+                if (col + 32 <= p.n_cols) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<uint4 *>(dst + col)[q] =
+                            make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                } else {
+                    for (int q = 0; q < 32 && col + q < p.n_cols; ++q) dst[col + q] = __uint_as_float(r[q]);
+                }
+            }
+        }
+    }
+    if (p.ksplit > 1) {
+        // every thread of every slice: partials written (release) -> leader reads (acquire)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (warp < 4 && kslice == 0) {
+        // ---- epilogue phase 2 (leader): TMEM + partials (fixed slice order) -> output
         const int row = warp * 32 + lane;
         const bool row_ok = row < p.rows_valid;
         const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
+        const int64_t slice_stride = int64_t(gridDim.y) * p.rows_valid * p.n_cols;
         for (int c = 0; c < p.tn; c += 32) {
             uint32_t r[32];
             TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const int64_t col = n0 + c;
-            if (!row_ok || col >= p.n_cols) continue;
+            if (!row_ok || col >= p.n_cols || (p.debug & 4)) continue;
             const bool full = col + 32 <= p.n_cols;
+            if (p.ksplit > 1) {
+                const float *part = wsp + (m0 + row) * p.n_cols + col;
+                for (int k = 1; k < p.ksplit; ++k, part += slice_stride) {
+                    if (full) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 v = __ldcg(reinterpret_cast<const float4 *>(part) + q);
+                            r[4 * q] = __float_as_uint(__uint_as_float(r[4 * q]) + v.x);
+                            r[4 * q + 1] = __float_as_uint(__uint_as_float(r[4 * q + 1]) + v.y);
+                            r[4 * q + 2] = __float_as_uint(__uint_as_float(r[4 * q + 2]) + v.z);
+                            r[4 * q + 3] = __float_as_uint(__uint_as_float(r[4 * q + 3]) + v.w);
+                        }
+                    } else {
+                        for (int q = 0; q < 32 && col + q < p.n_cols; ++q)
+                            r[q] = __float_as_uint(__uint_as_float(r[q]) + __ldcg(part + q));
+                    }
+                }
+            }
             if constexpr (OUT_BF16) {
                 __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(out) + (m0 + row) * p.ld_out + col;
                 if (full && (reinterpret_cast<uintptr_t>(dst) % 16 == 0)) {
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        uint4 pk;
                         uint32_t w[4];
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
@@ -322,8 +545,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const TcParams p, const E *_
                                 __uint_as_float(r[q * 8 + 2 * h]), __uint_as_float(r[q * 8 + 2 * h + 1]));
                             w[h] = *reinterpret_cast<uint32_t *>(&b2);
                         }
-                        pk = make_uint4(w[0], w[1], w[2], w[3]);
-                        reinterpret_cast<uint4 *>(dst)[q] = pk;
+                        reinterpret_cast<uint4 *>(dst)[q] = make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 } else {
                     for (int q = 0; q < 32 && col + q < p.n_cols; ++q)
@@ -342,6 +564,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const TcParams p, const E *_
             }
         }
     }
+    if (threadIdx.x == 0) trace(p.debug, 6, 2);
     tc_fence_before();
     __syncthreads();
     if (warp == 5) {
@@ -398,24 +621,59 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
     const int kbytes = c.tk * elt;
     p.a_swz = kbytes % 128 == 0 ? 128 : kbytes % 64 == 0 ? 64 : 32;
     p.a_stage_bytes = kBlockM * kbytes;
-    // widest N (<= 256) that still leaves >= 2 pipeline stages and enough CTAs
+    // compressed W tiles come in by TMA when a row of one step is whole 16-byte chunks
+    p.w_tma = (c.d_t * elt) % 16 == 0 && c.d_t <= 256 ? 1 : 0;
+    // W stage: as many consecutive steps as fit one box (<= 256 elements, <= 32 KB)
+    p.ws = 1;
+    while (p.w_tma && p.ws * 2 <= c.d_o && p.ws * 2 * c.d_t <= 256 &&
+           size_t(p.rows_valid) * p.ws * 2 * c.d_t * elt <= 16384)
+        p.ws *= 2;
+    p.w_stage_bytes = p.w_tma ? p.rows_valid * p.ws * c.d_t * elt : 0;
+    // Wide N tiles give fat TMA boxes (the I stream is bound by per-instruction TMA cost);
+    // split-K over a cluster then restores the SM count: ~one CTA per SM in total.
     const int64_t blocks_m = c.rows / p.rows_valid;
-    int tn = 256;
     const int tn_min = 128 / elt;  // one 128-byte swizzle atom of B along N
-    while (tn > tn_min && ((c.n_cols + tn - 1) / tn) * blocks_m < 2 * kNumSMs) tn /= 2;
+    int tn = 128;  // measured best on the VGG shapes (tools/tc_time.py); 256 only pays at large N
+    while (tn > tn_min && tn / 2 >= c.n_cols) tn /= 2;
+    if (const char *env = getenv("RBGP4_TC_TN")) tn = std::max(tn_min, std::min(256, atoi(env)));
+    p.adj_smem = size_t(c.u_i) * c.d_i * 4 <= 16384 ? 1 : 0;
     for (; tn >= tn_min; tn /= 2) {
         p.tn = tn;
         p.b_stage_bytes = c.tk * tn * elt;
-        const size_t fixed = 1024 + size_t(kBlockM) * c.d_t * 2 + 16 + 8 * (3 * 8 + 1) + 16;
-        const size_t per = size_t(p.a_stage_bytes) + p.b_stage_bytes;
-        if (fixed + 2 * per > kSmemCap) continue;
-        // two CTAs per SM when >= 3 stages fit in half the shared memory
-        int stages = int((kSmemCap / 2 - 1024 - fixed) / per);
-        if (stages < 3) stages = int((kSmemCap - fixed) / per);
-        if (stages > 6) stages = 6;
-        p.stages = stages;
+        // one CTA per SM: A ring 3 deep, W ring 2 x <=16 KB, the rest of smem to the I ring
+        // (the I stream is latency x depth bound: TMA latency under load is ~2-3 us)
+        p.na = 3;
+        p.nw = p.w_tma ? 2 : 1;
+        size_t fixed = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 + size_t(p.na) * p.a_stage_bytes +
+                       size_t(p.nw) * p.w_stage_bytes + (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0);
+        fixed += 8 * (2 * 16 + 2 * p.na + 2 * p.nw + 1);
+        while (fixed + 3 * size_t(p.b_stage_bytes) > kSmemCap && p.nw > 2 && p.w_tma) {
+            fixed -= p.w_stage_bytes;  // trade W depth first
+            --p.nw;
+        }
+        while (fixed + 3 * size_t(p.b_stage_bytes) > kSmemCap && p.na > 2) {
+            fixed -= p.a_stage_bytes;
+            --p.na;
+        }
+        if (fixed + 2 * size_t(p.b_stage_bytes) > kSmemCap && p.w_tma) {
+            // large compressed tiles: read W straight from global in the densify warps
+            fixed -= size_t(p.nw) * p.w_stage_bytes;
+            p.w_tma = 0;
+            p.ws = 1;
+            p.nw = 1;
+            p.w_stage_bytes = 0;
+        }
+        if (fixed + 2 * size_t(p.b_stage_bytes) > kSmemCap) continue;
+        p.nb = int(std::min<size_t>(16, (kSmemCap - fixed) / p.b_stage_bytes));
+        const int64_t tiles = ((c.n_cols + tn - 1) / tn) * blocks_m;
+        // split-K only when the tiles leave most SMs idle (cluster of ks CTAs per tile)
+        int ks = 1;
+        while (ks < 4 && tiles * ks * 2 <= kNumSMs && (ks * 2) <= c.d_o) ks *= 2;
+        if (const char *env = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(env)));
+        p.sps = (c.d_o + ks - 1) / ks;
+        p.ksplit = (c.d_o + p.sps - 1) / p.sps;  // no empty slices
         out->p = p;
-        out->smem = fixed + per * stages;
+        out->smem = fixed + size_t(p.nb) * p.b_stage_bytes;
         out->blocks_m = int(blocks_m);
         return 1;
     }
@@ -424,8 +682,9 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
 }
 
 template <typename E, bool OUT_BF16>
-int launch_typed(const TcPlan &pl, const CUtensorMap &map, const void *values,
-                 const int32_t *adj_o, const int32_t *adj_i, void *out, cudaStream_t stream) {
+int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wmap,
+                 const void *values, const int32_t *adj_o, const int32_t *adj_i, void *out,
+                 float *wsp, cudaStream_t stream) {
     auto kern = tc_kernel<E, OUT_BF16>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
@@ -433,9 +692,27 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const void *values,
         set_error("cudaFuncSetAttribute(tc): %s", cudaGetErrorString(e));
         return RBGP4_ECUDA;
     }
-    dim3 grid(unsigned((pl.p.n_cols + pl.p.tn - 1) / pl.p.tn), unsigned(pl.blocks_m));
-    kern<<<grid, kThreads, pl.smem, stream>>>(map, pl.p, static_cast<const E *>(values), adj_o,
-                                              adj_i, out);
+    dim3 grid(unsigned((pl.p.n_cols + pl.p.tn - 1) / pl.p.tn), unsigned(pl.blocks_m),
+              unsigned(pl.p.ksplit));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);  // the K slices of one tile co-reside
+    cfg.attrs = attr;
+    cfg.numAttrs = pl.p.ksplit > 1 ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, map, wmap, pl.p, static_cast<const E *>(values), adj_o, adj_i,
+                           out, wsp);
+    if (e != cudaSuccess) {
+        set_error("tc_kernel launch (grid %u x %u x %u, smem %zu): %s", grid.x, grid.y, grid.z,
+                  pl.smem, cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
     RBGP4_CHECK_LAUNCH("tc_kernel launch");
     return RBGP4_OK;
 }
@@ -451,11 +728,16 @@ int tc_supported(const ChainDims &c, int compute, int out_dtype) {
     return plan_tc(c, compute, &pl);
 }
 
-size_t tc_workspace_size(const ChainDims &, int) { return 0; }
+size_t tc_workspace_size(const ChainDims &c, int compute) {
+    TcPlan pl;
+    if (!plan_tc(c, compute, &pl) || pl.p.ksplit <= 1) return 0;
+    // (ksplit - 1) fp32 partial copies of the output, row-major (rows, n_cols)
+    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(c.n_cols) * 4;
+}
 
 int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values,
-              const int32_t *adj_o, const int32_t *adj_i, const void *inp, void *out, void *,
-              size_t, cudaStream_t stream) {
+              const int32_t *adj_o, const int32_t *adj_i, const void *inp, void *out,
+              void *workspace, size_t workspace_bytes, cudaStream_t stream) {
     if (c.n_cols == 0) return RBGP4_OK;
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
@@ -470,25 +752,81 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
         return RBGP4_ECUDA;
     }
     CUtensorMap map;
-    cuuint64_t dims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.cols)};
-    cuuint64_t strides[1] = {cuuint64_t(c.ld_in) * elt};
-    cuuint32_t box[2] = {cuuint32_t(128 / elt), cuuint32_t(c.tk)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
-                     2, const_cast<void *>(inp), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     elt == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    cuuint32_t estr[3] = {1, 1, 1};
+    const int atom_cols = 128 / elt;
+    CUresult r;
+    pl.p.i3d = (c.n_cols % atom_cols == 0) ? 1 : 0;
+    if (getenv("RBGP4_TC_2D")) pl.p.i3d = 0;
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char *e = getenv("RBGP4_TC_PROMO"))
+        promo = atoi(e) == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+              : atoi(e) == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : atoi(e) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (pl.p.i3d) {
+        // (atom cols, K rows, N atoms) view: one box = one whole I slab, atom-major in smem
+        cuuint64_t dims[3] = {cuuint64_t(atom_cols), cuuint64_t(c.cols), cuuint64_t(c.n_cols / atom_cols)};
+        cuuint64_t strides[2] = {cuuint64_t(c.ld_in) * elt, 128};
+        cuuint32_t box[3] = {cuuint32_t(atom_cols), cuuint32_t(c.tk), cuuint32_t(pl.p.tn / atom_cols)};
+        r = enc(&map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                const_cast<void *>(inp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                elt == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        cuuint64_t dims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.cols)};
+        cuuint64_t strides[1] = {cuuint64_t(c.ld_in) * elt};
+        cuuint32_t box[2] = {cuuint32_t(atom_cols), cuuint32_t(c.tk)};
+        r = enc(&map, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                const_cast<void *>(inp), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                elt == 4 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) {
         set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
         return RBGP4_ECUDA;
     }
+    if (const char *dbg = getenv("RBGP4_TC_DEBUG")) {
+        pl.p.debug = atoi(dbg);
+        if (pl.p.debug & 16) { pl.p.w_tma = 0; pl.p.nw = 1; pl.p.ws = 1; pl.p.w_stage_bytes = 0; }
+    }
+    // compressed W tiles: 2-D (row_nnz, rows) view of the values, box (d_t, rows of a CTA)
+    CUtensorMap wmap;
+    memset(&wmap, 0, sizeof(wmap));
+    if (pl.p.w_tma) {
+        cuuint64_t wdims[2] = {cuuint64_t(c.row_nnz), cuuint64_t(c.rows)};
+        cuuint64_t wstrides[1] = {cuuint64_t(c.row_nnz) * elt};
+        cuuint32_t wbox[2] = {cuuint32_t(pl.p.ws * c.d_t), cuuint32_t(pl.p.rows_valid)};
+        if (reinterpret_cast<uintptr_t>(values) % 16 != 0) {
+            set_error("tensor-core path needs 16-byte aligned values");
+            return RBGP4_EUNSUPPORTED;
+        }
+        r = enc(&wmap, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                2, const_cast<void *>(values), wdims, wstrides, wbox, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    float *wsp = static_cast<float *>(workspace);
+    if (pl.p.ksplit > 1 && (wsp == nullptr || workspace_bytes < tc_workspace_size(c, compute))) {
+        set_error("split-K (%d slices) needs %zu workspace bytes", pl.p.ksplit,
+                  tc_workspace_size(c, compute));
+        return RBGP4_EWORKSPACE;
+    }
     const bool obf = out_dtype == RBGP4_BF16;
     if (compute == RBGP4_COMPUTE_TF32)
-        return obf ? launch_typed<float, true>(pl, map, values, adj_o, adj_i, out, stream)
-                   : launch_typed<float, false>(pl, map, values, adj_o, adj_i, out, stream);
-    return obf ? launch_typed<__nv_bfloat16, true>(pl, map, values, adj_o, adj_i, out, stream)
-               : launch_typed<__nv_bfloat16, false>(pl, map, values, adj_o, adj_i, out, stream);
+        return obf ? launch_typed<float, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
+                   : launch_typed<float, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
+    return obf ? launch_typed<__nv_bfloat16, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
+               : launch_typed<__nv_bfloat16, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
 }
 
 }  // namespace rbgp4
+
+// debug-only (not part of include/rbgp4.h): copy the CTA-0 trace to the host
+extern "C" int rbgp4_debug_trace(unsigned long long *host, int n) {
+    if (n > 10 * rbgp4::kTraceSteps) n = 10 * rbgp4::kTraceSteps;
+    return cudaMemcpyFromSymbol(host, rbgp4::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
+               ? 0 : -3;
+}

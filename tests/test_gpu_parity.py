@@ -137,7 +137,7 @@ def test_general_chain_reference_on_gpu():
 @pytest.mark.parametrize("compute,tol", [("tf32", 1e-2), ("bf16", 1e-2)])
 def test_tensor_core_modes(golden, compute, tol):
     lib = _native.lib()
-    for cid in ("c1b", "vgg-c10-875", "vgg-c10-tc", "t2-o50-i50"):
+    for cid in golden["cases"]:
         entry = golden["cases"][cid]
         chain, w, inp = wl.make_operands(case_config(entry, "f32", cid))
         p = ks.tiling_for_chain(chain, tn=entry["tn"], rn=entry["rn"], bn=entry["bn"])
