@@ -56,6 +56,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--factorisation", choices=["tc", "paper"], default="tc",
+                    help="base-graph factorisation of every layer (both are 87.5%% RBGP4)")
+    ap.add_argument("--no-alt", action="store_true", help="skip timing the other factorisation")
     return ap.parse_args()
 
 
@@ -67,12 +70,20 @@ def dist_env():
 
 
 # ----------------------------------------------------------------- workload
-def build_layers(sparsity: float, batch: int):
+FACTORISATIONS = {
+    "tc": ("G_o(4,K/128)@.5 G_r(1,1) G_i(16,16) G_b(8,8): tile 128x128, 8x8 dense element blocks "
+           "(tensor-core-friendly, SURVEY §7 hard part 1)"),
+    "paper": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1): tile 128x64 (paper family, G_b=(1,1))",
+}
+
+
+def build_layers(sparsity: float, batch: int, fact: str = "tc"):
     import paper_2006_13486_b200 as ks
     from paper_2006_13486_b200 import workloads as wl
 
+    maker = wl.vgg19_cifar_512_tc if fact == "tc" else wl.vgg19_cifar_512
     layers = []
-    for cfg in wl.vgg19_cifar_512(sparsity, batch=batch):
+    for cfg in maker(sparsity, batch=batch):
         chain = wl.build_chain(cfg)
         rng = ks.make_rng(np.random.SeedSequence([cfg.seed, 1]).generate_state(1)[0])
         w = ks.init_random(chain, rng, precision="f32")
@@ -207,7 +218,7 @@ def run_reference(args):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0))
-    layers = build_layers(args.sparsity, args.batch)
+    layers = build_layers(args.sparsity, args.batch, args.factorisation)
     import oracle
     oracle.build()
     cols = CPU_SAMPLE_COLS
@@ -244,7 +255,7 @@ def workload_config(args, world):
     return {"workload": f"vgg19-cifar-512ch-convs-im2col-sp{args.sparsity * 100:g}",
             "layers": "conv9-16 (M,K,N)=(512,2304|4608,256*HW)",
             "batch_per_gpu": args.batch, "global_batch": args.batch * world,
-            "sparsity": args.sparsity, "factorisation": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1)",
+            "sparsity": args.sparsity, "factorisation": FACTORISATIONS[args.factorisation],
             "compute": args.compute, "parallelism": f"batch-shard x{world}",
             "l2": "inputs (170 MB bf16) larger than L2 (126 MB); no explicit flush"}
 
@@ -273,84 +284,90 @@ def run_ours(args):
     s_in = 2 if compute == "bf16" else 4
     s_out = s_in
 
-    layers = build_layers(args.sparsity, args.batch)
-    # every rank gets its own batch shard: same W (replicated), distinct inputs
-    for lay in layers:
-        lay["rng"] = ks.make_rng(np.random.SeedSequence([lay["cfg"].seed, 1, rank]).generate_state(1)[0])
-    host_in, dev_in, dev_out, fmts = [], [], [], []
-    for lay in layers:
-        x32 = torch.from_numpy(make_input(lay))
-        xh = x32.to(op_dt).pin_memory()
-        host_in.append(xh)
-        dev_in.append(xh.to(dev))
-        dev_out.append(torch.empty((lay["m"], lay["n"]), dtype=out_dt, device=dev))
-        fmts.append(device_format(lay["w"], dev, op_dt))
-    torch.cuda.synchronize()
+    def setup(fact):
+        layers = build_layers(args.sparsity, args.batch, fact)
+        # every rank gets its own batch shard: same W (replicated), distinct inputs
+        for lay in layers:
+            lay["rng"] = ks.make_rng(
+                np.random.SeedSequence([lay["cfg"].seed, 1, rank]).generate_state(1)[0])
+        host_in, dev_in, dev_out, fmts = [], [], [], []
+        for lay in layers:
+            x32 = torch.from_numpy(make_input(lay))
+            xh = x32.to(op_dt).pin_memory()
+            host_in.append(xh)
+            dev_in.append(xh.to(dev))
+            dev_out.append(torch.empty((lay["m"], lay["n"]), dtype=out_dt, device=dev))
+            fmts.append(device_format(lay["w"], dev, op_dt))
+        torch.cuda.synchronize()
+        # one CUDA graph per layer: the launch is captured once, replays cost ~us
+        graphs = []
+        with torch.cuda.stream(stream):
+            for fmt, x, o in zip(fmts, dev_in, dev_out):
+                launch_sdmm(fmt, compute, x, o, dev)  # eager warm-up (attributes, prep)
+            stream.synchronize()
+            for fmt, x, o in zip(fmts, dev_in, dev_out):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    launch_sdmm(fmt, compute, x, o, dev)
+                graphs.append(g)
+        torch.cuda.synchronize()
+        return layers, host_in, dev_out, graphs
 
-    # one CUDA graph per layer: the launch is captured once, replays cost ~us
+    def timed(graphs, dom, steps, warmup, sampler=None):
+        ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
+        ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
+
+        def step(record=None):
+            for i, g in enumerate(graphs):
+                if record is not None and i in dom:
+                    ev_s[record[0]].record(stream)
+                    g.replay()
+                    ev_e[record[0]].record(stream)
+                    record[0] += 1
+                else:
+                    g.replay()
+
+        with torch.cuda.stream(stream):
+            for _ in range(warmup):
+                step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        if sampler is not None:
+            sampler.start()
+            time.sleep(0.3)  # sampler warm-up (first samples land before the timed region)
+        _native.reset_launch_count()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            t_start.record(stream)
+            cursor = [0]
+            for _ in range(steps):
+                step(cursor)
+            t_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = sampler.stop() if sampler is not None else None
+        elapsed_ms = t_start.elapsed_time(t_end)
+        if world > 1:
+            t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            elapsed_ms = float(t.item())
+        dom_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+        return elapsed_ms, (statistics.mean(dom_ms) if dom_ms else float("nan")), clocks
+
     stream = torch.cuda.Stream(device=dev)
-    graphs = []
-    with torch.cuda.stream(stream):
-        for fmt, x, o in zip(fmts, dev_in, dev_out):
-            launch_sdmm(fmt, compute, x, o, dev)  # eager warm-up (sets kernel attributes)
-        stream.synchronize()
-        for fmt, x, o in zip(fmts, dev_in, dev_out):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                launch_sdmm(fmt, compute, x, o, dev)
-            graphs.append(g)
-    torch.cuda.synchronize()
-
+    layers, host_in, dev_out, graphs = setup(args.factorisation)
     flops_step = sum(lay["flops"] for lay in layers)
     dom = [i for i, lay in enumerate(layers) if lay["k"] == 4608 and lay["n"] == 16 * args.batch]
-    n_ev = args.steps * len(dom)
-    ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-    ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
-
-    def step(record=None):
-        for i, g in enumerate(graphs):
-            if record is not None and i in dom:
-                ev_s[record[0]].record(stream)
-                g.replay()
-                ev_e[record[0]].record(stream)
-                record[0] += 1
-            else:
-                g.replay()
-
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    sampler = ClockSampler(dev.index)
-    sampler.start()
-    time.sleep(0.3)  # sampler warm-up (first samples land before the timed region)
-    _native.reset_launch_count()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
-        t_start.record(stream)
-        cursor = [0]
-        for _ in range(args.steps):
-            step(cursor)
-        t_end.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    elapsed_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms, dom_avg_ms, clocks = timed(graphs, dom, args.steps, args.warmup,
+                                           ClockSampler(dev.index))
     ms_per_step = elapsed_ms / args.steps
     value = flops_step * world / (ms_per_step * 1e-3) / 1e12
-    dom_ms = [s.elapsed_time(e) for s, e in zip(ev_s, ev_e)]
-    dom_avg_ms = statistics.mean(dom_ms) if dom_ms else float("nan")
     launches_in_region = len(graphs) * args.steps  # graph replays of our kernels
 
     # roofline of the dominant kernel (HBM-bound at this shape)
@@ -360,7 +377,8 @@ def run_ours(args):
     achieved = bytes_launch / (dom_avg_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": f"tc_kernel<bf16> conv10-12 (M,K,N)=({dom_layer['m']},{dom_layer['k']},"
+                "kernel": f"tc_kernel<bf16> conv10-12 ({args.factorisation} factorisation) "
+                          f"(M,K,N)=({dom_layer['m']},{dom_layer['k']},"
                           f"{dom_layer['n']})", "algorithmic_bytes_per_launch": bytes_launch,
                 "avg_launch_us": dom_avg_ms * 1e3, "peak_source": peak_src,
                 "tflops_eff": dom_layer["flops"] / (dom_avg_ms * 1e-3) / 1e12}
@@ -399,6 +417,19 @@ def run_ours(args):
         v, desc, _ = cpu_sample(layers, args.cpu_seconds, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
 
+    alt = None
+    if not args.no_alt:
+        other = "paper" if args.factorisation == "tc" else "tc"
+        a_layers, _, _, a_graphs = setup(other)
+        a_elapsed, a_dom, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
+        a_ms = a_elapsed / max(10, args.steps // 4)
+        a_flops = sum(lay["flops"] for lay in a_layers)
+        alt = {"factorisation": FACTORISATIONS[other],
+               "value": a_flops * world / (a_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": a_ms,
+               "dominant_kernel_us": a_dom * 1e3,
+               "dominant_frac_hbm": algorithmic_bytes(a_layers[dom[0]], s_in, s_out)
+               / (a_dom * 1e-3) / 1e9 / load_peak_hbm()[0]}
+
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -409,6 +440,7 @@ def run_ours(args):
             "config": workload_config(args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_in_region, "clocks": clocks,
+            "alt_factorisation": alt,
         }))
     if world > 1:
         dist.destroy_process_group()

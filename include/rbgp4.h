@@ -82,6 +82,23 @@ int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
                const void *inp, void *out, void *workspace, size_t workspace_bytes,
                void *stream);
 
+/*
+ * Per-matrix preparation for the tensor-core modes (optional, cacheable): the in-tile
+ * scatter map of the densified W tile depends only on the chain and the tiling, so it
+ * can be built once into a caller-owned device buffer of rbgp4_prepare_size() bytes and
+ * passed to rbgp4_sdmm_prepared(), which then skips rebuilding it in every CTA.
+ * Returns 0 size for the SIMT modes (nothing to prepare).
+ */
+size_t rbgp4_prepare_size(const rbgp4_desc *desc, int compute);
+int rbgp4_prepare(const rbgp4_desc *desc, int compute, const int32_t *adj_i, void *prep,
+                  size_t prep_bytes, void *stream);
+
+/* rbgp4_sdmm with the prepared buffer of rbgp4_prepare (prep may be NULL). */
+int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
+                        const void *values, const int32_t *adj_o, const int32_t *adj_i,
+                        const void *prep, const void *inp, void *out, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
 /* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
 

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b2
 F32, F64, BF16 = 0, 1, 2
 COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
 EXPORTED = (
-    "rbgp4_sdmm", "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
+    "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size",
+    "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count",
 )
@@ -56,6 +57,13 @@ def lib():
     vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
     h.rbgp4_sdmm.argtypes = [ctypes.POINTER(Desc), i32, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp]
     h.rbgp4_sdmm.restype = i32
+    h.rbgp4_sdmm_prepared.argtypes = [ctypes.POINTER(Desc), i32, i32, i32, vp, vp, vp, vp, vp, vp,
+                                      vp, sz, vp]
+    h.rbgp4_sdmm_prepared.restype = i32
+    h.rbgp4_prepare_size.argtypes = [ctypes.POINTER(Desc), i32]
+    h.rbgp4_prepare_size.restype = sz
+    h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, sz, vp]
+    h.rbgp4_prepare.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

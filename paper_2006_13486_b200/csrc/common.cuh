@@ -54,8 +54,11 @@ int simt_supported(const ChainDims &c, int dtype);
 
 // tcgen05 launchers (sdmm_tc.cu)
 int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values,
-              const int32_t *adj_o, const int32_t *adj_i, const void *inp, void *out,
-              void *workspace, size_t workspace_bytes, cudaStream_t stream);
+              const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *inp,
+              void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream);
+size_t tc_prep_size(const ChainDims &c, int compute);
+int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep, size_t bytes,
+               cudaStream_t stream);
 int tc_supported(const ChainDims &c, int compute, int out_dtype);
 size_t tc_workspace_size(const ChainDims &c, int compute);
 

@@ -128,9 +128,10 @@ int rbgp4_sdmm_supported(const rbgp4_desc *desc, int compute, int in_dtype, int 
     }
 }
 
-int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
-               const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *inp,
-               void *out, void *workspace, size_t workspace_bytes, void *stream) {
+int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
+                        const void *values, const int32_t *adj_o, const int32_t *adj_i,
+                        const void *prep, const void *inp, void *out, void *workspace,
+                        size_t workspace_bytes, void *stream) {
     ChainDims c;
     int rc = validate_desc(desc, &c);
     if (rc != RBGP4_OK) return rc;
@@ -145,8 +146,32 @@ int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
         set_error("tensor-core path needs %zu workspace bytes, got %zu", need, workspace_bytes);
         return RBGP4_EWORKSPACE;
     }
-    return launch_tc(c, compute, out_dtype, values, adj_o, adj_i, inp, out, workspace,
+    return launch_tc(c, compute, out_dtype, values, adj_o, adj_i, prep, inp, out, workspace,
                      workspace_bytes, s);
+}
+
+int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
+               const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *inp,
+               void *out, void *workspace, size_t workspace_bytes, void *stream) {
+    return rbgp4_sdmm_prepared(desc, compute, in_dtype, out_dtype, values, adj_o, adj_i, nullptr,
+                               inp, out, workspace, workspace_bytes, stream);
+}
+
+size_t rbgp4_prepare_size(const rbgp4_desc *desc, int compute) {
+    ChainDims c;
+    if (validate_desc(desc, &c) != RBGP4_OK) return 0;
+    if (compute == RBGP4_COMPUTE_TF32 || compute == RBGP4_COMPUTE_BF16) return tc_prep_size(c, compute);
+    return 0;
+}
+
+int rbgp4_prepare(const rbgp4_desc *desc, int compute, const int32_t *adj_i, void *prep,
+                  size_t prep_bytes, void *stream) {
+    ChainDims c;
+    int rc = validate_desc(desc, &c);
+    if (rc != RBGP4_OK) return rc;
+    if (compute != RBGP4_COMPUTE_TF32 && compute != RBGP4_COMPUTE_BF16) return RBGP4_OK;
+    RBGP4_REQUIRE(adj_i != nullptr, "null adj_i");
+    return tc_prepare(c, compute, adj_i, prep, prep_bytes, static_cast<cudaStream_t>(stream));
 }
 
 int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t n, void *stream) {

@@ -24,7 +24,7 @@
 // loads; warp 6 lane 0 the compressed-W TMA loads (separate rings so the I
 // stream never waits on densify progress); warp 5 allocates TMEM and lane 0
 // issues the MMAs.  An NS-stage mbarrier
-// ring links them:  full_b (TMA tx bytes), full_a (4 densify-warp arrivals),
+// ring links them:  full (TMA tx bytes + 4 densify-warp arrivals), empty (one commit),
 // empty (tcgen05.commit), tmem_full (last commit).
 //
 // Roofline: bound by HBM for the VGG/WRN layer shapes (compressed W + I +
@@ -70,6 +70,8 @@ struct TcParams {
     int32_t debug;           // ablation bits (RBGP4_TC_DEBUG): 1 no densify, 2 no MMA, 4 no epilogue
     int32_t ksplit, sps;     // split-K: CTAs per output tile (one cluster) and steps per slice
     int32_t adj_smem;        // g_i adjacency staged in shared memory for the table build
+    const uint16_t *prep;    // precomputed scatter table [phase][j][row] (rbgp4_prepare) or null
+    int32_t table_in_regs;   // densify keeps each row's offsets in registers (else smem table)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -143,6 +145,15 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred p;\n.reg .b32 r;\n"
+        "elect.sync r|p, 0xffffffff;\n"
+        "selp.b32 %0, 1, 0, p;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
 __device__ __forceinline__ void fence_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -204,6 +215,40 @@ __device__ __forceinline__ uint32_t swz(uint32_t off, int span) {
           "=r"(r[30]), "=r"(r[31])                                                         \
         : "r"(taddr))
 
+// Byte offset, inside one densified A stage, of nonzero j of CTA row r (the scatter map).
+// Row r walks j = ((rk*d_i + ink)*bk + k) with counters (reference sdmm.py:183-186).
+template <int kElt>
+__device__ __forceinline__ void row_offsets(const TcParams &p, const int32_t *adj, int row_in_tile0,
+                                            int r, uint16_t *dst, int dst_stride) {
+    const int ui = ((row_in_tile0 + r) / p.bm) % p.u_i;
+    const int32_t *arow = adj + ui * p.d_i;
+    const int sh = p.a_swz == 128 ? 7 : p.a_swz == 64 ? 6 : 5;  // log2(swizzle span)
+    const uint32_t rbase = uint32_t(r) << sh;
+    int k = 0, ink = 0, rk = 0;
+    int kbase = arow[0] * p.bk;  // (rk*v_i + adj_i[ui][ink])*bk
+    for (int j = 0; j < p.d_t; ++j) {
+        const uint32_t kb = uint32_t(kbase + k) * kElt;  // byte offset along K
+        dst[j * dst_stride] =
+            uint16_t(((kb >> sh) << (sh + 7)) + swz(rbase + (kb & (p.a_swz - 1)), p.a_swz));
+        if (++k == p.bk) {
+            k = 0;
+            if (++ink == p.d_i) { ink = 0; ++rk; }
+            if (rk < p.rk) kbase = (rk * p.v_i + arow[ink]) * p.bk;
+        }
+    }
+}
+
+// rbgp4_prepare: the scatter map depends only on the chain and the tiling, so it is built
+// once per matrix into [phase][j][row] (phase = which 128-row block of a tile-row).
+template <int kElt>
+__global__ void prep_kernel(const TcParams p, const int32_t *__restrict__ adj_i, uint16_t *out) {
+    const int phase = blockIdx.x;
+    const int r = threadIdx.x;
+    if (r < kBlockM)
+        row_offsets<kElt>(p, adj_i, phase * p.rows_valid, r,
+                          out + size_t(phase) * p.d_t * kBlockM + r, kBlockM);
+}
+
 // ---------------------------------------------------------------- the kernel
 template <typename E, bool OUT_BF16>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -227,9 +272,12 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         (reinterpret_cast<uintptr_t>(aoff + kBlockM * p.d_t) + 15) & ~uintptr_t(15));
     uint64_t *bars = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(adj_s + (p.adj_smem ? p.u_i * p.d_i : 0)) + 7) & ~uintptr_t(7));
+    // one ring of ns = na = nb stages, each holding an A tile and an I slab:
+    // full[st] completes on the TMA transaction bytes + 4 densify-warp arrivals,
+    // empty[st] on the MMA commit (one wait and one commit per step for the MMA warp)
     uint64_t *full_b = bars, *empty_b = full_b + p.nb;
-    uint64_t *full_a = empty_b + p.nb, *empty_a = full_a + p.na;
-    uint64_t *full_w = empty_a + p.na, *empty_w = full_w + p.nw;
+    uint64_t *full_a = full_b, *empty_a = empty_b;
+    uint64_t *full_w = empty_b + p.nb, *empty_w = full_w + p.nw;
     uint64_t *tmem_full = empty_w + p.nw;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
@@ -262,38 +310,26 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         uint4 *a4 = reinterpret_cast<uint4 *>(a_buf);
         for (int i = threadIdx.x; i < p.na * p.a_stage_bytes / 16; i += kThreads) a4[i] = z;
         const int32_t *adj = adj_i;
-        if (p.adj_smem && threadIdx.x < kBlockM) {
+        if (p.adj_smem && threadIdx.x < kBlockM && p.prep == nullptr) {
             // one coalesced copy instead of d_t dependent global loads per row; only the
             // four table-building warps synchronise on it (named barrier 1)
             for (int i = threadIdx.x; i < p.u_i * p.d_i; i += kBlockM) adj_s[i] = adj_i[i];
             asm volatile("bar.sync 1, 128;" ::: "memory");
             adj = adj_s;
         }
-        if (threadIdx.x < kBlockM) {
-            // thread r owns CTA row r: walk j = ((rk*d_i + ink)*bk + k) with counters
-            const int r = threadIdx.x;
-            const int ui = ((row_in_tile0 + r) / p.bm) % p.u_i;
-            const int32_t *arow = adj + ui * p.d_i;
-            const int sh = p.a_swz == 128 ? 7 : p.a_swz == 64 ? 6 : 5;  // log2(swizzle span)
-            const uint32_t rbase = uint32_t(r) << sh;
-            int k = 0, ink = 0, rk = 0;
-            int kbase = arow[0] * p.bk;  // (rk*v_i + adj_i[ui][ink])*bk
-            for (int j = 0; j < p.d_t; ++j) {
-                const uint32_t kb = uint32_t(kbase + k) * kElt;  // byte offset along K
-                aoff[j * kBlockM + r] =
-                    uint16_t(((kb >> sh) << (sh + 7)) + swz(rbase + (kb & (p.a_swz - 1)), p.a_swz));
-                if (++k == p.bk) {
-                    k = 0;
-                    if (++ink == p.d_i) { ink = 0; ++rk; }
-                    if (rk < p.rk) kbase = (rk * p.v_i + arow[ink]) * p.bk;
-                }
-            }
+        if (threadIdx.x < kBlockM && p.prep == nullptr)
+            row_offsets<kElt>(p, adj, row_in_tile0, threadIdx.x, aoff + threadIdx.x, kBlockM);
+        else if (p.prep != nullptr) {
+            // prepared map: one coalesced 16-byte copy into the shared table
+            const uint4 *src = reinterpret_cast<const uint4 *>(
+                p.prep + size_t(row_in_tile0 / p.rows_valid) * p.d_t * kBlockM);
+            uint4 *dst = reinterpret_cast<uint4 *>(aoff);
+            for (int i = threadIdx.x; i < p.d_t * kBlockM / 8; i += kThreads) dst[i] = __ldg(src + i);
         }
     }
     if (threadIdx.x == 0) trace(p.debug, 6, 4);
     if (warp == 4 && lane == 0) {
-        for (int i = 0; i < p.nb; ++i) { mbar_init(&full_b[i], 1); mbar_init(&empty_b[i], 1); }
-        for (int i = 0; i < p.na; ++i) { mbar_init(&full_a[i], 4); mbar_init(&empty_a[i], 1); }
+        for (int i = 0; i < p.nb; ++i) { mbar_init(&full_b[i], 1 + 4); mbar_init(&empty_b[i], 1); }
         for (int i = 0; i < p.nw; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
         mbar_init(tmem_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -309,18 +345,22 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     const int32_t *orow = adj_o + tbm * p.d_o + s_begin;
     if (threadIdx.x == 0) trace(p.debug, 6, 0);
 
+    // Role loops run warp-uniformly (all 32 lanes wait on the barriers); one lane,
+    // picked by elect.sync, issues the TMA / tcgen05 instructions.  Issuing from
+    // lane-0-only divergent code made the compiler wrap every UTCHMMA/UTMALDG in an
+    // elect loop with R2UR conversions (~500 cycles per step, tools/tc_trace.py).
     if (warp == 4) {
         // ================= TMA producer: I slabs (runs ahead by the B ring depth) ==========
-        if (lane == 0) {
-            const int atoms = p.tn * kElt / 128;           // 128-byte MN atoms per slab
-            const int atom_cols = 128 / kElt;
-            const uint32_t atom_bytes = uint32_t(p.tk) * 128;
-            for (int s = 0; s < nsteps; ++s) {
-                const int st = s % p.nb;
-                const uint32_t ph = (s / p.nb) & 1;
-                mbar_wait(&empty_b[st], ph ^ 1);
+        const int atoms = p.tn * kElt / 128;           // 128-byte MN atoms per slab
+        const int atom_cols = 128 / kElt;
+        const uint32_t atom_bytes = uint32_t(p.tk) * 128;
+        for (int s = 0; s < nsteps; ++s) {
+            const int st = s % p.nb;
+            const uint32_t ph = (s / p.nb) & 1;
+            mbar_wait(&empty_b[st], ph ^ 1);
+            const int32_t krow = orow[s] * p.tk;
+            if (elect_one()) {
                 mbar_expect_tx(&full_b[st], uint32_t(p.b_stage_bytes));
-                const int32_t krow = orow[s] * p.tk;
                 unsigned char *dst = b_buf + st * p.b_stage_bytes;
                 if (p.i3d) {
                     // one instruction for the whole slab: (atom cols, K rows, atoms) box
@@ -332,48 +372,54 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 }
                 trace(p.debug, 0, s);
             }
+            __syncwarp();
         }
     } else if (warp == 6) {
         // ================= TMA producer: compressed W tiles (own ring, own pace) ============
-        if (lane == 0 && p.w_tma) {
+        if (p.w_tma) {
             const int wstages = (nsteps + p.ws - 1) / p.ws;
             for (int g = 0; g < wstages; ++g) {
                 const int st = g % p.nw;
                 const uint32_t ph = (g / p.nw) & 1;
                 mbar_wait(&empty_w[st], ph ^ 1);
-                mbar_expect_tx(&full_w[st], uint32_t(p.w_stage_bytes));
-                tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st],
-                            (s_begin + g * p.ws) * p.d_t, int32_t(m0));
-                trace(p.debug, 1, g);
+                if (elect_one()) {
+                    mbar_expect_tx(&full_w[st], uint32_t(p.w_stage_bytes));
+                    tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st],
+                                (s_begin + g * p.ws) * p.d_t, int32_t(m0));
+                    trace(p.debug, 1, g);
+                }
+                __syncwarp();
             }
         }
     } else if (warp == 5) {
         // ================= MMA issuer =================
-        if (lane == 0) {
-            // instruction descriptor: D f32, A/B bf16|tf32, A K-major, B MN-major, N, M=128
-            const uint32_t fmt = kTF32 ? 2u : 1u;
-            const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
-                                   (uint32_t(p.tn >> 3) << 17) | (uint32_t(kBlockM >> 4) << 24);
-            const int ksteps = p.tk * kElt / 32;
-            // Descriptors are built once; per stage / K-step only the 14-bit start-address
-            // field (16-byte units, low word) moves, so the issue loop is pure adds.
-            const uint64_t a_desc0 =
-                smem_desc(smem_u32(a_buf), 0, 8 * p.a_swz, swizzle_layout_code(p.a_swz));
-            // MN-major B: bf16 -> SWIZZLE_128B (8-row K groups, SBO 1024);
-            // tf32 -> SWIZZLE_128B_BASE32B (32 B chunks, 4-row K groups, SBO 512)
-            const uint64_t b_desc0 = kTF32 ? smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 512, 1u)
-                                           : smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 1024, 2u);
-            const uint32_t a_stage16 = uint32_t(p.a_stage_bytes) >> 4;
-            const uint32_t b_stage16 = uint32_t(p.b_stage_bytes) >> 4;
-            const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
-            const uint32_t a_jump16 = uint32_t(kBlockM - 1) * a_span16;        // next K atom
-            const uint32_t b_step16 = uint32_t(32 / kElt) * 128 / 16;           // 32/E K-rows
-            for (int s = 0; s < nsteps; ++s) {
-                const int sb = s % p.nb, sa = s % p.na;
-                mbar_wait(&full_b[sb], (s / p.nb) & 1);
-                trace(p.debug, 7, s);
-                mbar_wait(&full_a[sa], (s / p.na) & 1);
-                tc_fence_after();
+        // instruction descriptor: D f32, A/B bf16|tf32, A K-major, B MN-major, N, M=128
+        const uint32_t fmt = kTF32 ? 2u : 1u;
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+                               (uint32_t(p.tn >> 3) << 17) | (uint32_t(kBlockM >> 4) << 24);
+        const int ksteps = p.tk * kElt / 32;
+        // Descriptors are built once; per stage / K-step only the 14-bit start-address
+        // field (16-byte units, low word) moves, so the issue loop is pure adds.
+        const uint64_t a_desc0 =
+            smem_desc(smem_u32(a_buf), 0, 8 * p.a_swz, swizzle_layout_code(p.a_swz));
+        // MN-major B: bf16 -> SWIZZLE_128B (8-row K groups, SBO 1024);
+        // tf32 -> SWIZZLE_128B_BASE32B (32 B chunks, 4-row K groups, SBO 512)
+        const uint64_t b_desc0 = kTF32 ? smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 512, 1u)
+                                       : smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 1024, 2u);
+        const uint32_t a_stage16 = uint32_t(p.a_stage_bytes) >> 4;
+        const uint32_t b_stage16 = uint32_t(p.b_stage_bytes) >> 4;
+        const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
+        const uint32_t a_jump16 = uint32_t(kBlockM - 1) * a_span16;        // next K atom
+        const uint32_t b_step16 = uint32_t(32 / kElt) * 128 / 16;           // 32/E K-rows
+        unsigned long long seg[3] = {0, 0, 0};
+        for (int s = 0; s < nsteps; ++s) {
+            const int sb = s % p.nb, sa = s % p.na;
+            const unsigned long long c0 = clock64();
+            mbar_wait(&full_b[sb], (s / p.nb) & 1);  // I slab landed and A tile densified
+            if (lane == 0) trace(p.debug, 7, s);
+            tc_fence_after();
+            const unsigned long long c1 = clock64();
+            if (elect_one()) {
                 trace(p.debug, 4, s);
                 uint64_t ad = a_desc0 + uint64_t(sa) * a_stage16;
                 uint64_t bd = b_desc0 + uint64_t(sb) * b_stage16;
@@ -385,16 +431,19 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                     if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
                     bd += b_step16;
                 }
-                if ((p.debug & 34) == 34) {  // ablation: no MMAs issued, release slots directly
-                    mbar_arrive(&empty_b[sb]);
-                    mbar_arrive(&empty_a[sa]);
-                } else {
-                    tc_commit(&empty_b[sb]);
-                    tc_commit(&empty_a[sa]);
-                }
+                tc_commit(&empty_b[sb]);  // frees both the I slab and the A tile of the stage
                 trace(p.debug, 5, s);
             }
-            tc_commit(tmem_full);
+            __syncwarp();
+            const unsigned long long c2 = clock64();
+            seg[0] += c1 - c0;
+            seg[1] += c2 - c1;
+        }
+        if (elect_one()) tc_commit(tmem_full);
+        __syncwarp();
+        if ((p.debug & (8 | 4096)) && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
+            g_trace[9][0] = seg[0];
+            g_trace[9][1] = seg[1];
         }
     } else {
         // ================= densify (warps 0-3), then epilogue =================
@@ -405,12 +454,18 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const E *vrow = values + (m0 + t) * p.row_nnz;
         // this row's scatter offsets never change: keep them in registers (2 per reg)
         uint32_t offp[kRegNnz / 2];
+        // G_b blocks of >= 16 bytes along K (bk % V == 0): each 16-byte chunk of a compressed
+        // row lands on one 16-byte unit of the swizzled A tile -> 16-byte stores
+        constexpr int kMaxChunks = 16;      // 16-byte chunks per row held in registers
+        const bool chunked = p.w_tma && (p.bk % V == 0) && p.d_t <= kMaxChunks * V;
         const bool reg_path = p.w_tma && p.d_t <= kRegNnz;
 #pragma unroll
         for (int i = 0; i < kRegNnz / 2; ++i) {
-            const int j = 2 * i;
+            // element offsets (reg_path) or, when chunked, the offsets of chunk starts
+            const int j = chunked ? 2 * i * V : 2 * i;
+            const int j2 = chunked ? j + V : j + 1;
             uint32_t lo = j < p.d_t ? aoff[j * kBlockM + t] : 0u;
-            uint32_t hi = j + 1 < p.d_t ? aoff[(j + 1) * kBlockM + t] : 0u;
+            uint32_t hi = j2 < p.d_t ? aoff[j2 * kBlockM + t] : 0u;
             offp[i] = lo | (hi << 16);
         }
         const uint32_t wrow = smem_u32(w_buf) + uint32_t(t * p.ws * p.d_t * kElt);
@@ -425,7 +480,24 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             if (t == 0) trace(p.debug, 2, s);
             const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
             if (active && !(p.debug & 1)) {
-                if (reg_path) {
+                if (chunked) {
+                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
+                                         uint32_t(wsub * p.d_t * kElt);
+                    const int nchunks = p.d_t / V;
+                    uint4 q[kMaxChunks];
+#pragma unroll
+                    for (int c = 0; c < kMaxChunks; ++c)
+                        if (c < nchunks) q[c] = lds128(src + 16 * c);
+#pragma unroll
+                    for (int c = 0; c < kMaxChunks; ++c) {
+                        if (c < nchunks) {
+                            const uint32_t o = (offp[c / 2] >> (16 * (c & 1))) & 0xFFFFu;
+                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a + o),
+                                         "r"(q[c].x), "r"(q[c].y), "r"(q[c].z), "r"(q[c].w)
+                                         : "memory");
+                        }
+                    }
+                } else if (reg_path) {
                     // compressed row t of this step (TMA-staged): 16-byte shared loads,
                     // all issued before the scatter so their latency overlaps
                     const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
@@ -462,7 +534,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             }
             // make the generic-proxy stores visible to the tensor core, then one
             // release-arrive per warp (full_a counts 4 warps)
-            fence_async_smem();
+            if (!(p.debug & 256)) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&full_a[sa]);
@@ -623,57 +695,61 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
     p.a_stage_bytes = kBlockM * kbytes;
     // compressed W tiles come in by TMA when a row of one step is whole 16-byte chunks
     p.w_tma = (c.d_t * elt) % 16 == 0 && c.d_t <= 256 ? 1 : 0;
-    // W stage: as many consecutive steps as fit one box (<= 256 elements, <= 32 KB)
+    // W stage: as many consecutive steps as fit one box (<= 256 elements, <= 8 KB)
     p.ws = 1;
     while (p.w_tma && p.ws * 2 <= c.d_o && p.ws * 2 * c.d_t <= 256 &&
-           size_t(p.rows_valid) * p.ws * 2 * c.d_t * elt <= 16384)
+           size_t(p.rows_valid) * p.ws * 2 * c.d_t * elt <= 8192)
         p.ws *= 2;
     p.w_stage_bytes = p.w_tma ? p.rows_valid * p.ws * c.d_t * elt : 0;
-    // Wide N tiles give fat TMA boxes (the I stream is bound by per-instruction TMA cost);
-    // split-K over a cluster then restores the SM count: ~one CTA per SM in total.
+    {
+        const int V = 16 / elt;
+        p.table_in_regs = p.w_tma && ((c.bk % V == 0 && c.d_t <= 16 * V) || c.d_t <= 64);
+    }
     const int64_t blocks_m = c.rows / p.rows_valid;
     const int tn_min = 128 / elt;  // one 128-byte swizzle atom of B along N
-    int tn = 128;  // measured best on the VGG shapes (tools/tc_time.py); 256 only pays at large N
+    // tn = 128, or 64 when 128-wide tiles leave more than half the SMs idle
+    // (measured on the VGG shapes with tools/tc_time.py)
+    int tn = 128;
     while (tn > tn_min && tn / 2 >= c.n_cols) tn /= 2;
+    if (tn > tn_min && ((c.n_cols + tn - 1) / tn) * blocks_m * 2 < kNumSMs) tn /= 2;
     if (const char *env = getenv("RBGP4_TC_TN")) tn = std::max(tn_min, std::min(256, atoi(env)));
     p.adj_smem = size_t(c.u_i) * c.d_i * 4 <= 16384 ? 1 : 0;
+    // Shared-memory budget, in priority order (one CTA per SM):
+    //   1. >= 96 KB of I slabs in flight (TMA latency under load is ~2 us: Little's law),
+    //   2. A ring 2..4 deep (densify runs ahead of the MMA),
+    //   3. W ring 2 x <= 8 KB,
+    //   4. everything left -> more I stages (<= 16).
     for (; tn >= tn_min; tn /= 2) {
         p.tn = tn;
         p.b_stage_bytes = c.tk * tn * elt;
-        // one CTA per SM: A ring 3 deep, W ring 2 x <=16 KB, the rest of smem to the I ring
-        // (the I stream is latency x depth bound: TMA latency under load is ~2-3 us)
-        p.na = 3;
         p.nw = p.w_tma ? 2 : 1;
-        size_t fixed = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 + size_t(p.na) * p.a_stage_bytes +
-                       size_t(p.nw) * p.w_stage_bytes + (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0);
-        fixed += 8 * (2 * 16 + 2 * p.na + 2 * p.nw + 1);
-        while (fixed + 3 * size_t(p.b_stage_bytes) > kSmemCap && p.nw > 2 && p.w_tma) {
-            fixed -= p.w_stage_bytes;  // trade W depth first
-            --p.nw;
-        }
-        while (fixed + 3 * size_t(p.b_stage_bytes) > kSmemCap && p.na > 2) {
-            fixed -= p.a_stage_bytes;
-            --p.na;
-        }
-        if (fixed + 2 * size_t(p.b_stage_bytes) > kSmemCap && p.w_tma) {
+        const size_t base = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 +
+                            (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 2 + 1);
+        size_t w_bytes = size_t(p.nw) * p.w_stage_bytes;
+        const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;  // A tile + I slab
+        if (base + w_bytes + 2 * stage > kSmemCap && p.w_tma) {
             // large compressed tiles: read W straight from global in the densify warps
-            fixed -= size_t(p.nw) * p.w_stage_bytes;
             p.w_tma = 0;
             p.ws = 1;
             p.nw = 1;
             p.w_stage_bytes = 0;
+            p.table_in_regs = 0;
+            w_bytes = 0;
         }
-        if (fixed + 2 * size_t(p.b_stage_bytes) > kSmemCap) continue;
-        p.nb = int(std::min<size_t>(16, (kSmemCap - fixed) / p.b_stage_bytes));
+        if (base + w_bytes + 2 * stage > kSmemCap) continue;
+        const size_t fixed = base + w_bytes;
+        const int ns = int(std::min<size_t>(16, (kSmemCap - fixed) / stage));
+        p.na = ns;
+        p.nb = ns;
         const int64_t tiles = ((c.n_cols + tn - 1) / tn) * blocks_m;
-        // split-K only when the tiles leave most SMs idle (cluster of ks CTAs per tile)
-        int ks = 1;
-        while (ks < 4 && tiles * ks * 2 <= kNumSMs && (ks * 2) <= c.d_o) ks *= 2;
+        // split-K in two (a 2-CTA cluster per tile) only when that still fits one wave;
+        // deeper splits measured slower (tools/tc_time.py)
+        int ks = (tiles * 2 <= kNumSMs && c.d_o >= 2) ? 2 : 1;
         if (const char *env = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(env)));
         p.sps = (c.d_o + ks - 1) / ks;
         p.ksplit = (c.d_o + p.sps - 1) / p.sps;  // no empty slices
         out->p = p;
-        out->smem = fixed + size_t(p.nb) * p.b_stage_bytes;
+        out->smem = fixed + size_t(ns) * stage;
         out->blocks_m = int(blocks_m);
         return 1;
     }
@@ -719,6 +795,31 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
 
 }  // namespace
 
+size_t tc_prep_size(const ChainDims &c, int compute) {
+    TcPlan pl;
+    if (!plan_tc(c, compute, &pl)) return 0;
+    const int phases = c.tm / pl.p.rows_valid;
+    return size_t(phases) * c.d_t * kBlockM * sizeof(uint16_t);
+}
+
+int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep, size_t bytes,
+               cudaStream_t stream) {
+    TcPlan pl;
+    if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
+    const size_t need = tc_prep_size(c, compute);
+    if (prep == nullptr || bytes < need) {
+        set_error("rbgp4_prepare needs %zu bytes", need);
+        return RBGP4_EWORKSPACE;
+    }
+    const int phases = c.tm / pl.p.rows_valid;
+    if (compute == RBGP4_COMPUTE_TF32)
+        prep_kernel<4><<<phases, kBlockM, 0, stream>>>(pl.p, adj_i, static_cast<uint16_t *>(prep));
+    else
+        prep_kernel<2><<<phases, kBlockM, 0, stream>>>(pl.p, adj_i, static_cast<uint16_t *>(prep));
+    RBGP4_CHECK_LAUNCH("prep_kernel launch");
+    return RBGP4_OK;
+}
+
 int tc_supported(const ChainDims &c, int compute, int out_dtype) {
     if (out_dtype != RBGP4_F32 && out_dtype != RBGP4_BF16) {
         set_error("tensor-core modes write f32 or bf16 outputs");
@@ -736,11 +837,12 @@ size_t tc_workspace_size(const ChainDims &c, int compute) {
 }
 
 int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values,
-              const int32_t *adj_o, const int32_t *adj_i, const void *inp, void *out,
-              void *workspace, size_t workspace_bytes, cudaStream_t stream) {
+              const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *inp,
+              void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream) {
     if (c.n_cols == 0) return RBGP4_OK;
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
+    pl.p.prep = static_cast<const uint16_t *>(prep);
     const int elt = compute == RBGP4_COMPUTE_TF32 ? 4 : 2;
     if (reinterpret_cast<uintptr_t>(inp) % 16 != 0 || (c.ld_in * elt) % 16 != 0) {
         set_error("tensor-core path needs a 16-byte aligned I with ld_in*%d %% 16 == 0", elt);
@@ -786,6 +888,9 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     }
     if (const char *dbg = getenv("RBGP4_TC_DEBUG")) {
         pl.p.debug = atoi(dbg);
+        if (pl.p.debug & 8192)
+            fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d ks=%d smem=%zu\n",
+                    pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.ksplit, pl.smem);
         if (pl.p.debug & 16) { pl.p.w_tma = 0; pl.p.nw = 1; pl.p.ws = 1; pl.p.w_stage_bytes = 0; }
     }
     // compressed W tiles: 2-D (row_nnz, rows) view of the values, box (d_t, rows of a CTA)

@@ -64,6 +64,7 @@ class DeviceFormat:
     adj_o: object           # (u_o, d_o) int32
     adj_i: object           # (u_i, d_i) int32
     desc_fields: dict       # chain sizes for rbgp4_desc
+    prep: dict = None       # compute mode -> prepared scatter map (tensor-core modes)
 
 
 def chain_fields(chain) -> dict:

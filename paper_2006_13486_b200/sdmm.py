@@ -252,6 +252,27 @@ def workspace(dev, nbytes: int):
     return buf
 
 
+def prepared(fmt, compute: str, dev, desc):
+    """Per-matrix scatter map for the tensor-core modes (built once, cached on `fmt`)."""
+    if compute not in ("tf32", "bf16"):
+        return None
+    if fmt.prep is None:
+        fmt.prep = {}
+    buf = fmt.prep.get(compute)
+    if buf is None:
+        lib = _native.lib()
+        code = _native.COMPUTE[compute]
+        nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
+        if nbytes == 0:
+            return None
+        buf = torch().empty(nbytes, dtype=torch().uint8, device=dev)
+        _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, fmt.adj_i.data_ptr(),
+                                        buf.data_ptr(), nbytes, stream_handle(dev)),
+                      "rbgp4_prepare")
+        fmt.prep[compute] = buf
+    return buf
+
+
 def launch_sdmm(fmt, compute: str, x, res, dev) -> None:
     """Queue one rbgp4_sdmm on the current stream of `dev` (no sync)."""
     lib = _native.lib()
@@ -260,10 +281,12 @@ def launch_sdmm(fmt, compute: str, x, res, dev) -> None:
     in_code, out_code = dtype_code(x.dtype), dtype_code(res.dtype)
     need = lib.rbgp4_workspace_size(ctypes.byref(desc), code, in_code)
     ws_ptr, ws_len = (workspace(dev, need).data_ptr(), need) if need else (None, 0)
+    prep = prepared(fmt, compute, dev, desc) if x.shape[1] else None
     _native.check(
-        lib.rbgp4_sdmm(ctypes.byref(desc), code, in_code, out_code, fmt.values.data_ptr(),
-                       fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(), x.data_ptr(), res.data_ptr(),
-                       ws_ptr, ws_len, stream_handle(dev)),
+        lib.rbgp4_sdmm_prepared(ctypes.byref(desc), code, in_code, out_code, fmt.values.data_ptr(),
+                                fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(),
+                                prep.data_ptr() if prep is not None else None, x.data_ptr(),
+                                res.data_ptr(), ws_ptr, ws_len, stream_handle(dev)),
         f"rbgp4_sdmm(compute={compute})",
     )
 

@@ -99,3 +99,24 @@ def vgg19_cifar_512(sparsity: float = 0.875, batch: int = 256, seed: int = 0):
             sp_i, (1, 1), n_cols=n, precision="f32", seed=seed + idx,
         ))
     return out
+
+
+def vgg19_cifar_512_tc(sparsity: float = 0.875, batch: int = 256, seed: int = 0):
+    """Same VGG19-CIFAR layers, tensor-core-friendly factorisation (SURVEY §7 hard part 1).
+
+    Tile 128 x 128 with G_r = (1,1), G_b = (8,8) dense 8x8 element blocks, G_o = (4, K/128)
+    at 50 % and G_i = (16,16) carrying the rest: 75 / 87.5 / 93.75 % are G_i at
+    50 / 75 / 87.5 %.  Every nonzero run along K is 8 elements (16 bytes of bf16), which
+    the tensor-core kernel scatters with 16-byte stores.
+    """
+    sp_i = {0.75: 0.5, 0.875: 0.75, 0.9375: 0.875}[sparsity]
+    layers = [("conv9", 512, 2304, batch * 16)]
+    layers += [(f"conv{i}", 512, 4608, batch * 16) for i in (10, 11, 12)]
+    layers += [(f"conv{i}", 512, 4608, batch * 4) for i in (13, 14, 15, 16)]
+    out = []
+    for idx, (name, m, k, n) in enumerate(layers):
+        out.append(SweepConfig(
+            f"vgg19tc-{name}-sp{sparsity * 100:g}", (m // 128, k // 128), 0.5, (1, 1), (16, 16),
+            sp_i, (8, 8), n_cols=n, precision="f32", seed=seed + idx,
+        ))
+    return out

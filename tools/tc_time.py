@@ -23,7 +23,8 @@ flush = torch.ones(128 << 20, dtype=torch.float32, device=dev)  # 512 MB
 layers = {"conv9": 0, "conv10": 1, "conv13": 4}
 which = sys.argv[1:] or list(layers)
 for name in which:
-    cfg = wl.vgg19_cifar_512(0.875)[layers[name]]
+    maker = wl.vgg19_cifar_512_tc if os.environ.get("FACT") == "tc" else wl.vgg19_cifar_512
+    cfg = maker(0.875)[layers[name]]
     w = ks.init_random(wl.build_chain(cfg), 1, precision="f32")
     x = (torch.rand((w.cols, cfg.n_cols), device=dev) * 2 - 1).to(torch.bfloat16)
     o = torch.empty((w.rows, cfg.n_cols), device=dev, dtype=torch.bfloat16)

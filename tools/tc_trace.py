@@ -11,7 +11,7 @@ import torch
 
 extra = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 li = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-os.environ["RBGP4_TC_DEBUG"] = str(8 | extra)
+os.environ["RBGP4_TC_DEBUG"] = str(extra if extra & 4096 else 8 | extra)
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2006_13486_b200 as ks  # noqa: E402
@@ -19,7 +19,7 @@ from paper_2006_13486_b200 import _native, workloads as wl  # noqa: E402
 from paper_2006_13486_b200.device import device_format  # noqa: E402
 from paper_2006_13486_b200.sdmm import launch_sdmm  # noqa: E402
 
-cfg = wl.vgg19_cifar_512(0.875)[li]
+cfg = (wl.vgg19_cifar_512_tc if os.environ.get("FACT") == "tc" else wl.vgg19_cifar_512)(0.875)[li]
 w = ks.init_random(wl.build_chain(cfg), 1, precision="f32")
 dev = torch.device("cuda", 0)
 x = torch.rand((w.cols, cfg.n_cols), device=dev).to(torch.bfloat16)
@@ -37,7 +37,8 @@ t = np.frombuffer(buf, dtype=np.uint64).reshape(10, 512).astype(np.int64)
 e0 = t[6, 3]
 print("entry->table", t[6, 4] - e0, "entry->tmem", t[6, 5] - e0, "entry->setup", t[6, 0] - e0,
       "setup->epi", t[6, 1] - t[6, 0], "epi", t[6, 2] - t[6, 1])
-d = int(os.environ.get("STEPS", "36"))
+print("MMA-warp totals over all steps: waits %d issue %d" % tuple(t[9, :2]))
+d = int(os.environ.get("STEPS", str(min(36, cfg.g_o[1] // 2))))
 print("step  B_iss  B_full(mma)  B_lat   A_ready(mma)  dens_s  dens_e  mma_e   W_iss(g) W_full(g)")
 for s in range(d):
     print(f"{s:4d} {t[0, s]-e0:7d} {t[7, s]-e0:9d} {t[7, s]-t[0, s]:7d} {t[4, s]-e0:11d} "

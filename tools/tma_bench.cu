@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -111,6 +112,30 @@ int main(int argc, char **argv) {
             for (int i = 0; i < 72; ++i) if ((i / 2 + tr) % 2 == 0) slab_list.push_back(i);
         }
     }
+    // random variant: a random biregular (4 x 72, d=36) pattern, each slab used by 2 tile-rows
+    std::vector<int> rnd_list;
+    {
+        srand(11);
+        std::vector<int> owners;  // 72 slabs x 2 owners
+        for (int attempt = 0; attempt < 1000; ++attempt) {
+            std::vector<std::vector<int>> rows(4);
+            std::vector<int> stubs;
+            for (int sl = 0; sl < 72; ++sl) { stubs.push_back(sl); stubs.push_back(sl); }
+            for (int i = int(stubs.size()) - 1; i > 0; --i) std::swap(stubs[i], stubs[rand() % (i + 1)]);
+            bool ok = true;
+            for (int tr = 0; tr < 4 && ok; ++tr) {
+                for (int j = 0; j < 36; ++j) rows[tr].push_back(stubs[tr * 36 + j]);
+                std::sort(rows[tr].begin(), rows[tr].end());
+                for (int j = 1; j < 36; ++j) if (rows[tr][j] == rows[tr][j - 1]) ok = false;
+            }
+            if (!ok) continue;
+            for (int tr = 0; tr < 4; ++tr) rnd_list.insert(rnd_list.end(), rows[tr].begin(), rows[tr].end());
+            break;
+        }
+    }
+    int *d_rnd;
+    cudaMalloc(&d_rnd, rnd_list.size() * sizeof(int));
+    cudaMemcpy(d_rnd, rnd_list.data(), rnd_list.size() * sizeof(int), cudaMemcpyHostToDevice);
     int *d_slabs;
     cudaMalloc(&d_slabs, slab_list.size() * sizeof(int));
     cudaMemcpy(d_slabs, slab_list.data(), slab_list.size() * sizeof(int), cudaMemcpyHostToDevice);
@@ -122,6 +147,8 @@ int main(int argc, char **argv) {
     cases.push_back({64, 2, 8, 1, -4});
     cases.push_back({64, 4, 4, 1, -4});
     cases.push_back({64, 2, 8, 0, -4});
+    cases.push_back({64, 2, 8, 1, -104});   // random slab lists
+    cases.push_back({64, 4, 4, 1, -104});
     // steady-state read bandwidth: LDG.128 over the 512 MB flush buffer
     for (int blocks : {592, 1184, 2368}) {
         cudaEvent_t a, b;
@@ -174,9 +201,9 @@ int main(int argc, char **argv) {
         c.col_blocks = N / (64 * cs.atoms);
         c.slabs = nullptr;
         if (cs.kgroups < 0) {   // slab-list mode
-            c.k_groups = -cs.kgroups;
+            c.k_groups = (-cs.kgroups) % 100;
             c.steps = 36;
-            c.slabs = d_slabs;
+            c.slabs = cs.kgroups < -100 ? d_rnd : d_slabs;
         } else {
             c.k_groups = cs.kgroups;
             c.steps = K / cs.rpb / cs.kgroups;
