@@ -72,6 +72,9 @@ struct TcParams {
     int32_t adj_smem;        // g_i adjacency staged in shared memory for the table build
     const uint16_t *prep;    // precomputed scatter table [phase][j][row] (rbgp4_prepare) or null
     int32_t table_in_regs;   // densify keeps each row's offsets in registers (else smem table)
+    int32_t a_tmem;          // A tiles assembled in TMEM (tcgen05.st) and read by TS-mode MMAs
+    int32_t a_tcols;         // TMEM columns per A stage (tk * elt / 4)
+    int32_t tmem_cols;       // TMEM allocation (power of two)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -182,6 +185,42 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_
             "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
     }
 }
+// A from TMEM (TS): A must be K-major (lane = row), B from shared memory.
+template <bool TF32>
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    if constexpr (TF32) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u));
+    }
+}
+#define TMEM_ST_32x32b_X32(taddr, r)                                                        \
+    asm volatile(                                                                           \
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"  \
+        "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" \
+        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),        \
+        "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),      \
+        "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]),  \
+        "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),  \
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory")
+// one of q[0..3] by a runtime index without local memory (SEL chains)
+__device__ __forceinline__ uint4 sel4(const uint4 &a, const uint4 &b, const uint4 &c, const uint4 &d,
+                                      uint32_t idx) {
+    const bool o = idx & 1, t = idx & 2;
+    uint4 x, y, r;
+    x.x = o ? b.x : a.x; x.y = o ? b.y : a.y; x.z = o ? b.z : a.z; x.w = o ? b.w : a.w;
+    y.x = o ? d.x : c.x; y.y = o ? d.y : c.y; y.z = o ? d.z : c.z; y.w = o ? d.w : c.w;
+    r.x = t ? y.x : x.x; r.y = t ? y.y : x.y; r.z = t ? y.z : x.z; r.w = t ? y.w : x.w;
+    return r;
+}
+
 // UMMA shared-memory matrix descriptor (sm_100: version 1 at bit 46).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
                                               uint32_t layout) {
@@ -296,7 +335,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(uint32_t(p.tn < 32 ? 32 : p.tn)));
+                     "r"(uint32_t(p.tmem_cols)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         if (lane == 0) trace(p.debug, 6, 5);
     }
@@ -424,12 +463,23 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 uint64_t ad = a_desc0 + uint64_t(sa) * a_stage16;
                 uint64_t bd = b_desc0 + uint64_t(sb) * b_stage16;
                 uint32_t in_atom = 0;
-                for (int kk = 0; kk < ksteps; ++kk) {
-                    if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
-                    ad += 2;  // 32 bytes along K inside the swizzle atom
-                    in_atom += 2;
-                    if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
-                    bd += b_step16;
+                if (p.a_tmem) {
+                    // A tile of this stage sits in TMEM columns [tn + sa*a_tcols, +a_tcols)
+                    uint32_t at = tmem_d + uint32_t(p.tn + sa * p.a_tcols);
+                    for (int kk = 0; kk < ksteps; ++kk) {
+                        if (!(p.debug & 2))
+                            tc_mma_ts<kTF32>(tmem_d, at, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                        at += 8;  // 32 bytes of K = 8 TMEM columns
+                        bd += b_step16;
+                    }
+                } else {
+                    for (int kk = 0; kk < ksteps; ++kk) {
+                        if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                        ad += 2;  // 32 bytes along K inside the swizzle atom
+                        in_atom += 2;
+                        if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
+                        bd += b_step16;
+                    }
                 }
                 tc_commit(&empty_b[sb]);  // frees both the I slab and the A tile of the stage
                 trace(p.debug, 5, s);
@@ -469,6 +519,20 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             offp[i] = lo | (hi << 16);
         }
         const uint32_t wrow = smem_u32(w_buf) + uint32_t(t * p.ws * p.d_t * kElt);
+        // TMEM path: per 16-byte K position P of the dense row, code = 8 | chunk index when the
+        // row has a nonzero chunk there (positions ascend with the chunks), else 0; 4 bits each
+        uint32_t pcode[4] = {0, 0, 0, 0};
+        const int npos = p.tk * kElt / 16;
+        if (p.a_tmem && active) {
+            const int ui = ((row_in_tile0 + t) / p.bm) % p.u_i;
+            for (int c = 0; c < p.d_t / V; ++c) {
+                const int j = c * V;
+                const int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
+                const int kcol = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;
+                const int P = kcol * kElt / 16;
+                pcode[P / 8] |= uint32_t(8 | c) << (4 * (P % 8));
+            }
+        }
         for (int s = 0; s < nsteps; ++s) {
             const int sa = s % p.na;
             const int wg = s / p.ws, wsub = s - wg * p.ws;  // W stage and slot inside it
@@ -479,7 +543,36 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             mbar_wait(&empty_a[sa], ((s / p.na) & 1) ^ 1);
             if (t == 0) trace(p.debug, 2, s);
             const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
-            if (active && !(p.debug & 1)) {
+            if (p.a_tmem) {
+                // assemble the dense row t of A in TMEM lane t: 32 columns (8 positions) per st
+                const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
+                                     uint32_t(wsub * p.d_t * kElt);
+                uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0, q2 = q0, q3 = q0;
+                const int nch = p.d_t / V;
+                if (active && !(p.debug & 1)) {
+                    q0 = lds128(src);
+                    if (nch > 1) q1 = lds128(src + 16);
+                    if (nch > 2) q2 = lds128(src + 32);
+                    if (nch > 3) q3 = lds128(src + 48);
+                }
+                const uint32_t at = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(p.tn + sa * p.a_tcols);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (g >= npos / 8) break;
+                    const uint32_t code = pcode[g];
+                    uint32_t r[32];
+#pragma unroll
+                    for (int pp = 0; pp < 8; ++pp) {
+                        const uint32_t bits = (code >> (4 * pp)) & 0xFu;
+                        uint4 v = sel4(q0, q1, q2, q3, bits & 3u);
+                        if (!(bits & 8u)) v = make_uint4(0, 0, 0, 0);
+                        r[4 * pp] = v.x; r[4 * pp + 1] = v.y; r[4 * pp + 2] = v.z; r[4 * pp + 3] = v.w;
+                    }
+                    TMEM_ST_32x32b_X32(at + uint32_t(g * 32), r);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
+            } else if (active && !(p.debug & 1)) {
                 if (chunked) {
                     const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
                                          uint32_t(wsub * p.d_t * kElt);
@@ -642,7 +735,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     if (warp == 5) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
-                     "r"(uint32_t(p.tn < 32 ? 32 : p.tn)));
+                     "r"(uint32_t(p.tmem_cols)));
     }
 }
 
@@ -726,6 +819,20 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
         const size_t base = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 +
                             (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 2 + 1);
         size_t w_bytes = size_t(p.nw) * p.w_stage_bytes;
+        if (getenv("RBGP4_TC_NOA")) p.a_stage_bytes = 0;  // ablation (debug 7 only): no A ring
+        // A in TMEM (opt-in, RBGP4_TC_TMEM_A=1): needs 16-byte K runs (bk % V == 0), <= 4 of
+        // them per row and <= 32 K positions; shared memory then holds only the I and W rings.
+        // Correct, but the register-select row assembly costs ~350 instructions per row per
+        // step and measured slower than the shared-memory A ring (34.8 vs 28.8 us, conv10).
+        {
+            const int V = 16 / elt;
+            p.a_tcols = c.tk * elt / 4;
+            const bool ok = p.w_tma && c.bk % V == 0 && c.d_t / V <= 4 && c.tk * elt / 16 <= 32 &&
+                            tn + 2 * p.a_tcols <= 512 && getenv("RBGP4_TC_TMEM_A") != nullptr;
+            p.a_tmem = ok ? 1 : 0;
+            if (p.a_tmem) p.a_stage_bytes = 0;
+            else p.a_stage_bytes = kBlockM * c.tk * elt;
+        }
         const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;  // A tile + I slab
         if (base + w_bytes + 2 * stage > kSmemCap && p.w_tma) {
             // large compressed tiles: read W straight from global in the densify warps
@@ -738,9 +845,12 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
         }
         if (base + w_bytes + 2 * stage > kSmemCap) continue;
         const size_t fixed = base + w_bytes;
-        const int ns = int(std::min<size_t>(16, (kSmemCap - fixed) / stage));
+        int ns = int(std::min<size_t>(16, (kSmemCap - fixed) / stage));
+        if (p.a_tmem) ns = std::min(ns, (512 - tn) / p.a_tcols);  // A stages share TMEM with D
         p.na = ns;
         p.nb = ns;
+        p.tmem_cols = 32;
+        while (p.tmem_cols < (p.a_tmem ? tn + ns * p.a_tcols : tn)) p.tmem_cols *= 2;
         const int64_t tiles = ((c.n_cols + tn - 1) / tn) * blocks_m;
         // split-K in two (a 2-CTA cluster per tile) only when that still fits one wave;
         // deeper splits measured slower (tools/tc_time.py)
@@ -889,8 +999,9 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     if (const char *dbg = getenv("RBGP4_TC_DEBUG")) {
         pl.p.debug = atoi(dbg);
         if (pl.p.debug & 8192)
-            fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d ks=%d smem=%zu\n",
-                    pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.ksplit, pl.smem);
+            fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d ks=%d smem=%zu a_tmem=%d tmem=%d\n",
+                    pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.ksplit, pl.smem,
+                    pl.p.a_tmem, pl.p.tmem_cols);
         if (pl.p.debug & 16) { pl.p.w_tma = 0; pl.p.nw = 1; pl.p.ws = 1; pl.p.w_stage_bytes = 0; }
     }
     // compressed W tiles: 2-D (row_nnz, rows) view of the values, box (d_t, rows of a CTA)
