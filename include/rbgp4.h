@@ -99,6 +99,26 @@ int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int o
                         const void *prep, const void *inp, void *out, void *workspace,
                         size_t workspace_bytes, void *stream);
 
+/*
+ * Implicit-im2col sparse convolution: O = W x im2col(X) without ever
+ * materialising im2col.  X is NHWC bf16 (batch, height, width, c_in), O is NHWC
+ * (batch, height, width, rows) in bf16 or f32, stride 1, "same" padding (pad = (k-1)/2).
+ * W is the chain matrix of the layer with rows = c_out and columns in tap-major im2col
+ * order, column = (i*kw + j)*c_in + c  (conv weight[c_out, c, i, j]); desc->n_cols must be
+ * batch*height*width (ld_in/ld_out are ignored).  relu != 0 fuses max(0, .) into the store.
+ * Tensor-core bf16 path only (compute = RBGP4_COMPUTE_BF16).
+ */
+typedef struct rbgp4_conv_desc {
+    int32_t batch, height, width, c_in;
+    int32_t kh, kw, pad, stride;
+    int32_t relu;
+} rbgp4_conv_desc;
+
+size_t rbgp4_conv2d_workspace_size(const rbgp4_desc *desc, const rbgp4_conv_desc *conv);
+int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dtype,
+                 const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
+                 const void *x, void *out, void *workspace, size_t workspace_bytes, void *stream);
+
 /* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
 

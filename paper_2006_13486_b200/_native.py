@@ -19,9 +19,17 @@ COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
 EXPORTED = (
     "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size",
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
+    "rbgp4_conv2d", "rbgp4_conv2d_workspace_size",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count",
 )
+
+
+class ConvDesc(ctypes.Structure):
+    """Mirror of `rbgp4_conv_desc` (include/rbgp4.h)."""
+
+    _fields_ = [(n, ctypes.c_int32) for n in ("batch", "height", "width", "c_in", "kh", "kw", "pad",
+                                              "stride", "relu")]
 
 
 class Desc(ctypes.Structure):
@@ -64,6 +72,11 @@ def lib():
     h.rbgp4_prepare_size.restype = sz
     h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, sz, vp]
     h.rbgp4_prepare.restype = i32
+    h.rbgp4_conv2d_workspace_size.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc)]
+    h.rbgp4_conv2d_workspace_size.restype = sz
+    h.rbgp4_conv2d.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc), i32, vp, vp, vp, vp,
+                               vp, vp, vp, sz, vp]
+    h.rbgp4_conv2d.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

@@ -1,0 +1,110 @@
+"""Sparse convolution and linear layers on the RBGP4 product.
+
+The reference represents convolutions only as an SDMM over an im2col'd input
+(reference SPEC.md:9); here the im2col is never materialised.  A convolution
+weight is a chain matrix with rows = output channels and columns in tap-major
+im2col order, column = (i*kw + j)*c_in + c for conv weight[c_out, c, i, j], and
+`sparse_conv2d` runs the implicit-im2col tcgen05 kernel (`rbgp4_conv2d`): each
+pipeline step TMA-loads the tap-shifted NHWC window of the input directly
+(out-of-bounds = zero padding).  Activations are NHWC bf16, outputs NHWC
+(bf16 or f32), with an optional fused ReLU.
+
+`SparseLinear` maps y = x W^T to the product's O = W x I with I = x^T.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .device import device_format, resolve_device, stream_handle, torch
+from .errors import InvalidArgumentError, ShapeError, UnsupportedChainError
+from .sdmm import make_desc, prepared, rbgp4mm, tiling_for_chain, workspace
+
+
+def conv_weight_to_columns(weight: np.ndarray) -> np.ndarray:
+    """(c_out, c_in, kh, kw) conv weight -> dense (c_out, kh*kw*c_in) in tap-major order."""
+    c_out, c_in, kh, kw = weight.shape
+    return np.ascontiguousarray(weight.transpose(0, 2, 3, 1).reshape(c_out, kh * kw * c_in))
+
+
+def columns_to_conv_weight(dense: np.ndarray, c_in: int, kh: int, kw: int) -> np.ndarray:
+    """Inverse of `conv_weight_to_columns`."""
+    c_out = dense.shape[0]
+    return np.ascontiguousarray(dense.reshape(c_out, kh, kw, c_in).transpose(0, 3, 1, 2))
+
+
+def sparse_conv2d(w, x, kernel_size: int = 3, *, relu: bool = False, out=None, out_dtype=None):
+    """NHWC conv of `x` (batch, H, W, c_in) with chain matrix `w`, stride 1, 'same' padding.
+
+    Returns an NHWC (batch, H, W, c_out) CUDA tensor.  `x` must be a CUDA bf16 tensor
+    (contiguous NHWC); the weight values are converted to bf16 once and cached.
+    """
+    t = torch()
+    if w.chain.k != 4:
+        raise UnsupportedChainError(f"sparse conv needs a 4-factor chain, got {w.chain.k}")
+    if not (isinstance(x, t.Tensor) and x.is_cuda and x.dim() == 4):
+        raise ShapeError("x must be a 4-D NHWC CUDA tensor")
+    if x.dtype != t.bfloat16:
+        raise ShapeError(f"x must be bf16, got {x.dtype}")
+    batch, height, width, c_in = x.shape
+    kh = kw = int(kernel_size)
+    if w.cols != kh * kw * c_in:
+        raise ShapeError(f"weight has {w.cols} columns, conv needs kh*kw*c_in = {kh * kw * c_in}")
+    if kh % 2 != 1:
+        raise InvalidArgumentError("only odd kernel sizes ('same' padding) are supported")
+    x = x.contiguous()
+    dev = resolve_device(x.device)
+    res_dt = out_dtype if out_dtype is not None else t.bfloat16
+    with t.cuda.device(dev):
+        fmt = device_format(w, dev, t.bfloat16)
+        n_cols = batch * height * width
+        desc = make_desc(fmt.desc_fields, n_cols, n_cols, n_cols)
+        cv = _native.ConvDesc(batch, height, width, c_in, kh, kw, (kh - 1) // 2, 1, int(bool(relu)))
+        if out is None:
+            res = t.empty((batch, height, width, w.rows), dtype=res_dt, device=dev)
+        else:
+            res = out
+            if tuple(res.shape) != (batch, height, width, w.rows) or not res.is_contiguous():
+                raise ShapeError("out must be a contiguous NHWC (batch, H, W, c_out) tensor")
+        if n_cols == 0:
+            return res
+        lib = _native.lib()
+        prep = prepared(fmt, "bf16", dev, desc)
+        need = lib.rbgp4_conv2d_workspace_size(ctypes.byref(desc), ctypes.byref(cv))
+        ws = workspace(dev, need) if need else None
+        code = {t.bfloat16: _native.BF16, t.float32: _native.F32}[res.dtype]
+        _native.check(lib.rbgp4_conv2d(
+            ctypes.byref(desc), ctypes.byref(cv), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),
+            fmt.adj_i.data_ptr(), prep.data_ptr() if prep is not None else None, x.data_ptr(),
+            res.data_ptr(), ws.data_ptr() if ws is not None else None, need, stream_handle(dev)),
+            "rbgp4_conv2d")
+    return res
+
+
+class SparseConv2d:
+    """3x3 (or kxk) stride-1 'same' convolution with an RBGP4-patterned weight (NHWC bf16)."""
+
+    def __init__(self, w, kernel_size: int = 3, relu: bool = True):
+        self.w, self.kernel_size, self.relu = w, kernel_size, relu
+
+    def __call__(self, x):
+        return sparse_conv2d(self.w, x, self.kernel_size, relu=self.relu)
+
+
+class SparseLinear:
+    """y = x W^T for a chain matrix W (out_features x in_features); x is (batch, in)."""
+
+    def __init__(self, w, compute: str = "bf16"):
+        self.w, self.compute = w, compute
+        self.params = tiling_for_chain(w.chain, tn=1, rn=1, bn=1)
+
+    def __call__(self, x):
+        t = torch()
+        xt = x.t().contiguous()
+        if self.compute == "bf16" and xt.dtype != t.bfloat16:
+            xt = xt.to(t.bfloat16)
+        y, _ = rbgp4mm(self.w, xt, self.params, compute=self.compute)
+        return y.t()

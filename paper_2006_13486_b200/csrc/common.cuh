@@ -60,6 +60,10 @@ size_t tc_prep_size(const ChainDims &c, int compute);
 int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep, size_t bytes,
                cudaStream_t stream);
 int tc_supported(const ChainDims &c, int compute, int out_dtype);
+size_t conv_workspace_size(const ChainDims &c, const rbgp4_conv_desc *cv);
+int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,
+                const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *x,
+                void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream);
 size_t tc_workspace_size(const ChainDims &c, int compute);
 
 }  // namespace rbgp4

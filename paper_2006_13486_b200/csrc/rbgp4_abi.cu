@@ -174,6 +174,27 @@ int rbgp4_prepare(const rbgp4_desc *desc, int compute, const int32_t *adj_i, voi
     return tc_prepare(c, compute, adj_i, prep, prep_bytes, static_cast<cudaStream_t>(stream));
 }
 
+size_t rbgp4_conv2d_workspace_size(const rbgp4_desc *desc, const rbgp4_conv_desc *conv) {
+    ChainDims c;
+    if (validate_desc(desc, &c) != RBGP4_OK) return 0;
+    return conv_workspace_size(c, conv);
+}
+
+int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dtype,
+                 const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
+                 const void *x, void *out, void *workspace, size_t workspace_bytes, void *stream) {
+    ChainDims c;
+    rbgp4_desc d = *desc;
+    d.ld_in = d.ld_out = d.n_cols;  // NHWC operands: leading dimensions are implied
+    int rc = validate_desc(&d, &c);
+    if (rc != RBGP4_OK) return rc;
+    RBGP4_REQUIRE(out_dtype == RBGP4_F32 || out_dtype == RBGP4_BF16, "conv writes f32 or bf16");
+    if (c.n_cols == 0) return RBGP4_OK;
+    RBGP4_REQUIRE(values && adj_o && adj_i && x && out, "null device pointer");
+    return launch_conv(c, conv, out_dtype, values, adj_o, adj_i, prep, x, out, workspace,
+                       workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
 int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t n, void *stream) {
     RBGP4_REQUIRE(n >= 0, "negative element count");
     if (n == 0) return RBGP4_OK;

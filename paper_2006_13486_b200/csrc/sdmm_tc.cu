@@ -75,6 +75,10 @@ struct TcParams {
     int32_t a_tmem;          // A tiles assembled in TMEM (tcgen05.st) and read by TS-mode MMAs
     int32_t a_tcols;         // TMEM columns per A stage (tk * elt / 4)
     int32_t tmem_cols;       // TMEM allocation (power of two)
+    // implicit-im2col convolution (K3): I is never materialised; x is NHWC bf16 and the
+    // slab of step s is the tap (i, j) / channel block of its K rows, fetched by a 4-D TMA
+    // box at the tap-shifted coordinates (out-of-bounds = zero padding); O is NHWC.
+    int32_t conv, c_in, img_h, img_w, kw, pad, relu, th, tb;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -146,6 +150,14 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int32_t x, int32_t y, int32_t z, int32_t w) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
         : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
@@ -289,7 +301,7 @@ __global__ void prep_kernel(const TcParams p, const int32_t *__restrict__ adj_i,
 }
 
 // ---------------------------------------------------------------- the kernel
-template <typename E, bool OUT_BF16>
+template <typename E, bool OUT_BF16, bool CONV>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
           const TcParams p, const E *__restrict__ values, const int32_t *__restrict__ adj_o,
@@ -401,7 +413,18 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             if (elect_one()) {
                 mbar_expect_tx(&full_b[st], uint32_t(p.b_stage_bytes));
                 unsigned char *dst = b_buf + st * p.b_stage_bytes;
-                if (p.i3d) {
+                if constexpr (CONV) {
+                    // K rows [krow, krow + tk) = tap (i, j), channels [c0, c0 + tk); the pixel
+                    // tile is tb images x th rows x the full width, shifted by the tap
+                    const int tap = krow / p.c_in, c0 = krow - tap * p.c_in;
+                    const int ti = tap / p.kw, tj = tap - ti * p.kw;
+                    const int hw = p.img_h * p.img_w;
+                    const int b0 = int(n0 / hw), h0 = int(n0 % hw) / p.img_w;
+                    const uint32_t k_atom_bytes = uint32_t(p.tn) * 128;
+                    for (int a = 0; a < p.tk / 64; ++a)
+                        tma_load_4d(dst + a * k_atom_bytes, &imap, &full_b[st], c0 + 64 * a,
+                                    tj - p.pad, h0 + ti - p.pad, b0);
+                } else if (p.i3d) {
                     // one instruction for the whole slab: (atom cols, K rows, atoms) box
                     tma_load_3d(dst, &imap, &full_b[st], 0, krow, int32_t(n0) / atom_cols);
                 } else {
@@ -434,7 +457,8 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         // ================= MMA issuer =================
         // instruction descriptor: D f32, A/B bf16|tf32, A K-major, B MN-major, N, M=128
         const uint32_t fmt = kTF32 ? 2u : 1u;
-        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (1u << 16) |
+        const uint32_t b_mn = CONV ? 0u : 1u;  // conv: B (im2col of NHWC) is K-major
+        const uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | (0u << 15) | (b_mn << 16) |
                                (uint32_t(p.tn >> 3) << 17) | (uint32_t(kBlockM >> 4) << 24);
         const int ksteps = p.tk * kElt / 32;
         // Descriptors are built once; per stage / K-step only the 14-bit start-address
@@ -443,8 +467,10 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             smem_desc(smem_u32(a_buf), 0, 8 * p.a_swz, swizzle_layout_code(p.a_swz));
         // MN-major B: bf16 -> SWIZZLE_128B (8-row K groups, SBO 1024);
         // tf32 -> SWIZZLE_128B_BASE32B (32 B chunks, 4-row K groups, SBO 512)
-        const uint64_t b_desc0 = kTF32 ? smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 512, 1u)
+        const uint64_t b_desc0 = CONV ? smem_desc(smem_u32(b_buf), 0, 1024, 2u)  // K-major SW128
+                               : kTF32 ? smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 512, 1u)
                                        : smem_desc(smem_u32(b_buf), uint32_t(p.tk) * 128, 1024, 2u);
+        const uint32_t bk_jump16 = uint32_t(p.tn - 1) * 8;  // conv: next 64-channel K atom
         const uint32_t a_stage16 = uint32_t(p.a_stage_bytes) >> 4;
         const uint32_t b_stage16 = uint32_t(p.b_stage_bytes) >> 4;
         const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
@@ -478,7 +504,12 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                         ad += 2;  // 32 bytes along K inside the swizzle atom
                         in_atom += 2;
                         if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
-                        bd += b_step16;
+                        if constexpr (CONV) {
+                            bd += 2;  // K-major B: 32 bytes along K inside its 128 B atom
+                            if ((kk & 3) == 3) bd += bk_jump16;
+                        } else {
+                            bd += b_step16;
+                        }
                     }
                 }
                 tc_commit(&empty_b[sb]);  // frees both the I slab and the A tile of the stage
@@ -698,6 +729,21 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                     }
                 }
             }
+            if constexpr (CONV) {
+                // NHWC output: pixel (col + q) is a row of c_out = p.ld_out channels
+                const int64_t ch = m0 + row;
+#pragma unroll 4
+                for (int q = 0; q < 32; ++q) {
+                    if (col + q >= p.n_cols) break;
+                    float v = __uint_as_float(r[q]);
+                    if (p.relu) v = fmaxf(v, 0.0f);
+                    if constexpr (OUT_BF16)
+                        static_cast<__nv_bfloat16 *>(out)[(col + q) * p.ld_out + ch] = __float2bfloat16_rn(v);
+                    else
+                        static_cast<float *>(out)[(col + q) * p.ld_out + ch] = v;
+                }
+                continue;
+            }
             if constexpr (OUT_BF16) {
                 __nv_bfloat16 *dst = static_cast<__nv_bfloat16 *>(out) + (m0 + row) * p.ld_out + col;
                 if (full && (reinterpret_cast<uintptr_t>(dst) % 16 == 0)) {
@@ -762,7 +808,7 @@ struct TcPlan {
 
 constexpr size_t kSmemCap = 227 * 1024;
 
-int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
+int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     const int elt = compute == RBGP4_COMPUTE_TF32 ? 4 : 2;
     if (!(c.tm == 64 || c.tm % kBlockM == 0)) {
         set_error("tensor-core path needs tile rows tm = 64 or a multiple of 128 (tm=%d)", c.tm);
@@ -806,6 +852,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
     while (tn > tn_min && tn / 2 >= c.n_cols) tn /= 2;
     if (tn > tn_min && ((c.n_cols + tn - 1) / tn) * blocks_m * 2 < kNumSMs) tn /= 2;
     if (const char *env = getenv("RBGP4_TC_TN")) tn = std::max(tn_min, std::min(256, atoi(env)));
+    if (force_tn) tn = force_tn;
     p.adj_smem = size_t(c.u_i) * c.d_i * 4 <= 16384 ? 1 : 0;
     // Shared-memory budget, in priority order (one CTA per SM):
     //   1. >= 96 KB of I slabs in flight (TMA latency under load is ~2 us: Little's law),
@@ -813,6 +860,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
     //   3. W ring 2 x <= 8 KB,
     //   4. everything left -> more I stages (<= 16).
     for (; tn >= tn_min; tn /= 2) {
+        if (force_tn && tn != force_tn) break;
         p.tn = tn;
         p.b_stage_bytes = c.tk * tn * elt;
         p.nw = p.w_tma ? 2 : 1;
@@ -867,11 +915,11 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out) {
     return 0;
 }
 
-template <typename E, bool OUT_BF16>
+template <typename E, bool OUT_BF16, bool CONV = false>
 int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wmap,
                  const void *values, const int32_t *adj_o, const int32_t *adj_i, void *out,
                  float *wsp, cudaStream_t stream) {
-    auto kern = tc_kernel<E, OUT_BF16>;
+    auto kern = tc_kernel<E, OUT_BF16, CONV>;
     cudaError_t e =
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) {
@@ -1036,6 +1084,113 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
                    : launch_typed<float, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
     return obf ? launch_typed<__nv_bfloat16, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
                : launch_typed<__nv_bfloat16, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
+}
+
+// ---------------------------------------------------------------- K3: implicit im2col
+namespace {
+int conv_tile(const rbgp4_conv_desc &cv, int tn, int *th, int *tb) {
+    const int hw = cv.height * cv.width;
+    if (tn % cv.width) return 0;
+    if (tn <= hw) {
+        *th = tn / cv.width;
+        *tb = 1;
+        return cv.height % *th == 0;
+    }
+    *th = cv.height;
+    *tb = tn / hw;
+    return tn % hw == 0 && *tb <= 256;
+}
+}  // namespace
+
+int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
+    RBGP4_REQUIRE(cv != nullptr, "null conv descriptor");
+    RBGP4_REQUIRE(cv->stride == 1 && cv->pad * 2 == cv->kh - 1 && cv->kh == cv->kw,
+                  "implicit-im2col path supports stride-1 'same' square convolutions (kh=%d, pad=%d, "
+                  "stride=%d)", cv->kh, cv->pad, cv->stride);
+    RBGP4_REQUIRE(c.cols == int64_t(cv->kh) * cv->kw * cv->c_in,
+                  "chain columns %lld != kh*kw*c_in = %d (tap-major im2col order)", (long long)c.cols,
+                  cv->kh * cv->kw * cv->c_in);
+    RBGP4_REQUIRE(c.n_cols == int64_t(cv->batch) * cv->height * cv->width,
+                  "n_cols %lld != batch*height*width", (long long)c.n_cols);
+    RBGP4_REQUIRE(c.tk % 64 == 0 && cv->c_in % c.tk == 0,
+                  "conv path needs tk %% 64 == 0 and c_in %% tk == 0 (tk=%d, c_in=%d)", c.tk, cv->c_in);
+    RBGP4_REQUIRE(cv->width <= 256 && cv->height <= 256, "feature map too large for one TMA box");
+    for (int tn : {128, 64}) {
+        int th, tb;
+        if (!conv_tile(*cv, tn, &th, &tb)) continue;
+        if (!plan_tc(c, RBGP4_COMPUTE_BF16, pl, tn)) continue;
+        pl->p.conv = 1;
+        pl->p.c_in = cv->c_in;
+        pl->p.img_h = cv->height;
+        pl->p.img_w = cv->width;
+        pl->p.kw = cv->kw;
+        pl->p.pad = cv->pad;
+        pl->p.relu = cv->relu;
+        pl->p.th = th;
+        pl->p.tb = tb;
+        pl->p.ld_out = c.rows;  // NHWC: a pixel row holds c_out channels
+        return 1;
+    }
+    set_error("no pixel tiling of %dx%d maps into 128 or 64 columns", cv->height, cv->width);
+    return 0;
+}
+
+size_t conv_workspace_size(const ChainDims &c, const rbgp4_conv_desc *cv) {
+    TcPlan pl;
+    if (!conv_plan(c, cv, &pl) || pl.p.ksplit <= 1) return 0;
+    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(c.n_cols) * 4;
+}
+
+int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,
+                const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *x,
+                void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream) {
+    TcPlan pl;
+    if (!conv_plan(c, cv, &pl)) return RBGP4_EUNSUPPORTED;
+    if (c.n_cols == 0) return RBGP4_OK;
+    pl.p.prep = static_cast<const uint16_t *>(prep);
+    RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && (cv->c_in * 2) % 16 == 0,
+                  "conv input must be 16-byte aligned NHWC bf16");
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return RBGP4_ECUDA;
+    }
+    // x: NHWC bf16 as a 4-D tensor (C, W, H, B); box = 64 channels x full width x th rows x tb
+    CUtensorMap map, wmap;
+    cuuint64_t dims[4] = {cuuint64_t(cv->c_in), cuuint64_t(cv->width), cuuint64_t(cv->height),
+                          cuuint64_t(cv->batch)};
+    cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
+                             cuuint64_t(cv->height) * cv->width * cv->c_in * 2};
+    cuuint32_t box[4] = {64, cuuint32_t(cv->width), cuuint32_t(pl.p.th), cuuint32_t(pl.p.tb)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled(conv input) failed (%d)", int(r));
+        return RBGP4_ECUDA;
+    }
+    memset(&wmap, 0, sizeof(wmap));
+    if (pl.p.w_tma) {
+        cuuint64_t wdims[2] = {cuuint64_t(c.row_nnz), cuuint64_t(c.rows)};
+        cuuint64_t wstrides[1] = {cuuint64_t(c.row_nnz) * 2};
+        cuuint32_t wbox[2] = {cuuint32_t(pl.p.ws * c.d_t), cuuint32_t(pl.p.rows_valid)};
+        r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(values), wdims,
+                wstrides, wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    float *wsp = static_cast<float *>(workspace);
+    if (pl.p.ksplit > 1 && (wsp == nullptr || workspace_bytes < conv_workspace_size(c, cv))) {
+        set_error("split-K conv needs %zu workspace bytes", conv_workspace_size(c, cv));
+        return RBGP4_EWORKSPACE;
+    }
+    return out_dtype == RBGP4_BF16
+               ? launch_typed<__nv_bfloat16, true, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
+               : launch_typed<__nv_bfloat16, false, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
 }
 
 }  // namespace rbgp4

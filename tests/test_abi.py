@@ -22,7 +22,7 @@ from conftest import ROOT
 
 def declared_functions():
     text = open(os.path.join(ROOT, "include", "rbgp4.h")).read()
-    return sorted(set(re.findall(r"\b(rbgp4_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(rbgp4_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_and_binding_agree():
