@@ -119,6 +119,11 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
                  const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
                  const void *x, void *out, void *workspace, size_t workspace_bytes, void *stream);
 
+/* 2x2 / stride-2 max pooling of a bf16 NHWC tensor (the VGG stage boundary);
+ * H, W even, channels % 8 == 0, 16-byte aligned. */
+int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int width, int channels,
+                          void *stream);
+
 /* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
 

@@ -19,7 +19,7 @@ COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
 EXPORTED = (
     "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size",
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
-    "rbgp4_conv2d", "rbgp4_conv2d_workspace_size",
+    "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count",
 )
@@ -77,6 +77,8 @@ def lib():
     h.rbgp4_conv2d.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc), i32, vp, vp, vp, vp,
                                vp, vp, vp, sz, vp]
     h.rbgp4_conv2d.restype = i32
+    h.rbgp4_maxpool2x2_nhwc.argtypes = [vp, vp, i32, i32, i32, i32, vp]
+    h.rbgp4_maxpool2x2_nhwc.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

@@ -1,0 +1,147 @@
+"""VGG19 for CIFAR with RBGP4-sparse convolutions -- inference.
+
+The paper's setup: every 3x3 convolution except the first is RBGP4
+sparse; the first convolution and the classifier stay dense.  Here:
+
+* sparse convs run `sparse_conv2d` (implicit-im2col tcgen05 kernel, NHWC bf16, ReLU fused);
+* 2x2 max pooling runs `rbgp4_maxpool2x2_nhwc`;
+* the dense first conv and the 512 -> classes classifier are plain library calls
+  (cuDNN / cuBLAS through torch), as the reference's dense baseline is BLAS;
+* batch norm is folded away and biases are omitted (synthetic, random-init weights).
+
+Factorisations are chosen per layer (`layer_chain`): tiles of up to 128 x 128 built from
+dense g_b = (b, b) element blocks (b = 8 when the sparsity split allows it, else 4 / 2),
+g_r = (1,1), g_o carrying up to 50 % when it has >= 4 tile-rows, g_i the rest.  Every factor
+is a certified Ramanujan lift chain from the reference's generator.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .conv import SparseConv2d
+from .device import stream_handle, torch
+from .errors import GenerationExhaustedError, InvalidArgumentError
+from .generate import LiftChainSpec, generate_ramanujan
+from .graphs import complete_graph
+from .products import RbgpChain
+from .rcubs import init_random
+
+#: VGG19 feature config (channels; "M" = 2x2 max pool)
+VGG19 = [64, 64, "M", 128, 128, "M", 256, 256, 256, 256, "M", 512, 512, 512, 512, "M",
+         512, 512, 512, 512, "M"]
+
+
+def _factor(shape, sp, seed):
+    if sp == 0.0:
+        return complete_graph(*shape)
+    return generate_ramanujan(LiftChainSpec(shape[0], shape[1], sp, rng_seed=seed, max_attempts=200)).graph
+
+
+def layer_chain(c_out: int, c_in: int, sparsity: float, seed: int = 0, k: int = 3) -> RbgpChain:
+    """A tensor-core-friendly RBGP4 chain for a (c_out, k*k*c_in) conv weight."""
+    tm = min(128, c_out)
+    tk = 128 if c_in % 128 == 0 else 64
+    if c_in % tk or c_out % tm:
+        raise InvalidArgumentError(f"unsupported conv shape {c_out}x{c_in}")
+    u_o, v_o = c_out // tm, k * k * c_in // tk
+    sp_o = 0.5 if u_o >= 4 else 0.0
+    sp_i = 1.0 - (1.0 - sparsity) / (1.0 - sp_o)
+    last = None
+    for b in (8, 4, 2):
+        u_i, v_i = tm // b, tk // b
+        d_i, d_r = v_i * (1 - sp_i), u_i * (1 - sp_i)
+        if d_i < 2 or d_r < 2 or d_i != int(d_i) or d_r != int(d_r):
+            continue
+        try:
+            return RbgpChain((_factor((u_o, v_o), sp_o, seed), complete_graph(1, 1),
+                              _factor((u_i, v_i), sp_i, seed + 1), complete_graph(b, b)))
+        except GenerationExhaustedError as exc:
+            last = exc
+    raise InvalidArgumentError(f"no RBGP4 factorisation for {c_out}x{c_in} at {sparsity}: {last}")
+
+
+def maxpool2x2(x):
+    t = torch()
+    b, h, w, c = x.shape
+    y = t.empty((b, h // 2, w // 2, c), dtype=x.dtype, device=x.device)
+    _native.check(_native.lib().rbgp4_maxpool2x2_nhwc(x.data_ptr(), y.data_ptr(), b, h, w, c,
+                                                      stream_handle(x.device)), "rbgp4_maxpool2x2_nhwc")
+    return y
+
+
+@dataclass
+class VGG19Sparse:
+    """Inference-only VGG19-CIFAR with RBGP4 sparse convolutions (NHWC bf16 activations)."""
+
+    sparsity: float = 0.875
+    num_classes: int = 100
+    seed: int = 0
+    device: str = "cuda"
+
+    def __post_init__(self):
+        t = torch()
+        gen = t.Generator().manual_seed(self.seed)
+        # dense first conv (3 -> 64), channels-last bf16
+        self.conv1 = (t.randn(64, 3, 3, 3, generator=gen) * (2.0 / 27) ** 0.5).to(
+            self.device, t.bfloat16).to(memory_format=t.channels_last)
+        self.layers = []   # ("conv", SparseConv2d) | ("pool", None)
+        self.chains = []
+        c_in, idx = 64, 0
+        for v in VGG19[1:]:
+            if v == "M":
+                self.layers.append(("pool", None))
+                continue
+            chain = layer_chain(v, c_in, self.sparsity, seed=self.seed * 1000 + 10 * idx)
+            w = init_random(chain, self.seed * 1000 + 10 * idx + 5, precision="f32")
+            self.layers.append(("conv", SparseConv2d(w, 3, relu=True)))
+            self.chains.append(chain)
+            c_in, idx = v, idx + 1
+        self.fc = (t.randn(self.num_classes, 512, generator=gen) / 512 ** 0.5).to(self.device, t.bfloat16)
+
+    def forward(self, x_nhwc):
+        """x: (batch, 32, 32, 3) bf16 CUDA tensor -> (batch, num_classes) logits."""
+        t = torch()
+        x = x_nhwc.permute(0, 3, 1, 2)  # NCHW view of channels-last memory
+        x = t.nn.functional.conv2d(x, self.conv1, padding=1).relu_()
+        x = x.permute(0, 2, 3, 1).contiguous()  # NHWC
+        for kind, layer in self.layers:
+            x = maxpool2x2(x) if kind == "pool" else layer(x)
+        return x.reshape(x.shape[0], -1) @ self.fc.t()
+
+    __call__ = forward
+
+    def reference_forward(self, x_nhwc):
+        """Same network with dense fp32 weights via torch (test oracle for the float path)."""
+        t = torch()
+        from .conv import columns_to_conv_weight
+        x = x_nhwc.permute(0, 3, 1, 2).float()
+        x = t.nn.functional.conv2d(x, self.conv1.float(), padding=1).relu()
+        c_in = 64
+        for kind, layer in self.layers:
+            if kind == "pool":
+                x = t.nn.functional.max_pool2d(x, 2)
+                continue
+            dense = layer.w.to_dense().astype(np.float32)
+            wgt = t.from_numpy(columns_to_conv_weight(dense, c_in, 3, 3)).to(x.device)
+            # mirror the bf16 rounding of weights and activations of the product path
+            wgt = wgt.to(t.bfloat16).float()
+            x = t.nn.functional.conv2d(x.to(t.bfloat16).float(), wgt, padding=1).relu()
+            c_in = layer.w.rows
+        x = x.to(t.bfloat16).float().reshape(x.shape[0], -1)
+        return x @ self.fc.float().t()
+
+    @property
+    def sparse_flops_per_image(self) -> float:
+        """2 * nnz * pixels over the sparse convolutions (the RBGP4 metric)."""
+        total, hw, i = 0.0, 32 * 32, 0
+        for kind, layer in self.layers:
+            if kind == "pool":
+                hw //= 4
+            else:
+                total += 2.0 * layer.w.nnz * hw
+        return total

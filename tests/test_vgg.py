@@ -1,0 +1,53 @@
+"""VGG19-CIFAR RBGP4 inference (BASELINE config 5).
+
+CPU: every sparse layer gets a certified factorisation at the paper's sparsities.
+GPU: the NHWC max-pool is bit-exact against torch, and the whole network (dense conv1,
+15 RBGP4 convs with fused ReLU, 5 pools, dense classifier) matches a torch fp32 forward
+with the same (bf16-rounded) dense weights to rel-L2 <= 2e-2 -- bf16 activations are
+re-rounded at every layer on the product path, so the error compounds over 16 layers.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2006_13486_b200.vgg import VGG19, layer_chain
+
+
+@pytest.mark.parametrize("sparsity", [0.5, 0.75, 0.875, 0.9375])
+def test_layer_factorisations(sparsity):
+    c_in = 64
+    for v in VGG19[1:]:
+        if v == "M":
+            continue
+        chain = layer_chain(v, c_in, sparsity)
+        assert chain.num_left == v and chain.num_right == 9 * c_in
+        assert abs(chain.sparsity - sparsity) < 1e-12
+        g_b = chain.graphs[3]
+        assert g_b.is_complete() and chain.graphs[1].is_complete()
+        c_in = v
+
+
+@pytest.mark.gpu
+def test_maxpool_bit_exact():
+    import torch
+    from paper_2006_13486_b200.vgg import maxpool2x2
+    x = torch.randn(3, 8, 6, 24, device="cuda").to(torch.bfloat16)
+    ref = torch.nn.functional.max_pool2d(x.permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1)
+    assert torch.equal(maxpool2x2(x), ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sparsity", [0.875, 0.5])
+def test_vgg19_forward_matches_dense(sparsity):
+    import torch
+    from paper_2006_13486_b200.vgg import VGG19Sparse
+    net = VGG19Sparse(sparsity=sparsity, seed=3)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(6, 32, 32, 3, device="cuda", generator=g).to(torch.bfloat16)
+    y = net(x).float()
+    ref = net.reference_forward(x)
+    rel = float((y - ref).norm() / ref.norm())
+    assert y.shape == (6, 100)
+    assert rel <= 2e-2, rel
