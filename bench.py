@@ -56,7 +56,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--factorisation", choices=["tc", "paper"], default="tc",
+    ap.add_argument("--factorisation", choices=["tc", "tc16", "paper"], default="tc",
                     help="base-graph factorisation of every layer (both are 87.5%% RBGP4)")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other factorisation")
     return ap.parse_args()
@@ -74,6 +74,8 @@ FACTORISATIONS = {
     "tc": ("G_o(4,K/128)@.5 G_r(1,1) G_i(16,16) G_b(8,8): tile 128x128, 8x8 dense element blocks "
            "(tensor-core-friendly, SURVEY §7 hard part 1)"),
     "paper": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1): tile 128x64 (paper family, G_b=(1,1))",
+    "tc16": ("G_o(4,K/128)@.5 G_r(1,1) G_i(8,8) G_b(16,16): tile 128x128, 16x16 dense element "
+             "blocks = whole MMA operands (gathered-block kernel, no densification)"),
 }
 
 
@@ -81,7 +83,8 @@ def build_layers(sparsity: float, batch: int, fact: str = "tc"):
     import paper_2006_13486_b200 as ks
     from paper_2006_13486_b200 import workloads as wl
 
-    maker = wl.vgg19_cifar_512_tc if fact == "tc" else wl.vgg19_cifar_512
+    maker = {"tc": wl.vgg19_cifar_512_tc, "tc16": wl.vgg19_cifar_512_tc16,
+             "paper": wl.vgg19_cifar_512}[fact]
     layers = []
     for cfg in maker(sparsity, batch=batch):
         chain = wl.build_chain(cfg)
@@ -314,18 +317,21 @@ def run_ours(args):
         return layers, host_in, dev_out, graphs
 
     def timed(graphs, dom, steps, warmup, sampler=None):
-        ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
-        ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
+        # events around every launch of the timed region (one graph replay = one kernel):
+        # per-layer means for the report, the dominant layers' mean for the roofline
+        ev_s = [[torch.cuda.Event(enable_timing=True) for _ in graphs] for _ in range(steps)]
+        ev_e = [[torch.cuda.Event(enable_timing=True) for _ in graphs] for _ in range(steps)]
 
         def step(record=None):
             for i, g in enumerate(graphs):
-                if record is not None and i in dom:
-                    ev_s[record[0]].record(stream)
+                if record is not None:
+                    ev_s[record[0]][i].record(stream)
                     g.replay()
-                    ev_e[record[0]].record(stream)
-                    record[0] += 1
+                    ev_e[record[0]][i].record(stream)
                 else:
                     g.replay()
+            if record is not None:
+                record[0] += 1
 
         with torch.cuda.stream(stream):
             for _ in range(warmup):
@@ -357,15 +363,17 @@ def run_ours(args):
             t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             elapsed_ms = float(t.item())
-        dom_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
-        return elapsed_ms, (statistics.mean(dom_ms) if dom_ms else float("nan")), clocks
+        per_layer = [statistics.mean(ev_s[k][i].elapsed_time(ev_e[k][i]) for k in range(steps))
+                     for i in range(len(graphs))]
+        dom_ms = statistics.mean(per_layer[i] for i in dom)
+        return elapsed_ms, dom_ms, clocks, per_layer
 
     stream = torch.cuda.Stream(device=dev)
     layers, host_in, dev_out, graphs = setup(args.factorisation)
     flops_step = sum(lay["flops"] for lay in layers)
     dom = [i for i, lay in enumerate(layers) if lay["k"] == 4608 and lay["n"] == 16 * args.batch]
-    elapsed_ms, dom_avg_ms, clocks = timed(graphs, dom, args.steps, args.warmup,
-                                           ClockSampler(dev.index))
+    elapsed_ms, dom_avg_ms, clocks, per_layer = timed(graphs, dom, args.steps, args.warmup,
+                                                      ClockSampler(dev.index))
     ms_per_step = elapsed_ms / args.steps
     value = flops_step * world / (ms_per_step * 1e-3) / 1e12
     launches_in_region = len(graphs) * args.steps  # graph replays of our kernels
@@ -421,7 +429,7 @@ def run_ours(args):
     if not args.no_alt:
         other = "paper" if args.factorisation == "tc" else "tc"
         a_layers, _, _, a_graphs = setup(other)
-        a_elapsed, a_dom, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
+        a_elapsed, a_dom, _, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
         a_ms = a_elapsed / max(10, args.steps // 4)
         a_flops = sum(lay["flops"] for lay in a_layers)
         alt = {"factorisation": FACTORISATIONS[other],
@@ -440,6 +448,8 @@ def run_ours(args):
             "config": workload_config(args, world),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_in_region, "clocks": clocks,
+            "layers_us": {lay["cfg"].config_id.split("-")[1]: round(ms * 1e3, 2)
+                          for lay, ms in zip(layers, per_layer)},
             "alt_factorisation": alt,
         }))
     if world > 1:

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RBGP4_ABI_VERSION 1
+#define RBGP4_ABI_VERSION 2
 
 /* status codes */
 #define RBGP4_OK 0
@@ -83,15 +83,24 @@ int rbgp4_sdmm(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
                void *stream);
 
 /*
- * Per-matrix preparation for the tensor-core modes (optional, cacheable): the in-tile
- * scatter map of the densified W tile depends only on the chain and the tiling, so it
- * can be built once into a caller-owned device buffer of rbgp4_prepare_size() bytes and
- * passed to rbgp4_sdmm_prepared(), which then skips rebuilding it in every CTA.
- * Returns 0 size for the SIMT modes (nothing to prepare).
+ * Per-matrix preparation for the tensor-core modes (optional, cacheable), into a
+ * caller-owned device buffer of rbgp4_prepare_size() bytes passed to rbgp4_sdmm_prepared():
+ *  - the in-tile scatter map of the densified W tile (depends only on the chain and the
+ *    tiling), so CTAs skip rebuilding it;
+ *  - the step schedule: the order in which each tile-row walks its g_o neighbours, chosen
+ *    so that tile-rows sharing a K-block read its I slab at the same step (one L2 pass
+ *    over I instead of d_r(g_o)).  Changes only the fp32 summation order of the steps.
+ *  - (bf16, g_b >= 16 x 16) the values re-laid out by g_i column block: a permutation of
+ *    `values` (same bytes) in which the row blocks sharing a column block are contiguous,
+ *    so the gathered-block kernel covers each column block with one MMA.  `values` are the
+ *    device values of the product (bf16 for compute = BF16); other modes ignore them.
+ * The schedule is searched on the host from adj_o, so this call synchronises `stream`
+ * (once per matrix; it is not on the multiply path).  Returns 0 size for the SIMT modes.
+ * ABI v2: values and adj_o added (v1 took adj_i only).
  */
 size_t rbgp4_prepare_size(const rbgp4_desc *desc, int compute);
-int rbgp4_prepare(const rbgp4_desc *desc, int compute, const int32_t *adj_i, void *prep,
-                  size_t prep_bytes, void *stream);
+int rbgp4_prepare(const rbgp4_desc *desc, int compute, const void *values, const int32_t *adj_o,
+                  const int32_t *adj_i, void *prep, size_t prep_bytes, void *stream);
 
 /* rbgp4_sdmm with the prepared buffer of rbgp4_prepare (prep may be NULL). */
 int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,

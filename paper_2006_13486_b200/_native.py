@@ -13,6 +13,8 @@ import os
 from .errors import DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b200.so")
+# A/B experiments only (tools/): load another build of the same ABI
+LIB_PATH = os.environ.get("RBGP4_LIB_PATH", LIB_PATH)
 
 F32, F64, BF16 = 0, 1, 2
 COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
@@ -70,7 +72,7 @@ def lib():
     h.rbgp4_sdmm_prepared.restype = i32
     h.rbgp4_prepare_size.argtypes = [ctypes.POINTER(Desc), i32]
     h.rbgp4_prepare_size.restype = sz
-    h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, sz, vp]
+    h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, vp, sz, vp]
     h.rbgp4_prepare.restype = i32
     h.rbgp4_conv2d_workspace_size.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc)]
     h.rbgp4_conv2d_workspace_size.restype = sz

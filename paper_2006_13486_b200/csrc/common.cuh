@@ -57,7 +57,8 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
               const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *inp,
               void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream);
 size_t tc_prep_size(const ChainDims &c, int compute);
-int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep, size_t bytes,
+int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_t *adj_o, const int32_t *adj_i,
+               void *prep, size_t bytes,
                cudaStream_t stream);
 int tc_supported(const ChainDims &c, int compute, int out_dtype);
 size_t conv_workspace_size(const ChainDims &c, const rbgp4_conv_desc *cv);
@@ -65,5 +66,20 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
                 const int32_t *adj_o, const int32_t *adj_i, const void *prep, const void *x,
                 void *out, void *workspace, size_t workspace_bytes, cudaStream_t stream);
 size_t tc_workspace_size(const ChainDims &c, int compute);
+
+// K4: gathered-block tcgen05 launchers (sdmm_gather.cu); `k4` = the prepared relayout
+// section of rbgp4_prepare (null: direct mode on RcubsMatrix.values as stored)
+int gather_relayout_ok(const ChainDims &c);
+int gather_supported(const ChainDims &c, int compute, int out_dtype, bool relayout);
+int launch_gather(const ChainDims &c, int out_dtype, const void *values, const int32_t *adj_o,
+                  const int32_t *adj_i, const int32_t *sched, const int32_t *pair, const void *k4,
+                  const void *inp, void *out, cudaStream_t stream);
+int gather_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, bool relayout);
+int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,
+                       const int32_t *adj_o, const int32_t *adj_i, const int32_t *sched, const int32_t *pair,
+                       const void *k4, const void *x, void *out, cudaStream_t stream);
+size_t gather_prep_bytes(const ChainDims &c);
+int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_host, void *k4,
+                   cudaStream_t stream);
 
 }  // namespace rbgp4

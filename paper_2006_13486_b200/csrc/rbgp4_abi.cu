@@ -164,14 +164,14 @@ size_t rbgp4_prepare_size(const rbgp4_desc *desc, int compute) {
     return 0;
 }
 
-int rbgp4_prepare(const rbgp4_desc *desc, int compute, const int32_t *adj_i, void *prep,
-                  size_t prep_bytes, void *stream) {
+int rbgp4_prepare(const rbgp4_desc *desc, int compute, const void *values, const int32_t *adj_o,
+                  const int32_t *adj_i, void *prep, size_t prep_bytes, void *stream) {
     ChainDims c;
     int rc = validate_desc(desc, &c);
     if (rc != RBGP4_OK) return rc;
     if (compute != RBGP4_COMPUTE_TF32 && compute != RBGP4_COMPUTE_BF16) return RBGP4_OK;
-    RBGP4_REQUIRE(adj_i != nullptr, "null adj_i");
-    return tc_prepare(c, compute, adj_i, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+    RBGP4_REQUIRE(adj_o != nullptr && adj_i != nullptr, "null adjacency");
+    return tc_prepare(c, compute, values, adj_o, adj_i, prep, prep_bytes, static_cast<cudaStream_t>(stream));
 }
 
 size_t rbgp4_conv2d_workspace_size(const rbgp4_desc *desc, const rbgp4_conv_desc *conv) {

@@ -1,0 +1,807 @@
+// sdmm_gather.cu -- K4: the RBGP4 product on tcgen05 WITHOUT densification.
+//
+// Replaces kronsparse.sdmm._tile_worker (reference sdmm.py:148-205) for compute="bf16" when
+// the dense element blocks g_b are at least 16 x 16 (the tensor-core factorisations,
+// SURVEY §7 hard part 1).  Transposed formulation, per output tile (tile-row tbm of W,
+// 128 batch columns n0..n0+127):
+//
+//     D^T (128 batch cols x tm rows) += I^T (128 x tk) * W_tile^T (tk x tm)
+//
+// and the MMA shapes follow the graph product instead of a dense tile:
+//   M = 128 batch columns (the I slab's columns; MN-major A, 128B swizzle, as TMA lands it)
+//   N = bm output rows (one g_b row block ui of the tile-row)
+//   K = 16 input rows inside one g_b column block, i.e. the slab rows
+//       (adj_i[ui][ink] * bk + 16 kk) -- the gather is the descriptor's start address
+//   B = the compressed values of row block ui, slots (ink * bk + 16 kk): exactly the
+//       (rows x d_t) tile of RcubsMatrix.values (sorted-column order, rcubs.py:79-98),
+//       TMA-staged K-major with the 32/64/128-byte swizzle that matches its row length.
+// A step (one g_o neighbour of the tile-row, sdmm.py:167-176) is u_i * d_i * bk/16 MMAs;
+// no zero is ever multiplied, nothing is densified, and the only shared-memory traffic is
+// the TMA fill, the MMA operand reads and the epilogue staging.
+//
+// Warp roles (192 threads): warps 0-3 epilogue (TMEM lanes 32w.. = batch columns), warp 4
+// TMA producer (I slab + W tile of a step on ONE mbarrier), warp 5 TMEM allocation + MMA
+// issue.  Ring of ns stages, one full / one empty barrier each: the producer of step s waits
+// for the MMA commit of step s - ns.  Split-K (small N): the steps of a tile are cut into
+// ksplit slices run by the CTAs of one cluster; slices > 0 park their fp32 tile in their own
+// shared memory and the leader adds them over DSMEM in fixed slice order (deterministic).
+//
+// Implicit-im2col convolution (K3 on this kernel): A is the NHWC pixel x channel tile of the
+// tap-shifted 4-D TMA box (K-major, 128B swizzle), O is NHWC.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+namespace rbgp4 {
+namespace {
+
+constexpr int kGThreads = 192;
+
+// Debug trace (RBGP4_TC_DEBUG bit 8): CTA (0,0,0) stamps clock64 per step:
+// [0] producer issued, [1] MMA saw full, [2] MMA issue done; [3][0..3] setup / epilogue marks
+constexpr int kGTraceSteps = 256;
+__device__ unsigned long long g_gtrace[4][kGTraceSteps];
+__device__ __forceinline__ void gtrace(int debug, int ev, int step) {
+    if ((debug & 8) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && step < kGTraceSteps)
+        g_gtrace[ev][step] = clock64();
+}
+constexpr int kBatch = 128;  // MMA M: batch columns (or pixels) per CTA
+constexpr int kMaxMma = 256; // MMAs per step (u_i * d_i * bk / 16)
+
+struct GParams {
+    int64_t n_cols, ld_out;
+    int32_t tm, tk, d_o, d_t, u_i, d_i, bm, bk;
+    int32_t ns;                 // ring stages
+    int32_t i_bytes, w_bytes;   // per stage
+    int32_t w_swz;              // W row bytes = swizzle span (32 / 64 / 128)
+    int32_t ksplit, sps;        // split-K slices (cluster z) and steps per slice
+    int32_t tmem_cols;
+    int32_t debug;
+    const int32_t *sched;       // step schedule (rbgp4_prepare) or null
+    // relayout mode (rbgp4_prepare): W tiles re-laid out by g_i column block, one MMA of
+    // N = d_r * bm per column block into its own TMEM columns; cols[ui][ink] = TMEM column of
+    // row block ui's partial for its ink-th neighbour (summed in the epilogue)
+    const int32_t *cols;
+    int32_t d_r, mma_n, w_rows;  // users per column block, MMA N, W tile rows per step
+    // multicast pairs (rbgp4_prepare): the u_o tile-rows of a column block form one cluster;
+    // pair[tbm][s] = the tile-row reading the same I slab at step s (or -1).  Paired CTAs each
+    // fetch one 64-column atom of the slab and multicast it to both, so L2 streams I once.
+    const int32_t *pair;
+    int32_t mc;
+    // implicit-im2col convolution
+    int32_t conv, c_in, img_h, img_w, kw, pad, relu;
+};
+
+template <bool OUT_BF16, bool CONV>
+__global__ void __launch_bounds__(kGThreads, 2)
+gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
+              const __grid_constant__ CUtensorMap omap, const GParams p,
+              const int32_t *__restrict__ adj_o, const int32_t *__restrict__ adj_i) {
+    extern __shared__ unsigned char smem_raw[];
+    // MMA table, one uint2 per MMA of a step: x = A offset | B offset << 16 (16-byte units,
+    // relative to the stage), y = TMEM column of D | 1 << 31 on the first MMA into it
+    __shared__ uint2 mma_tab[kMaxMma];
+    unsigned char *ring = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = p.i_bytes + p.w_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + size_t(p.ns) * stage_bytes);
+    uint64_t *empty = full + p.ns;
+    uint64_t *tmem_full = empty + p.ns;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) gtrace(p.debug, 3, 0);
+    const int64_t n0 = int64_t(blockIdx.x) * kBatch;
+    const int tbm = blockIdx.y;
+    const int64_t m0 = int64_t(tbm) * p.tm;
+    const int kslice = blockIdx.z;
+    const int s_begin = kslice * p.sps;
+    const int nsteps = min(p.d_o, s_begin + p.sps) - s_begin;
+    const int32_t *orow = adj_o + int64_t(tbm) * p.d_o;
+    const int32_t *srow = p.sched ? p.sched + int64_t(tbm) * p.d_o + s_begin : nullptr;
+    const int32_t *prow = p.mc ? p.pair + int64_t(tbm) * p.d_o : nullptr;
+
+    if (warp == 4 && lane == 0) {
+        // empty[st] of step s completes on two arrivals in multicast mode: this CTA's release
+        // of the slot and its step-s partner's (or this CTA's commit twice when unpaired)
+        for (int i = 0; i < p.ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], p.mc ? 2 : 1); }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+    }
+    const int kk_n = p.bk / 16;
+    const int v_blocks = p.cols ? p.u_i * p.d_i / p.d_r : 0;  // g_i column blocks (relayout)
+    const int n_mma = (p.cols ? v_blocks : p.u_i * p.d_i) * kk_n;
+    if (warp == 5) {
+        // the in-tile gather pattern g_i (x) g_b is the same for every step and tile-row
+        // (sdmm.py:183-186).  Direct mode: MMA (ui, ink, kk) reads slab rows
+        // adj_i[ui][ink]*bk + 16kk and compressed slots ink*bk + 16kk of row block ui.
+        // Relayout mode: MMA (kb, kk) reads slab rows kb*bk + 16kk once for all d_r row
+        // blocks that use column block kb (their rows are contiguous in the re-laid tile).
+        for (int i = lane; i < n_mma; i += 32) {
+            const int kk = i % kk_n;
+            int krow, b_row, slot, dcol;
+            if (p.cols) {
+                const int kb = i / kk_n;
+                krow = kb * p.bk + 16 * kk;
+                b_row = kb * p.d_r * p.bm;
+                slot = 16 * kk;
+                dcol = b_row;
+            } else {
+                const int ink = (i / kk_n) % p.d_i, ui = i / (kk_n * p.d_i);
+                krow = adj_i[ui * p.d_i + ink] * p.bk + 16 * kk;
+                b_row = ui * p.bm;
+                slot = ink * p.bk + 16 * kk;
+                dcol = ui * p.bm;
+            }
+            const uint32_t a_off = CONV ? uint32_t((krow / 64) * (kBatch * 128) + (krow % 64) * 2)
+                                        : uint32_t(krow * 128);
+            const uint32_t b_off = uint32_t(p.i_bytes + b_row * p.w_swz + slot * 2);
+            mma_tab[i] = make_uint2((a_off >> 4) | ((b_off >> 4) << 16),
+                                    uint32_t(dcol) | ((kk == 0 && (p.cols || slot == 0)) ? 0x80000000u : 0u));
+        }
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (p.mc) {
+        // peers must see the initialised barriers before any multicast lands or arrives
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 0) gtrace(p.debug, 3, 1);
+
+    if (warp == 4) {
+        // ================= TMA producer: I slab + W tile of each step, one barrier ======
+        for (int s = 0; s < nsteps; ++s) {
+            const int st = s % p.ns;
+            mbar_wait(&empty[st], ((s / p.ns) & 1) ^ 1);
+            const int j = srow ? srow[s] : s_begin + s;  // g_o adjacency slot of this step
+            const int32_t krow = orow[j] * p.tk;
+            const bool leader = elect_one();
+            if (leader && (p.debug & 128)) {
+                mbar_arrive(&full[st]);  // ablation: no loads (MMA / pipeline skeleton only)
+                gtrace(p.debug, 0, s);
+            } else if (leader) {
+                mbar_expect_tx(&full[st], uint32_t(stage_bytes));
+                unsigned char *dst = ring + size_t(st) * stage_bytes;
+                if constexpr (CONV) {
+                    // K rows [krow, krow + tk) = tap (i, j), channels [c0, c0 + tk): per 64-channel
+                    // atom one 4-D box of 128 pixels (rows of the map, tap-shifted; OOB = padding)
+                    const int tap = krow / p.c_in, c0 = krow - tap * p.c_in;
+                    const int ti = tap / p.kw, tj = tap - ti * p.kw;
+                    const int hw = p.img_h * p.img_w;
+                    const int b0 = int(n0 / hw), h0 = int(n0 % hw) / p.img_w;
+                    const int pb = p.mc ? prow[s] : -1;
+                    for (int a = 0; a < p.tk / 64; ++a) {
+                        if (pb >= 0) {  // paired: channel atoms alternate between the two CTAs
+                            if ((a & 1) != (tbm < pb ? 0 : 1)) continue;
+                            tma_load_4d_mc(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
+                                           tj - p.pad, h0 + ti - p.pad, b0, uint16_t((1u << tbm) | (1u << pb)));
+                        } else {
+                            tma_load_4d(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
+                                        tj - p.pad, h0 + ti - p.pad, b0);
+                        }
+                    }
+                } else if (p.mc) {
+                    // one-atom boxes (64 cols x tk rows); paired: fetch atom h for both CTAs
+                    const int pb = prow[s];
+                    if (pb >= 0) {
+                        const int h = tbm < pb ? 0 : 1;
+                        tma_load_3d_mc(dst + h * p.tk * 128, &imap, &full[st], 0, krow, int32_t(n0 / 64) + h,
+                                       uint16_t((1u << tbm) | (1u << pb)));
+                    } else {
+                        tma_load_3d(dst, &imap, &full[st], 0, krow, int32_t(n0 / 64));
+                        tma_load_3d(dst + p.tk * 128, &imap, &full[st], 0, krow, int32_t(n0 / 64) + 1);
+                    }
+                } else {
+                    // (64 cols, tk rows, 2 atoms) box: MN-major, atom-major in shared memory
+                    tma_load_3d(dst, &imap, &full[st], 0, krow, int32_t(n0 / 64));
+                }
+                if (p.cols)  // re-laid tiles: (bk, rows) view, tile (tbm, j) = w_rows rows
+                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
+                else
+                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, int32_t(m0));
+                gtrace(p.debug, 0, s);
+            }
+            __syncwarp();
+        }
+    } else if (warp == 5) {
+        // ================= MMA issuer =================
+        const uint32_t tmem_d = *tmem_slot;
+        // idesc: D f32, A/B bf16, A MN-major (SDMM: I slab) or K-major (conv: NHWC tile),
+        // B K-major (compressed W rows), N = bm, M = 128
+        const uint32_t a_mn = CONV ? 0u : 1u;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (0u << 16) |
+                               (uint32_t(p.mma_n >> 3) << 17) | (uint32_t(kBatch >> 4) << 24);
+        const uint32_t ring_a = smem_u32(ring);
+        const uint32_t w_code = p.w_swz == 128 ? 2u : p.w_swz == 64 ? 4u : 6u;
+        // descriptors of stage 0; a stage / table entry only moves the 14-bit start field
+        const uint64_t a_desc0 = CONV ? smem_desc(ring_a, 0, 1024, 2u)
+                                      : smem_desc(ring_a, uint32_t(p.tk) * 128, 1024, 2u);
+        const uint64_t b_desc0 = smem_desc(ring_a, 0, 8 * p.w_swz, w_code);
+        // up to kRegMma table entries live in registers for the whole kernel (plain shared
+        // loads the compiler can hoist); larger patterns stream the table from shared memory
+        constexpr int kRegMma = 32;
+        uint32_t rx[kRegMma], ry[kRegMma];
+#pragma unroll
+        for (int i = 0; i < kRegMma; ++i) {
+            const uint2 e = i < n_mma ? mma_tab[i] : make_uint2(0, 0);
+            rx[i] = e.x;
+            ry[i] = e.y;
+        }
+        const bool in_regs = n_mma <= kRegMma;
+        const bool no_mma = p.debug & 2;
+        for (int s = 0; s < nsteps; ++s) {
+            const int st = s % p.ns;
+            mbar_wait(&full[st], (s / p.ns) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                gtrace(p.debug, 1, s);
+                const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
+                const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
+                if (no_mma) {
+                } else if (p.cols) {
+                    // relayout: every descriptor is uniform arithmetic of (kb, kk) -- no table,
+                    // no register-to-uniform moves on the issue path
+                    const uint32_t n_blk = uint32_t(p.d_r * p.bm);
+                    const uint32_t b_blk16 = (n_blk * uint32_t(p.w_swz)) >> 4;
+                    uint64_t bd = b_st + (uint32_t(p.i_bytes) >> 4);
+                    uint32_t dcol = tmem_d;
+                    for (int kb = 0; kb < v_blocks; ++kb) {
+                        for (int kk = 0; kk < kk_n; ++kk) {
+                            const uint32_t krow = uint32_t(kb * p.bk + 16 * kk);
+                            const uint32_t a16 = CONV ? (((krow >> 6) * (kBatch * 128)) + (krow & 63) * 2) >> 4
+                                                      : krow * 8;  // krow * 128 bytes
+                            tc_mma<false>(dcol, a_st + a16, bd + uint32_t(2 * kk), idesc,
+                                          (s > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        bd += b_blk16;
+                        dcol += n_blk;
+                    }
+                } else if (in_regs) {
+#pragma unroll
+                    for (int i = 0; i < kRegMma; ++i)
+                        if (i < n_mma)
+                            tc_mma<false>(tmem_d + (ry[i] & 0xFFFFu), a_st + (rx[i] & 0xFFFFu), b_st + (rx[i] >> 16),
+                                          idesc, (s > 0 || !(ry[i] >> 31)) ? 1u : 0u);
+                } else {
+                    for (int i = 0; i < n_mma; ++i) {
+                        const uint2 e = mma_tab[i];
+                        tc_mma<false>(tmem_d + (e.y & 0xFFFFu), a_st + (e.x & 0xFFFFu), b_st + (e.x >> 16), idesc,
+                                      (s > 0 || !(e.y >> 31)) ? 1u : 0u);
+                    }
+                }
+                if (p.mc) {
+                    // release slot st for step s + ns to the CTAs that will fill it: this one and
+                    // its step-(s + ns) partner
+                    const int sn = s + p.ns;
+                    const int pb = sn < nsteps ? prow[sn] : -1;
+                    if (pb >= 0) {
+                        tc_commit_mc(&empty[st], uint16_t((1u << tbm) | (1u << pb)));
+                    } else {
+                        tc_commit(&empty[st]);
+                        tc_commit(&empty[st]);
+                    }
+                } else {
+                    tc_commit(&empty[st]);
+                }
+                gtrace(p.debug, 2, s);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) tc_commit(tmem_full);
+        __syncwarp();
+    } else {
+        // ================= epilogue (warps 0-3): TMEM lane = batch column =================
+        if (p.debug & 64) mbar_wait(tmem_full, 0);
+        else mbar_wait_sleep(tmem_full, 0, 256);
+        tc_fence_after();
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 2);
+    }
+
+    const uint32_t tmem_d = *tmem_slot;
+    const uint32_t ring_a = smem_u32(ring);
+    const int t = warp * 32 + lane;  // batch column inside the tile (warps 0-3)
+    const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
+    // output rows c..c+31 of this thread's batch column: direct mode reads the accumulator
+    // columns as they are; relayout mode sums each row block's d_i partial accumulators
+    auto load_rows = [&](int c, uint32_t (&r)[32]) {
+        if (!p.cols) {
+            TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            return;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int row = c + 16 * h, ui = row / p.bm, m = row % p.bm;
+            float acc[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] = 0.0f;
+            for (int ink = 0; ink < p.d_i; ++ink) {
+                uint32_t v[16];
+                TMEM_LD_32x32b_X16(lane_base + uint32_t(p.cols[ui * p.d_i + ink] + m), v);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int q = 0; q < 16; ++q) acc[q] += __uint_as_float(v[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[16 * h + q] = __float_as_uint(acc[q]);
+        }
+    };
+    if (p.ksplit > 1) {
+        // slices > 0: fp32 partial tile -> own shared memory [row][128 cols] (the ring is idle)
+        if (kslice > 0 && warp < 4) {
+            for (int c = 0; c < p.tm; c += 32) {
+                uint32_t r[32];
+                load_rows(c, r);
+#pragma unroll
+                for (int q = 0; q < 32; ++q) sts32(ring_a + uint32_t(((c + q) * kBatch + t) * 4), r[q]);
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    if (kslice == 0 && warp < 4 && !(p.debug & 4)) {
+        constexpr int kOutElt = OUT_BF16 ? 2 : 4;
+        for (int c = 0; c < p.tm; c += 32) {
+            uint32_t r[32];
+            load_rows(c, r);
+            for (int k = 1; k < p.ksplit; ++k) {
+                // peer slice k's partial, same offsets in its shared memory (DSMEM)
+                uint32_t peer;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(ring_a), "r"(k));
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    float v;
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v)
+                                 : "r"(peer + uint32_t(((c + q) * kBatch + t) * 4)));
+                    r[q] = __float_as_uint(__uint_as_float(r[q]) + v);
+                }
+            }
+            if constexpr (CONV) {
+                // NHWC: pixel t holds channels c..c+31 -> 4 x 16-byte chunks of its 128-byte
+                // rows in 64-channel atoms [atom][pixel][128 B], 128B-swizzled (chunk ^ pixel%8)
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    if (p.relu) r[q] = __float_as_uint(fmaxf(__uint_as_float(r[q]), 0.0f));
+                if constexpr (OUT_BF16) {
+                    const uint32_t atom = ring_a + uint32_t((c / 64) * (kBatch * 128) + t * 128);
+                    const uint32_t ch0 = uint32_t(c % 64) / 8;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * h]),
+                                                                      __uint_as_float(r[q * 8 + 2 * h + 1]));
+                            w[h] = *reinterpret_cast<uint32_t *>(&b2);
+                        }
+                        sts128(atom + (((ch0 + q) ^ uint32_t(t & 7)) << 4), w[0], w[1], w[2], w[3]);
+                    }
+                } else {
+                    const uint32_t atom = ring_a + uint32_t((c / 32) * (kBatch * 128) + t * 128);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        sts128(atom + ((uint32_t(q) ^ uint32_t(t & 7)) << 4), r[4 * q], r[4 * q + 1],
+                               r[4 * q + 2], r[4 * q + 3]);
+                }
+            } else {
+                // row-major O: column t of rows c..c+31 -> [atom of 128/elt cols][row][128 B],
+                // 128B-swizzled (chunk ^ row%8); lanes = consecutive columns
+                constexpr int kAtomCols = 128 / kOutElt;
+                const uint32_t atom = ring_a + uint32_t((t / kAtomCols) * (p.tm * 128));
+                const uint32_t cb = uint32_t(t % kAtomCols) * kOutElt;  // byte inside the row
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const uint32_t row = uint32_t(c + q);
+                    const uint32_t addr = atom + row * 128 + ((((cb >> 4) ^ (row & 7))) << 4) + (cb & 15);
+                    if constexpr (OUT_BF16) {
+                        const __nv_bfloat16 b = __float2bfloat16_rn(__uint_as_float(r[q]));
+                        sts16(addr, *reinterpret_cast<const uint16_t *>(&b));
+                    } else {
+                        sts32(addr, r[q]);
+                    }
+                }
+            }
+        }
+        fence_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 0 && elect_one()) {
+            if constexpr (CONV) {
+                constexpr int kAtomCh = 128 / kOutElt;
+                for (int a = 0; a < p.tm / kAtomCh; ++a)
+                    tma_store_2d(&omap, ring + a * (kBatch * 128), int32_t(m0) + a * kAtomCh, int32_t(n0));
+            } else {
+                constexpr int kAtomCols = 128 / kOutElt;
+                for (int a = 0; a < kBatch / kAtomCols; ++a)
+                    tma_store_2d(&omap, ring + a * (p.tm * 128), int32_t(n0) + a * kAtomCols, int32_t(m0));
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncwarp();
+    }
+    if (threadIdx.x == 0) gtrace(p.debug, 3, 3);
+    if (p.ksplit > 1 || p.mc) {
+        // peers keep their shared memory alive until the leader has read it
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                     "r"(uint32_t(p.tmem_cols)));
+    }
+}
+
+constexpr size_t kGSmemCap = 227 * 1024;
+
+struct GPlan {
+    GParams p;
+    size_t smem;
+    dim3 grid;
+};
+
+CUtensorMapSwizzle swizzle_of(int span) {
+    return span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : span == 64  ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+}
+
+}  // namespace
+
+// Shapes K4 takes: bf16, g_r = (1,1), g_b blocks of >= 16 x 16 (multiples of 16), a tile-row
+// of <= 256 rows (a multiple of 32), I slabs of <= 256 rows.  Direct mode needs one compressed
+// W row to be a swizzle span (32/64/128 bytes); relayout mode (prepared values) needs g_i
+// biregular, tm * d_i <= 256 (W tile rows per step = TMEM columns) and bk * 2 a span.
+int gather_relayout_ok(const ChainDims &c) {
+    if (c.rm != 1 || c.rk != 1 || c.bm % 16 || c.bk % 16 || c.tm % 32 || c.tm > 256) return 0;
+    if ((c.u_i * c.d_i) % c.v_i) return 0;
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    const int span = c.bk * 2;
+    if (span != 32 && span != 64 && span != 128) return 0;
+    if (c.tm * c.d_i > 256 || d_r * c.bm > 256) return 0;
+    // opt-in: one N = d_r*bm MMA per column block halves the MMA count, but the epilogue's
+    // d_i-way partial sums cost more than that saves on the VGG shapes (measured)
+    return getenv("RBGP4_TC_RELAYOUT") ? 1 : 0;
+}
+
+int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan *out, bool pairs = false) {
+    if (compute != RBGP4_COMPUTE_BF16) return 0;
+    if (getenv("RBGP4_TC_DENSE")) return 0;  // A/B switch: force the densify kernel (K2)
+    if (c.rm != 1 || c.rk != 1 || c.bm % 16 || c.bk % 16 || c.tm % 32 || c.tm > 256 || c.tk > 256) return 0;
+    if (relayout && !gather_relayout_ok(c)) return 0;
+    const int w_row = relayout ? c.bk * 2 : c.d_t * 2;
+    if (w_row != 32 && w_row != 64 && w_row != 128) return 0;
+    if (conv && c.tk % 64) return 0;
+    GParams p{};
+    p.n_cols = c.n_cols; p.ld_out = c.ld_out;
+    p.tm = c.tm; p.tk = c.tk; p.d_o = c.d_o; p.d_t = c.d_t; p.u_i = c.u_i; p.d_i = c.d_i;
+    p.bm = c.bm; p.bk = c.bk;
+    p.d_r = relayout ? c.u_i * c.d_i / c.v_i : 1;
+    p.mma_n = relayout ? p.d_r * c.bm : c.bm;
+    p.w_rows = relayout ? c.tm * c.d_i : c.tm;
+    const int n_mma = (relayout ? c.v_i : c.u_i * c.d_i) * (c.bk / 16);
+    if (n_mma > kMaxMma) return 0;
+    p.i_bytes = c.tk * kBatch * 2;
+    p.w_bytes = p.w_rows * w_row;  // = tm * d_t * 2 either way
+    p.w_swz = w_row;
+    const size_t stage = size_t(p.i_bytes) + p.w_bytes;
+    const size_t fixed = 1024 + 8 * (2 * 16 + 1) + 16 + 64 + size_t(kMaxMma) * 8;  // + static table
+    const int64_t col_blocks = (c.n_cols + kBatch - 1) / kBatch;
+    const int64_t tiles = col_blocks * c.u_o;
+    // Occupancy: a CTA's steps are a serial latency chain (load -> MMA issue -> commit), so
+    // when one tile per SM would leave SMs idle, the steps of a tile are split over a cluster
+    // (DSMEM reduction) and two CTAs share an SM with 2-stage rings (measured on the VGG
+    // shapes: 2 CTAs/SM x 2 stages beats 1 CTA/SM x 5 stages).  Large grids keep 1 CTA/SM
+    // with the deepest ring that fits.
+    int ks = 1;
+    bool dual = false;
+    if (tiles < kNumSMs) {
+        // (more than 4 slices measured slower: the DSMEM reduction grows with the slices)
+        while (ks < 4 && tiles * ks * 2 <= 2 * kNumSMs && c.d_o >= ks * 2 * 2) ks *= 2;
+        dual = tiles * ks > kNumSMs;
+    }
+    if (const char *e = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(e)));
+    int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed) / stage));
+    if (const char *e = getenv("RBGP4_TC_NS")) ns = std::max(2, std::min(16, atoi(e)));
+    if (fixed + size_t(ns) * stage > kGSmemCap) return 0;
+    p.ns = ns;
+    p.tmem_cols = 32;
+    while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm)) p.tmem_cols *= 2;
+    p.sps = (c.d_o + ks - 1) / ks;
+    p.ksplit = (c.d_o + p.sps - 1) / p.sps;
+    if (const char *e = getenv("RBGP4_TC_DEBUG")) p.debug = atoi(e);
+    // multicast pairs: the u_o tile-rows of a column block as one cluster (<= 8 portable)
+    // (SDMM slabs are two 64-column atoms; conv slabs must have an even number of channel atoms)
+    p.mc = (pairs && p.ksplit == 1 && c.u_o >= 2 && c.u_o <= 8 && (!conv || (c.tk / 64) % 2 == 0) &&
+            !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
+    out->p = p;
+    out->smem = fixed + size_t(ns) * stage;
+    out->grid = dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.ksplit));
+    return 1;
+}
+
+// ---------------------------------------------------------------- prepared relayout
+// prepared K4 section: [cols i32 u_i x d_i][users i32 v_i x d_r x 2][values bf16 u_o x d_o x tm x d_t]
+// Tile (tbm, j) of the re-laid values lists, for each g_i column block kb, its d_r user row
+// blocks (ascending) x bm rows x bk slots: value(kb, u, m, k) = W[tbm*tm + ui*bm + m]
+// [j*d_t + ink*bk + k] with (ui, ink) = users[kb][u].  A permutation of RcubsMatrix.values
+// (same bytes, still the succinct format), so one MMA covers a column block.
+namespace {
+size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+__global__ void relayout_kernel(const __nv_bfloat16 *__restrict__ values, int64_t row_nnz, int tm, int d_t,
+                                int d_o, int bm, int bk, int d_r, const int32_t *__restrict__ users,
+                                int64_t total, __nv_bfloat16 *__restrict__ out) {
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t tile = idx / (int64_t(tm) * d_t);
+        const int r = int(idx - tile * tm * d_t);
+        const int k = r % bk, m = (r / bk) % bm, u = (r / (bk * bm)) % d_r, kb = r / (bk * bm * d_r);
+        const int tbm = int(tile / d_o), j = int(tile % d_o);
+        const int ui = users[(kb * d_r + u) * 2], ink = users[(kb * d_r + u) * 2 + 1];
+        out[idx] = values[(int64_t(tbm) * tm + ui * bm + m) * row_nnz + int64_t(j) * d_t + ink * bk + k];
+    }
+}
+}  // namespace
+
+size_t gather_prep_bytes(const ChainDims &c) {
+    if (!gather_relayout_ok(c)) return 0;
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    return a16(size_t(c.u_i) * c.d_i * 4) + a16(size_t(c.v_i) * d_r * 8) + size_t(c.rows) * c.row_nnz * 2;
+}
+
+void gather_prep_views(const ChainDims &c, const void *k4, const int32_t **cols, const void **vals) {
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    *cols = static_cast<const int32_t *>(k4);
+    *vals = static_cast<const char *>(k4) + a16(size_t(c.u_i) * c.d_i * 4) + a16(size_t(c.v_i) * d_r * 8);
+}
+
+int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_host, void *k4,
+                   cudaStream_t stream) {
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    std::vector<int32_t> cols(size_t(c.u_i) * c.d_i), users(size_t(c.v_i) * d_r * 2, -1);
+    std::vector<int> fill(c.v_i, 0);
+    for (int ui = 0; ui < c.u_i; ++ui)
+        for (int ink = 0; ink < c.d_i; ++ink) {
+            const int kb = adj_i_host[ui * c.d_i + ink];
+            if (kb < 0 || kb >= c.v_i || fill[kb] >= d_r) {
+                set_error("gather relayout: g_i is not biregular (column %d)", kb);
+                return RBGP4_EINVAL;
+            }
+            const int u = fill[kb]++;
+            users[(size_t(kb) * d_r + u) * 2] = ui;
+            users[(size_t(kb) * d_r + u) * 2 + 1] = ink;
+            cols[size_t(ui) * c.d_i + ink] = (kb * d_r + u) * c.bm;  // TMEM column of the partial
+        }
+    const int32_t *cols_d;
+    const void *vals_d;
+    gather_prep_views(c, k4, &cols_d, &vals_d);
+    int32_t *users_d = reinterpret_cast<int32_t *>(static_cast<char *>(k4) + a16(size_t(c.u_i) * c.d_i * 4));
+    cudaError_t e = cudaMemcpyAsync(const_cast<int32_t *>(cols_d), cols.data(), cols.size() * 4,
+                                    cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(users_d, users.data(), users.size() * 4, cudaMemcpyHostToDevice, stream);
+    const int64_t total = c.rows * c.row_nnz;
+    if (e == cudaSuccess) {
+        relayout_kernel<<<int(std::min<int64_t>((total + 255) / 256, 4 * kNumSMs)), 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, c.bm, c.bk, d_r,
+            users_d, total, static_cast<__nv_bfloat16 *>(const_cast<void *>(vals_d)));
+        e = cudaGetLastError();
+        if (e == cudaSuccess) note_launch();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // host tables are temporaries
+    if (e != cudaSuccess) {
+        set_error("gather relayout: %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    return RBGP4_OK;
+}
+
+namespace {
+template <bool OUT_BF16, bool CONV>
+int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensorMap &wmap,
+                        const CUtensorMap &omap, const int32_t *adj_o, const int32_t *adj_i,
+                        cudaStream_t stream) {
+    auto kern = gather_kernel<OUT_BF16, CONV>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(gather): %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = pl.grid;
+    cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = pl.p.mc ? pl.grid.y : 1;
+    attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);
+    cfg.attrs = attr;
+    cfg.numAttrs = (pl.p.ksplit > 1 || pl.p.mc) ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, pl.p, adj_o, adj_i);
+    if (e != cudaSuccess) {
+        set_error("gather_kernel launch (grid %u x %u x %u, smem %zu): %s", pl.grid.x, pl.grid.y,
+                  pl.grid.z, pl.smem, cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    RBGP4_CHECK_LAUNCH("gather_kernel launch");
+    return RBGP4_OK;
+}
+
+int encode_w_map(CUtensorMap *wmap, const ChainDims &c, const GParams &p, const void *values) {
+    auto enc = encode_fn();
+    cuuint64_t wdims[2], wstrides[1];
+    cuuint32_t wbox[2];
+    if (p.cols) {  // re-laid tiles: (bk, u_o * d_o * w_rows)
+        wdims[0] = cuuint64_t(c.bk); wdims[1] = cuuint64_t(c.u_o) * c.d_o * p.w_rows;
+        wstrides[0] = cuuint64_t(c.bk) * 2;
+        wbox[0] = cuuint32_t(c.bk); wbox[1] = cuuint32_t(p.w_rows);
+    } else {       // RcubsMatrix.values as stored: (row_nnz, rows)
+        wdims[0] = cuuint64_t(c.row_nnz); wdims[1] = cuuint64_t(c.rows);
+        wstrides[0] = cuuint64_t(c.row_nnz) * 2;
+        wbox[0] = cuuint32_t(c.d_t); wbox[1] = cuuint32_t(c.tm);
+    }
+    cuuint32_t estr[2] = {1, 1};
+    if (reinterpret_cast<uintptr_t>(values) % 16 != 0 || wstrides[0] % 16 != 0) {
+        set_error("gather path needs 16-byte aligned values rows");
+        return RBGP4_EUNSUPPORTED;
+    }
+    CUresult r = enc(wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(values), wdims, wstrides,
+                     wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_of(p.w_swz),
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));
+        return RBGP4_ECUDA;
+    }
+    return RBGP4_OK;
+}
+}  // namespace
+
+int launch_gather(const ChainDims &c, int out_dtype, const void *values, const int32_t *adj_o,
+                  const int32_t *adj_i, const int32_t *sched, const int32_t *pair, const void *k4,
+                  const void *inp, void *out, cudaStream_t stream) {
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    GPlan pl;
+    if (!gather_plan(c, RBGP4_COMPUTE_BF16, false, k4 != nullptr, &pl, pair != nullptr)) return RBGP4_EUNSUPPORTED;
+    pl.p.sched = sched;
+    pl.p.pair = pair;
+    if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return RBGP4_ECUDA;
+    }
+    RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(inp) % 16 == 0 && (c.ld_in * 2) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(out) % 16 == 0 && (c.ld_out * oelt) % 16 == 0,
+                  "gather path needs 16-byte aligned I / O rows");
+    CUtensorMap imap, wmap, omap;
+    cuuint32_t estr[3] = {1, 1, 1};
+    {
+        // I as (64 cols, K rows, N/64 atoms): one box = a whole 128-column slab, atom-major
+        cuuint64_t dims[3] = {64, cuuint64_t(c.cols), cuuint64_t((c.n_cols + 63) / 64)};
+        cuuint64_t strides[2] = {cuuint64_t(c.ld_in) * 2, 128};
+        cuuint32_t box[3] = {64, cuuint32_t(c.tk), pl.p.mc ? 1u : 2u};
+        if (c.n_cols % 64) {
+            // ragged last atom: a 2-atom view would read past the row; fall back to the
+            // column-exact 2-D view with one box per atom (OOB columns zero-filled)
+            set_error("gather path: n_cols %% 64 != 0");
+            return RBGP4_EUNSUPPORTED;
+        }
+        CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(inp), dims, strides,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(I) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    if (int rc = encode_w_map(&wmap, c, pl.p, values)) return rc;
+    {
+        cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
+        cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
+        cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(c.tm)};
+        CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         2, out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(O) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    return oelt == 2 ? gather_launch_typed<true, false>(pl, imap, wmap, omap, adj_o, adj_i, stream)
+                     : gather_launch_typed<false, false>(pl, imap, wmap, omap, adj_o, adj_i, stream);
+}
+
+int gather_supported(const ChainDims &c, int compute, int out_dtype, bool relayout) {
+    GPlan pl;
+    (void)out_dtype;
+    return c.n_cols % 64 == 0 && gather_plan(c, compute, false, relayout, &pl);
+}
+
+int gather_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, bool relayout) {
+    GPlan pl;
+    if (!gather_plan(c, RBGP4_COMPUTE_BF16, true, relayout, &pl)) return 0;
+    const int hw = cv->height * cv->width;
+    // a 128-pixel tile = whole rows of one image, or whole images
+    const bool tiles = (kBatch <= hw) ? (hw % kBatch == 0 && kBatch % cv->width == 0) : (kBatch % hw == 0);
+    return tiles && cv->c_in % 64 == 0 && cv->c_in % c.tk == 0 && cv->stride == 1 &&
+           (c.rows * (out_dtype == RBGP4_BF16 ? 2 : 4)) % 16 == 0;
+}
+
+int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,
+                       const int32_t *adj_o, const int32_t *adj_i, const int32_t *sched, const int32_t *pair,
+                       const void *k4, const void *x, void *out, cudaStream_t stream) {
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    GPlan pl;
+    if (!gather_plan(c, RBGP4_COMPUTE_BF16, true, k4 != nullptr, &pl, pair != nullptr)) return RBGP4_EUNSUPPORTED;
+    pl.p.sched = sched;
+    pl.p.pair = pair;
+    if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
+    pl.p.conv = 1;
+    pl.p.c_in = cv->c_in;
+    pl.p.img_h = cv->height;
+    pl.p.img_w = cv->width;
+    pl.p.kw = cv->kw;
+    pl.p.pad = cv->pad;
+    pl.p.relu = cv->relu;
+    auto enc = encode_fn();
+    RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0,
+                  "conv input / output must be 16-byte aligned");
+    const int hw = cv->height * cv->width;
+    const int th = kBatch <= hw ? kBatch / cv->width : cv->height;
+    const int tb = kBatch <= hw ? 1 : kBatch / hw;
+    CUtensorMap imap, wmap, omap;
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    {
+        cuuint64_t dims[4] = {cuuint64_t(cv->c_in), cuuint64_t(cv->width), cuuint64_t(cv->height),
+                              cuuint64_t(cv->batch)};
+        cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
+                                 cuuint64_t(hw) * cv->c_in * 2};
+        cuuint32_t box[4] = {64, cuuint32_t(cv->width), cuuint32_t(th), cuuint32_t(tb)};
+        CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(conv input) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    if (int rc = encode_w_map(&wmap, c, pl.p, values)) return rc;
+    {
+        // NHWC output as (c_out, pixels): box = one 128-byte channel atom x 128 pixels
+        cuuint64_t odims[2] = {cuuint64_t(c.rows), cuuint64_t(c.n_cols)};
+        cuuint64_t ostrides[1] = {cuuint64_t(c.rows) * oelt};
+        cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(kBatch)};
+        CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         2, out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(conv output) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    return oelt == 2 ? gather_launch_typed<true, true>(pl, imap, wmap, omap, adj_o, adj_i, stream)
+                     : gather_launch_typed<false, true>(pl, imap, wmap, omap, adj_o, adj_i, stream);
+}
+
+}  // namespace rbgp4
+
+// debug-only (not part of include/rbgp4.h): copy the K4 CTA-0 trace to the host
+extern "C" int rbgp4_debug_trace_gather(unsigned long long *host, int n) {
+    if (n > 4 * rbgp4::kGTraceSteps) n = 4 * rbgp4::kGTraceSteps;
+    return cudaMemcpyFromSymbol(host, rbgp4::g_gtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
+}

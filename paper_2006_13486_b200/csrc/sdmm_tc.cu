@@ -31,6 +31,7 @@
 // O once); the MMA does 1/(1-sp_i) times the useful work, which stays under
 // the HBM time while (1-sp_i) * P_tc >= AI * BW (SURVEY §7 hard part 1).
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -38,6 +39,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 namespace rbgp4 {
 namespace {
@@ -71,200 +73,16 @@ struct TcParams {
     int32_t ksplit, sps;     // split-K: CTAs per output tile (one cluster) and steps per slice
     int32_t adj_smem;        // g_i adjacency staged in shared memory for the table build
     const uint16_t *prep;    // precomputed scatter table [phase][j][row] (rbgp4_prepare) or null
+    const int32_t *sched;    // step schedule [tile-row][s] -> g_o adjacency slot (rbgp4_prepare) or null
     int32_t table_in_regs;   // densify keeps each row's offsets in registers (else smem table)
-    int32_t a_tmem;          // A tiles assembled in TMEM (tcgen05.st) and read by TS-mode MMAs
-    int32_t a_tcols;         // TMEM columns per A stage (tk * elt / 4)
     int32_t tmem_cols;       // TMEM allocation (power of two)
     // implicit-im2col convolution (K3): I is never materialised; x is NHWC bf16 and the
     // slab of step s is the tap (i, j) / channel block of its K rows, fetched by a 4-D TMA
     // box at the tap-shifted coordinates (out-of-bounds = zero padding); O is NHWC.
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, th, tb;
+    int32_t ostore;          // epilogue stages the output tile in shared memory and TMA-stores it
+    int32_t w_swz;           // swizzle span (bytes) of the compressed-W stage rows: 0 / 32 / 64 / 128
 };
-
-// ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-#ifndef RBGP4_MBAR_POLL
-#define RBGP4_MBAR_POLL 0
-#endif
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t addr = smem_u32(bar);
-#if RBGP4_MBAR_POLL
-    // pure polling: test_wait never suspends the thread
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(addr), "r"(parity) : "memory");
-#else
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(addr), "r"(parity) : "memory");
-#endif
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                            int32_t x, int32_t y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
-    asm volatile("st.shared.b16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
-__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-template <typename E>
-__device__ __forceinline__ void sts_elem(uint32_t addr, E v) {
-    if constexpr (sizeof(E) == 2) sts16(addr, *reinterpret_cast<uint16_t *>(&v));
-    else sts32(addr, *reinterpret_cast<uint32_t *>(&v));
-}
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                            int32_t x, int32_t y, int32_t z) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                            int32_t x, int32_t y, int32_t z, int32_t w) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred = 0;
-    asm volatile(
-        "{\n.reg .pred p;\n.reg .b32 r;\n"
-        "elect.sync r|p, 0xffffffff;\n"
-        "selp.b32 %0, 1, 0, p;\n}\n"
-        : "=r"(pred));
-    return pred != 0;
-}
-__device__ __forceinline__ void fence_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
-                     "r"(smem_u32(bar)) : "memory");
-}
-template <bool TF32>
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                       uint32_t idesc, uint32_t accumulate) {
-    if constexpr (TF32) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-    } else {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-            "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-    }
-}
-// A from TMEM (TS): A must be K-major (lane = row), B from shared memory.
-template <bool TF32>
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                          uint32_t idesc, uint32_t accumulate) {
-    if constexpr (TF32) {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(d_tmem),
-            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u));
-    } else {
-        asm volatile(
-            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %5, %5, %5}, p;\n}\n" ::"r"(d_tmem),
-            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u));
-    }
-}
-#define TMEM_ST_32x32b_X32(taddr, r)                                                        \
-    asm volatile(                                                                           \
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"  \
-        "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" \
-        ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),        \
-        "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]),      \
-        "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]),  \
-        "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),  \
-        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) : "memory")
-// one of q[0..3] by a runtime index without local memory (SEL chains)
-__device__ __forceinline__ uint4 sel4(const uint4 &a, const uint4 &b, const uint4 &c, const uint4 &d,
-                                      uint32_t idx) {
-    const bool o = idx & 1, t = idx & 2;
-    uint4 x, y, r;
-    x.x = o ? b.x : a.x; x.y = o ? b.y : a.y; x.z = o ? b.z : a.z; x.w = o ? b.w : a.w;
-    y.x = o ? d.x : c.x; y.y = o ? d.y : c.y; y.z = o ? d.z : c.z; y.w = o ? d.w : c.w;
-    r.x = t ? y.x : x.x; r.y = t ? y.y : x.y; r.z = t ? y.z : x.z; r.w = t ? y.w : x.w;
-    return r;
-}
-
-// UMMA shared-memory matrix descriptor (sm_100: version 1 at bit 46).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
-                                              uint32_t layout) {
-    uint64_t d = 0;
-    d |= uint64_t((addr >> 4) & 0x3FFF);
-    d |= uint64_t((lbo >> 4) & 0x3FFF) << 16;
-    d |= uint64_t((sbo >> 4) & 0x3FFF) << 32;
-    d |= uint64_t(1) << 46;
-    d |= uint64_t(layout & 7) << 61;
-    return d;
-}
-__device__ __forceinline__ uint32_t swizzle_layout_code(int span) {
-    return span == 128 ? 2u : span == 64 ? 4u : 6u;  // SWIZZLE_128B / 64B / 32B
-}
-// byte offset -> swizzled byte offset inside a (8 rows x span) atom region
-__device__ __forceinline__ uint32_t swz(uint32_t off, int span) {
-    const uint32_t mask = span == 128 ? 7u : span == 64 ? 3u : 1u;
-    return off ^ (((off >> 7) & mask) << 4);
-}
-
-#define TMEM_LD_32x32b_X32(taddr, r)                                                       \
-    asm volatile(                                                                          \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"    \
-        "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}," \
-        " [%32];"                                                                          \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),          \
-          "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),        \
-          "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),    \
-          "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),    \
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),    \
-          "=r"(r[30]), "=r"(r[31])                                                         \
-        : "r"(taddr))
 
 // Byte offset, inside one densified A stage, of nonzero j of CTA row r (the scatter map).
 // Row r walks j = ((rk*d_i + ink)*bk + k) with counters (reference sdmm.py:183-186).
@@ -304,7 +122,7 @@ __global__ void prep_kernel(const TcParams p, const int32_t *__restrict__ adj_i,
 template <typename E, bool OUT_BF16, bool CONV>
 __global__ void __launch_bounds__(kThreads, 1)
 tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
-          const TcParams p, const E *__restrict__ values, const int32_t *__restrict__ adj_o,
+          const __grid_constant__ CUtensorMap omap, const TcParams p, const E *__restrict__ values, const int32_t *__restrict__ adj_o,
           const int32_t *__restrict__ adj_i, void *__restrict__ out, float *__restrict__ wsp) {
     constexpr bool kTF32 = sizeof(E) == 4;
     constexpr int kElt = sizeof(E);
@@ -323,11 +141,13 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         (reinterpret_cast<uintptr_t>(aoff + kBlockM * p.d_t) + 15) & ~uintptr_t(15));
     uint64_t *bars = reinterpret_cast<uint64_t *>(
         (reinterpret_cast<uintptr_t>(adj_s + (p.adj_smem ? p.u_i * p.d_i : 0)) + 7) & ~uintptr_t(7));
-    // one ring of ns = na = nb stages, each holding an A tile and an I slab:
-    // full[st] completes on the TMA transaction bytes + 4 densify-warp arrivals,
-    // empty[st] on the MMA commit (one wait and one commit per step for the MMA warp)
+    // one barrier ring of nb stages indexed by step (s % nb): the I slab of step s lives in
+    // B stage s % nb, its dense A tile in A stage s % na (na <= nb: the A ring only needs to
+    // cover densify-ahead, the I ring covers the load latency).  full[s % nb] completes on
+    // the TMA transaction bytes + 4 densify-warp arrivals, empty[s % nb] on the MMA commit of
+    // step s (one wait and one commit per step for the MMA warp); the A stage of step s is
+    // free once empty[(s - na) % nb] has completed for step s - na.
     uint64_t *full_b = bars, *empty_b = full_b + p.nb;
-    uint64_t *full_a = full_b, *empty_a = empty_b;
     uint64_t *full_w = empty_b + p.nb, *empty_w = full_w + p.nw;
     uint64_t *tmem_full = empty_w + p.nw;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
@@ -343,42 +163,9 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     const int s_begin = kslice * p.sps;
     const int nsteps = min(p.d_o, s_begin + p.sps) - s_begin;
 
-    // TMEM first: the allocation latency overlaps the table build below
-    if (warp == 5) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(tmem_slot)),
-                     "r"(uint32_t(p.tmem_cols)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        if (lane == 0) trace(p.debug, 6, 5);
-    }
-    // ---- one-time setup: zero the A ring, scatter-offset table, barriers, TMEM.
-    // The in-tile pattern is the same for every step, so the (row, j) -> A
-    // position map is computed once here and the per-step densify is a pure
-    // table-driven scatter (reference index map: sdmm.py:183-186).  Zeros
-    // written now are never overwritten: every step fills the same positions.
-    {
-        uint4 z = make_uint4(0, 0, 0, 0);
-        uint4 *a4 = reinterpret_cast<uint4 *>(a_buf);
-        for (int i = threadIdx.x; i < p.na * p.a_stage_bytes / 16; i += kThreads) a4[i] = z;
-        const int32_t *adj = adj_i;
-        if (p.adj_smem && threadIdx.x < kBlockM && p.prep == nullptr) {
-            // one coalesced copy instead of d_t dependent global loads per row; only the
-            // four table-building warps synchronise on it (named barrier 1)
-            for (int i = threadIdx.x; i < p.u_i * p.d_i; i += kBlockM) adj_s[i] = adj_i[i];
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            adj = adj_s;
-        }
-        if (threadIdx.x < kBlockM && p.prep == nullptr)
-            row_offsets<kElt>(p, adj, row_in_tile0, threadIdx.x, aoff + threadIdx.x, kBlockM);
-        else if (p.prep != nullptr) {
-            // prepared map: one coalesced 16-byte copy into the shared table
-            const uint4 *src = reinterpret_cast<const uint4 *>(
-                p.prep + size_t(row_in_tile0 / p.rows_valid) * p.d_t * kBlockM);
-            uint4 *dst = reinterpret_cast<uint4 *>(aoff);
-            for (int i = threadIdx.x; i < p.d_t * kBlockM / 8; i += kThreads) dst[i] = __ldg(src + i);
-        }
-    }
-    if (threadIdx.x == 0) trace(p.debug, 6, 4);
+    // ---- barriers first, so the TMA producers start streaming before the rest of the
+    // setup (TMEM allocation, A-ring zeroing, scatter table) -- that setup only gates
+    // the densify warps and the MMA warp, and overlaps the first I-slab loads.
     if (warp == 4 && lane == 0) {
         for (int i = 0; i < p.nb; ++i) { mbar_init(&full_b[i], 1 + 4); mbar_init(&empty_b[i], 1); }
         for (int i = 0; i < p.nw; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
@@ -388,18 +175,59 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         if (p.w_tma)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     }
-    fence_async_smem();
-    tc_fence_before();
     __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_d = *tmem_slot;
-    const int32_t *orow = adj_o + tbm * p.d_o + s_begin;
+    // g_o adjacency row of this tile-row and the order its slots are walked in: the
+    // schedule lets tile-rows that share a K-block read its I slab at the same step
+    const int32_t *orow = adj_o + tbm * p.d_o;
+    const int32_t *srow = p.sched ? p.sched + tbm * p.d_o + s_begin : nullptr;
     if (threadIdx.x == 0) trace(p.debug, 6, 0);
+
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(uint32_t(p.tmem_cols)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tc_fence_before();
+        __syncwarp();
+        tc_fence_after();
+        if (lane == 0) trace(p.debug, 6, 5);
+    }
+    if (warp < 4) {
+        // ---- densify-warp setup: zero the A ring and load the scatter-offset table.
+        // The in-tile pattern is the same for every step, so the (row, j) -> A position
+        // map is computed once here and the per-step densify is a pure table-driven
+        // scatter (reference index map: sdmm.py:183-186).  Zeros written now are never
+        // overwritten: every step fills the same positions.
+        const int t = threadIdx.x;
+        uint4 z = make_uint4(0, 0, 0, 0);
+        uint4 *a4 = reinterpret_cast<uint4 *>(a_buf);
+        for (int i = t; i < p.na * p.a_stage_bytes / 16; i += kBlockM) a4[i] = z;
+        const int32_t *adj = adj_i;
+        if (p.prep != nullptr) {
+            // prepared map: one coalesced 16-byte copy into the shared table
+            const uint4 *src = reinterpret_cast<const uint4 *>(
+                p.prep + size_t(row_in_tile0 / p.rows_valid) * p.d_t * kBlockM);
+            uint4 *dst = reinterpret_cast<uint4 *>(aoff);
+            for (int i = t; i < p.d_t * kBlockM / 8; i += kBlockM) dst[i] = __ldg(src + i);
+        } else {
+            if (p.adj_smem) {
+                // one coalesced copy instead of d_t dependent global loads per row
+                for (int i = t; i < p.u_i * p.d_i; i += kBlockM) adj_s[i] = adj_i[i];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                adj = adj_s;
+            }
+            row_offsets<kElt>(p, adj, row_in_tile0, t, aoff + t, kBlockM);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // table + zeros complete (warps 0-3)
+        if (t == 0) trace(p.debug, 6, 4);
+        if (p.debug & 32) asm volatile("bar.sync 2, 160;" ::: "memory");
+    }
 
     // Role loops run warp-uniformly (all 32 lanes wait on the barriers); one lane,
     // picked by elect.sync, issues the TMA / tcgen05 instructions.  Issuing from
     // lane-0-only divergent code made the compiler wrap every UTCHMMA/UTMALDG in an
     // elect loop with R2UR conversions (~500 cycles per step, tools/tc_trace.py).
+    if ((p.debug & 32) && warp == 4) asm volatile("bar.sync 2, 160;" ::: "memory");  // late start
     if (warp == 4) {
         // ================= TMA producer: I slabs (runs ahead by the B ring depth) ==========
         const int atoms = p.tn * kElt / 128;           // 128-byte MN atoms per slab
@@ -409,7 +237,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             const int st = s % p.nb;
             const uint32_t ph = (s / p.nb) & 1;
             mbar_wait(&empty_b[st], ph ^ 1);
-            const int32_t krow = orow[s] * p.tk;
+            const int32_t krow = orow[srow ? srow[s] : s_begin + s] * p.tk;
             if (elect_one()) {
                 mbar_expect_tx(&full_b[st], uint32_t(p.b_stage_bytes));
                 unsigned char *dst = b_buf + st * p.b_stage_bytes;
@@ -446,8 +274,9 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 mbar_wait(&empty_w[st], ph ^ 1);
                 if (elect_one()) {
                     mbar_expect_tx(&full_w[st], uint32_t(p.w_stage_bytes));
-                    tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st],
-                                (s_begin + g * p.ws) * p.d_t, int32_t(m0));
+                    const int j = srow ? srow[g] : s_begin + g;  // ws == 1: stage g = step g
+                    tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st], j * p.d_t,
+                                int32_t(m0));
                     trace(p.debug, 1, g);
                 }
                 __syncwarp();
@@ -455,6 +284,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         }
     } else if (warp == 5) {
         // ================= MMA issuer =================
+        const uint32_t tmem_d = *tmem_slot;
         // instruction descriptor: D f32, A/B bf16|tf32, A K-major, B MN-major, N, M=128
         const uint32_t fmt = kTF32 ? 2u : 1u;
         const uint32_t b_mn = CONV ? 0u : 1u;  // conv: B (im2col of NHWC) is K-major
@@ -476,56 +306,35 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
         const uint32_t a_jump16 = uint32_t(kBlockM - 1) * a_span16;        // next K atom
         const uint32_t b_step16 = uint32_t(32 / kElt) * 128 / 16;           // 32/E K-rows
-        unsigned long long seg[3] = {0, 0, 0};
         for (int s = 0; s < nsteps; ++s) {
             const int sb = s % p.nb, sa = s % p.na;
-            const unsigned long long c0 = clock64();
             mbar_wait(&full_b[sb], (s / p.nb) & 1);  // I slab landed and A tile densified
             if (lane == 0) trace(p.debug, 7, s);
             tc_fence_after();
-            const unsigned long long c1 = clock64();
             if (elect_one()) {
                 trace(p.debug, 4, s);
                 uint64_t ad = a_desc0 + uint64_t(sa) * a_stage16;
                 uint64_t bd = b_desc0 + uint64_t(sb) * b_stage16;
                 uint32_t in_atom = 0;
-                if (p.a_tmem) {
-                    // A tile of this stage sits in TMEM columns [tn + sa*a_tcols, +a_tcols)
-                    uint32_t at = tmem_d + uint32_t(p.tn + sa * p.a_tcols);
-                    for (int kk = 0; kk < ksteps; ++kk) {
-                        if (!(p.debug & 2))
-                            tc_mma_ts<kTF32>(tmem_d, at, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
-                        at += 8;  // 32 bytes of K = 8 TMEM columns
+                for (int kk = 0; kk < ksteps; ++kk) {
+                    if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                    ad += 2;  // 32 bytes along K inside the swizzle atom
+                    in_atom += 2;
+                    if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
+                    if constexpr (CONV) {
+                        bd += 2;  // K-major B: 32 bytes along K inside its 128 B atom
+                        if ((kk & 3) == 3) bd += bk_jump16;
+                    } else {
                         bd += b_step16;
                     }
-                } else {
-                    for (int kk = 0; kk < ksteps; ++kk) {
-                        if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
-                        ad += 2;  // 32 bytes along K inside the swizzle atom
-                        in_atom += 2;
-                        if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
-                        if constexpr (CONV) {
-                            bd += 2;  // K-major B: 32 bytes along K inside its 128 B atom
-                            if ((kk & 3) == 3) bd += bk_jump16;
-                        } else {
-                            bd += b_step16;
-                        }
-                    }
                 }
-                tc_commit(&empty_b[sb]);  // frees both the I slab and the A tile of the stage
+                tc_commit(&empty_b[sb]);  // frees the I slab (and, na steps later, the A tile)
                 trace(p.debug, 5, s);
             }
             __syncwarp();
-            const unsigned long long c2 = clock64();
-            seg[0] += c1 - c0;
-            seg[1] += c2 - c1;
         }
         if (elect_one()) tc_commit(tmem_full);
         __syncwarp();
-        if ((p.debug & (8 | 4096)) && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) {
-            g_trace[9][0] = seg[0];
-            g_trace[9][1] = seg[1];
-        }
     } else {
         // ================= densify (warps 0-3), then epilogue =================
         const int t = threadIdx.x;  // 0..127: this thread densifies CTA row t
@@ -549,21 +358,11 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             uint32_t hi = j2 < p.d_t ? aoff[j2 * kBlockM + t] : 0u;
             offp[i] = lo | (hi << 16);
         }
-        const uint32_t wrow = smem_u32(w_buf) + uint32_t(t * p.ws * p.d_t * kElt);
-        // TMEM path: per 16-byte K position P of the dense row, code = 8 | chunk index when the
-        // row has a nonzero chunk there (positions ascend with the chunks), else 0; 4 bits each
-        uint32_t pcode[4] = {0, 0, 0, 0};
-        const int npos = p.tk * kElt / 16;
-        if (p.a_tmem && active) {
-            const int ui = ((row_in_tile0 + t) / p.bm) % p.u_i;
-            for (int c = 0; c < p.d_t / V; ++c) {
-                const int j = c * V;
-                const int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
-                const int kcol = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;
-                const int P = kcol * kElt / 16;
-                pcode[P / 8] |= uint32_t(8 | c) << (4 * (P % 8));
-            }
-        }
+        // compressed row t of a W stage: ws*d_t elements; when the stage is swizzled (TMA
+        // SWIZZLE_32B/64B/128B, rows of exactly w_swz bytes) 16-byte chunk c sits at c ^ wxor
+        const uint32_t wrow_bytes = uint32_t(p.ws * p.d_t * kElt);
+        const uint32_t wrow = smem_u32(w_buf) + uint32_t(t) * wrow_bytes;
+        const uint32_t wxor = p.w_swz ? ((uint32_t(t) * wrow_bytes) >> 7) & uint32_t(p.w_swz / 16 - 1) : 0u;
         for (int s = 0; s < nsteps; ++s) {
             const int sa = s % p.na;
             const int wg = s / p.ws, wsub = s - wg * p.ws;  // W stage and slot inside it
@@ -571,65 +370,35 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 mbar_wait(&full_w[wg % p.nw], (wg / p.nw) & 1);
                 if (t == 0) trace(p.debug, 8, wg);
             }
-            mbar_wait(&empty_a[sa], ((s / p.na) & 1) ^ 1);
+            if (s >= p.na) {  // A stage sa was last read by the MMAs of step s - na
+                const int sp = s - p.na;
+                mbar_wait(&empty_b[sp % p.nb], (sp / p.nb) & 1);
+            }
             if (t == 0) trace(p.debug, 2, s);
             const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
-            if (p.a_tmem) {
-                // assemble the dense row t of A in TMEM lane t: 32 columns (8 positions) per st
-                const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
-                                     uint32_t(wsub * p.d_t * kElt);
-                uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0, q2 = q0, q3 = q0;
-                const int nch = p.d_t / V;
-                if (active && !(p.debug & 1)) {
-                    q0 = lds128(src);
-                    if (nch > 1) q1 = lds128(src + 16);
-                    if (nch > 2) q2 = lds128(src + 32);
-                    if (nch > 3) q3 = lds128(src + 48);
-                }
-                const uint32_t at = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(p.tn + sa * p.a_tcols);
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    if (g >= npos / 8) break;
-                    const uint32_t code = pcode[g];
-                    uint32_t r[32];
-#pragma unroll
-                    for (int pp = 0; pp < 8; ++pp) {
-                        const uint32_t bits = (code >> (4 * pp)) & 0xFu;
-                        uint4 v = sel4(q0, q1, q2, q3, bits & 3u);
-                        if (!(bits & 8u)) v = make_uint4(0, 0, 0, 0);
-                        r[4 * pp] = v.x; r[4 * pp + 1] = v.y; r[4 * pp + 2] = v.z; r[4 * pp + 3] = v.w;
-                    }
-                    TMEM_ST_32x32b_X32(at + uint32_t(g * 32), r);
-                }
-                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                tc_fence_before();
-            } else if (active && !(p.debug & 1)) {
+            const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes);
+            const uint32_t c0 = uint32_t(wsub * p.d_t * kElt / 16);  // first chunk of this step
+            if (active && !(p.debug & 1)) {
                 if (chunked) {
-                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
-                                         uint32_t(wsub * p.d_t * kElt);
                     const int nchunks = p.d_t / V;
                     uint4 q[kMaxChunks];
 #pragma unroll
                     for (int c = 0; c < kMaxChunks; ++c)
-                        if (c < nchunks) q[c] = lds128(src + 16 * c);
+                        if (c < nchunks) q[c] = lds128(src + (((c0 + c) ^ wxor) << 4));
 #pragma unroll
                     for (int c = 0; c < kMaxChunks; ++c) {
                         if (c < nchunks) {
                             const uint32_t o = (offp[c / 2] >> (16 * (c & 1))) & 0xFFFFu;
-                            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a + o),
-                                         "r"(q[c].x), "r"(q[c].y), "r"(q[c].z), "r"(q[c].w)
-                                         : "memory");
+                            sts128(a + o, q[c].x, q[c].y, q[c].z, q[c].w);
                         }
                     }
                 } else if (reg_path) {
                     // compressed row t of this step (TMA-staged): 16-byte shared loads,
                     // all issued before the scatter so their latency overlaps
-                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
-                                         uint32_t(wsub * p.d_t * kElt);
                     uint4 q[kRegNnz / V];
 #pragma unroll
                     for (int c = 0; c < kRegNnz / V; ++c)
-                        if (c * V < p.d_t) q[c] = lds128(src + 16 * c);
+                        if (c * V < p.d_t) q[c] = lds128(src + (((c0 + c) ^ wxor) << 4));
 #pragma unroll
                     for (int c = 0; c < kRegNnz / V; ++c) {
                         if (c * V < p.d_t) {
@@ -643,25 +412,23 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                         }
                     }
                 } else if (p.w_tma) {
-                    const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes) +
-                                         uint32_t(wsub * p.d_t * kElt);
                     for (int j = 0; j < p.d_t; j += V) {
-                        uint4 q = lds128(src + j * kElt);
+                        uint4 q = lds128(src + (((c0 + j / V) ^ wxor) << 4));
                         const E *qe = reinterpret_cast<const E *>(&q);
 #pragma unroll
                         for (int v = 0; v < V; ++v) sts_elem<E>(a + aoff[(j + v) * kBlockM + t], qe[v]);
                     }
                 } else {
-                    const E *vs = vrow + int64_t(s_begin + s) * p.d_t;
+                    const E *vs = vrow + int64_t(srow ? srow[s] : s_begin + s) * p.d_t;
                     for (int j = 0; j < p.d_t; ++j) sts_elem<E>(a + aoff[j * kBlockM + t], vs[j]);
                 }
             }
             // make the generic-proxy stores visible to the tensor core, then one
-            // release-arrive per warp (full_a counts 4 warps)
+            // release-arrive per warp (full counts 4 warps + the TMA)
             if (!(p.debug & 256)) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&full_a[sa]);
+                mbar_arrive(&full_b[s % p.nb]);
                 if (p.w_tma && (wsub == p.ws - 1 || s == nsteps - 1)) mbar_arrive(&empty_w[wg % p.nw]);
             }
             if (t == 0) trace(p.debug, 3, s);
@@ -672,6 +439,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         tc_fence_after();
         if (threadIdx.x == 0) trace(p.debug, 6, 1);
         if (kslice > 0) {
+            const uint32_t tmem_d = *tmem_slot;
             const int row = warp * 32 + lane;
             const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
             float *dst = wsp + (int64_t(kslice - 1) * (int64_t(gridDim.y) * p.rows_valid) + m0 + row) *
@@ -699,19 +467,26 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     if (warp < 4 && kslice == 0) {
-        // ---- epilogue phase 2 (leader): TMEM + partials (fixed slice order) -> output
+        // ---- epilogue phase 2 (leader): TMEM + partials (fixed slice order) -> output.
+        // With p.ostore the tile is staged in shared memory (the A and I rings are free:
+        // every MMA has completed) and written by TMA bulk stores -- full 128-byte lines
+        // instead of 32 row-strided 16-byte stores per warp instruction.
+        const uint32_t tmem_d = *tmem_slot;
+        constexpr int kOutElt = OUT_BF16 ? 2 : 4;
         const int row = warp * 32 + lane;
         const bool row_ok = row < p.rows_valid;
         const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
         const int64_t slice_stride = int64_t(gridDim.y) * p.rows_valid * p.n_cols;
+        const uint32_t stage = smem_u32(a_buf);
         for (int c = 0; c < p.tn; c += 32) {
             uint32_t r[32];
             TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const int64_t col = n0 + c;
-            if (!row_ok || col >= p.n_cols || (p.debug & 4)) continue;
+            if (!row_ok || (p.debug & 4)) continue;
+            if (!p.ostore && col >= p.n_cols) continue;
             const bool full = col + 32 <= p.n_cols;
-            if (p.ksplit > 1) {
+            if (p.ksplit > 1 && col < p.n_cols) {
                 const float *part = wsp + (m0 + row) * p.n_cols + col;
                 for (int k = 1; k < p.ksplit; ++k, part += slice_stride) {
                     if (full) {
@@ -730,17 +505,59 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 }
             }
             if constexpr (CONV) {
+                if (p.relu) {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(fmaxf(__uint_as_float(r[q]), 0.0f));
+                }
+                if (p.ostore) {
+                    // staging [pixel][rows_valid channels]: lanes = consecutive channels
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const uint32_t addr = stage + uint32_t(((c + q) * p.rows_valid + row) * kOutElt);
+                        if constexpr (OUT_BF16) {
+                            const __nv_bfloat16 b = __float2bfloat16_rn(__uint_as_float(r[q]));
+                            sts16(addr, *reinterpret_cast<const uint16_t *>(&b));
+                        } else {
+                            sts32(addr, r[q]);
+                        }
+                    }
+                    continue;
+                }
                 // NHWC output: pixel (col + q) is a row of c_out = p.ld_out channels
                 const int64_t ch = m0 + row;
 #pragma unroll 4
                 for (int q = 0; q < 32; ++q) {
                     if (col + q >= p.n_cols) break;
-                    float v = __uint_as_float(r[q]);
-                    if (p.relu) v = fmaxf(v, 0.0f);
+                    const float v = __uint_as_float(r[q]);
                     if constexpr (OUT_BF16)
                         static_cast<__nv_bfloat16 *>(out)[(col + q) * p.ld_out + ch] = __float2bfloat16_rn(v);
                     else
                         static_cast<float *>(out)[(col + q) * p.ld_out + ch] = v;
+                }
+                continue;
+            }
+            if (p.ostore) {
+                // staging: 128-byte column atoms of rows_valid rows, 128B-swizzled (chunk ^ row%8)
+                if constexpr (OUT_BF16) {
+                    const uint32_t atom = stage + uint32_t((c / 64) * p.rows_valid * 128 + row * 128);
+                    const uint32_t ch0 = uint32_t(c % 64) / 8;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            __nv_bfloat162 b2 = __floats2bfloat162_rn(
+                                __uint_as_float(r[q * 8 + 2 * h]), __uint_as_float(r[q * 8 + 2 * h + 1]));
+                            w[h] = *reinterpret_cast<uint32_t *>(&b2);
+                        }
+                        sts128(atom + (((ch0 + q) ^ uint32_t(row & 7)) << 4), w[0], w[1], w[2], w[3]);
+                    }
+                } else {
+                    const uint32_t atom = stage + uint32_t((c / 32) * p.rows_valid * 128 + row * 128);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        sts128(atom + ((uint32_t(q) ^ uint32_t(row & 7)) << 4), r[4 * q], r[4 * q + 1],
+                               r[4 * q + 2], r[4 * q + 3]);
                 }
                 continue;
             }
@@ -774,30 +591,39 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 }
             }
         }
+        if (p.ostore && !(p.debug & 4)) {
+            fence_async_smem();  // staged tile -> visible to the TMA (async proxy)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (warp == 0 && elect_one()) {
+                if constexpr (CONV) {
+                    tma_store_2d(&omap, a_buf, int32_t(m0), int32_t(n0));
+                } else {
+                    const int atom_cols = 128 / kOutElt;
+                    for (int a = 0; a < p.tn / atom_cols; ++a)
+                        tma_store_2d(&omap, a_buf + a * p.rows_valid * 128, int32_t(n0) + a * atom_cols,
+                                     int32_t(m0));
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncwarp();
+        }
     }
     if (threadIdx.x == 0) trace(p.debug, 6, 2);
     tc_fence_before();
     __syncthreads();
     if (warp == 5) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot),
                      "r"(uint32_t(p.tmem_cols)));
     }
 }
 
 // ---------------------------------------------------------------- host side
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void *ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    });
-    return fn;
+CUtensorMapSwizzle w_swizzle(int span) {
+    return span == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : span == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+         : span == 32  ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
 }
 
 struct TcPlan {
@@ -835,10 +661,9 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     // compressed W tiles come in by TMA when a row of one step is whole 16-byte chunks
     p.w_tma = (c.d_t * elt) % 16 == 0 && c.d_t <= 256 ? 1 : 0;
     // W stage: as many consecutive steps as fit one box (<= 256 elements, <= 8 KB)
+    // one W box (one step's compressed tile) per W stage: with a step schedule consecutive
+    // steps are not contiguous in `values`
     p.ws = 1;
-    while (p.w_tma && p.ws * 2 <= c.d_o && p.ws * 2 * c.d_t <= 256 &&
-           size_t(p.rows_valid) * p.ws * 2 * c.d_t * elt <= 8192)
-        p.ws *= 2;
     p.w_stage_bytes = p.w_tma ? p.rows_valid * p.ws * c.d_t * elt : 0;
     {
         const int V = 16 / elt;
@@ -854,35 +679,24 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     if (const char *env = getenv("RBGP4_TC_TN")) tn = std::max(tn_min, std::min(256, atoi(env)));
     if (force_tn) tn = force_tn;
     p.adj_smem = size_t(c.u_i) * c.d_i * 4 <= 16384 ? 1 : 0;
-    // Shared-memory budget, in priority order (one CTA per SM):
-    //   1. >= 96 KB of I slabs in flight (TMA latency under load is ~2 us: Little's law),
-    //   2. A ring 2..4 deep (densify runs ahead of the MMA),
-    //   3. W ring 2 x <= 8 KB,
-    //   4. everything left -> more I stages (<= 16).
+    // Shared-memory budget (one CTA per SM).  The main loop is bound by I-slab bytes in
+    // flight per SM (TMA latency under load is ~2 us: Little's law, tools/tc_trace.py), so:
+    //   1. A ring 2 deep (densify one step ahead of the MMA is enough),
+    //   2. W ring 2 x <= 8 KB,
+    //   3. everything left -> I stages (2..16).
     for (; tn >= tn_min; tn /= 2) {
         if (force_tn && tn != force_tn) break;
         p.tn = tn;
         p.b_stage_bytes = c.tk * tn * elt;
+        p.a_stage_bytes = kBlockM * c.tk * elt;
         p.nw = p.w_tma ? 2 : 1;
         const size_t base = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 +
-                            (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 2 + 1);
+                            (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 16 + 1);
         size_t w_bytes = size_t(p.nw) * p.w_stage_bytes;
-        if (getenv("RBGP4_TC_NOA")) p.a_stage_bytes = 0;  // ablation (debug 7 only): no A ring
-        // A in TMEM (opt-in, RBGP4_TC_TMEM_A=1): needs 16-byte K runs (bk % V == 0), <= 4 of
-        // them per row and <= 32 K positions; shared memory then holds only the I and W rings.
-        // Correct, but the register-select row assembly costs ~350 instructions per row per
-        // step and measured slower than the shared-memory A ring (34.8 vs 28.8 us, conv10).
-        {
-            const int V = 16 / elt;
-            p.a_tcols = c.tk * elt / 4;
-            const bool ok = p.w_tma && c.bk % V == 0 && c.d_t / V <= 4 && c.tk * elt / 16 <= 32 &&
-                            tn + 2 * p.a_tcols <= 512 && getenv("RBGP4_TC_TMEM_A") != nullptr;
-            p.a_tmem = ok ? 1 : 0;
-            if (p.a_tmem) p.a_stage_bytes = 0;
-            else p.a_stage_bytes = kBlockM * c.tk * elt;
-        }
-        const size_t stage = size_t(p.a_stage_bytes) + p.b_stage_bytes;  // A tile + I slab
-        if (base + w_bytes + 2 * stage > kSmemCap && p.w_tma) {
+        int na = 2;
+        if (const char *env = getenv("RBGP4_TC_NA")) na = std::max(1, std::min(8, atoi(env)));
+        const size_t a_ring = size_t(na) * p.a_stage_bytes;
+        if (base + w_bytes + a_ring + 2 * size_t(p.b_stage_bytes) > kSmemCap && p.w_tma) {
             // large compressed tiles: read W straight from global in the densify warps
             p.w_tma = 0;
             p.ws = 1;
@@ -891,14 +705,42 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
             p.table_in_regs = 0;
             w_bytes = 0;
         }
-        if (base + w_bytes + 2 * stage > kSmemCap) continue;
-        const size_t fixed = base + w_bytes;
-        int ns = int(std::min<size_t>(16, (kSmemCap - fixed) / stage));
-        if (p.a_tmem) ns = std::min(ns, (512 - tn) / p.a_tcols);  // A stages share TMEM with D
-        p.na = ns;
-        p.nb = ns;
+        if (base + w_bytes + a_ring + 2 * size_t(p.b_stage_bytes) > kSmemCap) continue;
+        // I and W rings share the rest: both chains (I slab of step s waits for the MMA of
+        // s - nb, W tile of step s for the densify of s - nw) progress nb resp. nw steps per
+        // load latency, so maximise min(nb, nw), then nb
+        const size_t avail = kSmemCap - (base + a_ring);
+        int nb = 0, nw = 0;
+        for (int cand = 16; cand >= 2; --cand) {
+            const size_t ib = size_t(cand) * p.b_stage_bytes;
+            if (ib + (p.w_tma ? 2 * size_t(p.w_stage_bytes) : 0) > avail) continue;
+            const int cw = p.w_tma ? int(std::min<size_t>(cand, (avail - ib) / p.w_stage_bytes)) : 1;
+            if (std::min(cand, cw) > std::min(nb, nw) || nb == 0) { nb = cand; nw = cw; }
+        }
+        if (const char *env = getenv("RBGP4_TC_NB")) {
+            const int want = std::max(2, std::min(16, atoi(env)));
+            if (size_t(want) * p.b_stage_bytes + 2 * size_t(p.w_stage_bytes) <= avail) {
+                nb = want;
+                nw = p.w_tma ? int(std::min<size_t>(want, (avail - size_t(nb) * p.b_stage_bytes) / p.w_stage_bytes)) : 1;
+            }
+        }
+        if (const char *env = getenv("RBGP4_TC_NW"))
+            if (p.w_tma)
+                nw = std::max(2, std::min({16, atoi(env), int((avail - size_t(nb) * p.b_stage_bytes) / p.w_stage_bytes)}));
+        if (nb < na || nb < 2) continue;
+        p.na = na;
+        p.nb = nb;
+        p.nw = nw;
+        w_bytes = size_t(nw) * p.w_stage_bytes;
+        const size_t fixed = base + w_bytes + a_ring;
+        // compressed-W stage rows of exactly 32/64/128 bytes are TMA-swizzled, so the 32 rows a
+        // densify warp reads land on distinct banks (unswizzled 64-byte rows are 16-way conflicted)
+        {
+            const int wb = p.ws * c.d_t * elt;
+            p.w_swz = (p.w_tma && (wb == 32 || wb == 64 || wb == 128) && !getenv("RBGP4_TC_NOWSWZ")) ? wb : 0;
+        }
         p.tmem_cols = 32;
-        while (p.tmem_cols < (p.a_tmem ? tn + ns * p.a_tcols : tn)) p.tmem_cols *= 2;
+        while (p.tmem_cols < tn) p.tmem_cols *= 2;
         const int64_t tiles = ((c.n_cols + tn - 1) / tn) * blocks_m;
         // split-K in two (a 2-CTA cluster per tile) only when that still fits one wave;
         // deeper splits measured slower (tools/tc_time.py)
@@ -907,7 +749,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         p.sps = (c.d_o + ks - 1) / ks;
         p.ksplit = (c.d_o + p.sps - 1) / p.sps;  // no empty slices
         out->p = p;
-        out->smem = fixed + size_t(ns) * stage;
+        out->smem = fixed + size_t(nb) * p.b_stage_bytes;
         out->blocks_m = int(blocks_m);
         return 1;
     }
@@ -915,9 +757,15 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     return 0;
 }
 
+// The TMA-store epilogue stages the whole output tile in the (then idle) A + I rings.
+bool staging_fits(const TcPlan &pl, int out_elt) {
+    const size_t rings = size_t(pl.p.na) * pl.p.a_stage_bytes + size_t(pl.p.nb) * pl.p.b_stage_bytes;
+    return size_t(pl.p.rows_valid) * pl.p.tn * out_elt <= rings && !getenv("RBGP4_TC_NOSTORE");
+}
+
 template <typename E, bool OUT_BF16, bool CONV = false>
 int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wmap,
-                 const void *values, const int32_t *adj_o, const int32_t *adj_i, void *out,
+                 const CUtensorMap &omap, const void *values, const int32_t *adj_o, const int32_t *adj_i, void *out,
                  float *wsp, cudaStream_t stream) {
     auto kern = tc_kernel<E, OUT_BF16, CONV>;
     cudaError_t e =
@@ -940,7 +788,7 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
     attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);  // the K slices of one tile co-reside
     cfg.attrs = attr;
     cfg.numAttrs = pl.p.ksplit > 1 ? 1 : 0;
-    e = cudaLaunchKernelEx(&cfg, kern, map, wmap, pl.p, static_cast<const E *>(values), adj_o, adj_i,
+    e = cudaLaunchKernelEx(&cfg, kern, map, wmap, omap, pl.p, static_cast<const E *>(values), adj_o, adj_i,
                            out, wsp);
     if (e != cudaSuccess) {
         set_error("tc_kernel launch (grid %u x %u x %u, smem %zu): %s", grid.x, grid.y, grid.z,
@@ -953,15 +801,155 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
 
 }  // namespace
 
+// ---------------------------------------------------------------- step schedule
+// Every tile-row walks only its g_o neighbours (as the reference does), but in which order
+// is free for the tensor-core modes (fp32 accumulation; no bit-exactness claim).  When
+// d_r(g_o) >= 2, several tile-rows read the same I slab: if they read it at the SAME step,
+// their CTAs (same column block, launched in the same wave) request the same lines at about
+// the same time and L2 serves them once, instead of a second full pass over I later.  The
+// schedule picks, per step, a set of vertex-disjoint K-blocks covering as many tile-rows as
+// possible.  For u_o = 4 and right degree 2 (the VGG/WRN factorisations) the K-blocks are the
+// edges of a d_o-regular multigraph on 4 vertices, which always splits into the 3 perfect
+// matchings {01,23} {02,13} {03,12} (x01 = x23, x02 = x13, x03 = x12 follows from
+// regularity), so every slab is read by both of its tile-rows at the same step.
+namespace {
+struct Lcg {
+    uint64_t x;
+    uint32_t next() { x = x * 6364136223846793005ull + 1442695040888963407ull; return uint32_t(x >> 33); }
+};
+
+// sched[u * d_o + s] = adjacency slot j of tile-row u read at step s; returns #slab reads
+int64_t schedule_cost(int u_o, int d_o, const int32_t *adj, const std::vector<int32_t> &sched) {
+    std::vector<std::pair<int, int>> reads;  // (step, K-block)
+    for (int u = 0; u < u_o; ++u)
+        for (int s = 0; s < d_o; ++s) reads.emplace_back(s, adj[u * d_o + sched[u * d_o + s]]);
+    std::sort(reads.begin(), reads.end());
+    return std::unique(reads.begin(), reads.end()) - reads.begin();
+}
+
+void build_schedule(int u_o, int v_o, int d_o, const int32_t *adj, int32_t *out) {
+    std::vector<int32_t> best(size_t(u_o) * d_o);
+    for (int u = 0; u < u_o; ++u)
+        for (int s = 0; s < d_o; ++s) best[u * d_o + s] = s;  // reference order
+    int64_t best_cost = schedule_cost(u_o, d_o, adj, best);
+    // slot of K-block kb in tile-row u's adjacency row (-1 if not adjacent)
+    std::vector<int> slot(size_t(u_o) * v_o, -1);
+    std::vector<std::vector<int>> users(v_o);
+    for (int u = 0; u < u_o; ++u)
+        for (int j = 0; j < d_o; ++j) {
+            slot[size_t(u) * v_o + adj[u * d_o + j]] = j;
+            users[adj[u * d_o + j]].push_back(u);
+        }
+    auto consider = [&](const std::vector<int32_t> &cand) {
+        const int64_t cost = schedule_cost(u_o, d_o, adj, cand);
+        if (cost < best_cost) { best_cost = cost; best = cand; }
+    };
+    if (u_o == 4) {
+        bool deg2 = true;
+        for (int kb = 0; kb < v_o; ++kb) deg2 &= users[kb].empty() || users[kb].size() == 2;
+        if (deg2) {
+            // edges per vertex pair, then the three perfect matchings in turn
+            std::vector<int> pairs[4][4];
+            for (int kb = 0; kb < v_o; ++kb)
+                if (!users[kb].empty()) pairs[users[kb][0]][users[kb][1]].push_back(kb);
+            const int mt[3][2][2] = {{{0, 1}, {2, 3}}, {{0, 2}, {1, 3}}, {{0, 3}, {1, 2}}};
+            std::vector<int32_t> cand(size_t(u_o) * d_o, -1);
+            std::vector<int> step(u_o, 0);
+            bool ok = true;
+            for (auto &m : mt) {
+                const auto &e0 = pairs[m[0][0]][m[0][1]], &e1 = pairs[m[1][0]][m[1][1]];
+                ok &= e0.size() == e1.size();
+                for (int i = 0; ok && i < int(e0.size()); ++i)
+                    for (int h = 0; h < 2; ++h) {
+                        const int kb = h ? e1[i] : e0[i];
+                        for (int v : {m[h][0], m[h][1]}) cand[v * d_o + step[v]++] = slot[size_t(v) * v_o + kb];
+                    }
+            }
+            for (int u = 0; u < u_o; ++u) ok &= step[u] == d_o;
+            if (ok) consider(cand);
+        }
+    }
+    // general case: seeded randomised greedy; per step take vertex-disjoint shared K-blocks,
+    // then let leftover tile-rows read a K-block whose sharing is already lost
+    Lcg rng{0x9E3779B97F4A7C15ull};
+    for (int trial = 0; trial < 48 && u_o > 1; ++trial) {
+        std::vector<int32_t> cand(size_t(u_o) * d_o, -1);
+        std::vector<std::vector<char>> rem(u_o, std::vector<char>(v_o, 0));
+        std::vector<int> left(v_o, 0);  // users that still have kb pending
+        for (int u = 0; u < u_o; ++u)
+            for (int j = 0; j < d_o; ++j) { rem[u][adj[u * d_o + j]] = 1; ++left[adj[u * d_o + j]]; }
+        std::vector<int> order(v_o);
+        for (int i = 0; i < v_o; ++i) order[i] = i;
+        for (int s = 0; s < d_o; ++s) {
+            for (int i = v_o - 1; i > 0; --i) std::swap(order[i], order[rng.next() % (i + 1)]);
+            std::vector<char> busy(u_o, 0);
+            for (int kb : order) {
+                if (left[kb] < 2 || left[kb] != int(users[kb].size())) continue;
+                bool free = true;
+                for (int u : users[kb]) free &= !busy[u];
+                if (!free) continue;
+                for (int u : users[kb]) {
+                    busy[u] = 1; rem[u][kb] = 0;
+                    cand[u * d_o + s] = slot[size_t(u) * v_o + kb];
+                }
+                left[kb] = 0;
+            }
+            for (int u = 0; u < u_o; ++u) {
+                if (busy[u]) continue;
+                int pick = -1;
+                for (int j = 0; j < d_o; ++j) {
+                    const int kb = adj[u * d_o + j];
+                    if (rem[u][kb] && (pick < 0 || left[kb] < left[pick])) pick = kb;
+                }
+                rem[u][pick] = 0;
+                --left[pick];
+                cand[u * d_o + s] = slot[size_t(u) * v_o + pick];
+            }
+        }
+        consider(cand);
+    }
+    std::copy(best.begin(), best.end(), out);
+}
+
+size_t scatter_bytes(const ChainDims &c, const TcPlan &pl) {
+    const int phases = c.tm / pl.p.rows_valid;
+    return (size_t(phases) * c.d_t * kBlockM * sizeof(uint16_t) + 15) & ~size_t(15);
+}
+}  // namespace
+
+// prepared buffer: [scatter map u16: phase x d_t x 128, 16-byte padded][schedule i32: u_o x d_o,
+// padded][K4 relayout section (bf16 only, sdmm_gather.cu)]
+namespace {
+// schedule then partner table ([tile-row][s] -> tile-row reading the same slab at step s, or -1)
+size_t sched_end(const ChainDims &c, const TcPlan &pl) {
+    return (scatter_bytes(c, pl) + 2 * size_t(c.u_o) * c.d_o * sizeof(int32_t) + 15) & ~size_t(15);
+}
+size_t k4_bytes(const ChainDims &c, int compute) {
+    return compute == RBGP4_COMPUTE_BF16 ? gather_prep_bytes(c) : 0;
+}
+}  // namespace
+
 size_t tc_prep_size(const ChainDims &c, int compute) {
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return 0;
-    const int phases = c.tm / pl.p.rows_valid;
-    return size_t(phases) * c.d_t * kBlockM * sizeof(uint16_t);
+    return sched_end(c, pl) + k4_bytes(c, compute);
 }
 
-int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep, size_t bytes,
-               cudaStream_t stream) {
+const int32_t *tc_prep_schedule(const ChainDims &c, const TcPlan &pl, const void *prep) {
+    return prep ? reinterpret_cast<const int32_t *>(static_cast<const char *>(prep) + scatter_bytes(c, pl))
+                : nullptr;
+}
+
+const int32_t *tc_prep_pair(const ChainDims &c, const TcPlan &pl, const void *prep) {
+    return prep ? tc_prep_schedule(c, pl, prep) + size_t(c.u_o) * c.d_o : nullptr;
+}
+
+const void *tc_prep_k4(const ChainDims &c, const TcPlan &pl, int compute, const void *prep) {
+    return prep && k4_bytes(c, compute) ? static_cast<const char *>(prep) + sched_end(c, pl) : nullptr;
+}
+
+int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_t *adj_o,
+               const int32_t *adj_i, void *prep, size_t bytes, cudaStream_t stream) {
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
     const size_t need = tc_prep_size(c, compute);
@@ -975,6 +963,51 @@ int tc_prepare(const ChainDims &c, int compute, const int32_t *adj_i, void *prep
     else
         prep_kernel<2><<<phases, kBlockM, 0, stream>>>(pl.p, adj_i, static_cast<uint16_t *>(prep));
     RBGP4_CHECK_LAUNCH("prep_kernel launch");
+    // the step schedule is a small host-side search over g_o's adjacency (once per matrix)
+    std::vector<int32_t> adj(size_t(c.u_o) * c.d_o), sched(adj.size()), adji(size_t(c.u_i) * c.d_i);
+    cudaError_t e = cudaMemcpyAsync(adj.data(), adj_o, adj.size() * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(adji.data(), adj_i, adji.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) {
+        set_error("rbgp4_prepare: reading the adjacency: %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    build_schedule(c.u_o, c.v_o, c.d_o, adj.data(), sched.data());
+    if (getenv("RBGP4_TC_NOSCHED"))
+        for (int u = 0; u < c.u_o; ++u)
+            for (int s2 = 0; s2 < c.d_o; ++s2) sched[size_t(u) * c.d_o + s2] = s2;
+    // pairs: per step, tile-rows reading the same K-block are matched two by two (symmetric)
+    std::vector<int32_t> both(2 * sched.size(), -1);
+    std::copy(sched.begin(), sched.end(), both.begin());
+    int32_t *pair = both.data() + sched.size();
+    for (int s2 = 0; s2 < c.d_o; ++s2)
+        for (int u = 0; u < c.u_o; ++u) {
+            if (pair[size_t(u) * c.d_o + s2] >= 0) continue;
+            const int kb = adj[size_t(u) * c.d_o + sched[size_t(u) * c.d_o + s2]];
+            for (int v = u + 1; v < c.u_o; ++v)
+                if (pair[size_t(v) * c.d_o + s2] < 0 && adj[size_t(v) * c.d_o + sched[size_t(v) * c.d_o + s2]] == kb) {
+                    pair[size_t(u) * c.d_o + s2] = v;
+                    pair[size_t(v) * c.d_o + s2] = u;
+                    break;
+                }
+        }
+    sched.swap(both);
+    e = cudaMemcpyAsync(const_cast<int32_t *>(tc_prep_schedule(c, pl, prep)), sched.data(),
+                        sched.size() * sizeof(int32_t), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // `sched` is a host temporary
+    if (e != cudaSuccess) {
+        set_error("rbgp4_prepare: writing the schedule: %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    if (const void *k4 = tc_prep_k4(c, pl, compute, prep)) {
+        if (values == nullptr) {
+            set_error("rbgp4_prepare: values needed for the bf16 relayout");
+            return RBGP4_EINVAL;
+        }
+        return gather_prepare(c, values, adji.data(), const_cast<void *>(k4), stream);
+    }
     return RBGP4_OK;
 }
 
@@ -988,6 +1021,9 @@ int tc_supported(const ChainDims &c, int compute, int out_dtype) {
 }
 
 size_t tc_workspace_size(const ChainDims &c, int compute) {
+    // K4 splits K over DSMEM (either mode)
+    if (gather_supported(c, compute, RBGP4_BF16, false) || gather_supported(c, compute, RBGP4_BF16, true))
+        return 0;
     TcPlan pl;
     if (!plan_tc(c, compute, &pl) || pl.p.ksplit <= 1) return 0;
     // (ksplit - 1) fp32 partial copies of the output, row-major (rows, n_cols)
@@ -1001,6 +1037,14 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
     pl.p.prep = static_cast<const uint16_t *>(prep);
+    pl.p.sched = tc_prep_schedule(c, pl, prep);
+    // g_b blocks >= 16 x 16: the gathered-block kernel (K4), no densification
+    {
+        const void *k4 = tc_prep_k4(c, pl, compute, prep);
+        if (gather_supported(c, compute, out_dtype, k4 != nullptr))
+            return launch_gather(c, out_dtype, values, adj_o, adj_i, pl.p.sched, tc_prep_pair(c, pl, prep), k4,
+                                 inp, out, stream);
+    }
     const int elt = compute == RBGP4_COMPUTE_TF32 ? 4 : 2;
     if (reinterpret_cast<uintptr_t>(inp) % 16 != 0 || (c.ld_in * elt) % 16 != 0) {
         set_error("tensor-core path needs a 16-byte aligned I with ld_in*%d %% 16 == 0", elt);
@@ -1047,10 +1091,28 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     if (const char *dbg = getenv("RBGP4_TC_DEBUG")) {
         pl.p.debug = atoi(dbg);
         if (pl.p.debug & 8192)
-            fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d ks=%d smem=%zu a_tmem=%d tmem=%d\n",
-                    pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.ksplit, pl.smem,
-                    pl.p.a_tmem, pl.p.tmem_cols);
-        if (pl.p.debug & 16) { pl.p.w_tma = 0; pl.p.nw = 1; pl.p.ws = 1; pl.p.w_stage_bytes = 0; }
+            fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d w_swz=%d ks=%d smem=%zu tmem=%d\n",
+                    pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.w_swz, pl.p.ksplit, pl.smem,
+                    pl.p.tmem_cols);
+        if (pl.p.debug & 16) { pl.p.w_tma = 0; pl.p.nw = 1; pl.p.ws = 1; pl.p.w_stage_bytes = 0; pl.p.w_swz = 0; }
+    }
+    // output tile store: (n_cols, rows) view, box = one 128-byte column atom x rows of a CTA
+    CUtensorMap omap;
+    memset(&omap, 0, sizeof(omap));
+    {
+        const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+        pl.p.ostore = staging_fits(pl, oelt) && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                      (c.ld_out * oelt) % 16 == 0 && (pl.p.tn * oelt) % 128 == 0;
+        if (pl.p.ostore) {
+            cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
+            cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
+            cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(pl.p.rows_valid)};
+            r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) pl.p.ostore = 0;
+        }
     }
     // compressed W tiles: 2-D (row_nnz, rows) view of the values, box (d_t, rows of a CTA)
     CUtensorMap wmap;
@@ -1065,7 +1127,7 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
         }
         r = enc(&wmap, elt == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                 2, const_cast<void *>(values), wdims, wstrides, wbox, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, w_swizzle(pl.p.w_swz),
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));
@@ -1080,10 +1142,10 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     }
     const bool obf = out_dtype == RBGP4_BF16;
     if (compute == RBGP4_COMPUTE_TF32)
-        return obf ? launch_typed<float, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
-                   : launch_typed<float, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
-    return obf ? launch_typed<__nv_bfloat16, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
-               : launch_typed<__nv_bfloat16, false>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
+        return obf ? launch_typed<float, true>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream)
+                   : launch_typed<float, false>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream);
+    return obf ? launch_typed<__nv_bfloat16, true>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream)
+               : launch_typed<__nv_bfloat16, false>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream);
 }
 
 // ---------------------------------------------------------------- K3: implicit im2col
@@ -1136,6 +1198,9 @@ int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
 }
 
 size_t conv_workspace_size(const ChainDims &c, const rbgp4_conv_desc *cv) {
+    if (cv != nullptr && (gather_conv_supported(c, cv, RBGP4_BF16, false) ||
+                          gather_conv_supported(c, cv, RBGP4_BF16, true)))
+        return 0;
     TcPlan pl;
     if (!conv_plan(c, cv, &pl) || pl.p.ksplit <= 1) return 0;
     return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(c.n_cols) * 4;
@@ -1148,6 +1213,13 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
     if (!conv_plan(c, cv, &pl)) return RBGP4_EUNSUPPORTED;
     if (c.n_cols == 0) return RBGP4_OK;
     pl.p.prep = static_cast<const uint16_t *>(prep);
+    pl.p.sched = tc_prep_schedule(c, pl, prep);
+    {
+        const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep);
+        if (gather_conv_supported(c, cv, out_dtype, k4 != nullptr))
+            return launch_gather_conv(c, cv, out_dtype, values, adj_o, adj_i, pl.p.sched, tc_prep_pair(c, pl, prep),
+                                      k4, x, out, stream);
+    }
     RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && (cv->c_in * 2) % 16 == 0,
                   "conv input must be 16-byte aligned NHWC bf16");
     auto enc = encode_fn();
@@ -1170,13 +1242,31 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
         set_error("cuTensorMapEncodeTiled(conv input) failed (%d)", int(r));
         return RBGP4_ECUDA;
     }
+    // NHWC output store: (c_out, pixels) view, box = the CTA's channels x tn pixels
+    CUtensorMap omap;
+    memset(&omap, 0, sizeof(omap));
+    {
+        const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+        pl.p.ostore = staging_fits(pl, oelt) && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+                      (c.rows * oelt) % 16 == 0 && pl.p.rows_valid * oelt >= 16;
+        if (pl.p.ostore) {
+            cuuint64_t odims[2] = {cuuint64_t(c.rows), cuuint64_t(c.n_cols)};
+            cuuint64_t ostrides[1] = {cuuint64_t(c.rows) * oelt};
+            cuuint32_t obox[2] = {cuuint32_t(pl.p.rows_valid), cuuint32_t(pl.p.tn)};
+            r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                    out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) pl.p.ostore = 0;
+        }
+    }
     memset(&wmap, 0, sizeof(wmap));
     if (pl.p.w_tma) {
         cuuint64_t wdims[2] = {cuuint64_t(c.row_nnz), cuuint64_t(c.rows)};
         cuuint64_t wstrides[1] = {cuuint64_t(c.row_nnz) * 2};
         cuuint32_t wbox[2] = {cuuint32_t(pl.p.ws * c.d_t), cuuint32_t(pl.p.rows_valid)};
         r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(values), wdims,
-                wstrides, wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                wstrides, wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, w_swizzle(pl.p.w_swz),
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));
@@ -1189,8 +1279,8 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
         return RBGP4_EWORKSPACE;
     }
     return out_dtype == RBGP4_BF16
-               ? launch_typed<__nv_bfloat16, true, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream)
-               : launch_typed<__nv_bfloat16, false, true>(pl, map, wmap, values, adj_o, adj_i, out, wsp, stream);
+               ? launch_typed<__nv_bfloat16, true, true>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream)
+               : launch_typed<__nv_bfloat16, false, true>(pl, map, wmap, omap, values, adj_o, adj_i, out, wsp, stream);
 }
 
 }  // namespace rbgp4

@@ -266,7 +266,8 @@ def prepared(fmt, compute: str, dev, desc):
         if nbytes == 0:
             return None
         buf = torch().empty(nbytes, dtype=torch().uint8, device=dev)
-        _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, fmt.adj_i.data_ptr(),
+        _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),
+                                        fmt.adj_i.data_ptr(),
                                         buf.data_ptr(), nbytes, stream_handle(dev)),
                       "rbgp4_prepare")
         fmt.prep[compute] = buf

@@ -120,3 +120,23 @@ def vgg19_cifar_512_tc(sparsity: float = 0.875, batch: int = 256, seed: int = 0)
             sp_i, (8, 8), n_cols=n, precision="f32", seed=seed + idx,
         ))
     return out
+
+
+def vgg19_cifar_512_tc16(sparsity: float = 0.875, batch: int = 256, seed: int = 0):
+    """Same VGG19-CIFAR layers with 16 x 16 dense element blocks ("VGG c10 TC").
+
+    Tile 128 x 128 with G_r = (1,1), G_b = (16,16), G_o = (4, K/128) at 50 % and G_i = (8,8)
+    carrying the rest: 75 / 87.5 % are G_i at 50 / 75 %.  Blocks of 16 x 16 are whole MMA
+    operands, so the product runs on the gathered-block kernel (no densification).
+    """
+    sp_i = {0.75: 0.5, 0.875: 0.75}[sparsity]
+    layers = [("conv9", 512, 2304, batch * 16)]
+    layers += [(f"conv{i}", 512, 4608, batch * 16) for i in (10, 11, 12)]
+    layers += [(f"conv{i}", 512, 4608, batch * 4) for i in (13, 14, 15, 16)]
+    out = []
+    for idx, (name, m, k, n) in enumerate(layers):
+        out.append(SweepConfig(
+            f"vgg19tc16-{name}-sp{sparsity * 100:g}", (m // 128, k // 128), 0.5, (1, 1), (8, 8),
+            sp_i, (16, 16), n_cols=n, precision="f32", seed=seed + idx,
+        ))
+    return out

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     lib = _native.lib()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.rbgp4_abi_version() == 1
+    assert lib.rbgp4_abi_version() == 2
 
 
 def test_desc_struct_layout():

@@ -31,7 +31,7 @@ def f64_oracle(w, inp):
 
 def test_device_and_library_present():
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    assert _native.lib().rbgp4_abi_version() == 1
+    assert _native.lib().rbgp4_abi_version() == 2
 
 
 @pytest.mark.parametrize("precision", ["f32", "f64"])

@@ -68,15 +68,19 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n, int mode, int iters,
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tslot;
     if (warp == 1) {
-        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (uint32_t(mode == 0) << 16) |
+        // mode 2 / 3: the gathered-block kernel's shapes -- A MN-major (2 = SDMM) or K-major
+        // (3 = conv) SW128, B K-major SW64 (compressed W rows of 64 bytes)
+        const uint32_t a_mn = mode == 2 ? 1u : 0u;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (uint32_t(mode == 0) << 16) |
                                (uint32_t(n >> 3) << 17) | (8u << 24);
-        const uint64_t ad = smem_desc(smem_u32(buf), 0, 1024, 2);
+        const uint64_t ad = mode == 2 ? smem_desc(smem_u32(buf), 64 * 128, 1024, 2) : smem_desc(smem_u32(buf), 0, 1024, 2);
         const uint64_t bd = mode == 0 ? smem_desc(smem_u32(buf + 16384), 64 * 128, 1024, 2)
-                                      : smem_desc(smem_u32(buf + 16384), 0, 1024, 2);
+                          : mode == 1 ? smem_desc(smem_u32(buf + 16384), 0, 1024, 2)
+                                      : smem_desc(smem_u32(buf + 16384), 0, 512, 4);
         long long t0 = 0, t1 = 0, t2 = 0;
         if (elect_one()) {
             // warm
-            for (int i = 0; i < 16; ++i) mma(tmem, ad + 2 * (i & 3), bd + (mode == 0 ? 128 * (i & 3) : 2 * (i & 3)), idesc, 1);
+            for (int i = 0; i < 16; ++i) mma(tmem, ad + (mode == 2 ? 128 * (i & 3) : 2 * (i & 3)), bd + (mode == 0 ? 128 * (i & 3) : mode >= 2 ? 2 * (i & 1) : 2 * (i & 3)), idesc, 1);
             tc_commit(&bar);
         }
         __syncwarp();
@@ -84,7 +88,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(int n, int mode, int iters,
         if (elect_one()) {
             t0 = clock64();
             for (int i = 0; i < iters; ++i)
-                mma(tmem, ad + 2 * (i & 3), bd + (mode == 0 ? 128 * (i & 3) : 2 * (i & 3)), idesc, 1);
+                mma(tmem, ad + (mode == 2 ? 128 * (i & 3) : 2 * (i & 3)), bd + (mode == 0 ? 128 * (i & 3) : mode >= 2 ? 2 * (i & 1) : 2 * (i & 3)), idesc, 1);
             t1 = clock64();
             tc_commit(&bar);
         }
@@ -172,15 +176,16 @@ int main() {
     long long *d, h[16];
     cudaMalloc(&d, 16 * sizeof(long long));
     const int iters = 1024;
-    for (int n : {64, 128, 256}) {
-        for (int mode : {0, 1}) {
+    for (int n : {16, 32, 64, 128, 256}) {
+        for (int mode : {0, 1, 2, 3}) {
+            if (mode < 2 && n < 64) continue;
             const size_t smem = 1024 + 16384 + n * 128;
             cudaFuncSetAttribute(mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             mma_kernel<<<1, 128, smem>>>(n, mode, iters, d);
             cudaError_t e = cudaDeviceSynchronize();
             cudaMemcpy(h, d, 2 * sizeof(long long), cudaMemcpyDeviceToHost);
             printf("MMA M128 N%-3d K16 B %s : issue %6.1f cyc/instr, complete %6.1f cyc/instr (floor %d) %s\n",
-                   n, mode == 0 ? "MN-major" : "K-major ", double(h[0]) / iters, double(h[1]) / iters,
+                   n, mode == 0 ? "MN-major" : mode == 1 ? "K-major " : mode == 2 ? "A-MN/B-K64" : "A-K/B-K64", double(h[0]) / iters, double(h[1]) / iters,
                    128 * n / 256, e == cudaSuccess ? "" : cudaGetErrorString(e));
         }
     }
