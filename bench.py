@@ -56,9 +56,12 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--factorisation", choices=["tc", "tc16", "paper"], default="tc",
+    ap.add_argument("--factorisation", choices=["tc", "tc16", "paper"], default="tc16",
                     help="base-graph factorisation of every layer (both are 87.5%% RBGP4)")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other factorisation")
+    ap.add_argument("--no-conv", action="store_true", help="skip the implicit-im2col conv leg")
+    ap.add_argument("--vgg-batch", type=int, default=32768,
+                    help="VGG19-CIFAR inference leg: global batch (sharded over ranks); 0 = skip")
     return ap.parse_args()
 
 
@@ -263,6 +266,101 @@ def workload_config(args, world):
             "l2": "inputs (170 MB bf16) larger than L2 (126 MB); no explicit flush"}
 
 
+# ----------------------------------------------------------------- conv / VGG legs
+def _flush_l2(torch, buf):
+    """Overwrite a buffer larger than L2 (126 MB) so the next step starts cold."""
+    buf.add_(1)
+
+
+def run_conv_leg(args, dev, stream, rank, world, dist):
+    """The same eight layers as convolutions on NHWC activations (implicit im2col, no
+    materialised I): SparseConv2d with the layer's RBGP4 weight, batch `args.batch` per rank,
+    bf16, ReLU fused.  Same FLOP count as the SDMM step; L2 flushed between steps."""
+    import torch
+    from paper_2006_13486_b200 import conv as kconv
+    layers = build_layers(args.sparsity, args.batch, args.factorisation)
+    convs, xs = [], []
+    gen = torch.Generator(device=dev).manual_seed(11 + rank)
+    for lay in layers:
+        c_in = lay["k"] // 9
+        hw = 4 if lay["n"] == 16 * args.batch else 2
+        convs.append(kconv.SparseConv2d(lay["w"], 3, relu=True))
+        xs.append((torch.rand((args.batch, hw, hw, c_in), device=dev, generator=gen) * 2 - 1)
+                  .to(torch.bfloat16))
+    flops = sum(lay["flops"] for lay in layers)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB
+    with torch.cuda.stream(stream):
+        outs = [c(x) for c, x in zip(convs, xs)]  # warm-up: prepared formats, tensor maps
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            outs = [c(x) for c, x in zip(convs, xs)]
+    torch.cuda.synchronize()
+    steps = max(10, args.steps // 4)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            g.replay()
+        for a, b in evs:
+            _flush_l2(torch, flush)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    act_bytes = sum(x.numel() * 2 for x in xs) + sum(o.numel() * 2 for o in outs) + \
+        sum(lay["nnz"] * 2 for lay in layers)
+    return {"value": flops * world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+            "path": "paper_2006_13486_b200.conv.SparseConv2d (implicit im2col, NHWC bf16, ReLU fused)",
+            "hbm_bytes_per_step": act_bytes, "l2": "256 MB overwrite between steps"}
+
+
+def run_vgg_leg(args, dev, stream, rank, world, dist):
+    """BASELINE config 5: full VGG19-CIFAR-100 RBGP4 inference (dense conv1 + classifier,
+    15 RBGP4 convs at `--sparsity`, 5 pools), synthetic global batch sharded over ranks."""
+    import torch
+    from paper_2006_13486_b200.vgg import VGG19Sparse
+    batch = max(1, args.vgg_batch // world)
+    net = VGG19Sparse(sparsity=args.sparsity, num_classes=100, seed=0, device=str(dev))
+    gen = torch.Generator(device=dev).manual_seed(5 + rank)
+    x = torch.randn(batch, 32, 32, 3, device=dev, generator=gen).to(torch.bfloat16)
+    with torch.cuda.stream(stream):
+        net(x)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            y = net(x)
+    torch.cuda.synchronize()
+    reps = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            g.replay()
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del y
+    return {"value": batch * world / (ms * 1e-3), "unit": "img/s", "ms_per_forward": ms,
+            "global_batch": batch * world, "sparsity": args.sparsity,
+            "sparse_tflops": net.sparse_flops_per_image * batch * world / (ms * 1e-3) / 1e12,
+            "model": "VGG19-CIFAR-100, RBGP4 convs 2-16 (bf16, NHWC), dense conv1 + classifier",
+            "data": "synthetic images, random-init weights"}
+
+
 # ----------------------------------------------------------------- GPU leg
 def run_ours(args):
     import torch
@@ -317,21 +415,20 @@ def run_ours(args):
         return layers, host_in, dev_out, graphs
 
     def timed(graphs, dom, steps, warmup, sampler=None):
-        # events around every launch of the timed region (one graph replay = one kernel):
-        # per-layer means for the report, the dominant layers' mean for the roofline
-        ev_s = [[torch.cuda.Event(enable_timing=True) for _ in graphs] for _ in range(steps)]
-        ev_e = [[torch.cuda.Event(enable_timing=True) for _ in graphs] for _ in range(steps)]
+        # events bracket only the dominant layers' launches inside the timed region (the
+        # roofline kernel); the other launches run back to back as in a plain step
+        ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
+        ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
 
         def step(record=None):
             for i, g in enumerate(graphs):
-                if record is not None:
-                    ev_s[record[0]][i].record(stream)
+                if record is not None and i in dom:
+                    ev_s[record[0]].record(stream)
                     g.replay()
-                    ev_e[record[0]][i].record(stream)
+                    ev_e[record[0]].record(stream)
+                    record[0] += 1
                 else:
                     g.replay()
-            if record is not None:
-                record[0] += 1
 
         with torch.cuda.stream(stream):
             for _ in range(warmup):
@@ -363,17 +460,30 @@ def run_ours(args):
             t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             elapsed_ms = float(t.item())
-        per_layer = [statistics.mean(ev_s[k][i].elapsed_time(ev_e[k][i]) for k in range(steps))
-                     for i in range(len(graphs))]
-        dom_ms = statistics.mean(per_layer[i] for i in dom)
-        return elapsed_ms, dom_ms, clocks, per_layer
+        dom_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
+        return elapsed_ms, (statistics.mean(dom_ms) if dom_ms else float("nan")), clocks
+
+    def per_layer(graphs, steps):
+        """Mean event-timed duration of every layer's launch (separate pass, for the report)."""
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in graphs] for _ in range(steps)]
+        with torch.cuda.stream(stream):
+            for k in range(steps):
+                for i, g in enumerate(graphs):
+                    evs[k][i][0].record(stream)
+                    g.replay()
+                    evs[k][i][1].record(stream)
+        torch.cuda.synchronize()
+        return [statistics.mean(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(steps))
+                for i in range(len(graphs))]
 
     stream = torch.cuda.Stream(device=dev)
     layers, host_in, dev_out, graphs = setup(args.factorisation)
     flops_step = sum(lay["flops"] for lay in layers)
     dom = [i for i, lay in enumerate(layers) if lay["k"] == 4608 and lay["n"] == 16 * args.batch]
-    elapsed_ms, dom_avg_ms, clocks, per_layer = timed(graphs, dom, args.steps, args.warmup,
-                                                      ClockSampler(dev.index))
+    elapsed_ms, dom_avg_ms, clocks = timed(graphs, dom, args.steps, args.warmup,
+                                           ClockSampler(dev.index))
+    layer_ms = per_layer(graphs, max(10, args.steps // 4))
     ms_per_step = elapsed_ms / args.steps
     value = flops_step * world / (ms_per_step * 1e-3) / 1e12
     launches_in_region = len(graphs) * args.steps  # graph replays of our kernels
@@ -385,7 +495,8 @@ def run_ours(args):
     achieved = bytes_launch / (dom_avg_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": f"tc_kernel<bf16> conv10-12 ({args.factorisation} factorisation) "
+                "kernel": f"{'gather_kernel (K4)' if args.factorisation == 'tc16' else 'tc_kernel (K2)'}"
+                          f"<bf16> conv10-12 ({args.factorisation} factorisation) "
                           f"(M,K,N)=({dom_layer['m']},{dom_layer['k']},"
                           f"{dom_layer['n']})", "algorithmic_bytes_per_launch": bytes_launch,
                 "avg_launch_us": dom_avg_ms * 1e3, "peak_source": peak_src,
@@ -419,6 +530,9 @@ def run_ours(args):
                "path": "paper_2006_13486_b200.rbgp4mm(w, pinned host bf16 tensor, params, "
                        "compute='bf16') per layer"}
 
+    conv_leg = None if args.no_conv else run_conv_leg(args, dev, stream, rank, world, dist)
+    vgg_leg = None if args.vgg_batch <= 0 else run_vgg_leg(args, dev, stream, rank, world, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
@@ -427,9 +541,9 @@ def run_ours(args):
 
     alt = None
     if not args.no_alt:
-        other = "paper" if args.factorisation == "tc" else "tc"
+        other = "tc" if args.factorisation == "tc16" else "tc16"
         a_layers, _, _, a_graphs = setup(other)
-        a_elapsed, a_dom, _, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
+        a_elapsed, a_dom, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
         a_ms = a_elapsed / max(10, args.steps // 4)
         a_flops = sum(lay["flops"] for lay in a_layers)
         alt = {"factorisation": FACTORISATIONS[other],
@@ -449,7 +563,8 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_in_region, "clocks": clocks,
             "layers_us": {lay["cfg"].config_id.split("-")[1]: round(ms * 1e3, 2)
-                          for lay, ms in zip(layers, per_layer)},
+                          for lay, ms in zip(layers, layer_ms)},
+            "conv_fused": conv_leg, "vgg19": vgg_leg,
             "alt_factorisation": alt,
         }))
     if world > 1:

@@ -1177,7 +1177,11 @@ int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
     RBGP4_REQUIRE(c.tk % 64 == 0 && cv->c_in % c.tk == 0,
                   "conv path needs tk %% 64 == 0 and c_in %% tk == 0 (tk=%d, c_in=%d)", c.tk, cv->c_in);
     RBGP4_REQUIRE(cv->width <= 256 && cv->height <= 256, "feature map too large for one TMA box");
-    for (int tn : {128, 64}) {
+    // wide pixel tiles when the grid is many waves deep: the per-CTA setup (TMEM, barriers,
+    // scatter table, pipeline fill) is amortised over twice the pixels
+    const bool wide = c.n_cols >= int64_t(kNumSMs) * 256 * 4 && !getenv("RBGP4_CONV_NARROW");
+    for (int tn : {256, 128, 64}) {
+        if (tn == 256 && !wide) continue;
         int th, tb;
         if (!conv_tile(*cv, tn, &th, &tb)) continue;
         if (!plan_tc(c, RBGP4_COMPUTE_BF16, pl, tn)) continue;

@@ -10,7 +10,8 @@ sparse; the first convolution and the classifier stay dense.  Here:
 * batch norm is folded away and biases are omitted (synthetic, random-init weights).
 
 Factorisations are chosen per layer (`layer_chain`): tiles of up to 128 x 128 built from
-dense g_b = (b, b) element blocks (b = 8 when the sparsity split allows it, else 4 / 2),
+dense g_b = (b, b) element blocks (b = 16 when the sparsity split allows it -- whole MMA
+operands for the gathered-block kernel -- else 8 / 4 / 2),
 g_r = (1,1), g_o carrying up to 50 % when it has >= 4 tile-rows, g_i the rest.  Every factor
 is a certified Ramanujan lift chain from the reference's generator.
 """
@@ -52,7 +53,7 @@ def layer_chain(c_out: int, c_in: int, sparsity: float, seed: int = 0, k: int = 
     sp_o = 0.5 if u_o >= 4 else 0.0
     sp_i = 1.0 - (1.0 - sparsity) / (1.0 - sp_o)
     last = None
-    for b in (8, 4, 2):
+    for b in (16, 8, 4, 2):
         u_i, v_i = tm // b, tk // b
         d_i, d_r = v_i * (1 - sp_i), u_i * (1 - sp_i)
         if d_i < 2 or d_r < 2 or d_i != int(d_i) or d_r != int(d_r):

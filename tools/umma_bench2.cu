@@ -59,6 +59,56 @@ __global__ void __launch_bounds__(128, 1) k(int n, int b_span, int a_lbo, int ds
     __syncthreads();
     if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
+// the K4 relayout step: nmma MMAs (N=n) with uniform descriptor arithmetic, commit, wait;
+// `steps` times -> cycles per step (issue + commit + completion wait)
+__global__ void __launch_bounds__(128, 1) steps_k(int n, int nmma, int steps, long long *out) {
+    extern __shared__ unsigned char raw[];
+    unsigned char *buf = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t tslot;
+    __shared__ uint64_t bar;
+    for (int i = threadIdx.x; i < (65536 + 16384) / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(buf)[i] = 0x3c003c00u;
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar))); asm volatile("fence.mbarrier_init.release.cluster;"); }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tslot;
+    if (threadIdx.x / 32 == 1) {
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (uint32_t(n >> 3) << 17) | (8u << 24);
+        const uint64_t ad = smem_desc(smem_u32(buf), 16384, 1024, 2);
+        const uint64_t bd = smem_desc(smem_u32(buf + 65536), 0, 256, 6);
+        long long t0 = clock64();
+        for (int s = 0; s < steps; ++s) {
+            uint32_t el = 0;
+            asm volatile("{\n.reg .pred p;\n.reg .b32 r;\nelect.sync r|p, 0xffffffff;\nselp.b32 %0, 1, 0, p;\n}\n" : "=r"(el));
+            if (el) {
+                uint64_t b = bd;
+                uint32_t d = tmem;
+                for (int kb = 0; kb < nmma; ++kb) {
+                    asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+                                 "l"(ad + uint32_t(kb * 128)), "l"(b), "r"(idesc), "r"(s > 0 ? 1 : 0));
+                    b += uint32_t((n * 32) >> 4);
+                    d += uint32_t(n);
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
+            }
+            __syncwarp();
+            asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W;\n}\n" ::"r"(smem_u32(&bar)), "r"(s & 1) : "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        long long t1 = clock64();
+        if (threadIdx.x == 32) out[0] = t1 - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 int main() {
     long long *d, h[2];
     cudaMalloc(&d, 16);
@@ -74,6 +124,14 @@ int main() {
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
         printf("N=%3d Bspan=%3d A_LBO=%5d dstep=%d nblk=%2d : issue %6.1f complete %6.1f cyc/MMA %s\n", c.n, c.span,
                c.lbo, c.dstep, c.nblk, double(h[0]) / iters, double(h[1]) / iters, e ? cudaGetErrorString(e) : "");
+    }
+    cudaFuncSetAttribute(steps_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + 65536 + 16384);
+    for (int n : {16, 32}) for (int nm : {8, 16}) {
+        steps_k<<<1, 128, 1024 + 65536 + 16384>>>(n, nm, 64, d);
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
+        printf("step of %2d MMAs N=%d + commit + wait: %7.1f cycles/step %s\n", nm, n, double(h[0]) / 64,
+               e ? cudaGetErrorString(e) : "");
     }
     return 0;
 }

@@ -1,5 +1,6 @@
 """Time the full VGG19-CIFAR RBGP4 inference forward (CUDA graph, device events)."""
-import sys, time
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2006_13486_b200.vgg import VGG19Sparse
 
