@@ -60,6 +60,8 @@ def parse_args():
                     help="base-graph factorisation of every layer (both are 87.5%% RBGP4)")
     ap.add_argument("--no-alt", action="store_true", help="skip timing the other factorisation")
     ap.add_argument("--no-conv", action="store_true", help="skip the implicit-im2col conv leg")
+    ap.add_argument("--wrn-batch", type=int, default=512,
+                    help="WRN-40-4 leg (config 3): batch per rank; 0 = skip")
     ap.add_argument("--vgg-batch", type=int, default=32768,
                     help="VGG19-CIFAR inference leg: global batch (sharded over ranks); 0 = skip")
     return ap.parse_args()
@@ -361,6 +363,39 @@ def run_vgg_leg(args, dev, stream, rank, world, dist):
             "data": "synthetic images, random-init weights"}
 
 
+def run_wrn_leg(args, dev, stream, rank, world, dist):
+    """BASELINE config 3: WideResNet-40-4 CIFAR-10, all 39 non-first convs RBGP4 sparse,
+    synthetic batch `--wrn-batch` per rank; the bf16 tcgen05 path against the fp32 FFMA path."""
+    import torch
+    from paper_2006_13486_b200.wrn import WRN40_4Sparse
+    batch = args.wrn_batch
+    net = WRN40_4Sparse(sparsity=args.sparsity, seed=0, device=str(dev))
+    gen = torch.Generator(device=dev).manual_seed(7 + rank)
+    x = torch.randn(batch, 32, 32, 3, device=dev, generator=gen)
+    flops = net.sparse_flops(batch)
+    res = {"global_batch": batch * world, "sparsity": args.sparsity,
+           "model": "WideResNet-40-4 CIFAR-10: dense conv1 + FC, 39 RBGP4 convs (36 3x3 + 3 1x1 shortcuts)",
+           "data": "synthetic images, random-init weights", "sparse_gflop_per_forward": flops / 1e9}
+    for compute in ("bf16", "ffma"):
+        with torch.cuda.stream(stream):
+            net(x, compute=compute)  # warm-up: prepared formats, tensor maps
+            reps = 3
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(reps):
+                net(x, compute=compute)
+            b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        res[compute] = {"ms_per_forward": ms, "img_s": batch * world / (ms * 1e-3),
+                        "sparse_tflops": flops * world / (ms * 1e-3) / 1e12}
+    return res
+
+
 # ----------------------------------------------------------------- GPU leg
 def run_ours(args):
     import torch
@@ -532,6 +567,7 @@ def run_ours(args):
 
     conv_leg = None if args.no_conv else run_conv_leg(args, dev, stream, rank, world, dist)
     vgg_leg = None if args.vgg_batch <= 0 else run_vgg_leg(args, dev, stream, rank, world, dist)
+    wrn_leg = None if args.wrn_batch <= 0 else run_wrn_leg(args, dev, stream, rank, world, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -564,7 +600,7 @@ def run_ours(args):
             "gpu_launches": launches_in_region, "clocks": clocks,
             "layers_us": {lay["cfg"].config_id.split("-")[1]: round(ms * 1e3, 2)
                           for lay, ms in zip(layers, layer_ms)},
-            "conv_fused": conv_leg, "vgg19": vgg_leg,
+            "conv_fused": conv_leg, "vgg19": vgg_leg, "wrn40_4": wrn_leg,
             "alt_factorisation": alt,
         }))
     if world > 1:

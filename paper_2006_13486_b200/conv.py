@@ -36,11 +36,19 @@ def columns_to_conv_weight(dense: np.ndarray, c_in: int, kh: int, kw: int) -> np
     return np.ascontiguousarray(dense.reshape(c_out, kh, kw, c_in).transpose(0, 3, 1, 2))
 
 
-def sparse_conv2d(w, x, kernel_size: int = 3, *, relu: bool = False, out=None, out_dtype=None):
-    """NHWC conv of `x` (batch, H, W, c_in) with chain matrix `w`, stride 1, 'same' padding.
+def conv_out_hw(height: int, width: int, k: int, stride: int):
+    """Output map of a 'same'-padded (pad = (k-1)/2) k x k convolution of stride 1 or 2."""
+    pad = (k - 1) // 2
+    return (height + 2 * pad - k) // stride + 1, (width + 2 * pad - k) // stride + 1
 
-    Returns an NHWC (batch, H, W, c_out) CUDA tensor.  `x` must be a CUDA bf16 tensor
-    (contiguous NHWC); the weight values are converted to bf16 once and cached.
+
+def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = False, out=None,
+                  out_dtype=None):
+    """NHWC conv of `x` (batch, H, W, c_in) with chain matrix `w`, 'same' padding, stride 1 or 2.
+
+    Returns an NHWC (batch, H', W', c_out) CUDA tensor.  `x` must be a CUDA bf16 tensor
+    (contiguous NHWC); the weight values are converted to bf16 once and cached.  Stride 2 is
+    read by strided TMA boxes (every other input pixel); 1 x 1 kernels have no padding.
     """
     t = torch()
     if w.chain.k != 4:
@@ -55,20 +63,23 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, relu: bool = False, out=None, o
         raise ShapeError(f"weight has {w.cols} columns, conv needs kh*kw*c_in = {kh * kw * c_in}")
     if kh % 2 != 1:
         raise InvalidArgumentError("only odd kernel sizes ('same' padding) are supported")
+    if stride not in (1, 2):
+        raise InvalidArgumentError(f"stride must be 1 or 2, got {stride}")
     x = x.contiguous()
     dev = resolve_device(x.device)
     res_dt = out_dtype if out_dtype is not None else t.bfloat16
+    oh, ow = conv_out_hw(height, width, kh, stride)
     with t.cuda.device(dev):
         fmt = device_format(w, dev, t.bfloat16)
-        n_cols = batch * height * width
+        n_cols = batch * oh * ow
         desc = make_desc(fmt.desc_fields, n_cols, n_cols, n_cols)
-        cv = _native.ConvDesc(batch, height, width, c_in, kh, kw, (kh - 1) // 2, 1, int(bool(relu)))
+        cv = _native.ConvDesc(batch, height, width, c_in, kh, kw, (kh - 1) // 2, stride, int(bool(relu)))
         if out is None:
-            res = t.empty((batch, height, width, w.rows), dtype=res_dt, device=dev)
+            res = t.empty((batch, oh, ow, w.rows), dtype=res_dt, device=dev)
         else:
             res = out
-            if tuple(res.shape) != (batch, height, width, w.rows) or not res.is_contiguous():
-                raise ShapeError("out must be a contiguous NHWC (batch, H, W, c_out) tensor")
+            if tuple(res.shape) != (batch, oh, ow, w.rows) or not res.is_contiguous():
+                raise ShapeError("out must be a contiguous NHWC (batch, H', W', c_out) tensor")
         if n_cols == 0:
             return res
         lib = _native.lib()
@@ -85,13 +96,13 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, relu: bool = False, out=None, o
 
 
 class SparseConv2d:
-    """3x3 (or kxk) stride-1 'same' convolution with an RBGP4-patterned weight (NHWC bf16)."""
+    """k x k 'same' convolution (stride 1 or 2) with an RBGP4-patterned weight (NHWC bf16)."""
 
-    def __init__(self, w, kernel_size: int = 3, relu: bool = True):
-        self.w, self.kernel_size, self.relu = w, kernel_size, relu
+    def __init__(self, w, kernel_size: int = 3, relu: bool = True, stride: int = 1):
+        self.w, self.kernel_size, self.relu, self.stride = w, kernel_size, relu, stride
 
     def __call__(self, x):
-        return sparse_conv2d(self.w, x, self.kernel_size, relu=self.relu)
+        return sparse_conv2d(self.w, x, self.kernel_size, stride=self.stride, relu=self.relu)
 
 
 class SparseLinear:

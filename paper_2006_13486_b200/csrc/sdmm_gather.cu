@@ -72,7 +72,7 @@ struct GParams {
     const int32_t *pair;
     int32_t mc;
     // implicit-im2col convolution
-    int32_t conv, c_in, img_h, img_w, kw, pad, relu;
+    int32_t conv, c_in, img_h, img_w, kw, pad, relu, stride;  // img_h/img_w: OUTPUT map
 };
 
 template <bool OUT_BF16, bool CONV>
@@ -184,10 +184,11 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         if (pb >= 0) {  // paired: channel atoms alternate between the two CTAs
                             if ((a & 1) != (tbm < pb ? 0 : 1)) continue;
                             tma_load_4d_mc(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
-                                           tj - p.pad, h0 + ti - p.pad, b0, uint16_t((1u << tbm) | (1u << pb)));
+                                           tj - p.pad, h0 * p.stride + ti - p.pad, b0,
+                                           uint16_t((1u << tbm) | (1u << pb)));
                         } else {
                             tma_load_4d(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
-                                        tj - p.pad, h0 + ti - p.pad, b0);
+                                        tj - p.pad, h0 * p.stride + ti - p.pad, b0);
                         }
                     }
                 } else if (p.mc) {
@@ -734,11 +735,13 @@ int gather_supported(const ChainDims &c, int compute, int out_dtype, bool relayo
 int gather_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, bool relayout) {
     GPlan pl;
     if (!gather_plan(c, RBGP4_COMPUTE_BF16, true, relayout, &pl)) return 0;
-    const int hw = cv->height * cv->width;
-    // a 128-pixel tile = whole rows of one image, or whole images
-    const bool tiles = (kBatch <= hw) ? (hw % kBatch == 0 && kBatch % cv->width == 0) : (kBatch % hw == 0);
-    return tiles && cv->c_in % 64 == 0 && cv->c_in % c.tk == 0 && cv->stride == 1 &&
-           (c.rows * (out_dtype == RBGP4_BF16 ? 2 : 4)) % 16 == 0;
+    const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
+    const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
+    const int hw = oh * ow;
+    // a 128-pixel tile = whole output rows of one image, or whole images
+    const bool tiles = (kBatch <= hw) ? (hw % kBatch == 0 && kBatch % ow == 0) : (kBatch % hw == 0);
+    return tiles && cv->c_in % 64 == 0 && cv->c_in % c.tk == 0 && (cv->stride == 1 || cv->stride == 2) &&
+           ow * cv->stride <= 256 && (c.rows * (out_dtype == RBGP4_BF16 ? 2 : 4)) % 16 == 0;
 }
 
 int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,
@@ -752,25 +755,31 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
     pl.p.conv = 1;
     pl.p.c_in = cv->c_in;
-    pl.p.img_h = cv->height;
-    pl.p.img_w = cv->width;
+    const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
+    const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
+    pl.p.img_h = oh;
+    pl.p.img_w = ow;
+    pl.p.stride = cv->stride;
     pl.p.kw = cv->kw;
     pl.p.pad = cv->pad;
     pl.p.relu = cv->relu;
     auto enc = encode_fn();
     RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0,
                   "conv input / output must be 16-byte aligned");
-    const int hw = cv->height * cv->width;
-    const int th = kBatch <= hw ? kBatch / cv->width : cv->height;
+    const int hw = oh * ow;
+    const int th = kBatch <= hw ? kBatch / ow : oh;
     const int tb = kBatch <= hw ? 1 : kBatch / hw;
     CUtensorMap imap, wmap, omap;
-    cuuint32_t estr[4] = {1, 1, 1, 1};
+    const cuuint32_t sd = cuuint32_t(cv->stride);
+    cuuint32_t estr[4] = {1, sd, sd, 1};        // strided conv: every stride-th input pixel
+    const cuuint32_t ones4[4] = {1, 1, 1, 1};   // W and O maps
     {
+        const int64_t ihw = int64_t(cv->height) * cv->width;
         cuuint64_t dims[4] = {cuuint64_t(cv->c_in), cuuint64_t(cv->width), cuuint64_t(cv->height),
                               cuuint64_t(cv->batch)};
         cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
-                                 cuuint64_t(hw) * cv->c_in * 2};
-        cuuint32_t box[4] = {64, cuuint32_t(cv->width), cuuint32_t(th), cuuint32_t(tb)};
+                                 cuuint64_t(ihw) * cv->c_in * 2};
+        cuuint32_t box[4] = {64, cuuint32_t(ow) * sd, cuuint32_t(th) * sd, cuuint32_t(tb)};
         CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -786,7 +795,7 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
         cuuint64_t ostrides[1] = {cuuint64_t(c.rows) * oelt};
         cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(kBatch)};
         CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                         2, out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         2, out, odims, ostrides, obox, ones4, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {

@@ -79,7 +79,8 @@ struct TcParams {
     // implicit-im2col convolution (K3): I is never materialised; x is NHWC bf16 and the
     // slab of step s is the tap (i, j) / channel block of its K rows, fetched by a 4-D TMA
     // box at the tap-shifted coordinates (out-of-bounds = zero padding); O is NHWC.
-    int32_t conv, c_in, img_h, img_w, kw, pad, relu, th, tb;
+    // (img_h, img_w = OUTPUT map; the input map is stride x larger, read by strided TMA boxes)
+    int32_t conv, c_in, img_h, img_w, kw, pad, relu, th, tb, stride;
     int32_t ostore;          // epilogue stages the output tile in shared memory and TMA-stores it
     int32_t w_swz;           // swizzle span (bytes) of the compressed-W stage rows: 0 / 32 / 64 / 128
 };
@@ -251,7 +252,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                     const uint32_t k_atom_bytes = uint32_t(p.tn) * 128;
                     for (int a = 0; a < p.tk / 64; ++a)
                         tma_load_4d(dst + a * k_atom_bytes, &imap, &full_b[st], c0 + 64 * a,
-                                    tj - p.pad, h0 + ti - p.pad, b0);
+                                    tj - p.pad, h0 * p.stride + ti - p.pad, b0);
                 } else if (p.i3d) {
                     // one instruction for the whole slab: (atom cols, K rows, atoms) box
                     tma_load_3d(dst, &imap, &full_b[st], 0, krow, int32_t(n0) / atom_cols);
@@ -1150,15 +1151,22 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
 
 // ---------------------------------------------------------------- K3: implicit im2col
 namespace {
+// output map of a 'same'-padded (pad = (k-1)/2) convolution with stride 1 or 2
+void conv_out(const rbgp4_conv_desc &cv, int *oh, int *ow) {
+    *oh = (cv.height + 2 * cv.pad - cv.kh) / cv.stride + 1;
+    *ow = (cv.width + 2 * cv.pad - cv.kw) / cv.stride + 1;
+}
 int conv_tile(const rbgp4_conv_desc &cv, int tn, int *th, int *tb) {
-    const int hw = cv.height * cv.width;
-    if (tn % cv.width) return 0;
+    int oh, ow;
+    conv_out(cv, &oh, &ow);
+    const int hw = oh * ow;
+    if (tn % ow) return 0;
     if (tn <= hw) {
-        *th = tn / cv.width;
+        *th = tn / ow;
         *tb = 1;
-        return cv.height % *th == 0;
+        return oh % *th == 0;
     }
-    *th = cv.height;
+    *th = oh;
     *tb = tn / hw;
     return tn % hw == 0 && *tb <= 256;
 }
@@ -1166,14 +1174,16 @@ int conv_tile(const rbgp4_conv_desc &cv, int tn, int *th, int *tb) {
 
 int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
     RBGP4_REQUIRE(cv != nullptr, "null conv descriptor");
-    RBGP4_REQUIRE(cv->stride == 1 && cv->pad * 2 == cv->kh - 1 && cv->kh == cv->kw,
-                  "implicit-im2col path supports stride-1 'same' square convolutions (kh=%d, pad=%d, "
-                  "stride=%d)", cv->kh, cv->pad, cv->stride);
+    RBGP4_REQUIRE((cv->stride == 1 || cv->stride == 2) && cv->pad * 2 == cv->kh - 1 && cv->kh == cv->kw,
+                  "implicit-im2col path supports 'same'-padded square convolutions of stride 1 or 2 "
+                  "(kh=%d, pad=%d, stride=%d)", cv->kh, cv->pad, cv->stride);
     RBGP4_REQUIRE(c.cols == int64_t(cv->kh) * cv->kw * cv->c_in,
                   "chain columns %lld != kh*kw*c_in = %d (tap-major im2col order)", (long long)c.cols,
                   cv->kh * cv->kw * cv->c_in);
-    RBGP4_REQUIRE(c.n_cols == int64_t(cv->batch) * cv->height * cv->width,
-                  "n_cols %lld != batch*height*width", (long long)c.n_cols);
+    int oh, ow;
+    conv_out(*cv, &oh, &ow);
+    RBGP4_REQUIRE(c.n_cols == int64_t(cv->batch) * oh * ow,
+                  "n_cols %lld != batch*out_height*out_width", (long long)c.n_cols);
     RBGP4_REQUIRE(c.tk % 64 == 0 && cv->c_in % c.tk == 0,
                   "conv path needs tk %% 64 == 0 and c_in %% tk == 0 (tk=%d, c_in=%d)", c.tk, cv->c_in);
     RBGP4_REQUIRE(cv->width <= 256 && cv->height <= 256, "feature map too large for one TMA box");
@@ -1187,8 +1197,9 @@ int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
         if (!plan_tc(c, RBGP4_COMPUTE_BF16, pl, tn)) continue;
         pl->p.conv = 1;
         pl->p.c_in = cv->c_in;
-        pl->p.img_h = cv->height;
-        pl->p.img_w = cv->width;
+        pl->p.img_h = oh;
+        pl->p.img_w = ow;
+        pl->p.stride = cv->stride;
         pl->p.kw = cv->kw;
         pl->p.pad = cv->pad;
         pl->p.relu = cv->relu;
@@ -1237,8 +1248,11 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
                           cuuint64_t(cv->batch)};
     cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
                              cuuint64_t(cv->height) * cv->width * cv->c_in * 2};
-    cuuint32_t box[4] = {64, cuuint32_t(cv->width), cuuint32_t(pl.p.th), cuuint32_t(pl.p.tb)};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
+    // strided convolution: the box spans stride x the output extent and loads every stride-th pixel
+    const cuuint32_t sd = cuuint32_t(cv->stride);
+    cuuint32_t box[4] = {64, cuuint32_t(pl.p.img_w) * sd, cuuint32_t(pl.p.th) * sd, cuuint32_t(pl.p.tb)};
+    cuuint32_t estr[4] = {1, sd, sd, 1};
+    const cuuint32_t ones4[4] = {1, 1, 1, 1};
     CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides,
                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1258,7 +1272,7 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
             cuuint64_t ostrides[1] = {cuuint64_t(c.rows) * oelt};
             cuuint32_t obox[2] = {cuuint32_t(pl.p.rows_valid), cuuint32_t(pl.p.tn)};
             r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                    out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    out, odims, ostrides, obox, ones4, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) pl.p.ostore = 0;
@@ -1270,7 +1284,7 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
         cuuint64_t wstrides[1] = {cuuint64_t(c.row_nnz) * 2};
         cuuint32_t wbox[2] = {cuuint32_t(pl.p.ws * c.d_t), cuuint32_t(pl.p.rows_valid)};
         r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(values), wdims,
-                wstrides, wbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, w_swizzle(pl.p.w_swz),
+                wstrides, wbox, ones4, CU_TENSOR_MAP_INTERLEAVE_NONE, w_swizzle(pl.p.w_swz),
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) {
             set_error("cuTensorMapEncodeTiled(values) failed (%d)", int(r));

@@ -21,16 +21,17 @@ def conv_chain(c_out, c_in, k=3, sp_i=0.5, seed=0):
     return wl.build_chain(cfg)
 
 
-def im2col_nhwc(x, k):
-    """(B, H, W, C) -> (k*k*C, B*H*W), tap-major rows, 'same' zero padding."""
+def im2col_nhwc(x, k, stride=1):
+    """(B, H, W, C) -> (k*k*C, B*H'*W'), tap-major rows, 'same' zero padding, stride 1 or 2."""
     b, h, w, c = x.shape
     p = k // 2
+    oh, ow = (h + 2 * p - k) // stride + 1, (w + 2 * p - k) // stride + 1
     xp = np.zeros((b, h + 2 * p, w + 2 * p, c), dtype=x.dtype)
     xp[:, p:p + h, p:p + w] = x
     rows = []
     for i in range(k):
         for j in range(k):
-            rows.append(xp[:, i:i + h, j:j + w, :].reshape(b * h * w, c).T)
+            rows.append(xp[:, i:i + stride * oh:stride, j:j + stride * ow:stride, :].reshape(b * oh * ow, c).T)
     return np.concatenate(rows, axis=0)
 
 
@@ -91,3 +92,47 @@ def test_sparse_linear_matches_oracle():
     xb = x.to(torch.bfloat16).float().numpy().astype(np.float64)
     want = (w.to_dense().astype(np.float64) @ xb.T).T
     assert oracle.rel_l2(y, want) < 1e-2
+
+
+def test_im2col_oracle_stride2_matches_direct_conv():
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((2, 6, 8, 3))
+    wgt = rng.standard_normal((5, 3, 3, 3))
+    got = (conv.conv_weight_to_columns(wgt) @ im2col_nhwc(x, 3, 2)).T.reshape(2, 3, 4, 5)
+    xp = np.pad(x, ((0, 0), (1, 1), (1, 1), (0, 0)))
+    want = np.zeros((2, 3, 4, 5))
+    for i in range(3):
+        for j in range(3):
+            want += np.einsum("bhwc,oc->bhwo", xp[:, i:i + 6:2, j:j + 8:2, :], wgt[:, :, i, j])
+    assert np.allclose(got, want)
+    assert conv.conv_out_hw(32, 32, 3, 2) == (16, 16) and conv.conv_out_hw(32, 32, 1, 2) == (16, 16)
+
+
+STRIDED = [  # (c_out, c_in, k, stride, hw, batch, g_b)
+    (128, 128, 3, 2, 16, 2, (8, 8)), (128, 128, 1, 1, 8, 2, (8, 8)), (128, 128, 1, 2, 16, 4, (8, 8)),
+    (128, 128, 3, 2, 16, 2, (16, 16)), (128, 128, 1, 2, 8, 16, (16, 16)), (256, 128, 3, 2, 32, 1, (16, 16)),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c_out,c_in,k,stride,hw,batch,g_b", STRIDED)
+def test_strided_and_pointwise_conv_match_oracle(c_out, c_in, k, stride, hw, batch, g_b):
+    import torch
+    v_o = k * k * c_in // 128
+    g_i = (128 // g_b[0], 128 // g_b[1])
+    cfg = wl.SweepConfig("sconv", (c_out // 128, v_o), 0.0, (1, 1), g_i, 0.75 if g_b == (16, 16) else 0.5,
+                         g_b, n_cols=1, seed=c_out + k + stride + hw)
+    chain = wl.build_chain(cfg)
+    w = ks.init_random(chain, 9, precision="f32")
+    x = np.random.default_rng(5).uniform(-1, 1, (batch, hw, hw, c_in)).astype(np.float32)
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    got = conv.sparse_conv2d(w, xb.cuda(), k, stride=stride, out_dtype=torch.float32).cpu().numpy()
+    oh = (hw + 2 * (k // 2) - k) // stride + 1
+    w64 = ks.RcubsMatrix(chain, torch.from_numpy(w.values.astype(np.float32)).to(torch.bfloat16)
+                         .double().numpy())
+    ref = oracle.reference_product(w64, np.ascontiguousarray(im2col_nhwc(xb.float().numpy().astype(np.float64),
+                                                                          k, stride)), threads=8)
+    ref = ref.T.reshape(batch, oh, oh, c_out)
+    assert got.shape == ref.shape
+    assert oracle.rel_l2(got, ref) < 1e-5
+
