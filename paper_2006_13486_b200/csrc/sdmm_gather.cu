@@ -75,7 +75,10 @@ struct GParams {
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, stride;  // img_h/img_w: OUTPUT map
 };
 
-template <bool OUT_BF16, bool CONV>
+// MMA_N (= bm, or d_r * bm in relayout mode) is a template constant so the instruction
+// descriptor is an immediate: computed at run time, ptxas rematerialised it from the constant
+// bank through a uniform->vector->uniform round trip before every UTCHMMA (tools/k4_trace.py)
+template <bool OUT_BF16, bool CONV, int MMA_N>
 __global__ void __launch_bounds__(kGThreads, 2)
 gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
               const __grid_constant__ CUtensorMap omap, const GParams p,
@@ -162,7 +165,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // ================= TMA producer: I slab + W tile of each step, one barrier ======
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
-            mbar_wait(&empty[st], ((s / p.ns) & 1) ^ 1);
+            if (p.debug & 256) mbar_wait_sleep(&empty[st], ((s / p.ns) & 1) ^ 1, 64);
+            else mbar_wait(&empty[st], ((s / p.ns) & 1) ^ 1);
             const int j = srow ? srow[s] : s_begin + s;  // g_o adjacency slot of this step
             const int32_t krow = orow[j] * p.tk;
             const bool leader = elect_one();
@@ -221,7 +225,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // B K-major (compressed W rows), N = bm, M = 128
         const uint32_t a_mn = CONV ? 0u : 1u;
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (0u << 16) |
-                               (uint32_t(p.mma_n >> 3) << 17) | (uint32_t(kBatch >> 4) << 24);
+                               (uint32_t(MMA_N >> 3) << 17) | (uint32_t(kBatch >> 4) << 24);
         const uint32_t ring_a = smem_u32(ring);
         const uint32_t w_code = p.w_swz == 128 ? 2u : p.w_swz == 64 ? 4u : 6u;
         // descriptors of stage 0; a stage / table entry only moves the 14-bit start field
@@ -491,6 +495,7 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     p.d_r = relayout ? c.u_i * c.d_i / c.v_i : 1;
     p.mma_n = relayout ? p.d_r * c.bm : c.bm;
     p.w_rows = relayout ? c.tm * c.d_i : c.tm;
+    if (p.mma_n != 16 && p.mma_n != 32 && p.mma_n != 48 && p.mma_n != 64 && p.mma_n != 128) return 0;
     const int n_mma = (relayout ? c.v_i : c.u_i * c.d_i) * (c.bk / 16);
     if (n_mma > kMaxMma) return 0;
     p.i_bytes = c.tk * kBatch * 2;
@@ -613,7 +618,17 @@ template <bool OUT_BF16, bool CONV>
 int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensorMap &wmap,
                         const CUtensorMap &omap, const int32_t *adj_o, const int32_t *adj_i,
                         cudaStream_t stream) {
-    auto kern = gather_kernel<OUT_BF16, CONV>;
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, GParams, const int32_t *, const int32_t *) = nullptr;
+    switch (pl.p.mma_n) {
+        case 16: kern = gather_kernel<OUT_BF16, CONV, 16>; break;
+        case 32: kern = gather_kernel<OUT_BF16, CONV, 32>; break;
+        case 48: kern = gather_kernel<OUT_BF16, CONV, 48>; break;
+        case 64: kern = gather_kernel<OUT_BF16, CONV, 64>; break;
+        case 128: kern = gather_kernel<OUT_BF16, CONV, 128>; break;
+        default:
+            set_error("gather kernel: no instantiation for MMA N = %d", pl.p.mma_n);
+            return RBGP4_EUNSUPPORTED;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(gather): %s", cudaGetErrorString(e));
