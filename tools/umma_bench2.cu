@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(128, 1) k(int n, int b_span, int a_lbo, int ds
 }
 // the K4 relayout step: nmma MMAs (N=n) with uniform descriptor arithmetic, commit, wait;
 // `steps` times -> cycles per step (issue + commit + completion wait)
-__global__ void __launch_bounds__(128, 1) steps_k(int n, int nmma, int steps, long long *out) {
+__global__ void __launch_bounds__(128, 1) steps_k(int n, int nmma, int steps, long long *out, int bspan = 32, int kcycle = 1, int dsame = 0) {
     extern __shared__ unsigned char raw[];
     unsigned char *buf = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint32_t tslot;
@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(128, 1) steps_k(int n, int nmma, int steps, lo
     if (threadIdx.x / 32 == 1) {
         const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (uint32_t(n >> 3) << 17) | (8u << 24);
         const uint64_t ad = smem_desc(smem_u32(buf), 16384, 1024, 2);
-        const uint64_t bd = smem_desc(smem_u32(buf + 65536), 0, 256, 6);
+        const uint32_t bcode = bspan == 128 ? 2u : bspan == 64 ? 4u : 6u;
+        const uint64_t bd = smem_desc(smem_u32(buf + 65536), 0, 8 * bspan, bcode);
         long long t0 = clock64();
         for (int s = 0; s < steps; ++s) {
             uint32_t el = 0;
@@ -89,11 +90,16 @@ __global__ void __launch_bounds__(128, 1) steps_k(int n, int nmma, int steps, lo
                 uint64_t b = bd;
                 uint32_t d = tmem;
                 for (int kb = 0; kb < nmma; ++kb) {
+                    // kcycle > 1: K offsets inside the B swizzle row cycle like the kernel's ink slots
+                    const uint32_t koff = uint32_t((kb % kcycle) * 2);
+                    const uint32_t aoff = uint32_t(((kb * 5) % 8) * 128);   // scattered K-blocks
                     asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
-                                 "l"(ad + uint32_t(kb * 128)), "l"(b), "r"(idesc), "r"(s > 0 ? 1 : 0));
-                    b += uint32_t((n * 32) >> 4);
-                    d += uint32_t(n);
+                                 "l"(ad + aoff), "l"(b + koff), "r"(idesc), "r"(s > 0 ? 1 : 0));
+                    if ((kb % kcycle) == kcycle - 1) {
+                        b += uint32_t((n * bspan) >> 4);
+                        if (!dsame) d += uint32_t(n);
+                    }
                 }
                 asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)) : "memory");
             }
@@ -126,12 +132,14 @@ int main() {
                c.lbo, c.dstep, c.nblk, double(h[0]) / iters, double(h[1]) / iters, e ? cudaGetErrorString(e) : "");
     }
     cudaFuncSetAttribute(steps_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 + 65536 + 16384);
-    for (int n : {16, 32}) for (int nm : {8, 16}) {
-        steps_k<<<1, 128, 1024 + 65536 + 16384>>>(n, nm, 64, d);
+    struct S { int n, nm, bspan, kcycle; };
+    S ss[] = {{16, 16, 32, 1}, {16, 16, 64, 2}, {16, 16, 128, 4}, {32, 8, 32, 1}, {16, 8, 32, 1}};
+    for (auto c : ss) {
+        steps_k<<<1, 128, 1024 + 65536 + 16384>>>(c.n, c.nm, 64, d, c.bspan, c.kcycle, 0);
         cudaError_t e = cudaDeviceSynchronize();
         cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
-        printf("step of %2d MMAs N=%d + commit + wait: %7.1f cycles/step %s\n", nm, n, double(h[0]) / 64,
-               e ? cudaGetErrorString(e) : "");
+        printf("step of %2d MMAs N=%d Bspan=%3d kcycle=%d + commit + wait: %7.1f cycles/step %s\n", c.nm, c.n,
+               c.bspan, c.kcycle, double(h[0]) / 64, e ? cudaGetErrorString(e) : "");
     }
     return 0;
 }
