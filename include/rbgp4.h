@@ -133,6 +133,19 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
 int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int width, int channels,
                           void *stream);
 
+/*
+ * Training direction: the weight gradient restricted to the pattern,
+ *   grad_values[u, j] = sum_n d_out[u, n] * inp[c(u, j), n],
+ * in the (rows, row_nnz) layout of `values` (c = the closed-form column map of the chain).
+ * d_out is rows x n_cols (row stride ld_do), inp is cols x n_cols (row stride ld_in);
+ * desc->n_cols = n_cols (desc->ld_in/ld_out are ignored).  F32 (fp32 FMA) or F64.
+ * The input gradient W^T x dO is rbgp4_sdmm on the transposed chain (a valid RBGP4 chain
+ * of the transposed factors; paper_2006_13486_b200.training.transpose builds it).
+ */
+int rbgp4_sddmm(const rbgp4_desc *desc, int dtype, const int32_t *adj_o, const int32_t *adj_i,
+                const void *d_out, int64_t ld_do, const void *inp, int64_t ld_in, void *grad_values,
+                void *stream);
+
 /* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
 

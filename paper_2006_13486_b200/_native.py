@@ -23,7 +23,7 @@ EXPORTED = (
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
     "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
-    "rbgp4_reset_launch_count",
+    "rbgp4_reset_launch_count", "rbgp4_sddmm",
 )
 
 
@@ -73,6 +73,8 @@ def lib():
     h.rbgp4_prepare_size.argtypes = [ctypes.POINTER(Desc), i32]
     h.rbgp4_prepare_size.restype = sz
     h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, vp, sz, vp]
+    h.rbgp4_sddmm.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
+    h.rbgp4_sddmm.restype = i32
     h.rbgp4_prepare.restype = i32
     h.rbgp4_conv2d_workspace_size.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc)]
     h.rbgp4_conv2d_workspace_size.restype = sz

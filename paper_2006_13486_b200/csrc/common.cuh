@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdarg>
+#include <algorithm>
 
 #include "../../include/rbgp4.h"
 
