@@ -44,6 +44,14 @@ constexpr int kGThreads = 192;
 // [0] producer issued, [1] MMA saw full, [2] MMA issue done; [3][0..3] setup / epilogue marks
 constexpr int kGTraceSteps = 256;
 __device__ unsigned long long g_gtrace[4][kGTraceSteps];
+// RBGP4_TC_DEBUG bit 512: every CTA stamps %globaltimer (ns) at entry and exit
+constexpr int kCtaStamps = 4096;
+__device__ unsigned long long g_cta_stamp[2][kCtaStamps];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void gtrace(int debug, int ev, int step) {
     if ((debug & 8) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && step < kGTraceSteps)
         g_gtrace[ev][step] = clock64();
@@ -71,6 +79,7 @@ struct GParams {
     // fetch one 64-column atom of the slab and multicast it to both, so L2 streams I once.
     const int32_t *pair;
     int32_t mc;
+    int32_t sym, stage_off;  // symmetric split-K epilogue; output staging offset in the ring
     // implicit-im2col convolution
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, stride;  // img_h/img_w: OUTPUT map
 };
@@ -97,6 +106,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) gtrace(p.debug, 3, 0);
+    const int cta_id = int(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    if ((p.debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[0][cta_id] = gtimer();
     const int64_t n0 = int64_t(blockIdx.x) * kBatch;
     const int tbm = blockIdx.y;
     const int64_t m0 = int64_t(tbm) * p.tm;
@@ -341,8 +352,42 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             for (int q = 0; q < 16; ++q) r[16 * h + q] = __float_as_uint(acc[q]);
         }
     };
-    if (p.ksplit > 1) {
-        // slices > 0: fp32 partial tile -> own shared memory [row][128 cols] (the ring is idle)
+    // ---- output rows of this CTA: everything (no split), nothing (legacy split, slices > 0),
+    // or its own 1/ksplit of the rows (symmetric split: each slice reduces and stores a part)
+    const int rp = p.sym ? p.tm / p.ksplit : p.tm;
+    const int r_lo = p.sym ? kslice * rp : 0;
+    const bool outputs = p.sym || kslice == 0;
+    // symmetric split: receive buffer [source slot][rp rows][128 cols] fp32 at the ring start,
+    // output staging after it
+    const uint32_t recv = ring_a;
+    const uint32_t stage_base = ring_a + uint32_t(p.sym ? p.stage_off : 0);
+    unsigned char *stage_ptr = ring + (p.sym ? p.stage_off : 0);
+    if (p.ksplit > 1 && p.sym) {
+        // the receive buffers alias the rings: every slice's main loop must be over (slices run
+        // different step counts) before any partial lands in a peer
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (warp < 4) {
+            // push the partial rows other slices own: posted DSMEM stores into their receive buffer
+            for (int c = 0; c < p.tm; c += 32) {
+                const int owner = c / rp;
+                if (owner == kslice) continue;
+                uint32_t r[32];
+                load_rows(c, r);
+                const int slot = kslice < owner ? kslice : kslice - 1;
+                uint32_t dst;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(recv), "r"(owner));
+                dst += uint32_t(((slot * rp + (c - owner * rp)) * kBatch + t) * 4);
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(dst + uint32_t(q * kBatch * 4)), "r"(r[q])
+                                 : "memory");
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (p.ksplit > 1) {
+        // legacy: slices > 0 park the whole fp32 partial tile in their own shared memory
         if (kslice > 0 && warp < 4) {
             for (int c = 0; c < p.tm; c += 32) {
                 uint32_t r[32];
@@ -354,23 +399,36 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    if (kslice == 0 && warp < 4 && !(p.debug & 4)) {
+    if (outputs && warp < 4 && !(p.debug & 4)) {
         constexpr int kOutElt = OUT_BF16 ? 2 : 4;
-        for (int c = 0; c < p.tm; c += 32) {
+        for (int c = r_lo; c < r_lo + rp; c += 32) {
             uint32_t r[32];
             load_rows(c, r);
-            for (int k = 1; k < p.ksplit; ++k) {
-                // peer slice k's partial, same offsets in its shared memory (DSMEM)
-                uint32_t peer;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(ring_a), "r"(k));
+            if (p.sym) {
+                for (int k = 0; k < p.ksplit - 1; ++k) {
+                    const uint32_t src = recv + uint32_t(((k * rp + (c - r_lo)) * kBatch + t) * 4);
 #pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    float v;
-                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v)
-                                 : "r"(peer + uint32_t(((c + q) * kBatch + t) * 4)));
-                    r[q] = __float_as_uint(__uint_as_float(r[q]) + v);
+                    for (int q = 0; q < 32; ++q) {
+                        float v;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(src + uint32_t(q * kBatch * 4)));
+                        r[q] = __float_as_uint(__uint_as_float(r[q]) + v);
+                    }
+                }
+            } else {
+                for (int k = 1; k < p.ksplit; ++k) {
+                    // peer slice k's partial, same offsets in its shared memory (DSMEM)
+                    uint32_t peer;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(peer) : "r"(ring_a), "r"(k));
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        float v;
+                        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v)
+                                     : "r"(peer + uint32_t(((c + q) * kBatch + t) * 4)));
+                        r[q] = __float_as_uint(__uint_as_float(r[q]) + v);
+                    }
                 }
             }
+            const int cr = c - r_lo;  // row inside this CTA's output range
             if constexpr (CONV) {
                 // NHWC: pixel t holds channels c..c+31 -> 4 x 16-byte chunks of its 128-byte
                 // rows in 64-channel atoms [atom][pixel][128 B], 128B-swizzled (chunk ^ pixel%8)
@@ -378,8 +436,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 for (int q = 0; q < 32; ++q)
                     if (p.relu) r[q] = __float_as_uint(fmaxf(__uint_as_float(r[q]), 0.0f));
                 if constexpr (OUT_BF16) {
-                    const uint32_t atom = ring_a + uint32_t((c / 64) * (kBatch * 128) + t * 128);
-                    const uint32_t ch0 = uint32_t(c % 64) / 8;
+                    const uint32_t atom = stage_base + uint32_t((cr / 64) * (kBatch * 128) + t * 128);
+                    const uint32_t ch0 = uint32_t(cr % 64) / 8;
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         uint32_t w[4];
@@ -392,7 +450,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         sts128(atom + (((ch0 + q) ^ uint32_t(t & 7)) << 4), w[0], w[1], w[2], w[3]);
                     }
                 } else {
-                    const uint32_t atom = ring_a + uint32_t((c / 32) * (kBatch * 128) + t * 128);
+                    const uint32_t atom = stage_base + uint32_t((cr / 32) * (kBatch * 128) + t * 128);
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         sts128(atom + ((uint32_t(q) ^ uint32_t(t & 7)) << 4), r[4 * q], r[4 * q + 1],
@@ -402,15 +460,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 // row-major O: column t of rows c..c+31 -> [atom of 128/elt cols][row][128 B],
                 // 128B-swizzled (chunk ^ row%8); lanes = consecutive columns
                 constexpr int kAtomCols = 128 / kOutElt;
-                const uint32_t atom = ring_a + uint32_t((t / kAtomCols) * (p.tm * 128));
+                const uint32_t atom = stage_base + uint32_t((t / kAtomCols) * (rp * 128));
                 const uint32_t cb = uint32_t(t % kAtomCols) * kOutElt;  // byte inside the row
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const uint32_t row = uint32_t(c + q);
+                    const uint32_t row = uint32_t(cr + q);
                     const uint32_t addr = atom + row * 128 + ((((cb >> 4) ^ (row & 7))) << 4) + (cb & 15);
                     if constexpr (OUT_BF16) {
-                        const __nv_bfloat16 b = __float2bfloat16_rn(__uint_as_float(r[q]));
-                        sts16(addr, *reinterpret_cast<const uint16_t *>(&b));
+                        const __nv_bfloat16 bv = __float2bfloat16_rn(__uint_as_float(r[q]));
+                        sts16(addr, *reinterpret_cast<const uint16_t *>(&bv));
                     } else {
                         sts32(addr, r[q]);
                     }
@@ -422,12 +480,14 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         if (warp == 0 && elect_one()) {
             if constexpr (CONV) {
                 constexpr int kAtomCh = 128 / kOutElt;
-                for (int a = 0; a < p.tm / kAtomCh; ++a)
-                    tma_store_2d(&omap, ring + a * (kBatch * 128), int32_t(m0) + a * kAtomCh, int32_t(n0));
+                for (int a = 0; a < rp / kAtomCh; ++a)
+                    tma_store_2d(&omap, stage_ptr + a * (kBatch * 128), int32_t(m0) + r_lo + a * kAtomCh,
+                                 int32_t(n0));
             } else {
                 constexpr int kAtomCols = 128 / kOutElt;
                 for (int a = 0; a < kBatch / kAtomCols; ++a)
-                    tma_store_2d(&omap, ring + a * (p.tm * 128), int32_t(n0) + a * kAtomCols, int32_t(m0));
+                    tma_store_2d(&omap, stage_ptr + a * (rp * 128), int32_t(n0) + a * kAtomCols,
+                                 int32_t(m0) + r_lo);
             }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -435,8 +495,9 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         __syncwarp();
     }
     if (threadIdx.x == 0) gtrace(p.debug, 3, 3);
-    if (p.ksplit > 1 || p.mc) {
-        // peers keep their shared memory alive until the leader has read it
+    if ((p.ksplit > 1 && !p.sym) || p.mc) {
+        // peers keep their shared memory alive until the leader has read it (legacy split);
+        // multicast peers may still arrive on this CTA's barriers
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
@@ -447,6 +508,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
                      "r"(uint32_t(p.tmem_cols)));
     }
+    if ((p.debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[1][cta_id] = gtimer();
 }
 
 constexpr size_t kGSmemCap = 227 * 1024;
@@ -535,6 +597,23 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     out->smem = fixed + size_t(ns) * stage;
     out->grid = dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.ksplit));
     return 1;
+}
+
+// symmetric split-K epilogue: each of the ksplit slices reduces and stores tm / ksplit rows
+// (32-row chunks; conv: whole 128-byte channel atoms), receiving the other slices' partials by
+// posted DSMEM stores; the receive buffer and the output staging share the idle ring
+void set_symmetric(GPlan *pl, int oelt, bool conv) {
+    GParams &p = pl->p;
+    p.sym = 0;
+    p.stage_off = 0;
+    if (p.ksplit <= 1 || p.tm % p.ksplit || getenv("RBGP4_TC_NOSYM")) return;
+    const int rp = p.tm / p.ksplit;
+    if (rp % 32 || (conv && rp % (128 / oelt))) return;
+    const size_t recv = size_t(p.ksplit - 1) * rp * kBatch * 4;
+    const size_t off = (recv + 1023) & ~size_t(1023);
+    if (off + size_t(rp) * oelt * 128 > size_t(p.ns) * (p.i_bytes + p.w_bytes)) return;
+    p.sym = 1;
+    p.stage_off = int32_t(off);
 }
 
 // ---------------------------------------------------------------- prepared relayout
@@ -694,6 +773,7 @@ int launch_gather(const ChainDims &c, int out_dtype, const void *values, const i
     pl.p.sched = sched;
     pl.p.pair = pair;
     if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
+    set_symmetric(&pl, oelt, false);
     auto enc = encode_fn();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable from the driver");
@@ -727,7 +807,7 @@ int launch_gather(const ChainDims &c, int out_dtype, const void *values, const i
     {
         cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
         cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
-        cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(c.tm)};
+        cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(pl.p.sym ? c.tm / pl.p.ksplit : c.tm)};
         CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          2, out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -768,6 +848,7 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     pl.p.sched = sched;
     pl.p.pair = pair;
     if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
+    set_symmetric(&pl, oelt, true);
     pl.p.conv = 1;
     pl.p.c_in = cv->c_in;
     const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
@@ -828,4 +909,10 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
 extern "C" int rbgp4_debug_trace_gather(unsigned long long *host, int n) {
     if (n > 4 * rbgp4::kGTraceSteps) n = 4 * rbgp4::kGTraceSteps;
     return cudaMemcpyFromSymbol(host, rbgp4::g_gtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
+}
+
+// debug-only: per-CTA entry / exit %globaltimer stamps (RBGP4_TC_DEBUG bit 512)
+extern "C" int rbgp4_debug_cta_stamps(unsigned long long *host, int n) {
+    if (n > 2 * rbgp4::kCtaStamps) n = 2 * rbgp4::kCtaStamps;
+    return cudaMemcpyFromSymbol(host, rbgp4::g_cta_stamp, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
 }
