@@ -367,6 +367,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // different step counts) before any partial lands in a peer
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 4);
         if (warp < 4) {
             // push the partial rows other slices own: posted DSMEM stores into their receive buffer
             for (int c = 0; c < p.tm; c += 32) {
@@ -384,8 +385,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                                  : "memory");
             }
         }
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 5);
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 6);
     } else if (p.ksplit > 1) {
         // legacy: slices > 0 park the whole fp32 partial tile in their own shared memory
         if (kslice > 0 && warp < 4) {
@@ -475,8 +478,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
         }
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 7);
         fence_async_smem();
         asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) gtrace(p.debug, 3, 8);
         if (warp == 0 && elect_one()) {
             if constexpr (CONV) {
                 constexpr int kAtomCh = 128 / kOutElt;
