@@ -171,9 +171,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     if (threadIdx.x == 0) gtrace(p.debug, 3, 1);
+    // programmatic dependent launch: the next kernel in the stream may be scheduled now (its
+    // setup overlaps this kernel); it waits in griddepcontrol.wait before reading anything
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (warp == 4) {
         // ================= TMA producer: I slab + W tile of each step, one barrier ======
+        // inputs may be the previous kernel's outputs: wait for it to complete (no-op when this
+        // launch has no programmatic dependency)
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
             if (p.debug & 256) mbar_wait_sleep(&empty[st], ((s / p.ns) & 1) ^ 1, 64);
@@ -728,8 +734,16 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = pl.p.mc ? pl.grid.y : 1;
     attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);
-    cfg.attrs = attr;
-    cfg.numAttrs = (pl.p.ksplit > 1 || pl.p.mc) ? 1 : 0;
+    int na = (pl.p.ksplit > 1 || pl.p.mc) ? 1 : 0;
+    cudaLaunchAttribute attrs[2];
+    if (na) attrs[0] = attr[0];
+    if (!getenv("RBGP4_NO_PDL")) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = unsigned(na);
     e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, pl.p, adj_o, adj_i);
     if (e != cudaSuccess) {
         set_error("gather_kernel launch (grid %u x %u x %u, smem %zu): %s", pl.grid.x, pl.grid.y,

@@ -177,6 +177,10 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
     }
     __syncthreads();
+    // programmatic dependent launch: let the next kernel schedule now; every thread waits for
+    // the previous kernel (which may have produced I or W) before its first global read
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // g_o adjacency row of this tile-row and the order its slots are walked in: the
     // schedule lets tile-rows that share a K-block read its I slab at the same step
     const int32_t *orow = adj_o + tbm * p.d_o;
@@ -787,8 +791,16 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);  // the K slices of one tile co-reside
-    cfg.attrs = attr;
-    cfg.numAttrs = pl.p.ksplit > 1 ? 1 : 0;
+    cudaLaunchAttribute attrs[2];
+    unsigned na = 0;
+    if (pl.p.ksplit > 1) attrs[na++] = attr[0];
+    if (!getenv("RBGP4_NO_PDL")) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
     e = cudaLaunchKernelEx(&cfg, kern, map, wmap, omap, pl.p, static_cast<const E *>(values), adj_o, adj_i,
                            out, wsp);
     if (e != cudaSuccess) {
