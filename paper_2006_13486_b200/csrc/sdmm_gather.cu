@@ -80,6 +80,7 @@ struct GParams {
     const int32_t *pair;
     int32_t mc;
     int32_t sym, stage_off;  // symmetric split-K epilogue; output staging offset in the ring
+    int32_t persistent, u_o; // persistent tile loop (many-wave grids); tile-rows
     // implicit-im2col convolution
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, stride;  // img_h/img_w: OUTPUT map
 };
@@ -522,12 +523,217 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     if ((p.debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[1][cta_id] = gtimer();
 }
 
+// ---------------------------------------------------------------- persistent variant
+// Many-wave grids (e.g. the VGG layers at batch 32768: 16k+ tiles): one CTA per SM loops over
+// tiles (column block-major, so the u_o tile-rows sharing a slab run side by side).  The ring
+// and its phases continue across tiles; the accumulator is double-buffered in TMEM, so the
+// epilogue warps drain tile i (straight from registers to global memory, coalesced) while the
+// MMA warp already accumulates tile i+1 and the producer streams without a pipeline restart.
+// Setup, TMEM allocation and the first-load latency are paid once per SM instead of per tile.
+template <bool OUT_BF16, bool CONV, int MMA_N>
+__global__ void __launch_bounds__(kGThreads, 1)
+gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
+                         const GParams p, const int32_t *__restrict__ adj_o, const int32_t *__restrict__ adj_i,
+                         void *__restrict__ out, int64_t n_tiles) {
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ uint2 mma_tab[kMaxMma];
+    unsigned char *ring = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = p.i_bytes + p.w_bytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + size_t(p.ns) * stage_bytes);
+    uint64_t *empty = full + p.ns;
+    uint64_t *acc_full = empty + p.ns;     // [2]: last MMA of a tile committed
+    uint64_t *acc_empty = acc_full + 2;    // [2]: the epilogue has read the accumulator
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_empty + 2);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int kk_n = p.bk / 16;
+    const int n_mma = p.u_i * p.d_i * kk_n;
+    const int u_o = p.u_o;
+
+    if (warp == 4 && lane == 0) {
+        for (int i = 0; i < p.ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&wmap)) : "memory");
+    }
+    if (warp == 5) {
+        for (int i = lane; i < n_mma; i += 32) {
+            const int kk = i % kk_n, ink = (i / kk_n) % p.d_i, ui = i / (kk_n * p.d_i);
+            const int krow = adj_i[ui * p.d_i + ink] * p.bk + 16 * kk;
+            const int slot = ink * p.bk + 16 * kk;
+            const uint32_t a_off = CONV ? uint32_t((krow / 64) * (kBatch * 128) + (krow % 64) * 2)
+                                        : uint32_t(krow * 128);
+            const uint32_t b_off = uint32_t(p.i_bytes + ui * p.bm * p.w_swz + slot * 2);
+            mma_tab[i] = make_uint2((a_off >> 4) | ((b_off >> 4) << 16),
+                                    uint32_t(ui * p.bm) | (slot == 0 ? 0x80000000u : 0u));
+        }
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const uint32_t tmem_d = *tmem_slot;
+
+    if (warp == 4) {
+        // ================= producer: I slab + W tile of every step of every tile =================
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        int64_t g = 0;
+        for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            const int tbm = int(tile % u_o);
+            const int64_t n0 = (tile / u_o) * kBatch;
+            const int32_t *orow = adj_o + int64_t(tbm) * p.d_o;
+            const int32_t *srow = p.sched ? p.sched + int64_t(tbm) * p.d_o : nullptr;
+            for (int s = 0; s < p.d_o; ++s, ++g) {
+                const int st = int(g % p.ns);
+                mbar_wait(&empty[st], uint32_t((g / p.ns) & 1) ^ 1u);
+                const int j = srow ? srow[s] : s;
+                const int32_t krow = orow[j] * p.tk;
+                if (elect_one()) {
+                    mbar_expect_tx(&full[st], uint32_t(stage_bytes));
+                    unsigned char *dst = ring + size_t(st) * stage_bytes;
+                    if constexpr (CONV) {
+                        const int tap = krow / p.c_in, c0 = krow - tap * p.c_in;
+                        const int ti = tap / p.kw, tj = tap - ti * p.kw;
+                        const int hw = p.img_h * p.img_w;
+                        const int b0 = int(n0 / hw), h0 = int(n0 % hw) / p.img_w;
+                        for (int a = 0; a < p.tk / 64; ++a)
+                            tma_load_4d(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a, tj - p.pad,
+                                        h0 * p.stride + ti - p.pad, b0);
+                    } else {
+                        tma_load_3d(dst, &imap, &full[st], 0, krow, int32_t(n0 / 64));
+                    }
+                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, tbm * p.tm);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 5) {
+        // ================= MMA issuer: accumulator b = tile parity =================
+        const uint32_t a_mn = CONV ? 0u : 1u;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (0u << 16) |
+                               (uint32_t(MMA_N >> 3) << 17) | (uint32_t(kBatch >> 4) << 24);
+        const uint32_t ring_a = smem_u32(ring);
+        const uint32_t w_code = p.w_swz == 128 ? 2u : p.w_swz == 64 ? 4u : 6u;
+        const uint64_t a_desc0 = CONV ? smem_desc(ring_a, 0, 1024, 2u) : smem_desc(ring_a, uint32_t(p.tk) * 128, 1024, 2u);
+        const uint64_t b_desc0 = smem_desc(ring_a, 0, 8 * p.w_swz, w_code);
+        constexpr int kRegMma = 32;
+        uint32_t rx[kRegMma], ry[kRegMma];
+#pragma unroll
+        for (int i = 0; i < kRegMma; ++i) {
+            const uint2 e = i < n_mma ? mma_tab[i] : make_uint2(0, 0);
+            rx[i] = e.x;
+            ry[i] = e.y;
+        }
+        int64_t g = 0, it = 0;
+        for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+            const int b = int(it & 1);
+            mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);  // epilogue done with it
+            tc_fence_after();
+            const uint32_t d_base = tmem_d + uint32_t(b * p.tm);
+            for (int s = 0; s < p.d_o; ++s, ++g) {
+                const int st = int(g % p.ns);
+                mbar_wait(&full[st], uint32_t((g / p.ns) & 1));
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
+                    const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
+                    if (n_mma <= kRegMma) {
+#pragma unroll
+                        for (int i = 0; i < kRegMma; ++i)
+                            if (i < n_mma)
+                                tc_mma<false>(d_base + (ry[i] & 0xFFFFu), a_st + (rx[i] & 0xFFFFu), b_st + (rx[i] >> 16),
+                                              idesc, (s > 0 || !(ry[i] >> 31)) ? 1u : 0u);
+                    } else {
+                        for (int i = 0; i < n_mma; ++i) {
+                            const uint2 e = mma_tab[i];
+                            tc_mma<false>(d_base + (e.y & 0xFFFFu), a_st + (e.x & 0xFFFFu), b_st + (e.x >> 16), idesc,
+                                          (s > 0 || !(e.y >> 31)) ? 1u : 0u);
+                        }
+                    }
+                    tc_commit(&empty[st]);
+                    if (s == p.d_o - 1) tc_commit(&acc_full[b]);
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ================= epilogue (warps 0-3): TMEM lane = batch column / pixel =================
+        const int t = warp * 32 + lane;
+        int64_t it = 0;
+        for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+            const int b = int(it & 1);
+            const int tbm = int(tile % u_o);
+            const int64_t n0 = (tile / u_o) * kBatch;
+            const int64_t m0 = int64_t(tbm) * p.tm;
+            mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
+            tc_fence_after();
+            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * p.tm);
+            const int64_t col = n0 + t;
+            const bool ok = col < p.n_cols;
+            for (int c = 0; c < p.tm; c += 32) {
+                uint32_t r[32];
+                TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (!ok) continue;
+                if constexpr (CONV) {
+                    // NHWC: this pixel's channels m0+c .. +31 are contiguous
+#pragma unroll
+                    for (int q = 0; q < 32; ++q)
+                        if (p.relu) r[q] = __float_as_uint(fmaxf(__uint_as_float(r[q]), 0.0f));
+                    if constexpr (OUT_BF16) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + col * p.ld_out + m0 + c);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            uint32_t w[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                __nv_bfloat162 b2 = __floats2bfloat162_rn(__uint_as_float(r[q * 8 + 2 * h]),
+                                                                          __uint_as_float(r[q * 8 + 2 * h + 1]));
+                                w[h] = *reinterpret_cast<uint32_t *>(&b2);
+                            }
+                            dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    } else {
+                        uint4 *dst = reinterpret_cast<uint4 *>(static_cast<float *>(out) + col * p.ld_out + m0 + c);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+                    }
+                } else {
+                    // row-major O: lanes = consecutive columns of one row (coalesced)
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        if constexpr (OUT_BF16)
+                            static_cast<__nv_bfloat16 *>(out)[(m0 + c + q) * p.ld_out + col] =
+                                __float2bfloat16_rn(__uint_as_float(r[q]));
+                        else
+                            static_cast<float *>(out)[(m0 + c + q) * p.ld_out + col] = __uint_as_float(r[q]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(uint32_t(p.tmem_cols)));
+    }
+}
+
 constexpr size_t kGSmemCap = 227 * 1024;
 
 struct GPlan {
     GParams p;
     size_t smem;
     dim3 grid;
+    int64_t n_tiles;
 };
 
 CUtensorMapSwizzle swizzle_of(int span) {
@@ -585,28 +791,36 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     // with the deepest ring that fits.
     int ks = 1;
     bool dual = false;
+    // many waves: one persistent CTA per SM loops over the tiles (no split, no pairs)
+    p.u_o = c.u_o;
+    p.persistent = ((tiles >= 2 * kNumSMs || getenv("RBGP4_TC_PERSIST")) && !relayout &&
+                    !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
     if (tiles < kNumSMs) {
         // (more than 4 slices measured slower: the DSMEM reduction grows with the slices)
         while (ks < 4 && tiles * ks * 2 <= 2 * kNumSMs && c.d_o >= ks * 2 * 2) ks *= 2;
         dual = tiles * ks > kNumSMs;
     }
     if (const char *e = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(e)));
-    int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed) / stage));
+    if (p.persistent) ks = 1, dual = false;
+    int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed - 64) / stage));
     if (const char *e = getenv("RBGP4_TC_NS")) ns = std::max(2, std::min(16, atoi(e)));
     if (fixed + size_t(ns) * stage > kGSmemCap) return 0;
     p.ns = ns;
     p.tmem_cols = 32;
-    while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm)) p.tmem_cols *= 2;
+    while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm) * (p.persistent ? 2 : 1)) p.tmem_cols *= 2;
+    if (p.tmem_cols > 512) p.persistent = 0, p.tmem_cols = 256;
     p.sps = (c.d_o + ks - 1) / ks;
     p.ksplit = (c.d_o + p.sps - 1) / p.sps;
     if (const char *e = getenv("RBGP4_TC_DEBUG")) p.debug = atoi(e);
     // multicast pairs: the u_o tile-rows of a column block as one cluster (<= 8 portable)
     // (SDMM slabs are two 64-column atoms; conv slabs must have an even number of channel atoms)
-    p.mc = (pairs && p.ksplit == 1 && c.u_o >= 2 && c.u_o <= 8 && (!conv || (c.tk / 64) % 2 == 0) &&
+    p.mc = (pairs && p.ksplit == 1 && !p.persistent && c.u_o >= 2 && c.u_o <= 8 && (!conv || (c.tk / 64) % 2 == 0) &&
             !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
     out->p = p;
     out->smem = fixed + size_t(ns) * stage;
-    out->grid = dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.ksplit));
+    out->grid = p.persistent ? dim3(unsigned(std::min<int64_t>(tiles, kNumSMs)), 1, 1)
+                             : dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.ksplit));
+    out->n_tiles = tiles;
     return 1;
 }
 
@@ -707,7 +921,43 @@ namespace {
 template <bool OUT_BF16, bool CONV>
 int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensorMap &wmap,
                         const CUtensorMap &omap, const int32_t *adj_o, const int32_t *adj_i,
-                        cudaStream_t stream) {
+                        void *out, cudaStream_t stream) {
+    if (pl.p.persistent) {
+        void (*pk)(CUtensorMap, CUtensorMap, GParams, const int32_t *, const int32_t *, void *, int64_t) = nullptr;
+        switch (pl.p.mma_n) {
+            case 16: pk = gather_persistent_kernel<OUT_BF16, CONV, 16>; break;
+            case 32: pk = gather_persistent_kernel<OUT_BF16, CONV, 32>; break;
+            case 48: pk = gather_persistent_kernel<OUT_BF16, CONV, 48>; break;
+            case 64: pk = gather_persistent_kernel<OUT_BF16, CONV, 64>; break;
+            case 128: pk = gather_persistent_kernel<OUT_BF16, CONV, 128>; break;
+            default:
+                set_error("gather kernel: no instantiation for MMA N = %d", pl.p.mma_n);
+                return RBGP4_EUNSUPPORTED;
+        }
+        cudaError_t e = cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+        if (e != cudaSuccess) {
+            set_error("cudaFuncSetAttribute(gather persistent): %s", cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = pl.grid;
+        cfg.blockDim = dim3(kGThreads);
+        cfg.dynamicSmemBytes = pl.smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = getenv("RBGP4_NO_PDL") ? 0 : 1;
+        e = cudaLaunchKernelEx(&cfg, pk, imap, wmap, pl.p, adj_o, adj_i, out, pl.n_tiles);
+        if (e != cudaSuccess) {
+            set_error("gather_persistent_kernel launch (%u CTAs, smem %zu): %s", pl.grid.x, pl.smem,
+                      cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+        RBGP4_CHECK_LAUNCH("gather_persistent_kernel launch");
+        return RBGP4_OK;
+    }
     void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, GParams, const int32_t *, const int32_t *) = nullptr;
     switch (pl.p.mma_n) {
         case 16: kern = gather_kernel<OUT_BF16, CONV, 16>; break;
@@ -836,8 +1086,8 @@ int launch_gather(const ChainDims &c, int out_dtype, const void *values, const i
             return RBGP4_ECUDA;
         }
     }
-    return oelt == 2 ? gather_launch_typed<true, false>(pl, imap, wmap, omap, adj_o, adj_i, stream)
-                     : gather_launch_typed<false, false>(pl, imap, wmap, omap, adj_o, adj_i, stream);
+    return oelt == 2 ? gather_launch_typed<true, false>(pl, imap, wmap, omap, adj_o, adj_i, out, stream)
+                     : gather_launch_typed<false, false>(pl, imap, wmap, omap, adj_o, adj_i, out, stream);
 }
 
 int gather_supported(const ChainDims &c, int compute, int out_dtype, bool relayout) {
@@ -869,6 +1119,7 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     if (k4) gather_prep_views(c, k4, &pl.p.cols, &values);
     set_symmetric(&pl, oelt, true);
     pl.p.conv = 1;
+    pl.p.ld_out = int64_t(c.rows);  // NHWC: a pixel row holds c_out channels
     pl.p.c_in = cv->c_in;
     const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
     const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
@@ -918,8 +1169,8 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
             return RBGP4_ECUDA;
         }
     }
-    return oelt == 2 ? gather_launch_typed<true, true>(pl, imap, wmap, omap, adj_o, adj_i, stream)
-                     : gather_launch_typed<false, true>(pl, imap, wmap, omap, adj_o, adj_i, stream);
+    return oelt == 2 ? gather_launch_typed<true, true>(pl, imap, wmap, omap, adj_o, adj_i, out, stream)
+                     : gather_launch_typed<false, true>(pl, imap, wmap, omap, adj_o, adj_i, out, stream);
 }
 
 }  // namespace rbgp4

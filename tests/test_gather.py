@@ -28,7 +28,7 @@ def chain_of(g_o, sp_o, g_i, sp_i, g_b, seed=0):
     return wl.build_chain(cfg)
 
 
-def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False):
+def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False):
     """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout (opt-in).
 
     The prepared buffer is cached per matrix, so relayout runs use a fresh RcubsMatrix copy."""
@@ -38,12 +38,15 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False):
     if relayout:
         os.environ["RBGP4_TC_RELAYOUT"] = "1"
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
+    if persistent:
+        os.environ["RBGP4_TC_PERSIST"] = "1"
     try:
         y, _ = ks.rbgp4mm(w, x, p, compute=compute, out_dtype=out_dtype)
         torch.cuda.synchronize()
     finally:
         os.environ.pop("RBGP4_TC_DENSE", None)
         os.environ.pop("RBGP4_TC_RELAYOUT", None)
+        os.environ.pop("RBGP4_TC_PERSIST", None)
     return y.float().cpu().numpy()
 
 
@@ -81,6 +84,9 @@ def test_gather_sdmm_matches_oracle(case):
     assert oracle.rel_l2(got, dense) < 4e-3
     relaid = run(w, x.cuda(), relayout=True)
     assert oracle.rel_l2(relaid, ref) < 4e-3
+    # persistent tile loop (taken by itself only for many-wave grids; forced here)
+    pers = run(w, x.cuda(), persistent=True)
+    assert oracle.rel_l2(pers, ref) < 4e-3
 
 
 def test_gather_f32_output_and_host_tensors():
@@ -110,7 +116,8 @@ CONV_CASES = [(128, 128, 4, 9), (256, 128, 8, 3), (128, 256, 16, 1), (128, 128, 
 
 @pytest.mark.parametrize("c_out,c_in,hw,batch", CONV_CASES)
 @pytest.mark.parametrize("relu", [False, True])
-def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu):
+@pytest.mark.parametrize("persistent", [False, True])
+def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent):
     from test_conv import im2col_nhwc
     cfg = wl.SweepConfig("conv16", (c_out // 128, 9 * c_in // 128), 0.0, (1, 1), (8, 8), 0.75,
                          (16, 16), n_cols=1, seed=c_out + c_in + hw)
@@ -118,9 +125,28 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu):
     w = ks.init_random(chain, 7, precision="f32")
     x = np.random.default_rng(3).uniform(-1, 1, (batch, hw, hw, c_in)).astype(np.float32)
     xb = torch.from_numpy(x).to(torch.bfloat16)
-    got = conv.sparse_conv2d(w, xb.cuda(), 3, relu=relu, out_dtype=torch.float32).cpu().numpy()
+    if persistent:
+        os.environ["RBGP4_TC_PERSIST"] = "1"
+    try:
+        got = conv.sparse_conv2d(w, xb.cuda(), 3, relu=relu, out_dtype=torch.float32).cpu().numpy()
+    finally:
+        os.environ.pop("RBGP4_TC_PERSIST", None)
     ref = f64_ref(w, np.ascontiguousarray(im2col_nhwc(xb.float().numpy(), 3)))
     ref = ref.T.reshape(batch, hw, hw, c_out)
     if relu:
         ref = np.maximum(ref, 0)
     assert oracle.rel_l2(got, ref) < 1e-5
+
+
+def test_gather_persistent_many_waves():
+    """A grid of 512 tiles (4 tile-rows x 128 column blocks) takes the persistent loop."""
+    chain = chain_of((4, 4), 0.5, (8, 8), 0.75, (16, 16), seed=21)
+    w = ks.init_random(chain, 6, precision="f32")
+    x = torch.from_numpy(np.random.default_rng(8).uniform(-1, 1, (w.cols, 16384)).astype(np.float32))
+    xb = x.to(torch.bfloat16)
+    ref = f64_ref(w, xb.float().numpy())
+    got = run(w, xb.cuda())
+    assert oracle.rel_l2(got, ref) < 4e-3
+    got32 = run(w, xb.cuda(), out_dtype=torch.float32)
+    assert oracle.rel_l2(got32, ref) < 1e-5
+
