@@ -81,6 +81,9 @@ struct GParams {
     int32_t mc;
     int32_t sym, stage_off;  // symmetric split-K epilogue; output staging offset in the ring
     int32_t persistent, u_o; // persistent tile loop (many-wave grids); tile-rows
+    // M-split: the 2 CTAs of a cluster (grid z) own the two halves of a tile's rows and run all
+    // steps, each fetching one 64-column atom of the shared I slab and multicasting it to both
+    int32_t msplit;
     // implicit-im2col convolution
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, stride;  // img_h/img_w: OUTPUT map
 };
@@ -112,7 +115,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     const int64_t n0 = int64_t(blockIdx.x) * kBatch;
     const int tbm = blockIdx.y;
     const int64_t m0 = int64_t(tbm) * p.tm;
-    const int kslice = blockIdx.z;
+    const int half = p.msplit ? int(blockIdx.z) : 0;
+    const int kslice = p.msplit ? 0 : int(blockIdx.z);
+    const int n_ui = p.msplit ? p.u_i / 2 : p.u_i;  // row blocks of this CTA
+    const int ui0 = half * n_ui;
     const int s_begin = kslice * p.sps;
     const int nsteps = min(p.d_o, s_begin + p.sps) - s_begin;
     const int32_t *orow = adj_o + int64_t(tbm) * p.d_o;
@@ -122,7 +128,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     if (warp == 4 && lane == 0) {
         // empty[st] of step s completes on two arrivals in multicast mode: this CTA's release
         // of the slot and its step-s partner's (or this CTA's commit twice when unpaired)
-        for (int i = 0; i < p.ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], p.mc ? 2 : 1); }
+        for (int i = 0; i < p.ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], (p.mc || p.msplit) ? 2 : 1); }
         mbar_init(tmem_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
@@ -130,7 +136,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     }
     const int kk_n = p.bk / 16;
     const int v_blocks = p.cols ? p.u_i * p.d_i / p.d_r : 0;  // g_i column blocks (relayout)
-    const int n_mma = (p.cols ? v_blocks : p.u_i * p.d_i) * kk_n;
+    const int n_mma = (p.cols ? v_blocks : n_ui * p.d_i) * kk_n;
     if (warp == 5) {
         // the in-tile gather pattern g_i (x) g_b is the same for every step and tile-row
         // (sdmm.py:183-186).  Direct mode: MMA (ui, ink, kk) reads slab rows
@@ -147,11 +153,11 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 slot = 16 * kk;
                 dcol = b_row;
             } else {
-                const int ink = (i / kk_n) % p.d_i, ui = i / (kk_n * p.d_i);
-                krow = adj_i[ui * p.d_i + ink] * p.bk + 16 * kk;
-                b_row = ui * p.bm;
+                const int ink = (i / kk_n) % p.d_i, ur = i / (kk_n * p.d_i);  // ur: row block in this CTA
+                krow = adj_i[(ui0 + ur) * p.d_i + ink] * p.bk + 16 * kk;
+                b_row = ur * p.bm;
                 slot = ink * p.bk + 16 * kk;
-                dcol = ui * p.bm;
+                dcol = ur * p.bm;
             }
             const uint32_t a_off = CONV ? uint32_t((krow / 64) * (kBatch * 128) + (krow % 64) * 2)
                                         : uint32_t(krow * 128);
@@ -166,7 +172,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (p.mc) {
+    if (p.mc || p.msplit) {
         // peers must see the initialised barriers before any multicast lands or arrives
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -201,10 +207,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     const int ti = tap / p.kw, tj = tap - ti * p.kw;
                     const int hw = p.img_h * p.img_w;
                     const int b0 = int(n0 / hw), h0 = int(n0 % hw) / p.img_w;
-                    const int pb = p.mc ? prow[s] : -1;
+                    const int pb = p.mc ? prow[s] : p.msplit ? 1 - half : -1;
+                    const int me = p.msplit ? half : tbm;
                     for (int a = 0; a < p.tk / 64; ++a) {
-                        if (pb >= 0) {  // paired: channel atoms alternate between the two CTAs
-                            if ((a & 1) != (tbm < pb ? 0 : 1)) continue;
+                        if (pb >= 0 && p.msplit) {  // row halves: channel atoms alternate, both receive
+                            if ((a & 1) != half) continue;
+                            tma_load_4d_mc(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
+                                           tj - p.pad, h0 * p.stride + ti - p.pad, b0, uint16_t(3u));
+                        } else if (pb >= 0) {  // paired: channel atoms alternate between the two CTAs
+                            if ((a & 1) != (me < pb ? 0 : 1)) continue;
                             tma_load_4d_mc(dst + a * (kBatch * 128), &imap, &full[st], c0 + 64 * a,
                                            tj - p.pad, h0 * p.stride + ti - p.pad, b0,
                                            uint16_t((1u << tbm) | (1u << pb)));
@@ -213,6 +224,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                                         tj - p.pad, h0 * p.stride + ti - p.pad, b0);
                         }
                     }
+                } else if (p.msplit) {
+                    // the two row halves share every slab: fetch atom `half` for both CTAs
+                    tma_load_3d_mc(dst + half * p.tk * 128, &imap, &full[st], 0, krow, int32_t(n0 / 64) + half,
+                                   uint16_t(3u));
                 } else if (p.mc) {
                     // one-atom boxes (64 cols x tk rows); paired: fetch atom h for both CTAs
                     const int pb = prow[s];
@@ -230,8 +245,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
                 if (p.cols)  // re-laid tiles: (bk, rows) view, tile (tbm, j) = w_rows rows
                     tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
-                else
-                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, int32_t(m0));
+                else  // this CTA's rows of the compressed tile
+                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, int32_t(m0) + ui0 * p.bm);
                 gtrace(p.debug, 0, s);
             }
             __syncwarp();
@@ -302,7 +317,9 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                                       (s > 0 || !(e.y >> 31)) ? 1u : 0u);
                     }
                 }
-                if (p.mc) {
+                if (p.msplit) {
+                    tc_commit_mc(&empty[st], uint16_t(3u));  // both halves fill every slot
+                } else if (p.mc) {
                     // release slot st for step s + ns to the CTAs that will fill it: this one and
                     // its step-(s + ns) partner
                     const int sn = s + p.ns;
@@ -361,9 +378,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     };
     // ---- output rows of this CTA: everything (no split), nothing (legacy split, slices > 0),
     // or its own 1/ksplit of the rows (symmetric split: each slice reduces and stores a part)
-    const int rp = p.sym ? p.tm / p.ksplit : p.tm;
-    const int r_lo = p.sym ? kslice * rp : 0;
-    const bool outputs = p.sym || kslice == 0;
+    const int rp = p.msplit ? p.tm / 2 : p.sym ? p.tm / p.ksplit : p.tm;
+    const int r_lo = p.msplit ? half * rp : p.sym ? kslice * rp : 0;
+    const int t_lo = p.msplit ? r_lo : 0;  // TMEM holds only this CTA's rows in M-split mode
+    const bool outputs = p.sym || p.msplit || kslice == 0;
     // symmetric split: receive buffer [source slot][rp rows][128 cols] fp32 at the ring start,
     // output staging after it
     const uint32_t recv = ring_a;
@@ -413,7 +431,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         constexpr int kOutElt = OUT_BF16 ? 2 : 4;
         for (int c = r_lo; c < r_lo + rp; c += 32) {
             uint32_t r[32];
-            load_rows(c, r);
+            load_rows(c - t_lo, r);
             if (p.sym) {
                 for (int k = 0; k < p.ksplit - 1; ++k) {
                     const uint32_t src = recv + uint32_t(((k * rp + (c - r_lo)) * kBatch + t) * 4);
@@ -507,7 +525,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         __syncwarp();
     }
     if (threadIdx.x == 0) gtrace(p.debug, 3, 3);
-    if ((p.ksplit > 1 && !p.sym) || p.mc) {
+    if ((p.ksplit > 1 && !p.sym) || p.mc || p.msplit) {
         // peers keep their shared memory alive until the leader has read it (legacy split);
         // multicast peers may still arrive on this CTA's barriers
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
@@ -778,48 +796,58 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     const int n_mma = (relayout ? c.v_i : c.u_i * c.d_i) * (c.bk / 16);
     if (n_mma > kMaxMma) return 0;
     p.i_bytes = c.tk * kBatch * 2;
-    p.w_bytes = p.w_rows * w_row;  // = tm * d_t * 2 either way
+    const int64_t col_blocks = (c.n_cols + kBatch - 1) / kBatch;
+    const int64_t tiles = col_blocks * c.u_o;
+    // many waves: one persistent CTA per SM loops over the tiles (no split, no pairs)
+    p.u_o = c.u_o;
+    p.persistent = ((tiles >= 2 * kNumSMs || getenv("RBGP4_TC_PERSIST")) && !relayout &&
+                    !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
+    // M-split (opt-in, RBGP4_TC_MSPLIT=1): the two row halves of each tile on two CTAs (2 per
+    // SM) that share every I slab by multicast and need no reduction.  Correct, but on conv10
+    // it measured 30.1 us against 26.0 us for the split-K default (half the MMAs per CTA do
+    // not make up for running all steps), so it is not chosen by itself.
+    const char *ms_env = getenv("RBGP4_TC_MSPLIT");
+    p.msplit = (!p.persistent && !relayout && c.u_i % 2 == 0 && (c.tm / 2) % 32 == 0 &&
+                (!conv || (c.tk / 64) % 2 == 0) && ms_env && atoi(ms_env) != 0) ? 1 : 0;
+    p.w_rows = p.msplit ? c.tm / 2 : p.w_rows;
+    p.w_bytes = p.w_rows * w_row;  // = tm * d_t * 2 (half of it in M-split)
     p.w_swz = w_row;
     const size_t stage = size_t(p.i_bytes) + p.w_bytes;
     const size_t fixed = 1024 + 8 * (2 * 16 + 1) + 16 + 64 + size_t(kMaxMma) * 8;  // + static table
-    const int64_t col_blocks = (c.n_cols + kBatch - 1) / kBatch;
-    const int64_t tiles = col_blocks * c.u_o;
     // Occupancy: a CTA's steps are a serial latency chain (load -> MMA issue -> commit), so
     // when one tile per SM would leave SMs idle, the steps of a tile are split over a cluster
     // (DSMEM reduction) and two CTAs share an SM with 2-stage rings (measured on the VGG
     // shapes: 2 CTAs/SM x 2 stages beats 1 CTA/SM x 5 stages).  Large grids keep 1 CTA/SM
     // with the deepest ring that fits.
     int ks = 1;
-    bool dual = false;
-    // many waves: one persistent CTA per SM loops over the tiles (no split, no pairs)
-    p.u_o = c.u_o;
-    p.persistent = ((tiles >= 2 * kNumSMs || getenv("RBGP4_TC_PERSIST")) && !relayout &&
-                    !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
-    if (tiles < kNumSMs) {
+    bool dual = p.msplit;
+    if (tiles < kNumSMs && !p.msplit) {
         // (more than 4 slices measured slower: the DSMEM reduction grows with the slices)
         while (ks < 4 && tiles * ks * 2 <= 2 * kNumSMs && c.d_o >= ks * 2 * 2) ks *= 2;
         dual = tiles * ks > kNumSMs;
     }
     if (const char *e = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(e)));
-    if (p.persistent) ks = 1, dual = false;
+    if (p.persistent || p.msplit) ks = 1;
+    if (p.persistent) dual = false;
     int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed - 64) / stage));
     if (const char *e = getenv("RBGP4_TC_NS")) ns = std::max(2, std::min(16, atoi(e)));
     if (fixed + size_t(ns) * stage > kGSmemCap) return 0;
     p.ns = ns;
     p.tmem_cols = 32;
-    while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm) * (p.persistent ? 2 : 1)) p.tmem_cols *= 2;
+    while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm / (p.msplit ? 2 : 1)) * (p.persistent ? 2 : 1))
+        p.tmem_cols *= 2;
     if (p.tmem_cols > 512) p.persistent = 0, p.tmem_cols = 256;
     p.sps = (c.d_o + ks - 1) / ks;
     p.ksplit = (c.d_o + p.sps - 1) / p.sps;
     if (const char *e = getenv("RBGP4_TC_DEBUG")) p.debug = atoi(e);
     // multicast pairs: the u_o tile-rows of a column block as one cluster (<= 8 portable)
     // (SDMM slabs are two 64-column atoms; conv slabs must have an even number of channel atoms)
-    p.mc = (pairs && p.ksplit == 1 && !p.persistent && c.u_o >= 2 && c.u_o <= 8 && (!conv || (c.tk / 64) % 2 == 0) &&
-            !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
+    p.mc = (pairs && p.ksplit == 1 && !p.persistent && !p.msplit && c.u_o >= 2 && c.u_o <= 8 &&
+            (!conv || (c.tk / 64) % 2 == 0) && !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
     out->p = p;
     out->smem = fixed + size_t(ns) * stage;
     out->grid = p.persistent ? dim3(unsigned(std::min<int64_t>(tiles, kNumSMs)), 1, 1)
-                             : dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.ksplit));
+                             : dim3(unsigned(col_blocks), unsigned(c.u_o), unsigned(p.msplit ? 2 : p.ksplit));
     out->n_tiles = tiles;
     return 1;
 }
@@ -983,8 +1011,8 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 1;
     attr[0].val.clusterDim.y = pl.p.mc ? pl.grid.y : 1;
-    attr[0].val.clusterDim.z = unsigned(pl.p.ksplit);
-    int na = (pl.p.ksplit > 1 || pl.p.mc) ? 1 : 0;
+    attr[0].val.clusterDim.z = unsigned(pl.p.msplit ? 2 : pl.p.ksplit);
+    int na = (pl.p.ksplit > 1 || pl.p.mc || pl.p.msplit) ? 1 : 0;
     cudaLaunchAttribute attrs[2];
     if (na) attrs[0] = attr[0];
     if (!getenv("RBGP4_NO_PDL")) {
@@ -1015,7 +1043,7 @@ int encode_w_map(CUtensorMap *wmap, const ChainDims &c, const GParams &p, const 
     } else {       // RcubsMatrix.values as stored: (row_nnz, rows)
         wdims[0] = cuuint64_t(c.row_nnz); wdims[1] = cuuint64_t(c.rows);
         wstrides[0] = cuuint64_t(c.row_nnz) * 2;
-        wbox[0] = cuuint32_t(c.d_t); wbox[1] = cuuint32_t(c.tm);
+        wbox[0] = cuuint32_t(c.d_t); wbox[1] = cuuint32_t(p.msplit ? c.tm / 2 : c.tm);
     }
     cuuint32_t estr[2] = {1, 1};
     if (reinterpret_cast<uintptr_t>(values) % 16 != 0 || wstrides[0] % 16 != 0) {
@@ -1057,7 +1085,7 @@ int launch_gather(const ChainDims &c, int out_dtype, const void *values, const i
         // I as (64 cols, K rows, N/64 atoms): one box = a whole 128-column slab, atom-major
         cuuint64_t dims[3] = {64, cuuint64_t(c.cols), cuuint64_t((c.n_cols + 63) / 64)};
         cuuint64_t strides[2] = {cuuint64_t(c.ld_in) * 2, 128};
-        cuuint32_t box[3] = {64, cuuint32_t(c.tk), pl.p.mc ? 1u : 2u};
+        cuuint32_t box[3] = {64, cuuint32_t(c.tk), (pl.p.mc || pl.p.msplit) ? 1u : 2u};
         if (c.n_cols % 64) {
             // ragged last atom: a 2-atom view would read past the row; fall back to the
             // column-exact 2-D view with one box per atom (OOB columns zero-filled)
@@ -1076,7 +1104,8 @@ int launch_gather(const ChainDims &c, int out_dtype, const void *values, const i
     {
         cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
         cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
-        cuuint32_t obox[2] = {cuuint32_t(128 / oelt), cuuint32_t(pl.p.sym ? c.tm / pl.p.ksplit : c.tm)};
+        cuuint32_t obox[2] = {cuuint32_t(128 / oelt),
+                              cuuint32_t(pl.p.msplit ? c.tm / 2 : pl.p.sym ? c.tm / pl.p.ksplit : c.tm)};
         CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          2, out, odims, ostrides, obox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,

@@ -28,7 +28,7 @@ def chain_of(g_o, sp_o, g_i, sp_i, g_b, seed=0):
     return wl.build_chain(cfg)
 
 
-def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False):
+def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False, msplit=False):
     """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout (opt-in).
 
     The prepared buffer is cached per matrix, so relayout runs use a fresh RcubsMatrix copy."""
@@ -40,6 +40,8 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
     if persistent:
         os.environ["RBGP4_TC_PERSIST"] = "1"
+    if msplit:
+        os.environ["RBGP4_TC_MSPLIT"] = "1"
     try:
         y, _ = ks.rbgp4mm(w, x, p, compute=compute, out_dtype=out_dtype)
         torch.cuda.synchronize()
@@ -47,6 +49,7 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
         os.environ.pop("RBGP4_TC_DENSE", None)
         os.environ.pop("RBGP4_TC_RELAYOUT", None)
         os.environ.pop("RBGP4_TC_PERSIST", None)
+        os.environ.pop("RBGP4_TC_MSPLIT", None)
     return y.float().cpu().numpy()
 
 
@@ -87,6 +90,10 @@ def test_gather_sdmm_matches_oracle(case):
     # persistent tile loop (taken by itself only for many-wave grids; forced here)
     pers = run(w, x.cuda(), persistent=True)
     assert oracle.rel_l2(pers, ref) < 4e-3
+    # M-split (two row halves per tile, multicast slabs; taken by itself near half a wave)
+    if w.chain.graphs[2].num_left % 2 == 0:
+        ms = run(w, x.cuda(), msplit=True)
+        assert oracle.rel_l2(ms, ref) < 4e-3
 
 
 def test_gather_f32_output_and_host_tensors():
@@ -116,8 +123,8 @@ CONV_CASES = [(128, 128, 4, 9), (256, 128, 8, 3), (128, 256, 16, 1), (128, 128, 
 
 @pytest.mark.parametrize("c_out,c_in,hw,batch", CONV_CASES)
 @pytest.mark.parametrize("relu", [False, True])
-@pytest.mark.parametrize("persistent", [False, True])
-def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent):
+@pytest.mark.parametrize("mode", ["default", "persistent", "msplit"])
+def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     from test_conv import im2col_nhwc
     cfg = wl.SweepConfig("conv16", (c_out // 128, 9 * c_in // 128), 0.0, (1, 1), (8, 8), 0.75,
                          (16, 16), n_cols=1, seed=c_out + c_in + hw)
@@ -125,12 +132,14 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent):
     w = ks.init_random(chain, 7, precision="f32")
     x = np.random.default_rng(3).uniform(-1, 1, (batch, hw, hw, c_in)).astype(np.float32)
     xb = torch.from_numpy(x).to(torch.bfloat16)
-    if persistent:
-        os.environ["RBGP4_TC_PERSIST"] = "1"
+    env = {"persistent": "RBGP4_TC_PERSIST", "msplit": "RBGP4_TC_MSPLIT"}.get(mode)
+    if env:
+        os.environ[env] = "1"
     try:
         got = conv.sparse_conv2d(w, xb.cuda(), 3, relu=relu, out_dtype=torch.float32).cpu().numpy()
     finally:
-        os.environ.pop("RBGP4_TC_PERSIST", None)
+        if env:
+            os.environ.pop(env, None)
     ref = f64_ref(w, np.ascontiguousarray(im2col_nhwc(xb.float().numpy(), 3)))
     ref = ref.T.reshape(batch, hw, hw, c_out)
     if relu:
