@@ -82,6 +82,11 @@ struct TcParams {
     // (img_h, img_w = OUTPUT map; the input map is stride x larger, read by strided TMA boxes)
     int32_t conv, c_in, img_h, img_w, kw, pad, relu, th, tb, stride;
     int32_t ostore;          // epilogue stages the output tile in shared memory and TMA-stores it
+    // persistent tile loop (many-wave conv / SDMM grids, tm <= 128, no split-K): CTAs stride over
+    // n_tiles tiles (column block-major); rings and barrier phases continue across tiles
+    int32_t persistent, blocks_m;
+    int64_t n_tiles;
+    int32_t pstage_bytes;    // persistent: dedicated output staging (the rings are streaming)
     int32_t w_swz;           // swizzle span (bytes) of the compressed-W stage rows: 0 / 32 / 64 / 128
 };
 
@@ -136,8 +141,11 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     unsigned char *a_buf = base;
     unsigned char *b_buf = a_buf + p.na * p.a_stage_bytes;
     unsigned char *w_buf = b_buf + p.nb * p.b_stage_bytes;
+    unsigned char *pstage = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(w_buf + p.nw * p.w_stage_bytes) + 1023) & ~uintptr_t(1023));
     // aoff[j * 128 + r]: byte offset (inside an A stage) of nonzero j of CTA row r
-    uint16_t *aoff = reinterpret_cast<uint16_t *>(w_buf + p.nw * p.w_stage_bytes);
+    uint16_t *aoff = reinterpret_cast<uint16_t *>(p.pstage_bytes ? pstage + p.pstage_bytes
+                                                                  : w_buf + p.nw * p.w_stage_bytes);
     int32_t *adj_s = reinterpret_cast<int32_t *>(
         (reinterpret_cast<uintptr_t>(aoff + kBlockM * p.d_t) + 15) & ~uintptr_t(15));
     uint64_t *bars = reinterpret_cast<uint64_t *>(
@@ -151,14 +159,14 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     uint64_t *full_b = bars, *empty_b = full_b + p.nb;
     uint64_t *full_w = empty_b + p.nb, *empty_w = full_w + p.nw;
     uint64_t *tmem_full = empty_w + p.nw;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
+    uint64_t *tmem_empty = tmem_full + 1;  // persistent: the epilogue has read the accumulator
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) trace(p.debug, 6, 3);
-    const int64_t n0 = int64_t(blockIdx.x) * p.tn;
-    const int64_t m0 = int64_t(blockIdx.y) * p.rows_valid;  // first W row of this CTA
-    const int64_t tbm = m0 / p.tm;
-    const int row_in_tile0 = int(m0 - tbm * p.tm);
+    // first tile of this CTA (the only one unless persistent)
+    const int64_t m0_first = int64_t(p.persistent ? blockIdx.x % p.blocks_m : blockIdx.y) * p.rows_valid;
+    const int row_in_tile0 = int(m0_first % p.tm);  // same for every tile (persistent: tm <= 128)
     // split-K: this CTA runs steps [s_begin, s_begin + nsteps) of the tile-row
     const int kslice = blockIdx.z;
     const int s_begin = kslice * p.sps;
@@ -171,6 +179,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         for (int i = 0; i < p.nb; ++i) { mbar_init(&full_b[i], 1 + 4); mbar_init(&empty_b[i], 1); }
         for (int i = 0; i < p.nw; ++i) { mbar_init(&full_w[i], 1); mbar_init(&empty_w[i], 4); }
         mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 4);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&imap)) : "memory");
         if (p.w_tma)
@@ -183,8 +192,6 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // g_o adjacency row of this tile-row and the order its slots are walked in: the
     // schedule lets tile-rows that share a K-block read its I slab at the same step
-    const int32_t *orow = adj_o + tbm * p.d_o;
-    const int32_t *srow = p.sched ? p.sched + tbm * p.d_o + s_begin : nullptr;
     if (threadIdx.x == 0) trace(p.debug, 6, 0);
 
     if (warp == 5) {
@@ -233,14 +240,24 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     // lane-0-only divergent code made the compiler wrap every UTCHMMA/UTMALDG in an
     // elect loop with R2UR conversions (~500 cycles per step, tools/tc_trace.py).
     if ((p.debug & 32) && warp == 4) asm volatile("bar.sync 2, 160;" ::: "memory");  // late start
+    const int64_t n_tiles = p.persistent ? p.n_tiles : 1;
+    const int64_t tile_stride = p.persistent ? gridDim.x : 1;
+    int64_t it = 0;
+    for (int64_t tile = p.persistent ? blockIdx.x : 0; tile < n_tiles; tile += tile_stride, ++it) {
+    const int64_t n0 = int64_t(p.persistent ? tile / p.blocks_m : blockIdx.x) * p.tn;
+    const int64_t m0 = int64_t(p.persistent ? tile % p.blocks_m : blockIdx.y) * p.rows_valid;
+    const int64_t tbm = m0 / p.tm;
+    const int32_t *orow = adj_o + tbm * p.d_o;
+    const int32_t *srow = p.sched ? p.sched + tbm * p.d_o + s_begin : nullptr;
+    const int g0 = int(it) * nsteps;  // ring position of this tile's first step
     if (warp == 4) {
         // ================= TMA producer: I slabs (runs ahead by the B ring depth) ==========
         const int atoms = p.tn * kElt / 128;           // 128-byte MN atoms per slab
         const int atom_cols = 128 / kElt;
         const uint32_t atom_bytes = uint32_t(p.tk) * 128;
         for (int s = 0; s < nsteps; ++s) {
-            const int st = s % p.nb;
-            const uint32_t ph = (s / p.nb) & 1;
+            const int st = (g0 + s) % p.nb;
+            const uint32_t ph = ((g0 + s) / p.nb) & 1;
             mbar_wait(&empty_b[st], ph ^ 1);
             const int32_t krow = orow[srow ? srow[s] : s_begin + s] * p.tk;
             if (elect_one()) {
@@ -274,8 +291,8 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         if (p.w_tma) {
             const int wstages = (nsteps + p.ws - 1) / p.ws;
             for (int g = 0; g < wstages; ++g) {
-                const int st = g % p.nw;
-                const uint32_t ph = (g / p.nw) & 1;
+                const int st = (g0 + g) % p.nw;
+                const uint32_t ph = ((g0 + g) / p.nw) & 1;
                 mbar_wait(&empty_w[st], ph ^ 1);
                 if (elect_one()) {
                     mbar_expect_tx(&full_w[st], uint32_t(p.w_stage_bytes));
@@ -311,9 +328,13 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const uint32_t a_span16 = uint32_t(p.a_swz) >> 4;                // 16B units per atom row
         const uint32_t a_jump16 = uint32_t(kBlockM - 1) * a_span16;        // next K atom
         const uint32_t b_step16 = uint32_t(32 / kElt) * 128 / 16;           // 32/E K-rows
+        if (it > 0) {  // persistent: the epilogue must have drained the accumulator
+            mbar_wait(tmem_empty, uint32_t((it - 1) & 1));
+            tc_fence_after();
+        }
         for (int s = 0; s < nsteps; ++s) {
-            const int sb = s % p.nb, sa = s % p.na;
-            mbar_wait(&full_b[sb], (s / p.nb) & 1);  // I slab landed and A tile densified
+            const int sb = (g0 + s) % p.nb, sa = (g0 + s) % p.na;
+            mbar_wait(&full_b[sb], ((g0 + s) / p.nb) & 1);  // I slab landed and A tile densified
             if (lane == 0) trace(p.debug, 7, s);
             tc_fence_after();
             if (elect_one()) {
@@ -369,19 +390,21 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const uint32_t wrow = smem_u32(w_buf) + uint32_t(t) * wrow_bytes;
         const uint32_t wxor = p.w_swz ? ((uint32_t(t) * wrow_bytes) >> 7) & uint32_t(p.w_swz / 16 - 1) : 0u;
         for (int s = 0; s < nsteps; ++s) {
-            const int sa = s % p.na;
+            const int gs = g0 + s;  // ring position (continues across persistent tiles)
+            const int sa = gs % p.na;
             const int wg = s / p.ws, wsub = s - wg * p.ws;  // W stage and slot inside it
+            const int wr = g0 + wg;                         // W ring position (ws == 1)
             if (p.w_tma && wsub == 0) {
-                mbar_wait(&full_w[wg % p.nw], (wg / p.nw) & 1);
+                mbar_wait(&full_w[wr % p.nw], (wr / p.nw) & 1);
                 if (t == 0) trace(p.debug, 8, wg);
             }
-            if (s >= p.na) {  // A stage sa was last read by the MMAs of step s - na
-                const int sp = s - p.na;
+            if (gs >= p.na) {  // A stage sa was last read by the MMAs of ring step gs - na
+                const int sp = gs - p.na;
                 mbar_wait(&empty_b[sp % p.nb], (sp / p.nb) & 1);
             }
             if (t == 0) trace(p.debug, 2, s);
             const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
-            const uint32_t src = wrow + uint32_t((wg % p.nw) * p.w_stage_bytes);
+            const uint32_t src = wrow + uint32_t((wr % p.nw) * p.w_stage_bytes);
             const uint32_t c0 = uint32_t(wsub * p.d_t * kElt / 16);  // first chunk of this step
             if (active && !(p.debug & 1)) {
                 if (chunked) {
@@ -433,14 +456,14 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             if (!(p.debug & 256)) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&full_b[s % p.nb]);
-                if (p.w_tma && (wsub == p.ws - 1 || s == nsteps - 1)) mbar_arrive(&empty_w[wg % p.nw]);
+                mbar_arrive(&full_b[gs % p.nb]);
+                if (p.w_tma && (wsub == p.ws - 1 || s == nsteps - 1)) mbar_arrive(&empty_w[wr % p.nw]);
             }
             if (t == 0) trace(p.debug, 3, s);
         }
         // ---- epilogue phase 1: wait for the accumulator; split-K slices > 0 park
         // their fp32 partial tile in the workspace (L2-resident) for the leader
-        mbar_wait(tmem_full, 0);
+        mbar_wait(tmem_full, uint32_t(it & 1));
         tc_fence_after();
         if (threadIdx.x == 0) trace(p.debug, 6, 1);
         if (kslice > 0) {
@@ -482,7 +505,8 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const bool row_ok = row < p.rows_valid;
         const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
         const int64_t slice_stride = int64_t(gridDim.y) * p.rows_valid * p.n_cols;
-        const uint32_t stage = smem_u32(a_buf);
+        unsigned char *stage_buf = p.pstage_bytes ? pstage : a_buf;  // idle rings unless persistent
+        const uint32_t stage = smem_u32(stage_buf);
         for (int c = 0; c < p.tn; c += 32) {
             uint32_t r[32];
             TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
@@ -601,11 +625,11 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (warp == 0 && elect_one()) {
                 if constexpr (CONV) {
-                    tma_store_2d(&omap, a_buf, int32_t(m0), int32_t(n0));
+                    tma_store_2d(&omap, stage_buf, int32_t(m0), int32_t(n0));
                 } else {
                     const int atom_cols = 128 / kOutElt;
                     for (int a = 0; a < p.tn / atom_cols; ++a)
-                        tma_store_2d(&omap, a_buf + a * p.rows_valid * 128, int32_t(n0) + a * atom_cols,
+                        tma_store_2d(&omap, stage_buf + a * p.rows_valid * 128, int32_t(n0) + a * atom_cols,
                                      int32_t(m0));
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -613,7 +637,13 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             }
             __syncwarp();
         }
+        if (p.persistent) {  // accumulator drained: the MMA warp may start the next tile
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tmem_empty);
+        }
     }
+    }  // tile loop
     if (threadIdx.x == 0) trace(p.debug, 6, 2);
     tc_fence_before();
     __syncthreads();
@@ -696,7 +726,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         p.a_stage_bytes = kBlockM * c.tk * elt;
         p.nw = p.w_tma ? 2 : 1;
         const size_t base = 1024 + size_t(kBlockM) * c.d_t * 2 + 64 +
-                            (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 16 + 1);
+                            (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 16 + 2) + 16;
         size_t w_bytes = size_t(p.nw) * p.w_stage_bytes;
         int na = 2;
         if (const char *env = getenv("RBGP4_TC_NA")) na = std::max(1, std::min(8, atoi(env)));
@@ -714,7 +744,19 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         // I and W rings share the rest: both chains (I slab of step s waits for the MMA of
         // s - nb, W tile of step s for the densify of s - nw) progress nb resp. nw steps per
         // load latency, so maximise min(nb, nw), then nb
-        const size_t avail = kSmemCap - (base + a_ring);
+        // many waves of tiles: persistent CTAs (setup, TMEM allocation and the pipeline fill
+        // once per SM; loads of tile i+1 stream under the epilogue of tile i) with a dedicated
+        // output staging area for the TMA-store epilogue
+        const int64_t tiles_here = ((c.n_cols + tn - 1) / tn) * blocks_m;
+        // Opt-in (RBGP4_TC_PERSIST=1): correct and tested, but measured no faster than one CTA
+        // per tile on the VGG layers (the densify warps are also the epilogue warps, so the
+        // densify -> MMA -> epilogue chain stays serial per tile); K4 has dedicated epilogue warps.
+        (void)tiles_here;
+        const bool persist = p.rows_valid == c.tm && getenv("RBGP4_TC_PERSIST") && !getenv("RBGP4_TC_NOPERSIST");
+        p.pstage_bytes = persist ? int32_t(size_t(p.rows_valid) * tn * 4) : 0;  // f32 worst case
+        const size_t pst = persist ? size_t(p.pstage_bytes) + 1024 : 0;
+        if (base + a_ring + pst + 4 * size_t(p.b_stage_bytes) > kSmemCap) { p.pstage_bytes = 0; }
+        const size_t avail = kSmemCap - (base + a_ring + (p.pstage_bytes ? pst : 0));
         int nb = 0, nw = 0;
         for (int cand = 16; cand >= 2; --cand) {
             const size_t ib = size_t(cand) * p.b_stage_bytes;
@@ -753,8 +795,14 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         if (const char *env = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(env)));
         p.sps = (c.d_o + ks - 1) / ks;
         p.ksplit = (c.d_o + p.sps - 1) / p.sps;  // no empty slices
+        // many waves of tiles: persistent CTAs (setup, TMEM allocation and the pipeline fill
+        // once per SM; loads of tile i+1 stream under the epilogue of tile i)
+        p.blocks_m = int(blocks_m);
+        p.n_tiles = tiles;
+        p.persistent = (p.ksplit == 1 && p.pstage_bytes && p.rows_valid == c.tm) ? 1 : 0;
+        if (!p.persistent) p.pstage_bytes = 0;
         out->p = p;
-        out->smem = fixed + size_t(nb) * p.b_stage_bytes;
+        out->smem = fixed + size_t(nb) * p.b_stage_bytes + (p.pstage_bytes ? size_t(p.pstage_bytes) + 1024 : 0);
         out->blocks_m = int(blocks_m);
         return 1;
     }
@@ -764,7 +812,8 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
 
 // The TMA-store epilogue stages the whole output tile in the (then idle) A + I rings.
 bool staging_fits(const TcPlan &pl, int out_elt) {
-    const size_t rings = size_t(pl.p.na) * pl.p.a_stage_bytes + size_t(pl.p.nb) * pl.p.b_stage_bytes;
+    const size_t rings = pl.p.pstage_bytes ? size_t(pl.p.pstage_bytes)
+                                           : size_t(pl.p.na) * pl.p.a_stage_bytes + size_t(pl.p.nb) * pl.p.b_stage_bytes;
     return size_t(pl.p.rows_valid) * pl.p.tn * out_elt <= rings && !getenv("RBGP4_TC_NOSTORE");
 }
 
@@ -779,8 +828,10 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
         set_error("cudaFuncSetAttribute(tc): %s", cudaGetErrorString(e));
         return RBGP4_ECUDA;
     }
-    dim3 grid(unsigned((pl.p.n_cols + pl.p.tn - 1) / pl.p.tn), unsigned(pl.blocks_m),
-              unsigned(pl.p.ksplit));
+    dim3 grid = pl.p.persistent
+                    ? dim3(unsigned(std::min<int64_t>(pl.p.n_tiles, kNumSMs)), 1, 1)
+                    : dim3(unsigned((pl.p.n_cols + pl.p.tn - 1) / pl.p.tn), unsigned(pl.blocks_m),
+                           unsigned(pl.p.ksplit));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);

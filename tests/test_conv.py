@@ -63,8 +63,11 @@ def test_im2col_oracle_matches_direct_conv():
 @pytest.mark.parametrize("c_out,c_in,hw,batch", [(128, 128, 4, 2), (256, 128, 8, 3), (128, 256, 2, 5),
                                                  (128, 128, 16, 1)])
 @pytest.mark.parametrize("relu", [False, True])
-def test_sparse_conv_matches_oracle(c_out, c_in, hw, batch, relu):
+@pytest.mark.parametrize("persistent", [False, True])
+def test_sparse_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent, monkeypatch):
     import torch
+    if persistent:  # persistent tile loop (chosen by itself for many-wave grids)
+        monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
     chain = conv_chain(c_out, c_in, seed=c_out + c_in + hw)
     w = ks.init_random(chain, 7, precision="f32")
     rng = np.random.default_rng(3)

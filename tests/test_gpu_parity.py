@@ -134,8 +134,11 @@ def test_general_chain_reference_on_gpu():
     assert np.array_equal(got, oracle.reference_product(w, inp))
 
 
+@pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("compute,tol", [("tf32", 1e-2), ("bf16", 1e-2)])
-def test_tensor_core_modes(golden, compute, tol):
+def test_tensor_core_modes(golden, compute, tol, persistent, monkeypatch):
+    if persistent:  # persistent tile loop of the tcgen05 kernels, forced
+        monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
     lib = _native.lib()
     for cid in golden["cases"]:
         entry = golden["cases"][cid]
