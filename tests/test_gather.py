@@ -67,6 +67,7 @@ CASES = [
     ((4, 36), 0.5, (8, 8), 0.5, (16, 16), 384),     # 75 %: d_t = 64 (128-byte W rows)
     ((2, 8), 0.0, (4, 4), 0.5, (32, 32), 256),      # 32 x 32 blocks: 2 MMAs per block
     ((8, 16), 0.5, (4, 4), 0.5, (16, 16), 640),     # 64-row tile-rows (TMEM 64 columns)
+    ((4, 12), 0.5, (8, 8), 0.75, (16, 16), 320),    # ragged last column tile (2.5 x 128)
 ]
 
 
