@@ -184,8 +184,22 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 
     if (warp == 4) {
         // ================= TMA producer: I slab + W tile of each step, one barrier ======
-        // inputs may be the previous kernel's outputs: wait for it to complete (no-op when this
-        // launch has no programmatic dependency)
+        // The weights are never the previous kernel's output: the W tiles of the first ring's
+        // worth of steps are requested before waiting on it.  The I slabs may be its output, so
+        // they wait (griddepcontrol.wait is a no-op without a programmatic dependency).
+        const int pre = (p.debug & 128) ? 0 : min(p.ns, nsteps);
+        if (elect_one()) {
+            for (int s = 0; s < pre; ++s) {
+                const int j = srow ? srow[s] : s_begin + s;
+                mbar_expect_tx(&full[s], uint32_t(stage_bytes));
+                unsigned char *wdst = ring + size_t(s) * stage_bytes + p.i_bytes;
+                if (p.cols)
+                    tma_load_2d(wdst, &wmap, &full[s], 0, (tbm * p.d_o + j) * p.w_rows);
+                else
+                    tma_load_2d(wdst, &wmap, &full[s], j * p.d_t, int32_t(m0) + ui0 * p.bm);
+            }
+        }
+        __syncwarp();
         asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
@@ -198,7 +212,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 mbar_arrive(&full[st]);  // ablation: no loads (MMA / pipeline skeleton only)
                 gtrace(p.debug, 0, s);
             } else if (leader) {
-                mbar_expect_tx(&full[st], uint32_t(stage_bytes));
+                if (s >= pre) mbar_expect_tx(&full[st], uint32_t(stage_bytes));
                 unsigned char *dst = ring + size_t(st) * stage_bytes;
                 if constexpr (CONV) {
                     // K rows [krow, krow + tk) = tap (i, j), channels [c0, c0 + tk): per 64-channel
@@ -243,7 +257,9 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     // (64 cols, tk rows, 2 atoms) box: MN-major, atom-major in shared memory
                     tma_load_3d(dst, &imap, &full[st], 0, krow, int32_t(n0 / 64));
                 }
-                if (p.cols)  // re-laid tiles: (bk, rows) view, tile (tbm, j) = w_rows rows
+                if (s < pre) {
+                    // W tile already requested before griddepcontrol.wait
+                } else if (p.cols)  // re-laid tiles: (bk, rows) view, tile (tbm, j) = w_rows rows
                     tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
                 else  // this CTA's rows of the compressed tile
                     tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, int32_t(m0) + ui0 * p.bm);
@@ -435,12 +451,13 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             if (p.sym) {
                 for (int k = 0; k < p.ksplit - 1; ++k) {
                     const uint32_t src = recv + uint32_t(((k * rp + (c - r_lo)) * kBatch + t) * 4);
+                    // all 32 loads in flight before the adds (one latency per slot, not per row)
+                    float v[32];
 #pragma unroll
-                    for (int q = 0; q < 32; ++q) {
-                        float v;
-                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(src + uint32_t(q * kBatch * 4)));
-                        r[q] = __float_as_uint(__uint_as_float(r[q]) + v);
-                    }
+                    for (int q = 0; q < 32; ++q)
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q]) : "r"(src + uint32_t(q * kBatch * 4)));
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) + v[q]);
                 }
             } else {
                 for (int k = 1; k < p.ksplit; ++k) {
