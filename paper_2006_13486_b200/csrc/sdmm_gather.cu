@@ -417,13 +417,13 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 uint32_t r[32];
                 load_rows(c, r);
                 const int slot = kslice < owner ? kslice : kslice - 1;
-                uint32_t dst;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(recv), "r"(owner));
-                dst += uint32_t(((slot * rp + (c - owner * rp)) * kBatch + t) * 4);
+                // generic address of the owner's receive row (mapa on a generic address), then
+                // plain stores the compiler can issue back to back (volatile asm serialised them)
+                float *mine = reinterpret_cast<float *>(ring) + (int64_t(slot) * rp + (c - owner * rp)) * kBatch + t;
+                float *dstp;
+                asm volatile("mapa.u64 %0, %1, %2;" : "=l"(dstp) : "l"(mine), "r"(owner));
 #pragma unroll
-                for (int q = 0; q < 32; ++q)
-                    asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(dst + uint32_t(q * kBatch * 4)), "r"(r[q])
-                                 : "memory");
+                for (int q = 0; q < 32; ++q) dstp[q * kBatch] = __uint_as_float(r[q]);
             }
         }
         if (threadIdx.x == 0) gtrace(p.debug, 3, 5);
@@ -448,16 +448,17 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         for (int c = r_lo; c < r_lo + rp; c += 32) {
             uint32_t r[32];
             load_rows(c - t_lo, r);
-            if (p.sym) {
+            if (p.debug & 1024) {
+                if (threadIdx.x == 0) gtrace(p.debug, 3, 9);
+            } else if (p.sym) {
+                // plain shared loads (the static __shared__ base keeps them LDS) so ptxas can keep
+                // all of them in flight; volatile asm loads measured latency-serialised
+                const float *rb = reinterpret_cast<const float *>(smem_raw + (ring - smem_raw));
                 for (int k = 0; k < p.ksplit - 1; ++k) {
-                    const uint32_t src = recv + uint32_t(((k * rp + (c - r_lo)) * kBatch + t) * 4);
-                    // all 32 loads in flight before the adds (one latency per slot, not per row)
-                    float v[32];
+                    const float *src = rb + (int64_t(k) * rp + (c - r_lo)) * kBatch + t;
 #pragma unroll
                     for (int q = 0; q < 32; ++q)
-                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q]) : "r"(src + uint32_t(q * kBatch * 4)));
-#pragma unroll
-                    for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) + v[q]);
+                        r[q] = __float_as_uint(__uint_as_float(r[q]) + src[q * kBatch]);
                 }
             } else {
                 for (int k = 1; k < p.ksplit; ++k) {
@@ -474,6 +475,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
             const int cr = c - r_lo;  // row inside this CTA's output range
+            if (threadIdx.x == 0) gtrace(p.debug, 3, 10);
+            if (p.debug & 2048) continue;
             if constexpr (CONV) {
                 // NHWC: pixel t holds channels c..c+31 -> 4 x 16-byte chunks of its 128-byte
                 // rows in 64-channel atoms [atom][pixel][128 B], 128B-swizzled (chunk ^ pixel%8)

@@ -35,7 +35,7 @@ e0 = t[3, 0]
 print("setup", t[3, 1] - e0, "tmem_full seen", t[3, 2] - e0, "epilogue done", t[3, 3] - e0)
 print("epilogue marks (rel. tmem_full): barrier1", t[3, 4] - t[3, 2], "pushed", t[3, 5] - t[3, 2],
       "barrier2", t[3, 6] - t[3, 2], "staged", t[3, 7] - t[3, 2], "bar.sync", t[3, 8] - t[3, 2],
-      "stored", t[3, 3] - t[3, 2])
+      "stored", t[3, 3] - t[3, 2], "| last chunk: rows loaded+reduced", t[3, 10] - t[3, 2])
 print("step   issue   full   lat   mma_done")
 for s in range(int(os.environ.get("STEPS", "18"))):
     print(f"{s:4d} {t[0, s]-e0:7d} {t[1, s]-e0:7d} {t[1, s]-t[0, s]:6d} {t[2, s]-e0:8d}")
