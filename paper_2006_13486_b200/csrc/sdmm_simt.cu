@@ -246,7 +246,15 @@ int plan_simt(const ChainDims &c, SimtPlan *plan) {
     int rt = (c.g % 4 == 0) ? 4 : (c.g % 2 == 0) ? 2 : 1;
     const int max_regs_chunks = sizeof(T) == 4 ? 16 : 8;  // NCH*RT bound (register budget)
     const size_t smem_cap = 227 * 1024;
+    // Column-block width 4*cthreads: the widest whose grid still covers every SM (one tile per
+    // CTA is a serial walk over the d_o steps, so idle SMs cost more than narrower tiles):
+    // measured on the VGG shapes, conv13 (N = 1024) 153 -> 64 us at 32 columns per CTA.
+    const char *ct_env = getenv("RBGP4_SIMT_CT");
+    SimtPlan fallback{};
+    bool have = false;
+    const int64_t row_blocks = c.rows / c.tm;
     for (int cthreads : {32, 16, 8}) {
+        if (ct_env && atoi(ct_env) != cthreads) continue;
         int rthreads = kThreads / cthreads;
         int chunks = c.tm / rt;
         int nch = 1;
@@ -254,9 +262,16 @@ int plan_simt(const ChainDims &c, SimtPlan *plan) {
         if (nch > 8 || nch * rt > max_regs_chunks) continue;
         size_t sm = smem_bytes<T>(c, cthreads);
         if (sm > smem_cap) continue;
-        // do not waste columns on narrow inputs
-        if (cthreads > 8 && 4 * cthreads >= 2 * c.n_cols) continue;
-        *plan = {rt, nch, cthreads, sm};
+        const int64_t grid = (c.n_cols + 4 * cthreads - 1) / (4 * cthreads) * row_blocks;
+        fallback = {rt, nch, cthreads, sm};
+        have = true;
+        if (ct_env || grid >= kNumSMs) {
+            *plan = fallback;
+            return 1;
+        }
+    }
+    if (have) {  // no width covers the SMs: the narrowest feasible one
+        *plan = fallback;
         return 1;
     }
     set_error("SIMT path: tile %dx%d (d_t=%d, u_i=%d) exceeds register/shared-memory budget",
