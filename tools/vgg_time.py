@@ -4,6 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2006_13486_b200.vgg import VGG19Sparse
 
+if len(sys.argv) > 3 and sys.argv[3] == "cudnn-benchmark":
+    torch.backends.cudnn.benchmark = True
+
 batch = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 sp = float(sys.argv[2]) if len(sys.argv) > 2 else 0.875
 net = VGG19Sparse(sparsity=sp)
