@@ -13,8 +13,6 @@ import os
 from .errors import DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b200.so")
-# A/B experiments only (tools/): load another build of the same ABI
-LIB_PATH = os.environ.get("RBGP4_LIB_PATH", LIB_PATH)
 
 F32, F64, BF16 = 0, 1, 2
 COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
