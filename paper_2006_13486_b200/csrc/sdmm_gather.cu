@@ -58,6 +58,8 @@ __device__ __forceinline__ void gtrace(int debug, int ev, int step) {
 }
 constexpr int kBatch = 128;  // MMA M: batch columns (or pixels) per CTA
 constexpr int kMaxMma = 256; // MMAs per step (u_i * d_i * bk / 16)
+constexpr int kMaxCols = 64; // relayout partials per tile (u_i * d_i)
+constexpr int kMaxSched = 256; // steps whose (adjacency slot, slab row) are staged in shared memory
 
 struct GParams {
     int64_t n_cols, ld_out;
@@ -100,6 +102,11 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     // MMA table, one uint2 per MMA of a step: x = A offset | B offset << 16 (16-byte units,
     // relative to the stage), y = TMEM column of D | 1 << 31 on the first MMA into it
     __shared__ uint2 mma_tab[kMaxMma];
+    // relayout: TMEM column of each (row block, neighbour) partial, read by the epilogue
+    __shared__ int32_t s_cols[kMaxCols];
+    // the producer's step list, read from global memory by its lanes during setup (the first
+    // slab no longer waits behind two dependent global loads)
+    __shared__ int32_t s_j[kMaxSched], s_krow[kMaxSched];
     unsigned char *ring = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stage_bytes = p.i_bytes + p.w_bytes;
@@ -125,6 +132,14 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     const int32_t *srow = p.sched ? p.sched + int64_t(tbm) * p.d_o + s_begin : nullptr;
     const int32_t *prow = p.mc ? p.pair + int64_t(tbm) * p.d_o : nullptr;
 
+    const bool staged_sched = nsteps <= kMaxSched;
+    if (warp == 4 && staged_sched) {
+        for (int i = lane; i < nsteps; i += 32) {
+            const int j = srow ? srow[i] : s_begin + i;
+            s_j[i] = j;
+            s_krow[i] = orow[j] * p.tk;
+        }
+    }
     if (warp == 4 && lane == 0) {
         // empty[st] of step s completes on two arrivals in multicast mode: this CTA's release
         // of the slot and its step-s partner's (or this CTA's commit twice when unpaired)
@@ -165,6 +180,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             mma_tab[i] = make_uint2((a_off >> 4) | ((b_off >> 4) << 16),
                                     uint32_t(dcol) | ((kk == 0 && (p.cols || slot == 0)) ? 0x80000000u : 0u));
         }
+        if (p.cols)
+            for (int i = lane; i < p.u_i * p.d_i; i += 32) s_cols[i] = p.cols[i];
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -190,7 +207,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         const int pre = (p.debug & 128) ? 0 : min(p.ns, nsteps);
         if (elect_one()) {
             for (int s = 0; s < pre; ++s) {
-                const int j = srow ? srow[s] : s_begin + s;
+                const int j = staged_sched ? s_j[s] : srow ? srow[s] : s_begin + s;
                 mbar_expect_tx(&full[s], uint32_t(stage_bytes));
                 unsigned char *wdst = ring + size_t(s) * stage_bytes + p.i_bytes;
                 if (p.cols)
@@ -205,8 +222,9 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int st = s % p.ns;
             if (p.debug & 256) mbar_wait_sleep(&empty[st], ((s / p.ns) & 1) ^ 1, 64);
             else mbar_wait(&empty[st], ((s / p.ns) & 1) ^ 1);
-            const int j = srow ? srow[s] : s_begin + s;  // g_o adjacency slot of this step
-            const int32_t krow = orow[j] * p.tk;
+            // g_o adjacency slot of this step and its first slab row
+            const int j = staged_sched ? s_j[s] : srow ? srow[s] : s_begin + s;
+            const int32_t krow = staged_sched ? s_krow[s] : orow[j] * p.tk;
             const bool leader = elect_one();
             if (leader && (p.debug & 128)) {
                 mbar_arrive(&full[st]);  // ablation: no loads (MMA / pipeline skeleton only)
@@ -293,6 +311,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
         const bool in_regs = n_mma <= kRegMma;
         const bool no_mma = p.debug & 2;
+        const bool fast8 = !CONV && MMA_N == 32 && p.cols && p.bk == 16 && v_blocks == 8 && p.w_swz == 32 &&
+                           !(p.debug & 16384);
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
             mbar_wait(&full[st], (s / p.ns) & 1);
@@ -302,6 +322,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
                 const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
                 if (no_mma) {
+                } else if (fast8) {
+                    // relayout, TC16 factorisation (8 column blocks of 16 rows, N = 32): every
+                    // offset is an immediate, so a step is 8 UTCHMMAs and a few uniform adds
+                    const uint32_t acc = s > 0 ? 1u : 0u;
+                    const uint64_t bd = b_st + (uint32_t(p.i_bytes) >> 4);
+#pragma unroll
+                    for (int kb = 0; kb < 8; ++kb)
+                        tc_mma<false>(tmem_d + uint32_t(kb * MMA_N), a_st + uint32_t(kb * 16 * 8),
+                                      bd + uint32_t(kb * ((MMA_N * 32) >> 4)), idesc, acc);
                 } else if (p.cols) {
                     // relayout: every descriptor is uniform arithmetic of (kb, kk) -- no table,
                     // no register-to-uniform moves on the issue path
@@ -355,10 +384,19 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
         if (elect_one()) tc_commit(tmem_full);
         __syncwarp();
+        if (!(p.debug & (4096 | 8192))) {
+            // hand the accumulator to the epilogue warps through a named barrier: they sleep
+            // in bar.sync for the whole main loop instead of polling tmem_full (polling warps
+            // measured to slow this warp's MMA issue)
+            mbar_wait(tmem_full, 0);
+            tc_fence_before();
+            asm volatile("bar.arrive 2, 160;" ::: "memory");
+        }
     } else {
         // ================= epilogue (warps 0-3): TMEM lane = batch column =================
-        if (p.debug & 64) mbar_wait(tmem_full, 0);
-        else mbar_wait_sleep(tmem_full, 0, 256);
+        if (p.debug & 4096) mbar_wait_sleep(tmem_full, 0, 256);  // A/B: polling with back-off
+        else if (p.debug & 8192) mbar_wait_parked(tmem_full, 0);
+        else asm volatile("bar.sync 2, 160;" ::: "memory");
         tc_fence_after();
         if (threadIdx.x == 0) gtrace(p.debug, 3, 2);
     }
@@ -375,6 +413,23 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             return;
         }
+        if (p.d_i == 2) {
+            uint32_t v[2][2][16];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int row = c + 16 * h, ui = row / p.bm, m = row % p.bm;
+#pragma unroll
+                for (int ink = 0; ink < 2; ++ink)
+                    TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[ui * 2 + ink] + m), v[h][ink]);
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    r[16 * h + q] = __float_as_uint(__uint_as_float(v[h][0][q]) + __uint_as_float(v[h][1][q]));
+            return;
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int row = c + 16 * h, ui = row / p.bm, m = row % p.bm;
@@ -383,7 +438,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             for (int q = 0; q < 16; ++q) acc[q] = 0.0f;
             for (int ink = 0; ink < p.d_i; ++ink) {
                 uint32_t v[16];
-                TMEM_LD_32x32b_X16(lane_base + uint32_t(p.cols[ui * p.d_i + ink] + m), v);
+                TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[ui * p.d_i + ink] + m), v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int q = 0; q < 16; ++q) acc[q] += __uint_as_float(v[q]);
@@ -707,7 +762,8 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             const int tbm = int(tile % u_o);
             const int64_t n0 = (tile / u_o) * kBatch;
             const int64_t m0 = int64_t(tbm) * p.tm;
-            mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
+            if (p.debug & 4096) mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
+            else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
             tc_fence_after();
             const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * p.tm);
             const int64_t col = n0 + t;
@@ -792,9 +848,12 @@ int gather_relayout_ok(const ChainDims &c) {
     const int span = c.bk * 2;
     if (span != 32 && span != 64 && span != 128) return 0;
     if (c.tm * c.d_i > 256 || d_r * c.bm > 256) return 0;
-    // opt-in: one N = d_r*bm MMA per column block halves the MMA count, but the epilogue's
-    // d_i-way partial sums cost more than that saves on the VGG shapes (measured)
-    return getenv("RBGP4_TC_RELAYOUT") ? 1 : 0;
+    if (getenv("RBGP4_TC_NORELAYOUT")) return 0;
+    if (getenv("RBGP4_TC_RELAYOUT")) return 1;
+    // default where the immediate-offset MMA loop applies (TC16: 8 column blocks of 16 rows,
+    // N = 32, d_i = 2): half the MMAs of the direct mode and no per-MMA descriptor arithmetic.
+    // Elsewhere the generic relayout loop loses to the direct mode (measured), so it is opt-in.
+    return (c.bk == 16 && c.v_i == 8 && d_r * c.bm == 32 && c.d_i == 2) ? 1 : 0;
 }
 
 int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan *out, bool pairs = false) {
@@ -833,7 +892,10 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     p.w_bytes = p.w_rows * w_row;  // = tm * d_t * 2 (half of it in M-split)
     p.w_swz = w_row;
     const size_t stage = size_t(p.i_bytes) + p.w_bytes;
-    const size_t fixed = 1024 + 8 * (2 * 16 + 1) + 16 + 64 + size_t(kMaxMma) * 8;  // + static table
+    // dynamic: alignment slack + barriers + ring; the static tables count against the same
+    // 227 KB per-CTA limit
+    const size_t fixed = 1024 + 8 * (2 * 16 + 1) + 16 + 64;
+    const size_t statics = size_t(kMaxMma) * 8 + size_t(kMaxCols) * 4 + size_t(kMaxSched) * 8 + 256;
     // Occupancy: a CTA's steps are a serial latency chain (load -> MMA issue -> commit), so
     // when one tile per SM would leave SMs idle, the steps of a tile are split over a cluster
     // (DSMEM reduction) and two CTAs share an SM with 2-stage rings (measured on the VGG
@@ -849,9 +911,9 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     if (const char *e = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(e)));
     if (p.persistent || p.msplit) ks = 1;
     if (p.persistent) dual = false;
-    int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed - 64) / stage));
+    int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed - statics) / stage));
     if (const char *e = getenv("RBGP4_TC_NS")) ns = std::max(2, std::min(16, atoi(e)));
-    if (fixed + size_t(ns) * stage > kGSmemCap) return 0;
+    if (fixed + statics + size_t(ns) * stage > kGSmemCap) return 0;
     p.ns = ns;
     p.tmem_cols = 32;
     while (p.tmem_cols < (relayout ? c.tm * c.d_i : c.tm / (p.msplit ? 2 : 1)) * (p.persistent ? 2 : 1))
@@ -862,7 +924,8 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     if (const char *e = getenv("RBGP4_TC_DEBUG")) p.debug = atoi(e);
     // multicast pairs: the u_o tile-rows of a column block as one cluster (<= 8 portable)
     // (SDMM slabs are two 64-column atoms; conv slabs must have an even number of channel atoms)
-    p.mc = (pairs && p.ksplit == 1 && !p.persistent && !p.msplit && c.u_o >= 2 && c.u_o <= 8 &&
+    // (relayout: measured slower with pairs -- 26.6 vs 25.2 us on conv10 -- so never paired)
+    p.mc = (pairs && p.ksplit == 1 && !p.persistent && !p.msplit && !relayout && c.u_o >= 2 && c.u_o <= 8 &&
             (!conv || (c.tk / 64) % 2 == 0) && !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
     out->p = p;
     out->smem = fixed + size_t(ns) * stage;
@@ -985,6 +1048,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
         cudaError_t e = cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
         if (e != cudaSuccess) {
             set_error("cudaFuncSetAttribute(gather persistent): %s", cudaGetErrorString(e));
+            (void)cudaGetLastError();  // not sticky: do not leave it for the next launch check
             return RBGP4_ECUDA;
         }
         cudaLaunchConfig_t cfg{};
@@ -1020,6 +1084,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(gather): %s", cudaGetErrorString(e));
+        (void)cudaGetLastError();  // not sticky: do not leave it for the next launch check
         return RBGP4_ECUDA;
     }
     cudaLaunchConfig_t cfg{};

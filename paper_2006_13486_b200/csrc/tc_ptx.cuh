@@ -49,6 +49,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(addr), "r"(parity) : "memory");
 #endif
 }
+// long waits without polling: try_wait with a suspend-time hint parks the thread in hardware
+// until the phase completes (or ~1 ms passes), so a waiting warp issues nothing meanwhile
+__device__ __forceinline__ void mbar_wait_parked(uint64_t *bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(addr), "r"(parity), "r"(1000000u) : "memory");
+}
 // long waits (the epilogue warps wait for the whole main loop): poll with a back-off so the
 // spinning warps do not take issue slots from the MMA / TMA warps sharing their SM sub-partition
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {

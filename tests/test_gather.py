@@ -28,15 +28,22 @@ def chain_of(g_o, sp_o, g_i, sp_i, g_b, seed=0):
     return wl.build_chain(cfg)
 
 
-def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False, msplit=False):
-    """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout (opt-in).
+def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False, msplit=False,
+        direct=False):
+    """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout for any
+    shape (by itself only where its immediate-offset loop applies, e.g. the VGG TC16 shape);
+    direct / persistent / msplit: K4 on the compressed values as stored (no relayout).
 
-    The prepared buffer is cached per matrix, so relayout runs use a fresh RcubsMatrix copy."""
+    The prepared buffer is cached per matrix and its layout follows the mode, so non-default
+    modes run on a fresh RcubsMatrix copy."""
     p = ks.tiling_for_chain(w.chain, tn=1, rn=1, bn=1)
     if dense:
         os.environ["RBGP4_TC_DENSE"] = "1"
     if relayout:
         os.environ["RBGP4_TC_RELAYOUT"] = "1"
+    if direct or persistent or msplit:
+        os.environ["RBGP4_TC_NORELAYOUT"] = "1"
+    if relayout or direct or persistent or msplit:
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
     if persistent:
         os.environ["RBGP4_TC_PERSIST"] = "1"
@@ -48,6 +55,7 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
     finally:
         os.environ.pop("RBGP4_TC_DENSE", None)
         os.environ.pop("RBGP4_TC_RELAYOUT", None)
+        os.environ.pop("RBGP4_TC_NORELAYOUT", None)
         os.environ.pop("RBGP4_TC_PERSIST", None)
         os.environ.pop("RBGP4_TC_MSPLIT", None)
     return y.float().cpu().numpy()
@@ -88,6 +96,8 @@ def test_gather_sdmm_matches_oracle(case):
     assert oracle.rel_l2(got, dense) < 4e-3
     relaid = run(w, x.cuda(), relayout=True)
     assert oracle.rel_l2(relaid, ref) < 4e-3
+    direct = run(w, x.cuda(), direct=True)
+    assert oracle.rel_l2(direct, ref) < 4e-3
     # persistent tile loop (taken by itself only for many-wave grids; forced here)
     pers = run(w, x.cuda(), persistent=True)
     assert oracle.rel_l2(pers, ref) < 4e-3

@@ -137,8 +137,9 @@ def test_general_chain_reference_on_gpu():
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("compute,tol", [("tf32", 1e-2), ("bf16", 1e-2)])
 def test_tensor_core_modes(golden, compute, tol, persistent, monkeypatch):
-    if persistent:  # persistent tile loop of the tcgen05 kernels, forced
+    if persistent:  # persistent tile loop of the tcgen05 kernels, forced (K4 on the stored values)
         monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
+        monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
     lib = _native.lib()
     for cid in golden["cases"]:
         entry = golden["cases"][cid]
