@@ -311,7 +311,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
         const bool in_regs = n_mma <= kRegMma;
         const bool no_mma = p.debug & 2;
-        const bool fast8 = !CONV && MMA_N == 32 && p.cols && p.bk == 16 && v_blocks == 8 && p.w_swz == 32 &&
+        const bool fast8 = MMA_N == 32 && p.cols && p.bk == 16 && v_blocks == 8 && p.w_swz == 32 &&
                            !(p.debug & 16384);
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
@@ -324,13 +324,19 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 if (no_mma) {
                 } else if (fast8) {
                     // relayout, TC16 factorisation (8 column blocks of 16 rows, N = 32): every
-                    // offset is an immediate, so a step is 8 UTCHMMAs and a few uniform adds
+                    // offset is an immediate, so a step is 8 UTCHMMAs and a few uniform adds.
+                    // A rows kb*16..+15: SDMM slab rows of 128 B; conv: 32-byte K offset inside
+                    // the 64-channel atom (kb % 4) of atom kb / 4
                     const uint32_t acc = s > 0 ? 1u : 0u;
                     const uint64_t bd = b_st + (uint32_t(p.i_bytes) >> 4);
 #pragma unroll
-                    for (int kb = 0; kb < 8; ++kb)
-                        tc_mma<false>(tmem_d + uint32_t(kb * MMA_N), a_st + uint32_t(kb * 16 * 8),
+                    for (int kb = 0; kb < 8; ++kb) {
+                        constexpr uint32_t kAtom16 = uint32_t(kBatch * 128) >> 4;
+                        const uint32_t a16 = CONV ? uint32_t(kb / 4) * kAtom16 + uint32_t(kb % 4) * 2
+                                                  : uint32_t(kb * 16 * 8);
+                        tc_mma<false>(tmem_d + uint32_t(kb * MMA_N), a_st + a16,
                                       bd + uint32_t(kb * ((MMA_N * 32) >> 4)), idesc, acc);
+                    }
                 } else if (p.cols) {
                     // relayout: every descriptor is uniform arithmetic of (kb, kk) -- no table,
                     // no register-to-uniform moves on the issue path

@@ -1293,9 +1293,7 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
     pl.p.prep = static_cast<const uint16_t *>(prep);
     pl.p.sched = tc_prep_schedule(c, pl, prep);
     {
-        // the relayout MMA loop has no immediate-offset form for the conv A layout: the conv
-        // takes the direct mode unless asked (RBGP4_TC_RELAYOUT)
-        const void *k4 = getenv("RBGP4_TC_RELAYOUT") ? tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep) : nullptr;
+        const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep);
         if (gather_conv_supported(c, cv, out_dtype, k4 != nullptr))
             return launch_gather_conv(c, cv, out_dtype, values, adj_o, adj_i, pl.p.sched, tc_prep_pair(c, pl, prep),
                                       k4, x, out, stream);

@@ -68,6 +68,7 @@ def test_sparse_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent, mo
     import torch
     if persistent:  # persistent tile loop (chosen by itself for many-wave grids)
         monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
+        monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
     chain = conv_chain(c_out, c_in, seed=c_out + c_in + hw)
     w = ks.init_random(chain, 7, precision="f32")
     rng = np.random.default_rng(3)

@@ -134,7 +134,7 @@ CONV_CASES = [(128, 128, 4, 9), (256, 128, 8, 3), (128, 256, 16, 1), (128, 128, 
 
 @pytest.mark.parametrize("c_out,c_in,hw,batch", CONV_CASES)
 @pytest.mark.parametrize("relu", [False, True])
-@pytest.mark.parametrize("mode", ["default", "persistent", "msplit"])
+@pytest.mark.parametrize("mode", ["default", "direct", "persistent", "msplit"])
 def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     from test_conv import im2col_nhwc
     cfg = wl.SweepConfig("conv16", (c_out // 128, 9 * c_in // 128), 0.0, (1, 1), (8, 8), 0.75,
@@ -143,14 +143,17 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     w = ks.init_random(chain, 7, precision="f32")
     x = np.random.default_rng(3).uniform(-1, 1, (batch, hw, hw, c_in)).astype(np.float32)
     xb = torch.from_numpy(x).to(torch.bfloat16)
-    env = {"persistent": "RBGP4_TC_PERSIST", "msplit": "RBGP4_TC_MSPLIT"}.get(mode)
-    if env:
-        os.environ[env] = "1"
+    # default: the TC16 relayout (immediate-offset MMA loop); the other modes run on the
+    # compressed values as stored
+    env = {"persistent": ["RBGP4_TC_PERSIST", "RBGP4_TC_NORELAYOUT"],
+           "msplit": ["RBGP4_TC_MSPLIT", "RBGP4_TC_NORELAYOUT"], "direct": ["RBGP4_TC_NORELAYOUT"]}.get(mode, [])
+    for e in env:
+        os.environ[e] = "1"
     try:
         got = conv.sparse_conv2d(w, xb.cuda(), 3, relu=relu, out_dtype=torch.float32).cpu().numpy()
     finally:
-        if env:
-            os.environ.pop(env, None)
+        for e in env:
+            os.environ.pop(e, None)
     ref = f64_ref(w, np.ascontiguousarray(im2col_nhwc(xb.float().numpy(), 3)))
     ref = ref.T.reshape(batch, hw, hw, c_out)
     if relu:
