@@ -636,9 +636,14 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                          void *__restrict__ out, int64_t n_tiles) {
     extern __shared__ unsigned char smem_raw[];
     __shared__ uint2 mma_tab[kMaxMma];
+    __shared__ int32_t s_cols[kMaxCols];  // relayout: TMEM column of each (row block, neighbour) partial
     unsigned char *ring = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stage_bytes = p.i_bytes + p.w_bytes;
+    // relayout (TC16 only here, the immediate-offset loop): 8 MMAs of N = 32 per step into the
+    // tile's d_i partial accumulators (tm * d_i columns per buffer)
+    const bool rl = p.cols != nullptr;
+    const int acc_cols = rl ? p.tm * p.d_i : p.tm;
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + size_t(p.ns) * stage_bytes);
     uint64_t *empty = full + p.ns;
     uint64_t *acc_full = empty + p.ns;     // [2]: last MMA of a tile committed
@@ -667,6 +672,8 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             mma_tab[i] = make_uint2((a_off >> 4) | ((b_off >> 4) << 16),
                                     uint32_t(ui * p.bm) | (slot == 0 ? 0x80000000u : 0u));
         }
+        if (rl)
+            for (int i = lane; i < p.u_i * p.d_i; i += 32) s_cols[i] = p.cols[i];
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -705,7 +712,10 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                     } else {
                         tma_load_3d(dst, &imap, &full[st], 0, krow, int32_t(n0 / 64));
                     }
-                    tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, tbm * p.tm);
+                    if (rl)  // re-laid tiles: (bk, rows) view, tile (tbm, j) = w_rows rows
+                        tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
+                    else
+                        tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, tbm * p.tm);
                 }
                 __syncwarp();
             }
@@ -732,7 +742,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             const int b = int(it & 1);
             mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);  // epilogue done with it
             tc_fence_after();
-            const uint32_t d_base = tmem_d + uint32_t(b * p.tm);
+            const uint32_t d_base = tmem_d + uint32_t(b * acc_cols);
             for (int s = 0; s < p.d_o; ++s, ++g) {
                 const int st = int(g % p.ns);
                 mbar_wait(&full[st], uint32_t((g / p.ns) & 1));
@@ -740,7 +750,22 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                 if (elect_one()) {
                     const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
                     const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
-                    if (n_mma <= kRegMma) {
+                    if constexpr (MMA_N == 32) {
+                        if (rl) {  // same immediate-offset step as gather_kernel's fast path
+                            const uint32_t acc = s > 0 ? 1u : 0u;
+                            const uint64_t bd = b_st + (uint32_t(p.i_bytes) >> 4);
+#pragma unroll
+                            for (int kb = 0; kb < 8; ++kb) {
+                                constexpr uint32_t kAtom16 = uint32_t(kBatch * 128) >> 4;
+                                const uint32_t a16 = CONV ? uint32_t(kb / 4) * kAtom16 + uint32_t(kb % 4) * 2
+                                                          : uint32_t(kb * 16 * 8);
+                                tc_mma<false>(d_base + uint32_t(kb * MMA_N), a_st + a16,
+                                              bd + uint32_t(kb * ((MMA_N * 32) >> 4)), idesc, acc);
+                            }
+                        }
+                    }
+                    if (rl) {
+                    } else if (n_mma <= kRegMma) {
 #pragma unroll
                         for (int i = 0; i < kRegMma; ++i)
                             if (i < n_mma)
@@ -771,13 +796,28 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             if (p.debug & 4096) mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
             else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
             tc_fence_after();
-            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * p.tm);
+            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * acc_cols);
             const int64_t col = n0 + t;
             const bool ok = col < p.n_cols;
             for (int c = 0; c < p.tm; c += 32) {
                 uint32_t r[32];
-                TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (rl) {  // rows c..c+31 = 2 row blocks of 16, each the sum of its 2 partials
+                    uint32_t v[2][2][16];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int ink = 0; ink < 2; ++ink)
+                            TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[((c + 16 * h) / 16) * 2 + ink]), v[h][ink]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int q = 0; q < 16; ++q)
+                            r[16 * h + q] = __float_as_uint(__uint_as_float(v[h][0][q]) + __uint_as_float(v[h][1][q]));
+                } else {
+                    TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
                 if (!ok) continue;
                 if constexpr (CONV) {
                     // NHWC: this pixel's channels m0+c .. +31 are contiguous
@@ -885,7 +925,9 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     const int64_t tiles = col_blocks * c.u_o;
     // many waves: one persistent CTA per SM loops over the tiles (no split, no pairs)
     p.u_o = c.u_o;
-    p.persistent = ((tiles >= 2 * kNumSMs || getenv("RBGP4_TC_PERSIST")) && !relayout &&
+    // (relayout: only the TC16 shape, whose immediate-offset step the persistent kernel has)
+    const bool rl_fast = c.bk == 16 && c.v_i == 8 && c.d_i == 2 && c.u_i * c.d_i / c.v_i * c.bm == 32;
+    p.persistent = ((tiles >= 2 * kNumSMs || getenv("RBGP4_TC_PERSIST")) && (!relayout || rl_fast) &&
                     !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
     // M-split (opt-in, RBGP4_TC_MSPLIT=1): the two row halves of each tile on two CTAs (2 per
     // SM) that share every I slab by multicast and need no reduction.  Correct, but on conv10

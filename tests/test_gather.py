@@ -29,7 +29,7 @@ def chain_of(g_o, sp_o, g_i, sp_i, g_b, seed=0):
 
 
 def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False, msplit=False,
-        direct=False):
+        direct=False, rl_persistent=False):
     """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout for any
     shape (by itself only where its immediate-offset loop applies, e.g. the VGG TC16 shape);
     direct / persistent / msplit: K4 on the compressed values as stored (no relayout).
@@ -43,9 +43,9 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
         os.environ["RBGP4_TC_RELAYOUT"] = "1"
     if direct or persistent or msplit:
         os.environ["RBGP4_TC_NORELAYOUT"] = "1"
-    if relayout or direct or persistent or msplit:
+    if relayout or direct or persistent or msplit or rl_persistent:
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
-    if persistent:
+    if persistent or rl_persistent:  # rl_persistent: the persistent kernel on the TC16 relayout
         os.environ["RBGP4_TC_PERSIST"] = "1"
     if msplit:
         os.environ["RBGP4_TC_MSPLIT"] = "1"
@@ -101,6 +101,8 @@ def test_gather_sdmm_matches_oracle(case):
     # persistent tile loop (taken by itself only for many-wave grids; forced here)
     pers = run(w, x.cuda(), persistent=True)
     assert oracle.rel_l2(pers, ref) < 4e-3
+    pers_rl = run(w, x.cuda(), rl_persistent=True)
+    assert oracle.rel_l2(pers_rl, ref) < 4e-3
     # M-split (two row halves per tile, multicast slabs; taken by itself near half a wave)
     if w.chain.graphs[2].num_left % 2 == 0:
         ms = run(w, x.cuda(), msplit=True)
@@ -134,7 +136,7 @@ CONV_CASES = [(128, 128, 4, 9), (256, 128, 8, 3), (128, 256, 16, 1), (128, 128, 
 
 @pytest.mark.parametrize("c_out,c_in,hw,batch", CONV_CASES)
 @pytest.mark.parametrize("relu", [False, True])
-@pytest.mark.parametrize("mode", ["default", "direct", "persistent", "msplit"])
+@pytest.mark.parametrize("mode", ["default", "direct", "persistent", "persistent_rl", "msplit"])
 def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     from test_conv import im2col_nhwc
     cfg = wl.SweepConfig("conv16", (c_out // 128, 9 * c_in // 128), 0.0, (1, 1), (8, 8), 0.75,
@@ -146,7 +148,8 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     # default: the TC16 relayout (immediate-offset MMA loop); the other modes run on the
     # compressed values as stored
     env = {"persistent": ["RBGP4_TC_PERSIST", "RBGP4_TC_NORELAYOUT"],
-           "msplit": ["RBGP4_TC_MSPLIT", "RBGP4_TC_NORELAYOUT"], "direct": ["RBGP4_TC_NORELAYOUT"]}.get(mode, [])
+           "msplit": ["RBGP4_TC_MSPLIT", "RBGP4_TC_NORELAYOUT"], "direct": ["RBGP4_TC_NORELAYOUT"],
+           "persistent_rl": ["RBGP4_TC_PERSIST"]}.get(mode, [])
     for e in env:
         os.environ[e] = "1"
     try:
@@ -172,4 +175,6 @@ def test_gather_persistent_many_waves():
     assert oracle.rel_l2(got, ref) < 4e-3
     got32 = run(w, xb.cuda(), out_dtype=torch.float32)
     assert oracle.rel_l2(got32, ref) < 1e-5
+    direct = run(w, xb.cuda(), direct=True)  # the persistent loop on the values as stored
+    assert oracle.rel_l2(direct, ref) < 4e-3
 
