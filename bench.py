@@ -80,7 +80,8 @@ FACTORISATIONS = {
            "(tensor-core-friendly, SURVEY §7 hard part 1)"),
     "paper": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1): tile 128x64 (paper family, G_b=(1,1))",
     "tc16": ("G_o(4,K/128)@.5 G_r(1,1) G_i(8,8) G_b(16,16): tile 128x128, 16x16 dense element "
-             "blocks = whole MMA operands (gathered-block kernel, no densification)"),
+             "blocks = whole MMA operands (gathered-block kernel, no densification; values "
+             "permuted once so one N=32 MMA covers a G_i column block)"),
 }
 
 
