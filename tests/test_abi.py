@@ -97,3 +97,23 @@ def test_product_path_fails_loudly_without_gpu():
     chain, w, inp = wl.make_operands(wl.C1A)
     with pytest.raises(ks.DeviceError):
         ks.rbgp4mm(w, inp, ks.tiling_for_chain(chain))
+
+
+def test_prepared_section_carries_the_tc16_relayout(monkeypatch):
+    """rbgp4_prepare_size (host-only arithmetic): the TC16 shape (16x16 blocks, g_i (8,8) of degree
+    2) gets the column-block relayout of its values (same byte count as the values) in its prepared
+    section; g_i of degree 4 does not, and RBGP4_TC_NORELAYOUT removes it."""
+    lib = _native.lib()
+
+    def prep_bytes(sp_i):
+        cfg = wl.SweepConfig("p", (4, 36), 0.5, (1, 1), (8, 8), sp_i, (16, 16), n_cols=1, seed=0)
+        chain = wl.build_chain(cfg)
+        d = make_desc(chain_fields(chain), 4096, 4096, 4096)
+        return lib.rbgp4_prepare_size(ctypes.byref(d), 3), chain.num_left * chain.row_nnz * 2
+
+    size, values = prep_bytes(0.75)
+    assert size >= values
+    size4, values4 = prep_bytes(0.5)
+    assert size4 < values4
+    monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
+    assert prep_bytes(0.75)[0] < values

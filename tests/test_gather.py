@@ -178,3 +178,16 @@ def test_gather_persistent_many_waves():
     direct = run(w, xb.cuda(), direct=True)  # the persistent loop on the values as stored
     assert oracle.rel_l2(direct, ref) < 4e-3
 
+
+def test_gather_persistent_ragged_last_tile():
+    """Persistent loop on the TC16 relayout with a half-filled last column tile (N = 128k + 64)."""
+    chain = chain_of((4, 4), 0.5, (8, 8), 0.75, (16, 16), seed=22)
+    w = ks.init_random(chain, 7, precision="f32")
+    n = 128 * 160 + 64
+    x = torch.from_numpy(np.random.default_rng(9).uniform(-1, 1, (w.cols, n)).astype(np.float32))
+    xb = x.to(torch.bfloat16)
+    ref = f64_ref(w, xb.float().numpy())
+    got = run(w, xb.cuda())
+    assert oracle.rel_l2(got, ref) < 4e-3
+    assert oracle.rel_l2(got[:, -64:], ref[:, -64:]) < 4e-3
+
