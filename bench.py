@@ -570,7 +570,7 @@ def run_ours(args):
     achieved = bytes_launch / (dom_avg_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": f"{'gather_kernel (K4)' if args.factorisation == 'tc16' else 'tc_kernel (K2)'}"
+                "kernel": f"{'gather_persistent_kernel (K4, TC16 relayout)' if args.factorisation == 'tc16' else 'tc_kernel (K2)'}"
                           f"<bf16> conv10-12 ({args.factorisation} factorisation) "
                           f"(M,K,N)=({dom_layer['m']},{dom_layer['k']},"
                           f"{dom_layer['n']})", "algorithmic_bytes_per_launch": bytes_launch,

@@ -29,7 +29,7 @@ def chain_of(g_o, sp_o, g_i, sp_i, g_b, seed=0):
 
 
 def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persistent=False, msplit=False,
-        direct=False, rl_persistent=False):
+        direct=False, rl_persistent=False, rl_split=False):
     """dense: force K2 (densify); relayout: K4 on the prepared column-block relayout for any
     shape (by itself only where its immediate-offset loop applies, e.g. the VGG TC16 shape);
     direct / persistent / msplit: K4 on the compressed values as stored (no relayout).
@@ -43,7 +43,9 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
         os.environ["RBGP4_TC_RELAYOUT"] = "1"
     if direct or persistent or msplit:
         os.environ["RBGP4_TC_NORELAYOUT"] = "1"
-    if relayout or direct or persistent or msplit or rl_persistent:
+    if rl_split:  # the TC16 relayout in the one-tile-per-CTA kernel (split-K clusters)
+        os.environ["RBGP4_TC_NOPERSIST"] = "1"
+    if relayout or direct or persistent or msplit or rl_persistent or rl_split:
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
     if persistent or rl_persistent:  # rl_persistent: the persistent kernel on the TC16 relayout
         os.environ["RBGP4_TC_PERSIST"] = "1"
@@ -57,6 +59,7 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
         os.environ.pop("RBGP4_TC_RELAYOUT", None)
         os.environ.pop("RBGP4_TC_NORELAYOUT", None)
         os.environ.pop("RBGP4_TC_PERSIST", None)
+        os.environ.pop("RBGP4_TC_NOPERSIST", None)
         os.environ.pop("RBGP4_TC_MSPLIT", None)
     return y.float().cpu().numpy()
 
@@ -103,6 +106,8 @@ def test_gather_sdmm_matches_oracle(case):
     assert oracle.rel_l2(pers, ref) < 4e-3
     pers_rl = run(w, x.cuda(), rl_persistent=True)
     assert oracle.rel_l2(pers_rl, ref) < 4e-3
+    split_rl = run(w, x.cuda(), rl_split=True)
+    assert oracle.rel_l2(split_rl, ref) < 4e-3
     # M-split (two row halves per tile, multicast slabs; taken by itself near half a wave)
     if w.chain.graphs[2].num_left % 2 == 0:
         ms = run(w, x.cuda(), msplit=True)
@@ -136,7 +141,7 @@ CONV_CASES = [(128, 128, 4, 9), (256, 128, 8, 3), (128, 256, 16, 1), (128, 128, 
 
 @pytest.mark.parametrize("c_out,c_in,hw,batch", CONV_CASES)
 @pytest.mark.parametrize("relu", [False, True])
-@pytest.mark.parametrize("mode", ["default", "direct", "persistent", "persistent_rl", "msplit"])
+@pytest.mark.parametrize("mode", ["default", "direct", "persistent", "persistent_rl", "split_rl", "msplit"])
 def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     from test_conv import im2col_nhwc
     cfg = wl.SweepConfig("conv16", (c_out // 128, 9 * c_in // 128), 0.0, (1, 1), (8, 8), 0.75,
@@ -149,7 +154,7 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     # compressed values as stored
     env = {"persistent": ["RBGP4_TC_PERSIST", "RBGP4_TC_NORELAYOUT"],
            "msplit": ["RBGP4_TC_MSPLIT", "RBGP4_TC_NORELAYOUT"], "direct": ["RBGP4_TC_NORELAYOUT"],
-           "persistent_rl": ["RBGP4_TC_PERSIST"]}.get(mode, [])
+           "persistent_rl": ["RBGP4_TC_PERSIST"], "split_rl": ["RBGP4_TC_NOPERSIST"]}.get(mode, [])
     for e in env:
         os.environ[e] = "1"
     try:
