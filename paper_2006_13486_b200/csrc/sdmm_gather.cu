@@ -928,10 +928,10 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     // (relayout: only the TC16 shape, whose immediate-offset step the persistent kernel has; there
     // the persistent loop also wins below a wave -- conv10 N = 4096: 20.8 vs 24.6 us with split-K
     // clusters, N = 8192: 30.4 vs 42.8 us, N = 1024: 19.1 vs 19.3 us -- so the SDMM always takes
-    // it; the implicit-im2col conv measured slower that way (conv_fused 78.3 -> 74.6 TF/s) and
-    // keeps the split-K clusters below two waves)
+    // it from half a wave up (at 32 tiles the two are even); the implicit-im2col conv measured
+    // slower that way (conv_fused 78.3 -> 74.6 TF/s) and keeps the split-K clusters)
     const bool rl_fast = c.bk == 16 && c.v_i == 8 && c.d_i == 2 && c.u_i * c.d_i / c.v_i * c.bm == 32;
-    p.persistent = ((tiles >= 2 * kNumSMs || (relayout && rl_fast && !conv) || getenv("RBGP4_TC_PERSIST")) &&
+    p.persistent = ((tiles >= 2 * kNumSMs || (relayout && rl_fast && !conv && tiles >= kNumSMs / 2) || getenv("RBGP4_TC_PERSIST")) &&
                     (!relayout || rl_fast) && !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
     // M-split (opt-in, RBGP4_TC_MSPLIT=1): the two row halves of each tile on two CTAs (2 per
     // SM) that share every I slab by multicast and need no reduction.  Correct, but on conv10
