@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define RBGP4_ABI_VERSION 2
+#define RBGP4_ABI_VERSION 3
 
 /* status codes */
 #define RBGP4_OK 0
@@ -179,6 +179,21 @@ int rbgp4_csr_sdmm(int64_t rows, const int64_t *indptr, const int32_t *indices, 
 /* dst[i] = (dst_dtype) src[i] for n elements (F32<->BF16, F64->BF16, F64<->F32). */
 int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t n,
                void *stream);
+
+/*
+ * Plan overrides (A/B switches for tests and tuning; the defaults are the production plan).
+ * Thread-local: a value set on one host thread affects only launches planned on that thread.
+ * Names: relayout, dense, persistent, msplit, ksplit, stages, multicast, sym, pdl, simt_ct,
+ * tc_tn, tc_na, tc_nb, tc_nw, wswz, ostore, sched, i3d, promo, conv_wide, debug (include the
+ * kernels' trace/ablation hooks only in a debug build, see rbgp4_debug_build).  Unknown names
+ * and out-of-range values return RBGP4_EINVAL.  None of them changes results beyond the fp32
+ * summation order of the tensor-core modes.  ABI v3.
+ */
+int rbgp4_set_option(const char *name, int64_t value);
+int rbgp4_get_option(const char *name, int64_t *value);
+void rbgp4_reset_options(void);
+/* 1 if this library was built with -DRBGP4_DEBUG=1 (trace / ablation hooks), else 0. */
+int rbgp4_debug_build(void);
 
 /* Thread-local description of the last failure on this thread. */
 const char *rbgp4_last_error(void);

@@ -7,6 +7,7 @@ come from PyTorch (plumbing only); the arithmetic is in the library.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -21,7 +22,8 @@ EXPORTED = (
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
     "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
-    "rbgp4_reset_launch_count", "rbgp4_sddmm",
+    "rbgp4_reset_launch_count", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
+    "rbgp4_reset_options", "rbgp4_debug_build",
 )
 
 
@@ -46,6 +48,15 @@ class Desc(ctypes.Structure):
 
 
 _lib = None
+
+
+def use_library(path: str) -> None:
+    """Load `path` instead of the release library (tools/: the -DRBGP4_DEBUG=1 build).
+    Must run before the first call that loads the library."""
+    global LIB_PATH
+    if _lib is not None and os.path.abspath(path) != os.path.abspath(LIB_PATH):
+        raise DeviceError(f"library already loaded from {LIB_PATH}")
+    LIB_PATH = path
 
 
 def lib():
@@ -95,6 +106,12 @@ def lib():
     h.rbgp4_abi_version.restype = i32
     h.rbgp4_launch_count.restype = i64
     h.rbgp4_reset_launch_count.restype = None
+    h.rbgp4_set_option.argtypes = [ctypes.c_char_p, i64]
+    h.rbgp4_set_option.restype = i32
+    h.rbgp4_get_option.argtypes = [ctypes.c_char_p, ctypes.POINTER(i64)]
+    h.rbgp4_get_option.restype = i32
+    h.rbgp4_reset_options.restype = None
+    h.rbgp4_debug_build.restype = i32
     _lib = h
     return h
 
@@ -106,6 +123,30 @@ def last_error() -> str:
 def check(rc: int, what: str) -> None:
     if rc != 0:
         raise DeviceError(f"{what} failed (code {rc}): {last_error()}")
+
+
+def set_option(name: str, value: int) -> None:
+    """Thread-local plan override (rbgp4_set_option); raises on unknown names / values."""
+    check(lib().rbgp4_set_option(name.encode(), int(value)), f"rbgp4_set_option({name}={value})")
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    check(lib().rbgp4_get_option(name.encode(), ctypes.byref(v)), f"rbgp4_get_option({name})")
+    return int(v.value)
+
+
+@contextlib.contextmanager
+def options(**kw):
+    """Set plan overrides for the calling thread inside a `with` block, then restore them."""
+    old = {k: get_option(k) for k in kw}
+    try:
+        for k, v in kw.items():
+            set_option(k, v)
+        yield
+    finally:
+        for k, v in old.items():
+            set_option(k, v)
 
 
 def launch_count() -> int:

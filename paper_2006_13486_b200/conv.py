@@ -68,6 +68,8 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
     x = x.contiguous()
     dev = resolve_device(x.device)
     res_dt = out_dtype if out_dtype is not None else t.bfloat16
+    if res_dt not in (t.bfloat16, t.float32):
+        raise InvalidArgumentError(f"conv writes bf16 or f32, got {res_dt}")
     oh, ow = conv_out_hw(height, width, kh, stride)
     with t.cuda.device(dev):
         fmt = device_format(w, dev, t.bfloat16)
@@ -78,14 +80,17 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
             res = t.empty((batch, oh, ow, w.rows), dtype=res_dt, device=dev)
         else:
             res = out
-            if tuple(res.shape) != (batch, oh, ow, w.rows) or not res.is_contiguous():
-                raise ShapeError("out must be a contiguous NHWC (batch, H', W', c_out) tensor")
+            if (not isinstance(res, t.Tensor) or res.device != dev
+                    or res.dtype not in (t.bfloat16, t.float32)
+                    or tuple(res.shape) != (batch, oh, ow, w.rows) or not res.is_contiguous()):
+                raise ShapeError(f"out must be a contiguous NHWC ({batch}, {oh}, {ow}, {w.rows}) bf16 or "
+                                 f"f32 tensor on {dev}")
         if n_cols == 0:
             return res
         lib = _native.lib()
         prep = prepared(fmt, "bf16", dev, desc)
         need = lib.rbgp4_conv2d_workspace_size(ctypes.byref(desc), ctypes.byref(cv))
-        ws = workspace(dev, need) if need else None
+        ws = workspace(dev, need, stream_handle(dev)) if need else None
         code = {t.bfloat16: _native.BF16, t.float32: _native.F32}[res.dtype]
         _native.check(lib.rbgp4_conv2d(
             ctypes.byref(desc), ctypes.byref(cv), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),

@@ -37,6 +37,42 @@ void note_launch(int n = 1);
 
 constexpr int kNumSMs = 148;
 
+// Ablation / tracing hooks inside the kernels exist only in debug builds of the library
+// (-DRBGP4_DEBUG=1, `python -m paper_2006_13486_b200.build --debug`); in the release library
+// DBG(x) is the constant 0 and every such branch is compiled out.
+#ifndef RBGP4_DEBUG
+#define RBGP4_DEBUG 0
+#endif
+#define DBG(x) (RBGP4_DEBUG ? (x) : 0)
+
+// Plan overrides (rbgp4_set_option / rbgp4_get_option, include/rbgp4.h).  Thread-local: a
+// setting affects only launches planned on the thread that made it, so concurrent callers
+// never see each other's A/B switches.  The defaults are the production plan.
+struct Options {
+    int32_t relayout = -1;    // K4 values relayout: -1 auto, 0 off, 1 wherever admissible
+    int32_t dense = 0;        // 1: bf16 always on the densify kernel (K2), never K4
+    int32_t persistent = -1;  // persistent tile loop: -1 auto (K4) / off (K2), 0 off, 1 on
+    int32_t msplit = 0;       // K4 row-half split over a 2-CTA cluster (opt-in)
+    int32_t ksplit = 0;       // split-K slices: 0 auto, else forced (1..8)
+    int32_t stages = 0;       // K4 ring stages: 0 auto, else forced (2..16)
+    int32_t multicast = -1;   // K4 multicast pairs: -1 auto, 0 off
+    int32_t sym = 1;          // K4 symmetric split-K epilogue
+    int32_t pdl = 1;          // programmatic dependent launch attribute
+    int32_t simt_ct = 0;      // K1 column threads per CTA: 0 auto, else 8 / 16 / 32
+    int32_t tc_tn = 0;        // K2 tile columns: 0 auto
+    int32_t tc_na = 0;        // K2 A-ring depth: 0 auto
+    int32_t tc_nb = 0;        // K2 I-ring depth: 0 auto
+    int32_t tc_nw = 0;        // K2 W-ring depth: 0 auto
+    int32_t wswz = 1;         // K2 swizzled W staging
+    int32_t ostore = 1;       // K2 TMA-store epilogue
+    int32_t sched = 1;        // rbgp4_prepare: paired step schedule (0: adjacency order)
+    int32_t i3d = 1;          // K2 3-D I boxes
+    int32_t promo = -1;       // K2 I-map L2 promotion bytes: -1 auto (256), 0 / 64 / 128 / 256
+    int32_t conv_wide = 1;    // K2 conv: 256-pixel tiles for many-wave grids
+    int32_t debug = 0;        // trace / ablation bits (debug builds only)
+};
+Options &opts();
+
 // Derived sizes of a four-factor chain (SURVEY §8 notation).
 struct ChainDims {
     int64_t rows, cols, n_cols, ld_in, ld_out;

@@ -7,6 +7,7 @@
 // unsupported (shape, compute) pair is an error, never a silent CPU path.
 #include "common.cuh"
 
+#include <cstring>
 #include <string>
 
 namespace rbgp4 {
@@ -14,7 +15,35 @@ namespace rbgp4 {
 namespace {
 thread_local char g_last_error[512] = "";
 thread_local int64_t g_launches = 0;
+thread_local Options g_opts;
+
+struct OptionSlot {
+    const char *name;
+    int32_t Options::*field;
+    int32_t lo, hi;
+};
+constexpr OptionSlot kOptionSlots[] = {
+    {"relayout", &Options::relayout, -1, 1},     {"dense", &Options::dense, 0, 1},
+    {"persistent", &Options::persistent, -1, 1}, {"msplit", &Options::msplit, 0, 1},
+    {"ksplit", &Options::ksplit, 0, 8},          {"stages", &Options::stages, 0, 16},
+    {"multicast", &Options::multicast, -1, 0},   {"sym", &Options::sym, 0, 1},
+    {"pdl", &Options::pdl, 0, 1},                {"simt_ct", &Options::simt_ct, 0, 32},
+    {"tc_tn", &Options::tc_tn, 0, 256},          {"tc_na", &Options::tc_na, 0, 8},
+    {"tc_nb", &Options::tc_nb, 0, 16},           {"tc_nw", &Options::tc_nw, 0, 16},
+    {"wswz", &Options::wswz, 0, 1},              {"ostore", &Options::ostore, 0, 1},
+    {"sched", &Options::sched, 0, 1},            {"i3d", &Options::i3d, 0, 1},
+    {"promo", &Options::promo, -1, 256},         {"conv_wide", &Options::conv_wide, 0, 1},
+    {"debug", &Options::debug, 0, 1 << 30},
+};
+const OptionSlot *find_option(const char *name) {
+    if (name == nullptr) return nullptr;
+    for (const auto &s : kOptionSlots)
+        if (strcmp(s.name, name) == 0) return &s;
+    return nullptr;
+}
 }  // namespace
+
+Options &opts() { return g_opts; }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -92,6 +121,29 @@ extern "C" {
 const char *rbgp4_last_error(void) { return g_last_error; }
 
 int rbgp4_abi_version(void) { return RBGP4_ABI_VERSION; }
+
+int rbgp4_debug_build(void) { return RBGP4_DEBUG; }
+
+int rbgp4_set_option(const char *name, int64_t value) {
+    const OptionSlot *s = find_option(name);
+    RBGP4_REQUIRE(s != nullptr, "unknown option '%s'", name ? name : "(null)");
+    RBGP4_REQUIRE(value >= s->lo && value <= s->hi, "option '%s' = %lld outside [%d, %d]", s->name,
+                  (long long)value, s->lo, s->hi);
+    RBGP4_REQUIRE(s->field != &Options::debug || value == 0 || RBGP4_DEBUG,
+                  "option 'debug' needs a debug build of the library (-DRBGP4_DEBUG=1)");
+    g_opts.*(s->field) = int32_t(value);
+    return RBGP4_OK;
+}
+
+int rbgp4_get_option(const char *name, int64_t *value) {
+    const OptionSlot *s = find_option(name);
+    RBGP4_REQUIRE(s != nullptr, "unknown option '%s'", name ? name : "(null)");
+    RBGP4_REQUIRE(value != nullptr, "null output pointer");
+    *value = g_opts.*(s->field);
+    return RBGP4_OK;
+}
+
+void rbgp4_reset_options(void) { g_opts = Options(); }
 
 int64_t rbgp4_launch_count(void) { return g_launches; }
 

@@ -40,21 +40,30 @@ namespace {
 
 constexpr int kGThreads = 192;
 
-// Debug trace (RBGP4_TC_DEBUG bit 8): CTA (0,0,0) stamps clock64 per step:
-// [0] producer issued, [1] MMA saw full, [2] MMA issue done; [3][0..3] setup / epilogue marks
+// Debug builds only (option debug, RBGP4_DEBUG=1): bit 8 -- CTA (0,0,0) stamps clock64 per
+// step: [0] producer issued, [1] MMA saw full, [2] MMA issue done; [3][0..3] setup / epilogue
+// marks; bit 512 -- every CTA stamps %globaltimer (ns) at entry and exit.
 constexpr int kGTraceSteps = 256;
-__device__ unsigned long long g_gtrace[4][kGTraceSteps];
-// RBGP4_TC_DEBUG bit 512: every CTA stamps %globaltimer (ns) at entry and exit
 constexpr int kCtaStamps = 4096;
+#if RBGP4_DEBUG
+__device__ unsigned long long g_gtrace[4][kGTraceSteps];
 __device__ unsigned long long g_cta_stamp[2][kCtaStamps];
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
 __device__ __forceinline__ void gtrace(int debug, int ev, int step) {
+#if RBGP4_DEBUG
     if ((debug & 8) && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && step < kGTraceSteps)
         g_gtrace[ev][step] = clock64();
+#endif
+}
+__device__ __forceinline__ void cta_stamp(int debug, int which, int cta_id) {
+#if RBGP4_DEBUG
+    if ((debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[which][cta_id] = gtimer();
+#endif
 }
 constexpr int kBatch = 128;  // MMA M: batch columns (or pixels) per CTA
 constexpr int kMaxMma = 256; // MMAs per step (u_i * d_i * bk / 16)
@@ -116,9 +125,9 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_full + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (threadIdx.x == 0) gtrace(p.debug, 3, 0);
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 0);
     const int cta_id = int(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
-    if ((p.debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[0][cta_id] = gtimer();
+    cta_stamp(DBG(p.debug), 0, cta_id);
     const int64_t n0 = int64_t(blockIdx.x) * kBatch;
     const int tbm = blockIdx.y;
     const int64_t m0 = int64_t(tbm) * p.tm;
@@ -194,7 +203,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    if (threadIdx.x == 0) gtrace(p.debug, 3, 1);
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 1);
     // programmatic dependent launch: the next kernel in the stream may be scheduled now (its
     // setup overlaps this kernel); it waits in griddepcontrol.wait before reading anything
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -204,7 +213,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // The weights are never the previous kernel's output: the W tiles of the first ring's
         // worth of steps are requested before waiting on it.  The I slabs may be its output, so
         // they wait (griddepcontrol.wait is a no-op without a programmatic dependency).
-        const int pre = (p.debug & 128) ? 0 : min(p.ns, nsteps);
+        const int pre = (DBG(p.debug) & 128) ? 0 : min(p.ns, nsteps);
         if (elect_one()) {
             for (int s = 0; s < pre; ++s) {
                 const int j = staged_sched ? s_j[s] : srow ? srow[s] : s_begin + s;
@@ -220,15 +229,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
-            if (p.debug & 256) mbar_wait_sleep(&empty[st], ((s / p.ns) & 1) ^ 1, 64);
+            if (DBG(p.debug) & 256) mbar_wait_sleep(&empty[st], ((s / p.ns) & 1) ^ 1, 64);
             else mbar_wait(&empty[st], ((s / p.ns) & 1) ^ 1);
             // g_o adjacency slot of this step and its first slab row
             const int j = staged_sched ? s_j[s] : srow ? srow[s] : s_begin + s;
             const int32_t krow = staged_sched ? s_krow[s] : orow[j] * p.tk;
             const bool leader = elect_one();
-            if (leader && (p.debug & 128)) {
+            if (leader && (DBG(p.debug) & 128)) {
                 mbar_arrive(&full[st]);  // ablation: no loads (MMA / pipeline skeleton only)
-                gtrace(p.debug, 0, s);
+                gtrace(DBG(p.debug), 0, s);
             } else if (leader) {
                 if (s >= pre) mbar_expect_tx(&full[st], uint32_t(stage_bytes));
                 unsigned char *dst = ring + size_t(st) * stage_bytes;
@@ -281,7 +290,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
                 else  // this CTA's rows of the compressed tile
                     tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, int32_t(m0) + ui0 * p.bm);
-                gtrace(p.debug, 0, s);
+                gtrace(DBG(p.debug), 0, s);
             }
             __syncwarp();
         }
@@ -310,15 +319,15 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             ry[i] = e.y;
         }
         const bool in_regs = n_mma <= kRegMma;
-        const bool no_mma = p.debug & 2;
+        const bool no_mma = DBG(p.debug) & 2;
         const bool fast8 = MMA_N == 32 && p.cols && p.bk == 16 && v_blocks == 8 && p.w_swz == 32 &&
-                           !(p.debug & 16384);
+                           !(DBG(p.debug) & 16384);
         for (int s = 0; s < nsteps; ++s) {
             const int st = s % p.ns;
             mbar_wait(&full[st], (s / p.ns) & 1);
             tc_fence_after();
             if (elect_one()) {
-                gtrace(p.debug, 1, s);
+                gtrace(DBG(p.debug), 1, s);
                 const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
                 const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
                 if (no_mma) {
@@ -384,13 +393,13 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 } else {
                     tc_commit(&empty[st]);
                 }
-                gtrace(p.debug, 2, s);
+                gtrace(DBG(p.debug), 2, s);
             }
             __syncwarp();
         }
         if (elect_one()) tc_commit(tmem_full);
         __syncwarp();
-        if (!(p.debug & (4096 | 8192))) {
+        if (!(DBG(p.debug) & (4096 | 8192))) {
             // hand the accumulator to the epilogue warps through a named barrier: they sleep
             // in bar.sync for the whole main loop instead of polling tmem_full (polling warps
             // measured to slow this warp's MMA issue)
@@ -400,11 +409,11 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
     } else {
         // ================= epilogue (warps 0-3): TMEM lane = batch column =================
-        if (p.debug & 4096) mbar_wait_sleep(tmem_full, 0, 256);  // A/B: polling with back-off
-        else if (p.debug & 8192) mbar_wait_parked(tmem_full, 0);
+        if (DBG(p.debug) & 4096) mbar_wait_sleep(tmem_full, 0, 256);  // A/B: polling with back-off
+        else if (DBG(p.debug) & 8192) mbar_wait_parked(tmem_full, 0);
         else asm volatile("bar.sync 2, 160;" ::: "memory");
         tc_fence_after();
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 2);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 2);
     }
 
     const uint32_t tmem_d = *tmem_slot;
@@ -469,7 +478,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // different step counts) before any partial lands in a peer
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 4);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 4);
         if (warp < 4) {
             // push the partial rows other slices own: posted DSMEM stores into their receive buffer
             for (int c = 0; c < p.tm; c += 32) {
@@ -487,10 +496,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 for (int q = 0; q < 32; ++q) dstp[q * kBatch] = __uint_as_float(r[q]);
             }
         }
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 5);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 5);
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 6);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 6);
     } else if (p.ksplit > 1) {
         // legacy: slices > 0 park the whole fp32 partial tile in their own shared memory
         if (kslice > 0 && warp < 4) {
@@ -504,13 +513,13 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    if (outputs && warp < 4 && !(p.debug & 4)) {
+    if (outputs && warp < 4 && !(DBG(p.debug) & 4)) {
         constexpr int kOutElt = OUT_BF16 ? 2 : 4;
         for (int c = r_lo; c < r_lo + rp; c += 32) {
             uint32_t r[32];
             load_rows(c - t_lo, r);
-            if (p.debug & 1024) {
-                if (threadIdx.x == 0) gtrace(p.debug, 3, 9);
+            if (DBG(p.debug) & 1024) {
+                if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 9);
             } else if (p.sym) {
                 // plain shared loads (the static __shared__ base keeps them LDS) so ptxas can keep
                 // all of them in flight; volatile asm loads measured latency-serialised
@@ -536,8 +545,8 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
             const int cr = c - r_lo;  // row inside this CTA's output range
-            if (threadIdx.x == 0) gtrace(p.debug, 3, 10);
-            if (p.debug & 2048) continue;
+            if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 10);
+            if (DBG(p.debug) & 2048) continue;
             if constexpr (CONV) {
                 // NHWC: pixel t holds channels c..c+31 -> 4 x 16-byte chunks of its 128-byte
                 // rows in 64-channel atoms [atom][pixel][128 B], 128B-swizzled (chunk ^ pixel%8)
@@ -584,10 +593,10 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
         }
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 7);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 7);
         fence_async_smem();
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 0) gtrace(p.debug, 3, 8);
+        if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 8);
         if (warp == 0 && elect_one()) {
             if constexpr (CONV) {
                 constexpr int kAtomCh = 128 / kOutElt;
@@ -605,7 +614,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
         __syncwarp();
     }
-    if (threadIdx.x == 0) gtrace(p.debug, 3, 3);
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 3);
     if ((p.ksplit > 1 && !p.sym) || p.mc || p.msplit) {
         // peers keep their shared memory alive until the leader has read it (legacy split);
         // multicast peers may still arrive on this CTA's barriers
@@ -619,7 +628,7 @@ gather_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
                      "r"(uint32_t(p.tmem_cols)));
     }
-    if ((p.debug & 512) && threadIdx.x == 0 && cta_id < kCtaStamps) g_cta_stamp[1][cta_id] = gtimer();
+    cta_stamp(DBG(p.debug), 1, cta_id);
 }
 
 // ---------------------------------------------------------------- persistent variant
@@ -793,7 +802,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             const int tbm = int(tile % u_o);
             const int64_t n0 = (tile / u_o) * kBatch;
             const int64_t m0 = int64_t(tbm) * p.tm;
-            if (p.debug & 4096) mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
+            if (DBG(p.debug) & 4096) mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
             else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
             tc_fence_after();
             const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * acc_cols);
@@ -801,13 +810,16 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             const bool ok = col < p.n_cols;
             for (int c = 0; c < p.tm; c += 32) {
                 uint32_t r[32];
-                if (rl) {  // rows c..c+31 = 2 row blocks of 16, each the sum of its 2 partials
+                if (rl) {  // rows c..c+31: two 16-row halves, each the sum of its row block's 2 partials
                     uint32_t v[2][2][16];
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
+                    for (int h = 0; h < 2; ++h) {
+                        // row -> (row block ui, row m inside it); bm is 16 or 32 on this path
+                        const int row = c + 16 * h, ui = row / p.bm, m = row - ui * p.bm;
 #pragma unroll
                         for (int ink = 0; ink < 2; ++ink)
-                            TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[((c + 16 * h) / 16) * 2 + ink]), v[h][ink]);
+                            TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[ui * 2 + ink] + m), v[h][ink]);
+                    }
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
@@ -894,8 +906,8 @@ int gather_relayout_ok(const ChainDims &c) {
     const int span = c.bk * 2;
     if (span != 32 && span != 64 && span != 128) return 0;
     if (c.tm * c.d_i > 256 || d_r * c.bm > 256) return 0;
-    if (getenv("RBGP4_TC_NORELAYOUT")) return 0;
-    if (getenv("RBGP4_TC_RELAYOUT")) return 1;
+    if (opts().relayout == 0) return 0;
+    if (opts().relayout == 1) return 1;
     // default where the immediate-offset MMA loop applies (TC16: 8 column blocks of 16 rows,
     // N = 32, d_i = 2): half the MMAs of the direct mode and no per-MMA descriptor arithmetic.
     // Elsewhere the generic relayout loop loses to the direct mode (measured), so it is opt-in.
@@ -904,7 +916,7 @@ int gather_relayout_ok(const ChainDims &c) {
 
 int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan *out, bool pairs = false) {
     if (compute != RBGP4_COMPUTE_BF16) return 0;
-    if (getenv("RBGP4_TC_DENSE")) return 0;  // A/B switch: force the densify kernel (K2)
+    if (opts().dense) return 0;  // A/B switch: force the densify kernel (K2)
     if (c.rm != 1 || c.rk != 1 || c.bm % 16 || c.bk % 16 || c.tm % 32 || c.tm > 256 || c.tk > 256) return 0;
     if (relayout && !gather_relayout_ok(c)) return 0;
     const int w_row = relayout ? c.bk * 2 : c.d_t * 2;
@@ -931,15 +943,15 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     // it from half a wave up (at 32 tiles the two are even); the implicit-im2col conv measured
     // slower that way (conv_fused 78.3 -> 74.6 TF/s) and keeps the split-K clusters)
     const bool rl_fast = c.bk == 16 && c.v_i == 8 && c.d_i == 2 && c.u_i * c.d_i / c.v_i * c.bm == 32;
-    p.persistent = ((tiles >= 2 * kNumSMs || (relayout && rl_fast && !conv && tiles >= kNumSMs / 2) || getenv("RBGP4_TC_PERSIST")) &&
-                    (!relayout || rl_fast) && !getenv("RBGP4_TC_NOPERSIST")) ? 1 : 0;
-    // M-split (opt-in, RBGP4_TC_MSPLIT=1): the two row halves of each tile on two CTAs (2 per
+    p.persistent = ((tiles >= 2 * kNumSMs || (relayout && rl_fast && !conv && tiles >= kNumSMs / 2) ||
+                     opts().persistent == 1) &&
+                    (!relayout || rl_fast) && opts().persistent != 0) ? 1 : 0;
+    // M-split (opt-in, option msplit=1): the two row halves of each tile on two CTAs (2 per
     // SM) that share every I slab by multicast and need no reduction.  Correct, but on conv10
     // it measured 30.1 us against 26.0 us for the split-K default (half the MMAs per CTA do
     // not make up for running all steps), so it is not chosen by itself.
-    const char *ms_env = getenv("RBGP4_TC_MSPLIT");
     p.msplit = (!p.persistent && !relayout && c.u_i % 2 == 0 && (c.tm / 2) % 32 == 0 &&
-                (!conv || (c.tk / 64) % 2 == 0) && ms_env && atoi(ms_env) != 0) ? 1 : 0;
+                (!conv || (c.tk / 64) % 2 == 0) && opts().msplit) ? 1 : 0;
     p.w_rows = p.msplit ? c.tm / 2 : p.w_rows;
     p.w_bytes = p.w_rows * w_row;  // = tm * d_t * 2 (half of it in M-split)
     p.w_swz = w_row;
@@ -960,11 +972,11 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
         while (ks < 4 && tiles * ks * 2 <= 2 * kNumSMs && c.d_o >= ks * 2 * 2) ks *= 2;
         dual = tiles * ks > kNumSMs;
     }
-    if (const char *e = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(e)));
+    if (opts().ksplit > 0) ks = std::min(8, int(opts().ksplit));
     if (p.persistent || p.msplit) ks = 1;
     if (p.persistent) dual = false;
     int ns = dual ? 2 : int(std::min<size_t>(16, (kGSmemCap - fixed - statics) / stage));
-    if (const char *e = getenv("RBGP4_TC_NS")) ns = std::max(2, std::min(16, atoi(e)));
+    if (opts().stages > 0) ns = std::max(2, std::min(16, int(opts().stages)));
     if (fixed + statics + size_t(ns) * stage > kGSmemCap) return 0;
     p.ns = ns;
     p.tmem_cols = 32;
@@ -973,12 +985,12 @@ int gather_plan(const ChainDims &c, int compute, bool conv, bool relayout, GPlan
     if (p.tmem_cols > 512) p.persistent = 0, p.tmem_cols = 256;
     p.sps = (c.d_o + ks - 1) / ks;
     p.ksplit = (c.d_o + p.sps - 1) / p.sps;
-    if (const char *e = getenv("RBGP4_TC_DEBUG")) p.debug = atoi(e);
+    p.debug = DBG(opts().debug);
     // multicast pairs: the u_o tile-rows of a column block as one cluster (<= 8 portable)
     // (SDMM slabs are two 64-column atoms; conv slabs must have an even number of channel atoms)
     // (relayout: measured slower with pairs -- 26.6 vs 25.2 us on conv10 -- so never paired)
     p.mc = (pairs && p.ksplit == 1 && !p.persistent && !p.msplit && !relayout && c.u_o >= 2 && c.u_o <= 8 &&
-            (!conv || (c.tk / 64) % 2 == 0) && !getenv("RBGP4_TC_NOMC")) ? 1 : 0;
+            (!conv || (c.tk / 64) % 2 == 0) && opts().multicast != 0) ? 1 : 0;
     out->p = p;
     out->smem = fixed + size_t(ns) * stage;
     out->grid = p.persistent ? dim3(unsigned(std::min<int64_t>(tiles, kNumSMs)), 1, 1)
@@ -994,7 +1006,7 @@ void set_symmetric(GPlan *pl, int oelt, bool conv) {
     GParams &p = pl->p;
     p.sym = 0;
     p.stage_off = 0;
-    if (p.ksplit <= 1 || p.tm % p.ksplit || getenv("RBGP4_TC_NOSYM")) return;
+    if (p.ksplit <= 1 || p.tm % p.ksplit || !opts().sym) return;
     const int rp = p.tm / p.ksplit;
     if (rp % 32 || (conv && rp % (128 / oelt))) return;
     const size_t recv = size_t(p.ksplit - 1) * rp * kBatch * 4;
@@ -1112,7 +1124,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
         at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
-        cfg.numAttrs = getenv("RBGP4_NO_PDL") ? 0 : 1;
+        cfg.numAttrs = opts().pdl ? 1 : 0;
         e = cudaLaunchKernelEx(&cfg, pk, imap, wmap, pl.p, adj_o, adj_i, out, pl.n_tiles);
         if (e != cudaSuccess) {
             set_error("gather_persistent_kernel launch (%u CTAs, smem %zu): %s", pl.grid.x, pl.smem,
@@ -1152,7 +1164,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
     int na = (pl.p.ksplit > 1 || pl.p.mc || pl.p.msplit) ? 1 : 0;
     cudaLaunchAttribute attrs[2];
     if (na) attrs[0] = attr[0];
-    if (!getenv("RBGP4_NO_PDL")) {
+    if (opts().pdl) {
         attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -1341,7 +1353,8 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
 
 }  // namespace rbgp4
 
-// debug-only (not part of include/rbgp4.h): copy the K4 CTA-0 trace to the host
+#if RBGP4_DEBUG
+// debug builds only (not part of include/rbgp4.h): copy the K4 CTA-0 trace to the host
 extern "C" int rbgp4_debug_trace_gather(unsigned long long *host, int n) {
     if (n > 4 * rbgp4::kGTraceSteps) n = 4 * rbgp4::kGTraceSteps;
     return cudaMemcpyFromSymbol(host, rbgp4::g_gtrace, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
@@ -1352,3 +1365,4 @@ extern "C" int rbgp4_debug_cta_stamps(unsigned long long *host, int n) {
     if (n > 2 * rbgp4::kCtaStamps) n = 2 * rbgp4::kCtaStamps;
     return cudaMemcpyFromSymbol(host, rbgp4::g_cta_stamp, sizeof(unsigned long long) * n) == cudaSuccess ? 0 : -3;
 }
+#endif  // RBGP4_DEBUG

@@ -249,12 +249,12 @@ int plan_simt(const ChainDims &c, SimtPlan *plan) {
     // Column-block width 4*cthreads: the widest whose grid still covers every SM (one tile per
     // CTA is a serial walk over the d_o steps, so idle SMs cost more than narrower tiles):
     // measured on the VGG shapes, conv13 (N = 1024) 153 -> 64 us at 32 columns per CTA.
-    const char *ct_env = getenv("RBGP4_SIMT_CT");
+    const int ct_opt = opts().simt_ct;
     SimtPlan fallback{};
     bool have = false;
     const int64_t row_blocks = c.rows / c.tm;
     for (int cthreads : {32, 16, 8}) {
-        if (ct_env && atoi(ct_env) != cthreads) continue;
+        if (ct_opt && ct_opt != cthreads) continue;
         int rthreads = kThreads / cthreads;
         int chunks = c.tm / rt;
         int nch = 1;
@@ -265,7 +265,7 @@ int plan_simt(const ChainDims &c, SimtPlan *plan) {
         const int64_t grid = (c.n_cols + 4 * cthreads - 1) / (4 * cthreads) * row_blocks;
         fallback = {rt, nch, cthreads, sm};
         have = true;
-        if (ct_env || grid >= kNumSMs) {
+        if (ct_opt || grid >= kNumSMs) {
             *plan = fallback;
             return 1;
         }

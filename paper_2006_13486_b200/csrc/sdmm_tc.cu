@@ -50,11 +50,16 @@ constexpr int kThreads = 224;
 // Layout: [event][step], event = 0 B issued, 1 W issued, 2 densify start, 3 densify end,
 // 4 MMA start, 5 MMA end; [6][0] setup done, [6][1] epilogue start, [6][2] epilogue end;
 // 7 MMA saw full_b, 8 densify saw full_w (per W stage).
+// (debug builds only: option debug, RBGP4_DEBUG=1)
 constexpr int kTraceSteps = 512;
+#if RBGP4_DEBUG
 __device__ unsigned long long g_trace[10][kTraceSteps];
+#endif
 __device__ __forceinline__ void trace(const int debug, int ev, int step) {
+#if RBGP4_DEBUG
     if ((debug & 8) && blockIdx.x == 0 && blockIdx.y == 0 && step < kTraceSteps)
         g_trace[ev][step] = clock64();
+#endif
 }
 constexpr int kBlockM = 128;
 
@@ -163,7 +168,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tmem_empty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (threadIdx.x == 0) trace(p.debug, 6, 3);
+    if (threadIdx.x == 0) trace(DBG(p.debug), 6, 3);
     // first tile of this CTA (the only one unless persistent)
     const int64_t m0_first = int64_t(p.persistent ? blockIdx.x % p.blocks_m : blockIdx.y) * p.rows_valid;
     const int row_in_tile0 = int(m0_first % p.tm);  // same for every tile (persistent: tm <= 128)
@@ -192,7 +197,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
     asm volatile("griddepcontrol.wait;" ::: "memory");
     // g_o adjacency row of this tile-row and the order its slots are walked in: the
     // schedule lets tile-rows that share a K-block read its I slab at the same step
-    if (threadIdx.x == 0) trace(p.debug, 6, 0);
+    if (threadIdx.x == 0) trace(DBG(p.debug), 6, 0);
 
     if (warp == 5) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -202,7 +207,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         tc_fence_before();
         __syncwarp();
         tc_fence_after();
-        if (lane == 0) trace(p.debug, 6, 5);
+        if (lane == 0) trace(DBG(p.debug), 6, 5);
     }
     if (warp < 4) {
         // ---- densify-warp setup: zero the A ring and load the scatter-offset table.
@@ -231,15 +236,15 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             row_offsets<kElt>(p, adj, row_in_tile0, t, aoff + t, kBlockM);
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");  // table + zeros complete (warps 0-3)
-        if (t == 0) trace(p.debug, 6, 4);
-        if (p.debug & 32) asm volatile("bar.sync 2, 160;" ::: "memory");
+        if (t == 0) trace(DBG(p.debug), 6, 4);
+        if (DBG(p.debug) & 32) asm volatile("bar.sync 2, 160;" ::: "memory");
     }
 
     // Role loops run warp-uniformly (all 32 lanes wait on the barriers); one lane,
     // picked by elect.sync, issues the TMA / tcgen05 instructions.  Issuing from
     // lane-0-only divergent code made the compiler wrap every UTCHMMA/UTMALDG in an
     // elect loop with R2UR conversions (~500 cycles per step, tools/tc_trace.py).
-    if ((p.debug & 32) && warp == 4) asm volatile("bar.sync 2, 160;" ::: "memory");  // late start
+    if ((DBG(p.debug) & 32) && warp == 4) asm volatile("bar.sync 2, 160;" ::: "memory");  // late start
     const int64_t n_tiles = p.persistent ? p.n_tiles : 1;
     const int64_t tile_stride = p.persistent ? gridDim.x : 1;
     int64_t it = 0;
@@ -282,7 +287,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                         tma_load_2d(dst + a * atom_bytes, &imap, &full_b[st],
                                     int32_t(n0) + a * atom_cols, krow);
                 }
-                trace(p.debug, 0, s);
+                trace(DBG(p.debug), 0, s);
             }
             __syncwarp();
         }
@@ -299,7 +304,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                     const int j = srow ? srow[g] : s_begin + g;  // ws == 1: stage g = step g
                     tma_load_2d(w_buf + st * p.w_stage_bytes, &wmap, &full_w[st], j * p.d_t,
                                 int32_t(m0));
-                    trace(p.debug, 1, g);
+                    trace(DBG(p.debug), 1, g);
                 }
                 __syncwarp();
             }
@@ -335,15 +340,15 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         for (int s = 0; s < nsteps; ++s) {
             const int sb = (g0 + s) % p.nb, sa = (g0 + s) % p.na;
             mbar_wait(&full_b[sb], ((g0 + s) / p.nb) & 1);  // I slab landed and A tile densified
-            if (lane == 0) trace(p.debug, 7, s);
+            if (lane == 0) trace(DBG(p.debug), 7, s);
             tc_fence_after();
             if (elect_one()) {
-                trace(p.debug, 4, s);
+                trace(DBG(p.debug), 4, s);
                 uint64_t ad = a_desc0 + uint64_t(sa) * a_stage16;
                 uint64_t bd = b_desc0 + uint64_t(sb) * b_stage16;
                 uint32_t in_atom = 0;
                 for (int kk = 0; kk < ksteps; ++kk) {
-                    if (!(p.debug & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
+                    if (!(DBG(p.debug) & 2)) tc_mma<kTF32>(tmem_d, ad, bd, idesc, (s > 0 || kk > 0) ? 1u : 0u);
                     ad += 2;  // 32 bytes along K inside the swizzle atom
                     in_atom += 2;
                     if (in_atom == a_span16) { ad += a_jump16; in_atom = 0; }
@@ -355,7 +360,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                     }
                 }
                 tc_commit(&empty_b[sb]);  // frees the I slab (and, na steps later, the A tile)
-                trace(p.debug, 5, s);
+                trace(DBG(p.debug), 5, s);
             }
             __syncwarp();
         }
@@ -396,17 +401,17 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             const int wr = g0 + wg;                         // W ring position (ws == 1)
             if (p.w_tma && wsub == 0) {
                 mbar_wait(&full_w[wr % p.nw], (wr / p.nw) & 1);
-                if (t == 0) trace(p.debug, 8, wg);
+                if (t == 0) trace(DBG(p.debug), 8, wg);
             }
             if (gs >= p.na) {  // A stage sa was last read by the MMAs of ring step gs - na
                 const int sp = gs - p.na;
                 mbar_wait(&empty_b[sp % p.nb], (sp / p.nb) & 1);
             }
-            if (t == 0) trace(p.debug, 2, s);
+            if (t == 0) trace(DBG(p.debug), 2, s);
             const uint32_t a = smem_u32(a_buf + sa * p.a_stage_bytes);
             const uint32_t src = wrow + uint32_t((wr % p.nw) * p.w_stage_bytes);
             const uint32_t c0 = uint32_t(wsub * p.d_t * kElt / 16);  // first chunk of this step
-            if (active && !(p.debug & 1)) {
+            if (active && !(DBG(p.debug) & 1)) {
                 if (chunked) {
                     const int nchunks = p.d_t / V;
                     uint4 q[kMaxChunks];
@@ -453,19 +458,19 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             }
             // make the generic-proxy stores visible to the tensor core, then one
             // release-arrive per warp (full counts 4 warps + the TMA)
-            if (!(p.debug & 256)) fence_async_smem();
+            if (!(DBG(p.debug) & 256)) fence_async_smem();
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&full_b[gs % p.nb]);
                 if (p.w_tma && (wsub == p.ws - 1 || s == nsteps - 1)) mbar_arrive(&empty_w[wr % p.nw]);
             }
-            if (t == 0) trace(p.debug, 3, s);
+            if (t == 0) trace(DBG(p.debug), 3, s);
         }
         // ---- epilogue phase 1: wait for the accumulator; split-K slices > 0 park
         // their fp32 partial tile in the workspace (L2-resident) for the leader
         mbar_wait(tmem_full, uint32_t(it & 1));
         tc_fence_after();
-        if (threadIdx.x == 0) trace(p.debug, 6, 1);
+        if (threadIdx.x == 0) trace(DBG(p.debug), 6, 1);
         if (kslice > 0) {
             const uint32_t tmem_d = *tmem_slot;
             const int row = warp * 32 + lane;
@@ -512,7 +517,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             const int64_t col = n0 + c;
-            if (!row_ok || (p.debug & 4)) continue;
+            if (!row_ok || (DBG(p.debug) & 4)) continue;
             if (!p.ostore && col >= p.n_cols) continue;
             const bool full = col + 32 <= p.n_cols;
             if (p.ksplit > 1 && col < p.n_cols) {
@@ -620,7 +625,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
                 }
             }
         }
-        if (p.ostore && !(p.debug & 4)) {
+        if (p.ostore && !(DBG(p.debug) & 4)) {
             fence_async_smem();  // staged tile -> visible to the TMA (async proxy)
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (warp == 0 && elect_one()) {
@@ -644,7 +649,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         }
     }
     }  // tile loop
-    if (threadIdx.x == 0) trace(p.debug, 6, 2);
+    if (threadIdx.x == 0) trace(DBG(p.debug), 6, 2);
     tc_fence_before();
     __syncthreads();
     if (warp == 5) {
@@ -711,7 +716,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     int tn = 128;
     while (tn > tn_min && tn / 2 >= c.n_cols) tn /= 2;
     if (tn > tn_min && ((c.n_cols + tn - 1) / tn) * blocks_m * 2 < kNumSMs) tn /= 2;
-    if (const char *env = getenv("RBGP4_TC_TN")) tn = std::max(tn_min, std::min(256, atoi(env)));
+    if (opts().tc_tn > 0) tn = std::max(tn_min, std::min(256, int(opts().tc_tn)));
     if (force_tn) tn = force_tn;
     p.adj_smem = size_t(c.u_i) * c.d_i * 4 <= 16384 ? 1 : 0;
     // Shared-memory budget (one CTA per SM).  The main loop is bound by I-slab bytes in
@@ -729,7 +734,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
                             (p.adj_smem ? size_t(c.u_i) * c.d_i * 4 + 16 : 0) + 8 * (2 * 16 + 2 * 16 + 2) + 16;
         size_t w_bytes = size_t(p.nw) * p.w_stage_bytes;
         int na = 2;
-        if (const char *env = getenv("RBGP4_TC_NA")) na = std::max(1, std::min(8, atoi(env)));
+        if (opts().tc_na > 0) na = std::min(8, int(opts().tc_na));
         const size_t a_ring = size_t(na) * p.a_stage_bytes;
         if (base + w_bytes + a_ring + 2 * size_t(p.b_stage_bytes) > kSmemCap && p.w_tma) {
             // large compressed tiles: read W straight from global in the densify warps
@@ -748,11 +753,11 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         // once per SM; loads of tile i+1 stream under the epilogue of tile i) with a dedicated
         // output staging area for the TMA-store epilogue
         const int64_t tiles_here = ((c.n_cols + tn - 1) / tn) * blocks_m;
-        // Opt-in (RBGP4_TC_PERSIST=1): correct and tested, but measured no faster than one CTA
+        // Opt-in (option persistent=1): correct and tested, but measured no faster than one CTA
         // per tile on the VGG layers (the densify warps are also the epilogue warps, so the
         // densify -> MMA -> epilogue chain stays serial per tile); K4 has dedicated epilogue warps.
         (void)tiles_here;
-        const bool persist = p.rows_valid == c.tm && getenv("RBGP4_TC_PERSIST") && !getenv("RBGP4_TC_NOPERSIST");
+        const bool persist = p.rows_valid == c.tm && opts().persistent == 1;
         p.pstage_bytes = persist ? int32_t(size_t(p.rows_valid) * tn * 4) : 0;  // f32 worst case
         const size_t pst = persist ? size_t(p.pstage_bytes) + 1024 : 0;
         if (base + a_ring + pst + 4 * size_t(p.b_stage_bytes) > kSmemCap) { p.pstage_bytes = 0; }
@@ -764,16 +769,15 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
             const int cw = p.w_tma ? int(std::min<size_t>(cand, (avail - ib) / p.w_stage_bytes)) : 1;
             if (std::min(cand, cw) > std::min(nb, nw) || nb == 0) { nb = cand; nw = cw; }
         }
-        if (const char *env = getenv("RBGP4_TC_NB")) {
-            const int want = std::max(2, std::min(16, atoi(env)));
+        if (opts().tc_nb > 0) {
+            const int want = std::max(2, std::min(16, int(opts().tc_nb)));
             if (size_t(want) * p.b_stage_bytes + 2 * size_t(p.w_stage_bytes) <= avail) {
                 nb = want;
                 nw = p.w_tma ? int(std::min<size_t>(want, (avail - size_t(nb) * p.b_stage_bytes) / p.w_stage_bytes)) : 1;
             }
         }
-        if (const char *env = getenv("RBGP4_TC_NW"))
-            if (p.w_tma)
-                nw = std::max(2, std::min({16, atoi(env), int((avail - size_t(nb) * p.b_stage_bytes) / p.w_stage_bytes)}));
+        if (opts().tc_nw > 0 && p.w_tma)
+            nw = std::max(2, std::min({16, int(opts().tc_nw), int((avail - size_t(nb) * p.b_stage_bytes) / p.w_stage_bytes)}));
         if (nb < na || nb < 2) continue;
         p.na = na;
         p.nb = nb;
@@ -784,7 +788,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         // densify warp reads land on distinct banks (unswizzled 64-byte rows are 16-way conflicted)
         {
             const int wb = p.ws * c.d_t * elt;
-            p.w_swz = (p.w_tma && (wb == 32 || wb == 64 || wb == 128) && !getenv("RBGP4_TC_NOWSWZ")) ? wb : 0;
+            p.w_swz = (p.w_tma && (wb == 32 || wb == 64 || wb == 128) && opts().wswz) ? wb : 0;
         }
         p.tmem_cols = 32;
         while (p.tmem_cols < tn) p.tmem_cols *= 2;
@@ -792,7 +796,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
         // split-K in two (a 2-CTA cluster per tile) only when that still fits one wave;
         // deeper splits measured slower (tools/tc_time.py)
         int ks = (tiles * 2 <= kNumSMs && c.d_o >= 2) ? 2 : 1;
-        if (const char *env = getenv("RBGP4_TC_KSPLIT")) ks = std::max(1, std::min(8, atoi(env)));
+        if (opts().ksplit > 0) ks = std::min(8, int(opts().ksplit));
         p.sps = (c.d_o + ks - 1) / ks;
         p.ksplit = (c.d_o + p.sps - 1) / p.sps;  // no empty slices
         // many waves of tiles: persistent CTAs (setup, TMEM allocation and the pipeline fill
@@ -814,7 +818,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
 bool staging_fits(const TcPlan &pl, int out_elt) {
     const size_t rings = pl.p.pstage_bytes ? size_t(pl.p.pstage_bytes)
                                            : size_t(pl.p.na) * pl.p.a_stage_bytes + size_t(pl.p.nb) * pl.p.b_stage_bytes;
-    return size_t(pl.p.rows_valid) * pl.p.tn * out_elt <= rings && !getenv("RBGP4_TC_NOSTORE");
+    return size_t(pl.p.rows_valid) * pl.p.tn * out_elt <= rings && opts().ostore;
 }
 
 template <typename E, bool OUT_BF16, bool CONV = false>
@@ -845,7 +849,7 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
     cudaLaunchAttribute attrs[2];
     unsigned na = 0;
     if (pl.p.ksplit > 1) attrs[na++] = attr[0];
-    if (!getenv("RBGP4_NO_PDL")) {
+    if (opts().pdl) {
         attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attrs[na].val.programmaticStreamSerializationAllowed = 1;
         ++na;
@@ -1039,7 +1043,7 @@ int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_
         return RBGP4_ECUDA;
     }
     build_schedule(c.u_o, c.v_o, c.d_o, adj.data(), sched.data());
-    if (getenv("RBGP4_TC_NOSCHED"))
+    if (!opts().sched)
         for (int u = 0; u < c.u_o; ++u)
             for (int s2 = 0; s2 < c.d_o; ++s2) sched[size_t(u) * c.d_o + s2] = s2;
     // pairs: per step, tile-rows reading the same K-block are matched two by two (symmetric)
@@ -1124,12 +1128,12 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     const int atom_cols = 128 / elt;
     CUresult r;
     pl.p.i3d = (c.n_cols % atom_cols == 0) ? 1 : 0;
-    if (getenv("RBGP4_TC_2D")) pl.p.i3d = 0;
+    if (!opts().i3d) pl.p.i3d = 0;
     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    if (const char *e = getenv("RBGP4_TC_PROMO"))
-        promo = atoi(e) == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-              : atoi(e) == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-              : atoi(e) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (opts().promo >= 0)
+        promo = opts().promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+              : opts().promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : opts().promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     if (pl.p.i3d) {
         // (atom cols, K rows, N atoms) view: one box = one whole I slab, atom-major in smem
         cuuint64_t dims[3] = {cuuint64_t(atom_cols), cuuint64_t(c.cols), cuuint64_t(c.n_cols / atom_cols)};
@@ -1152,8 +1156,8 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
         set_error("cuTensorMapEncodeTiled failed (%d)", int(r));
         return RBGP4_ECUDA;
     }
-    if (const char *dbg = getenv("RBGP4_TC_DEBUG")) {
-        pl.p.debug = atoi(dbg);
+    if (DBG(opts().debug)) {
+        pl.p.debug = DBG(opts().debug);
         if (pl.p.debug & 8192)
             fprintf(stderr, "[rbgp4 tc plan] tn=%d na=%d nb=%d nw=%d ws=%d w_tma=%d w_swz=%d ks=%d smem=%zu tmem=%d\n",
                     pl.p.tn, pl.p.na, pl.p.nb, pl.p.nw, pl.p.ws, pl.p.w_tma, pl.p.w_swz, pl.p.ksplit, pl.smem,
@@ -1252,7 +1256,7 @@ int conv_plan(const ChainDims &c, const rbgp4_conv_desc *cv, TcPlan *pl) {
     RBGP4_REQUIRE(cv->width <= 256 && cv->height <= 256, "feature map too large for one TMA box");
     // wide pixel tiles when the grid is many waves deep: the per-CTA setup (TMEM, barriers,
     // scatter table, pipeline fill) is amortised over twice the pixels
-    const bool wide = c.n_cols >= int64_t(kNumSMs) * 256 * 4 && !getenv("RBGP4_CONV_NARROW");
+    const bool wide = c.n_cols >= int64_t(kNumSMs) * 256 * 4 && opts().conv_wide;
     for (int tn : {256, 128, 64}) {
         if (tn == 256 && !wide) continue;
         int th, tb;
@@ -1366,9 +1370,11 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
 
 }  // namespace rbgp4
 
-// debug-only (not part of include/rbgp4.h): copy the CTA-0 trace to the host
+#if RBGP4_DEBUG
+// debug builds only (not part of include/rbgp4.h): copy the CTA-0 trace to the host
 extern "C" int rbgp4_debug_trace(unsigned long long *host, int n) {
     if (n > 10 * rbgp4::kTraceSteps) n = 10 * rbgp4::kTraceSteps;
     return cudaMemcpyFromSymbol(host, rbgp4::g_trace, sizeof(unsigned long long) * n) == cudaSuccess
                ? 0 : -3;
 }
+#endif  // RBGP4_DEBUG

@@ -21,6 +21,7 @@ tensor out with no host traffic; CPU tensors in -> CPU tensor out.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, replace
 
 import numpy as np
@@ -197,6 +198,9 @@ def rbgp4mm(w: RcubsMatrix, inp, params: TilingParams, *, compute: str = "exact"
     if n_cols % params.tn:
         raise ConfigurationError([f"input columns {n_cols} not divisible by tn={params.tn}"])
 
+    if not is_tensor and out is None and out_dtype == t.bfloat16:
+        raise InvalidArgumentError("numpy operands cannot hold a bfloat16 result; pass torch "
+                                   "tensors or out_dtype=torch.float32")
     dev = resolve_device(device if device is not None else (inp.device if is_tensor and inp.is_cuda else None))
     with t.cuda.device(dev):
         staged = Staged(inp, dev)
@@ -240,15 +244,25 @@ def make_desc(fields: dict, n_cols: int, ld_in: int, ld_out: int) -> _native.Des
 
 
 _WS = {}
+_WS_LOCK = threading.Lock()
 
 
-def workspace(dev, nbytes: int):
-    """Per-device scratch buffer for the tensor-core path (grown on demand)."""
+def workspace(dev, nbytes: int, stream: int):
+    """Scratch buffer of the tensor-core path, one per (device, stream), grown on demand.
+
+    Keyed by stream so products queued on different streams never share partial sums, and
+    allocated on that stream (torch's caching allocator then keeps a replaced buffer alive
+    until the work queued on its stream before the replacement has run).
+    """
     t = torch()
-    buf = _WS.get(str(dev))
-    if buf is None or buf.numel() < nbytes:
-        buf = t.empty(max(nbytes, 1), dtype=t.uint8, device=dev)
-        _WS[str(dev)] = buf
+    key = (str(dev), int(stream))
+    with _WS_LOCK:
+        buf = _WS.get(key)
+        if buf is None or buf.numel() < nbytes:
+            s = t.cuda.ExternalStream(stream, device=dev) if stream else t.cuda.default_stream(dev)
+            with t.cuda.stream(s):
+                buf = t.empty(max(nbytes, 1), dtype=t.uint8, device=dev)
+            _WS[key] = buf
     return buf
 
 
@@ -258,19 +272,20 @@ def prepared(fmt, compute: str, dev, desc):
         return None
     if fmt.prep is None:
         fmt.prep = {}
-    buf = fmt.prep.get(compute)
+    lib = _native.lib()
+    code = _native.COMPUTE[compute]
+    # the section's layout follows the plan (e.g. option relayout), so its size is in the key
+    nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
+    if nbytes == 0:
+        return None
+    buf = fmt.prep.get((compute, nbytes))
     if buf is None:
-        lib = _native.lib()
-        code = _native.COMPUTE[compute]
-        nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
-        if nbytes == 0:
-            return None
         buf = torch().empty(nbytes, dtype=torch().uint8, device=dev)
         _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),
                                         fmt.adj_i.data_ptr(),
                                         buf.data_ptr(), nbytes, stream_handle(dev)),
                       "rbgp4_prepare")
-        fmt.prep[compute] = buf
+        fmt.prep[(compute, nbytes)] = buf
     return buf
 
 
@@ -281,13 +296,14 @@ def launch_sdmm(fmt, compute: str, x, res, dev) -> None:
     code = _native.COMPUTE[compute]
     in_code, out_code = dtype_code(x.dtype), dtype_code(res.dtype)
     need = lib.rbgp4_workspace_size(ctypes.byref(desc), code, in_code)
-    ws_ptr, ws_len = (workspace(dev, need).data_ptr(), need) if need else (None, 0)
+    stream = stream_handle(dev)
+    ws_ptr, ws_len = (workspace(dev, need, stream).data_ptr(), need) if need else (None, 0)
     prep = prepared(fmt, compute, dev, desc) if x.shape[1] else None
     _native.check(
         lib.rbgp4_sdmm_prepared(ctypes.byref(desc), code, in_code, out_code, fmt.values.data_ptr(),
                                 fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(),
                                 prep.data_ptr() if prep is not None else None, x.data_ptr(),
-                                res.data_ptr(), ws_ptr, ws_len, stream_handle(dev)),
+                                res.data_ptr(), ws_ptr, ws_len, stream),
         f"rbgp4_sdmm(compute={compute})",
     )
 

@@ -89,8 +89,17 @@ class _Pattern:
 
 
 def _product(fmt, values, inp, compute):
-    """O = W x I with W's values given as a device tensor (the trainable parameter)."""
+    """O = W x I with W's values given as a device tensor (the trainable parameter).
+
+    The kernel reads `values` and `inp` in ONE element type (rbgp4_sdmm's in_dtype), so a
+    mismatch would reinterpret bytes; it is rejected here before any launch.
+    """
     t = torch()
+    if values.dtype != inp.dtype or values.dtype != fmt.values.dtype:
+        raise ShapeError(f"sparse linear: activations ({inp.dtype}), values ({values.dtype}) and the "
+                         f"pattern's format ({fmt.values.dtype}) must share one dtype")
+    if values.device != inp.device:
+        raise ShapeError(f"sparse linear: values on {values.device}, activations on {inp.device}")
     out = t.empty((fmt.desc_fields["rows"], inp.shape[1]), dtype=inp.dtype, device=inp.device)
     desc = make_desc(fmt.desc_fields, inp.shape[1], inp.stride(0), out.stride(0))
     code = dtype_code(inp.dtype)

@@ -29,6 +29,14 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA (B200) device and the built library")
 
 
+@pytest.fixture
+def plan_options():
+    """set_option(name, value) for this test's thread; every override is reset afterwards."""
+    from paper_2006_13486_b200 import _native
+    yield _native.set_option
+    _native.lib().rbgp4_reset_options()
+
+
 def sha16(a) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
 

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
     lib = _native.lib()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.rbgp4_abi_version() == 2
+    assert lib.rbgp4_abi_version() == 3
 
 
 def test_desc_struct_layout():
@@ -99,10 +99,10 @@ def test_product_path_fails_loudly_without_gpu():
         ks.rbgp4mm(w, inp, ks.tiling_for_chain(chain))
 
 
-def test_prepared_section_carries_the_tc16_relayout(monkeypatch):
+def test_prepared_section_carries_the_tc16_relayout(plan_options):
     """rbgp4_prepare_size (host-only arithmetic): the TC16 shape (16x16 blocks, g_i (8,8) of degree
     2) gets the column-block relayout of its values (same byte count as the values) in its prepared
-    section; g_i of degree 4 does not, and RBGP4_TC_NORELAYOUT removes it."""
+    section; g_i of degree 4 does not, and option relayout=0 removes it."""
     lib = _native.lib()
 
     def prep_bytes(sp_i):
@@ -115,5 +115,37 @@ def test_prepared_section_carries_the_tc16_relayout(monkeypatch):
     assert size >= values
     size4, values4 = prep_bytes(0.5)
     assert size4 < values4
-    monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
+    plan_options("relayout", 0)
     assert prep_bytes(0.75)[0] < values
+
+
+def test_plan_options_are_explicit_and_thread_local():
+    """Plan overrides go through rbgp4_set_option (thread-local), never the process environment."""
+    import threading
+
+    from paper_2006_13486_b200.errors import DeviceError
+    lib = _native.lib()
+    assert _native.get_option("relayout") == -1 and _native.get_option("pdl") == 1
+    with _native.options(relayout=0, ksplit=2):
+        assert _native.get_option("relayout") == 0 and _native.get_option("ksplit") == 2
+        seen = {}
+        th = threading.Thread(target=lambda: seen.update(r=_native.get_option("relayout")))
+        th.start()
+        th.join()
+        assert seen["r"] == -1          # another thread keeps the defaults
+    assert _native.get_option("relayout") == -1 and _native.get_option("ksplit") == 0
+    with pytest.raises(DeviceError, match="unknown option"):
+        _native.set_option("no_such_knob", 1)
+    with pytest.raises(DeviceError, match="outside"):
+        _native.set_option("stages", 99)
+    if not lib.rbgp4_debug_build():  # the release library carries no trace / ablation hooks
+        with pytest.raises(DeviceError, match="debug build"):
+            _native.set_option("debug", 8)
+    lib.rbgp4_reset_options()
+
+
+def test_no_environment_reads_in_the_library_sources():
+    """No getenv in the CUDA sources: the launch paths are steered only by rbgp4_set_option."""
+    import glob
+    for path in glob.glob(os.path.join(ROOT, "paper_2006_13486_b200", "csrc", "*.c*")):
+        assert "getenv" not in open(path).read(), path

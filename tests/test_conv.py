@@ -64,11 +64,11 @@ def test_im2col_oracle_matches_direct_conv():
                                                  (128, 128, 16, 1)])
 @pytest.mark.parametrize("relu", [False, True])
 @pytest.mark.parametrize("persistent", [False, True])
-def test_sparse_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent, monkeypatch):
+def test_sparse_conv_matches_oracle(c_out, c_in, hw, batch, relu, persistent, plan_options):
     import torch
     if persistent:  # persistent tile loop (chosen by itself for many-wave grids)
-        monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
-        monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
+        plan_options("persistent", 1)
+        plan_options("relayout", 0)
     chain = conv_chain(c_out, c_in, seed=c_out + c_in + hw)
     w = ks.init_random(chain, 7, precision="f32")
     rng = np.random.default_rng(3)

@@ -2,21 +2,19 @@
 
 Taken for compute="bf16" when the dense element blocks g_b are >= 16 x 16 (g_r = (1,1)).
 Bar: rel-L2 <= 1e-2 against the f64 oracle on the same bf16-rounded operands (north star),
-plus agreement with the densify kernel (K2, RBGP4_TC_DENSE=1) on the same inputs.
+plus agreement with the densify kernel (K2, option dense=1) on the same inputs.
 Covers: the VGG TC16 factorisation, split-K clusters (small N), f32 outputs, 32 x 32 blocks
 (two K=16 MMAs per block), 64-row tile-rows, and the implicit-im2col convolution.
 """
 
 from __future__ import annotations
 
-import os
-
 import numpy as np
 import pytest
 
 import oracle
 import paper_2006_13486_b200 as ks
-from paper_2006_13486_b200 import conv
+from paper_2006_13486_b200 import _native, conv
 from paper_2006_13486_b200 import workloads as wl
 
 pytestmark = pytest.mark.gpu
@@ -37,30 +35,24 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
     The prepared buffer is cached per matrix and its layout follows the mode, so non-default
     modes run on a fresh RcubsMatrix copy."""
     p = ks.tiling_for_chain(w.chain, tn=1, rn=1, bn=1)
+    opt = {}
     if dense:
-        os.environ["RBGP4_TC_DENSE"] = "1"
+        opt["dense"] = 1
     if relayout:
-        os.environ["RBGP4_TC_RELAYOUT"] = "1"
+        opt["relayout"] = 1
     if direct or persistent or msplit:
-        os.environ["RBGP4_TC_NORELAYOUT"] = "1"
+        opt["relayout"] = 0
     if rl_split:  # the TC16 relayout in the one-tile-per-CTA kernel (split-K clusters)
-        os.environ["RBGP4_TC_NOPERSIST"] = "1"
+        opt["persistent"] = 0
     if relayout or direct or persistent or msplit or rl_persistent or rl_split:
         w = ks.RcubsMatrix(w.chain, np.array(w.values))
     if persistent or rl_persistent:  # rl_persistent: the persistent kernel on the TC16 relayout
-        os.environ["RBGP4_TC_PERSIST"] = "1"
+        opt["persistent"] = 1
     if msplit:
-        os.environ["RBGP4_TC_MSPLIT"] = "1"
-    try:
+        opt["msplit"] = 1
+    with _native.options(**opt):
         y, _ = ks.rbgp4mm(w, x, p, compute=compute, out_dtype=out_dtype)
         torch.cuda.synchronize()
-    finally:
-        os.environ.pop("RBGP4_TC_DENSE", None)
-        os.environ.pop("RBGP4_TC_RELAYOUT", None)
-        os.environ.pop("RBGP4_TC_NORELAYOUT", None)
-        os.environ.pop("RBGP4_TC_PERSIST", None)
-        os.environ.pop("RBGP4_TC_NOPERSIST", None)
-        os.environ.pop("RBGP4_TC_MSPLIT", None)
     return y.float().cpu().numpy()
 
 
@@ -152,16 +144,11 @@ def test_gather_conv_matches_oracle(c_out, c_in, hw, batch, relu, mode):
     xb = torch.from_numpy(x).to(torch.bfloat16)
     # default: the TC16 relayout (immediate-offset MMA loop); the other modes run on the
     # compressed values as stored
-    env = {"persistent": ["RBGP4_TC_PERSIST", "RBGP4_TC_NORELAYOUT"],
-           "msplit": ["RBGP4_TC_MSPLIT", "RBGP4_TC_NORELAYOUT"], "direct": ["RBGP4_TC_NORELAYOUT"],
-           "persistent_rl": ["RBGP4_TC_PERSIST"], "split_rl": ["RBGP4_TC_NOPERSIST"]}.get(mode, [])
-    for e in env:
-        os.environ[e] = "1"
-    try:
+    opt = {"persistent": dict(persistent=1, relayout=0), "msplit": dict(msplit=1, relayout=0),
+           "direct": dict(relayout=0), "persistent_rl": dict(persistent=1),
+           "split_rl": dict(persistent=0)}.get(mode, {})
+    with _native.options(**opt):
         got = conv.sparse_conv2d(w, xb.cuda(), 3, relu=relu, out_dtype=torch.float32).cpu().numpy()
-    finally:
-        for e in env:
-            os.environ.pop(e, None)
     ref = f64_ref(w, np.ascontiguousarray(im2col_nhwc(xb.float().numpy(), 3)))
     ref = ref.T.reshape(batch, hw, hw, c_out)
     if relu:

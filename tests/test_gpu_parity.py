@@ -31,7 +31,7 @@ def f64_oracle(w, inp):
 
 def test_device_and_library_present():
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    assert _native.lib().rbgp4_abi_version() == 2
+    assert _native.lib().rbgp4_abi_version() == 3
 
 
 @pytest.mark.parametrize("precision", ["f32", "f64"])
@@ -136,10 +136,10 @@ def test_general_chain_reference_on_gpu():
 
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("compute,tol", [("tf32", 1e-2), ("bf16", 1e-2)])
-def test_tensor_core_modes(golden, compute, tol, persistent, monkeypatch):
+def test_tensor_core_modes(golden, compute, tol, persistent, plan_options):
     if persistent:  # persistent tile loop of the tcgen05 kernels, forced (K4 on the stored values)
-        monkeypatch.setenv("RBGP4_TC_PERSIST", "1")
-        monkeypatch.setenv("RBGP4_TC_NORELAYOUT", "1")
+        plan_options("persistent", 1)
+        plan_options("relayout", 0)
     lib = _native.lib()
     for cid in golden["cases"]:
         entry = golden["cases"][cid]
