@@ -1,24 +1,28 @@
 """RBGP4 SDMM benchmark (BASELINE.json metric: effective TFLOP/s = 2*nnz*N / time).
 
-Workload (BASELINE.json configs[1]): the 512-output-channel convolutions of
-VGG19-CIFAR lowered to SDMM via a materialised im2col, batch 256 per GPU,
-at 87.5 % RBGP4 sparsity (the dyadic grid point nearest the "90 %" of the
-config; SURVEY hard part 6):
+Workload (BASELINE.json configs[1]): the 512-output-channel convolutions of VGG19-CIFAR
+lowered to SDMM via a materialised im2col, batch 256 per GPU, at 87.5 % RBGP4 sparsity
+(the dyadic grid point nearest the config's "90 %"; only dyadic sparsities are generatable,
+SURVEY hard part 6):
 
     conv9      (M, K, N) = (512, 2304, 4096)
     conv10-12  (512, 4608, 4096)   <- dominant kernel (3 launches per step)
     conv13-16  (512, 4608, 1024)
 
-A "step" is one pass of those eight products over one batch (im2col'd
-activations resident in HBM as bf16, W in the succinct device format),
-computed by the tcgen05 bf16 kernel with fp32 accumulation and bf16
-outputs.  The eight inputs total 170 MB > the 126 MB L2, so each step
-streams its operands from HBM (no explicit flush).  Multi-GPU runs shard the
-batch (one process per GPU, weak scaling, no collective on the hot path).
+A "step" is one pass of those eight products over one batch (im2col'd activations resident
+in HBM as bf16, W in the succinct device format), computed by the tcgen05 bf16 kernels with
+fp32 accumulation and bf16 outputs.  The eight inputs total 170 MB > the 126 MB L2, so each
+step streams its operands from HBM; the `l2` leg adds an explicitly flushed (cold) and a
+warm figure.
+
+Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment re-launches
+itself under torch.distributed.run.  Every rank brings its own batch of 256 (weak scaling, no
+collective on the hot path); after the timed region one NCCL all-gather of a layer's output
+shards is checked against the same product computed on one GPU (`multi_gpu.verify`).
 
 `--impl reference` times the reference's CPU algorithm (the pinned C port of
-kronsparse._tile_worker in oracle/, all host threads) on a bounded column
-sample of the same workload, in the same metric.
+kronsparse._tile_worker in oracle/, all host threads) on a bounded column sample of the
+same workload, in the same metric.
 """
 
 from __future__ import annotations
@@ -26,6 +30,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,11 +45,12 @@ sys.path.insert(0, ROOT)
 METRIC = "RBGP4 SDMM effective TFLOP/s (2*nnz*N)"
 UNIT = "TFLOP/s"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+EXTRA_PEAKS_PATH = os.path.join(ROOT, "profiles", "measured_peaks_r02.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
 FALLBACK_HBM_GBS = 6650.0
 
 
-def parse_args():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -53,18 +59,23 @@ def parse_args():
     ap.add_argument("--sparsity", type=float, default=0.875)
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
     ap.add_argument("--compute", default="bf16", choices=["bf16", "tf32", "ffma", "exact"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--factorisation", choices=["tc", "tc16", "paper"], default="tc16",
-                    help="base-graph factorisation of every layer (both are 87.5%% RBGP4)")
-    ap.add_argument("--no-alt", action="store_true", help="skip timing the other factorisation")
-    ap.add_argument("--no-conv", action="store_true", help="skip the implicit-im2col conv leg")
+                    help="base-graph factorisation of every layer")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--quick", action="store_true", help="headline, roofline and e2e only")
+    for leg in ("cpu-baseline", "e2e", "alt", "conv", "sweep", "precision", "l2"):
+        ap.add_argument(f"--no-{leg}", action="store_true")
     ap.add_argument("--wrn-batch", type=int, default=512,
                     help="WRN-40-4 leg (config 3): batch per rank; 0 = skip")
     ap.add_argument("--vgg-batch", type=int, default=32768,
                     help="VGG19-CIFAR inference leg: global batch (sharded over ranks); 0 = skip")
-    return ap.parse_args()
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="CPU/gloo check of the spawn + shard + all-gather plumbing (no GPU work)")
+    args = ap.parse_args(argv)
+    if args.quick:
+        args.no_alt = args.no_conv = args.no_sweep = args.no_precision = args.no_l2 = True
+        args.wrn_batch = args.vgg_batch = 0
+    return args
 
 
 def dist_env():
@@ -74,31 +85,56 @@ def dist_env():
     return rank, world, local
 
 
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args, argv) -> bool:
+    """`--gpus N` (N > 1) outside torchrun: re-run this script as N ranks under
+    torch.distributed.run on 127.0.0.1.  Returns True in the parent (which just waits)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")            # communicator log (nranks) for the driver
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    rc = subprocess.call(cmd, env=env)
+    if rc != 0:
+        sys.exit(rc)
+    return True
+
+
 # ----------------------------------------------------------------- workload
 FACTORISATIONS = {
     "tc": ("G_o(4,K/128)@.5 G_r(1,1) G_i(16,16) G_b(8,8): tile 128x128, 8x8 dense element blocks "
-           "(tensor-core-friendly, SURVEY §7 hard part 1)"),
+           "(tensor-core-friendly, SURVEY §7 hard part 1; densify kernel K2)"),
     "paper": "G_o(4,K/64)@.5 G_r(4,1) G_i(32,64) G_b(1,1): tile 128x64 (paper family, G_b=(1,1))",
     "tc16": ("G_o(4,K/128)@.5 G_r(1,1) G_i(8,8) G_b(16,16): tile 128x128, 16x16 dense element "
-             "blocks = whole MMA operands (gathered-block kernel, no densification; values "
+             "blocks = whole MMA operands (gathered-block kernel K4, no densification; values "
              "permuted once so one N=32 MMA covers a G_i column block)"),
 }
 
 
-def build_layers(sparsity: float, batch: int, fact: str = "tc"):
+def build_layers(sparsity: float, batch: int, fact: str = "tc", configs=None):
     import paper_2006_13486_b200 as ks
     from paper_2006_13486_b200 import workloads as wl
 
-    maker = {"tc": wl.vgg19_cifar_512_tc, "tc16": wl.vgg19_cifar_512_tc16,
-             "paper": wl.vgg19_cifar_512}[fact]
+    if configs is None:
+        maker = {"tc": wl.vgg19_cifar_512_tc, "tc16": wl.vgg19_cifar_512_tc16,
+                 "paper": wl.vgg19_cifar_512}[fact]
+        configs = maker(sparsity, batch=batch)
     layers = []
-    for cfg in maker(sparsity, batch=batch):
+    for cfg in configs:
         chain = wl.build_chain(cfg)
         rng = ks.make_rng(np.random.SeedSequence([cfg.seed, 1]).generate_state(1)[0])
         w = ks.init_random(chain, rng, precision="f32")
         params = ks.tiling_for_chain(chain, tn=cfg.tn, rn=cfg.rn, bn=cfg.bn)
         g_o, _, g_i, _ = chain.graphs
         layers.append(dict(cfg=cfg, chain=chain, w=w, params=params, rng=rng,
+                           name=cfg.config_id.split("-")[1],
                            m=w.rows, k=w.cols, n=cfg.n_cols, nnz=w.nnz,
                            flops=2 * w.nnz * cfg.n_cols,
                            adj_ints=g_o.num_left * len(g_o.adjacency[0])
@@ -113,11 +149,11 @@ def algorithmic_bytes(layer, s_in: int, s_out: int) -> int:
 
 
 def make_input(layer, dtype_np=np.float32):
-    """I = uniform(-1, 1, (K, N)) on the layer's Philox stream (bench.py:138-140)."""
+    """I = uniform(-1, 1, (K, N)) on the layer's Philox stream (reference bench.py:138-140)."""
     return layer["rng"].uniform(-1.0, 1.0, size=(layer["k"], layer["n"])).astype(dtype_np)
 
 
-# ----------------------------------------------------------------- clocks
+# ----------------------------------------------------------------- clocks / peaks
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -172,41 +208,80 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_peak_hbm():
+def load_peaks():
+    """Roofline denominators: HBM and bf16 from the driver's MEASURED_PEAKS.json; fp32 FFMA and
+    tf32 from profiles/measured_peaks_r02.json (tools/peaks.py); each with its source."""
+    peaks = {"hbm_gbs": (FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"),
+             "bf16_tflops": (1590.0, "fallback (B200_PROFILING.md)")}
     try:
         with open(PEAKS_PATH) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+            m = json.load(fh)
+        peaks["hbm_gbs"] = (float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json)")
+        peaks["bf16_tflops"] = (float(m["bf16_tflops"]), "measured burst (MEASURED_PEAKS.json)")
     except (OSError, KeyError, ValueError):
-        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+        pass
+    derived_ffma = 2 * 128 * 148 * 1.965e9 / 1e12
+    peaks["ffma_tflops"] = (derived_ffma, "derived 2*128*148*1.965 GHz")
+    peaks["tf32_tflops"] = (peaks["bf16_tflops"][0] / 2, "derived bf16/2")
+    try:
+        with open(EXTRA_PEAKS_PATH) as fh:
+            m = json.load(fh)
+        peaks["ffma_tflops"] = (float(m["ffma_tflops"]), "measured (profiles/measured_peaks_r02.json, "
+                                                          "tools/ffma_peak.cu)")
+        peaks["tf32_tflops"] = (float(m["tf32_tflops"]), "measured (profiles/measured_peaks_r02.json, "
+                                                          "cuBLAS tf32 8192^3)")
+    except (OSError, KeyError, ValueError):
+        pass
+    return peaks
 
 
 def load_traffic():
     try:
         with open(TRAFFIC_PATH) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d.get("source")
     except (OSError, ValueError):
-        return None
+        return None, None
+
+
+def roofline(layer, ms, s_in, s_out, compute, peaks):
+    """Whichever of the compute and HBM roofline binds at this layer:
+    T* = max(F / P, B / BW); frac = T* / T."""
+    flops, nbytes = layer["flops"], algorithmic_bytes(layer, s_in, s_out)
+    pk = {"bf16": "bf16_tflops", "tf32": "tf32_tflops", "ffma": "ffma_tflops", "exact": "ffma_tflops"}[compute]
+    p_tf, p_src = peaks[pk]
+    # exact mode issues a separate multiply and add per MAC: half the FFMA rate
+    p_eff = p_tf / 2 if compute == "exact" else p_tf
+    t_compute = flops / (p_eff * 1e12)
+    bw, bw_src = peaks["hbm_gbs"]
+    t_mem = nbytes / (bw * 1e9)
+    t = ms * 1e-3
+    if t_compute >= t_mem:
+        return {"bound": "tensor" if compute in ("bf16", "tf32") else "ffma",
+                "achieved": flops / t / 1e12, "peak": p_eff, "unit": "TFLOP/s",
+                "frac": t_compute / t, "peak_source": p_src, "algorithmic_flops": flops}
+    return {"bound": "hbm", "achieved": nbytes / t / 1e9, "peak": bw, "unit": "GB/s", "frac": t_mem / t,
+            "peak_source": bw_src, "algorithmic_bytes": nbytes}
 
 
 # ----------------------------------------------------------------- CPU legs
 CPU_SAMPLE_COLS = 512  # 4 column tiles of the reference tn=128 -> 16 tiles per layer
 
 
+def cpu_inputs(layers, cols=CPU_SAMPLE_COLS):
+    return [(lay, make_input(dict(lay, n=cols, rng=np.random.default_rng(1)))) for lay in layers]
+
+
 def cpu_sample(layers, seconds: float, threads: int, cols: int = CPU_SAMPLE_COLS):
     """Reference algorithm (oracle C port of _tile_worker, f32) on a column slice.
 
-    Work is linear in N and tiles are independent (reference sdmm.py:167), so
-    a `cols`-wide slice of every layer is a faithful sample of the workload.
-    Returns (TFLOP/s, description, repetitions).
+    Work is linear in N and tiles are independent (reference sdmm.py:167), so a `cols`-wide
+    slice of every layer is a faithful sample of the workload.  Returns (TFLOP/s, description).
     """
     import oracle
     oracle.build()
-    samples = []
-    for layer in layers:
-        inp = make_input(dict(layer, n=cols, rng=np.random.default_rng(1)))
-        samples.append((layer, inp))
+    samples = cpu_inputs(layers, cols)
     flops = sum(2 * lay["nnz"] * cols for lay, _ in samples)
-    # one warm pass, then repeat until the time budget is used
     for lay, inp in samples:
         oracle.tiled(lay["w"], inp, lay["params"], threads=threads)
     reps, t0 = 0, time.perf_counter()
@@ -219,7 +294,28 @@ def cpu_sample(layers, seconds: float, threads: int, cols: int = CPU_SAMPLE_COLS
     dt = time.perf_counter() - t0
     desc = (f"all 8 layers, first {cols} of N columns each (linear in N), f32 exact-order "
             f"C port of kronsparse._tile_worker, {reps} reps in {dt:.1f}s")
-    return flops * reps / dt / 1e12, desc, reps
+    return flops * reps / dt / 1e12, desc
+
+
+def output_check(layers, outs, host_in, cols=CPU_SAMPLE_COLS, threads=8):
+    """Post-timing check of the bench's own outputs: for every layer, the first `cols` columns
+    of the GPU result (after the timed replays) against the f64 oracle on the same
+    bf16-rounded operands.  Runs inside the CPU-baseline leg (the oracle is the checker)."""
+    import torch
+
+    import oracle
+    import paper_2006_13486_b200 as ks
+    res = {}
+    for lay, o, xh in zip(layers, outs, host_in):
+        c = min(cols, lay["n"])
+        wb = torch.from_numpy(np.asarray(lay["w"].values, dtype=np.float32)).to(torch.bfloat16)
+        w64 = ks.RcubsMatrix(lay["chain"], wb.double().numpy())
+        x64 = np.ascontiguousarray(xh[:, :c].double().numpy())
+        ref = oracle.reference_product(w64, x64, threads=threads)
+        res[lay["name"]] = oracle.rel_l2(o[:, :c].float().cpu().numpy(), ref)
+    worst = max(res.values())
+    return {"rel_l2": res, "worst": worst, "tol": 1e-2, "ok": bool(worst < 1e-2),
+            "what": f"first {CPU_SAMPLE_COLS} columns of every layer vs f64 oracle on bf16-rounded operands"}
 
 
 def run_reference(args):
@@ -231,7 +327,7 @@ def run_reference(args):
     import oracle
     oracle.build()
     cols = CPU_SAMPLE_COLS
-    samples = [(lay, make_input(dict(lay, n=cols, rng=np.random.default_rng(1)))) for lay in layers]
+    samples = cpu_inputs(layers, cols)
     flops = sum(2 * lay["nnz"] * cols for lay, _ in samples)
 
     def step():
@@ -248,12 +344,14 @@ def run_reference(args):
     sample = (f"8 VGG19 512-ch layers at {args.sparsity * 100:g}%, first {cols} columns of each "
               f"(tn=128 tiles, work linear in N); f32 exact-order C port of "
               f"kronsparse._tile_worker on {threads} threads")
+    cfg = workload_config(args, world)
+    cfg["compute"] = "f32 exact-order (reference rounding), CPU"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference bench recipe)",
-        "config": workload_config(args, world),
+        "config": cfg,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -266,367 +364,308 @@ def workload_config(args, world):
             "batch_per_gpu": args.batch, "global_batch": args.batch * world,
             "sparsity": args.sparsity, "factorisation": FACTORISATIONS[args.factorisation],
             "compute": args.compute, "parallelism": f"batch-shard x{world}",
-            "l2": "inputs (170 MB bf16) larger than L2 (126 MB); no explicit flush"}
+            "l2": "inputs (170 MB bf16) larger than L2 (126 MB); no flush in the headline "
+                  "(the `l2` leg adds a flushed cold and a warm figure)"}
 
 
-# ----------------------------------------------------------------- conv / VGG legs
-def _flush_l2(torch, buf):
-    """Overwrite a buffer larger than L2 (126 MB) so the next step starts cold."""
-    buf.add_(1)
-
-
-def run_conv_leg(args, dev, stream, rank, world, dist):
-    """The same eight layers as convolutions on NHWC activations (implicit im2col, no
-    materialised I): SparseConv2d with the layer's RBGP4 weight, batch `args.batch` per rank,
-    bf16, ReLU fused.  Same FLOP count as the SDMM step; L2 flushed between steps."""
-    import torch
-    from paper_2006_13486_b200 import conv as kconv
-    layers = build_layers(args.sparsity, args.batch, args.factorisation)
-    convs, xs = [], []
-    gen = torch.Generator(device=dev).manual_seed(11 + rank)
-    for lay in layers:
-        c_in = lay["k"] // 9
-        hw = 4 if lay["n"] == 16 * args.batch else 2
-        convs.append(kconv.SparseConv2d(lay["w"], 3, relu=True))
-        xs.append((torch.rand((args.batch, hw, hw, c_in), device=dev, generator=gen) * 2 - 1)
-                  .to(torch.bfloat16))
-    flops = sum(lay["flops"] for lay in layers)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB
-    with torch.cuda.stream(stream):
-        outs = [c(x) for c, x in zip(convs, xs)]  # warm-up: prepared formats, tensor maps
-        stream.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            outs = [c(x) for c, x in zip(convs, xs)]
-    torch.cuda.synchronize()
-    steps = max(10, args.steps // 4)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(steps)]
-    with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
-            g.replay()
-        for a, b in evs:
-            _flush_l2(torch, flush)
-            a.record(stream)
-            g.replay()
-            b.record(stream)
-    torch.cuda.synchronize()
-    ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    act_bytes = sum(x.numel() * 2 for x in xs) + sum(o.numel() * 2 for o in outs) + \
-        sum(lay["nnz"] * 2 for lay in layers)
-    return {"value": flops * world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
-            "path": "paper_2006_13486_b200.conv.SparseConv2d (implicit im2col, NHWC bf16, ReLU fused)",
-            "hbm_bytes_per_step": act_bytes, "l2": "256 MB overwrite between steps"}
-
-
-def run_vgg_leg(args, dev, stream, rank, world, dist):
-    """BASELINE config 5: full VGG19-CIFAR-100 RBGP4 inference (dense conv1 + classifier,
-    15 RBGP4 convs at `--sparsity`, 5 pools), synthetic global batch sharded over ranks."""
-    import torch
-    from paper_2006_13486_b200.vgg import VGG19Sparse
-    batch = max(1, args.vgg_batch // world)
-    net = VGG19Sparse(sparsity=args.sparsity, num_classes=100, seed=0, device=str(dev))
-    gen = torch.Generator(device=dev).manual_seed(5 + rank)
-    x = torch.randn(batch, 32, 32, 3, device=dev, generator=gen).to(torch.bfloat16)
-    with torch.cuda.stream(stream):
-        net(x)
-        stream.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            y = net(x)
-    torch.cuda.synchronize()
-    reps = 5
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            g.replay()
-        if world > 1:
-            dist.barrier()
-        a.record(stream)
-        for _ in range(reps):
-            g.replay()
-        b.record(stream)
-    torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / reps
-    if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    del y
-    return {"value": batch * world / (ms * 1e-3), "unit": "img/s", "ms_per_forward": ms,
-            "global_batch": batch * world, "sparsity": args.sparsity,
-            "sparse_tflops": net.sparse_flops_per_image * batch * world / (ms * 1e-3) / 1e12,
-            "model": "VGG19-CIFAR-100, RBGP4 convs 2-16 (bf16, NHWC), dense conv1 + classifier",
-            "data": "synthetic images, random-init weights"}
-
-
-def run_wrn_leg(args, dev, stream, rank, world, dist):
-    """BASELINE config 3: WideResNet-40-4 CIFAR-10, all 39 non-first convs RBGP4 sparse,
-    synthetic batch `--wrn-batch` per rank; the bf16 tcgen05 path against the fp32 FFMA path."""
-    import torch
-    from paper_2006_13486_b200.wrn import WRN40_4Sparse
-    batch = args.wrn_batch
-    net = WRN40_4Sparse(sparsity=args.sparsity, seed=0, device=str(dev))
-    gen = torch.Generator(device=dev).manual_seed(7 + rank)
-    x = torch.randn(batch, 32, 32, 3, device=dev, generator=gen)
-    flops = net.sparse_flops(batch)
-    res = {"global_batch": batch * world, "sparsity": args.sparsity,
-           "model": "WideResNet-40-4 CIFAR-10: dense conv1 + FC, 39 RBGP4 convs (36 3x3 + 3 1x1 shortcuts)",
-           "data": "synthetic images, random-init weights", "sparse_gflop_per_forward": flops / 1e9}
-    for compute in ("bf16", "ffma"):
-        with torch.cuda.stream(stream):
-            net(x, compute=compute)  # warm-up: prepared formats, tensor maps
-            reps = 3
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            for _ in range(reps):
-                net(x, compute=compute)
-            b.record(stream)
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b) / reps
-        if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        res[compute] = {"ms_per_forward": ms, "img_s": batch * world / (ms * 1e-3),
-                        "sparse_tflops": flops * world / (ms * 1e-3) / 1e12}
-    return res
-
-
-# ----------------------------------------------------------------- GPU leg
-def run_ours(args):
+# ----------------------------------------------------------------- distributed self-test
+def run_dist_selftest(args):
+    """gloo, CPU only: spawn (maybe_spawn) -> rendezvous -> tile-aligned column shards ->
+    all-gather -> reassembly, checked against the unsharded array.  The per-rank "product" is
+    a deterministic function of the global column index, so the check is exact."""
     import torch
     import torch.distributed as dist
 
-    rank, world, local = dist_env()
+    from paper_2006_13486_b200 import sharding
+    rank, world, _ = dist_env()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(dev)
+        dist.init_process_group("gloo")
+    n, tn, rows = 4096 + 128 * 3, 128, 16
+    a, b = sharding.shard_of(n, world, rank, tn)
+    cols = torch.arange(a, b, dtype=torch.float64)
+    local = torch.stack([cols * (r + 1) for r in range(rows)])
+    full = sharding.gather_columns(local, n, tn) if world > 1 else local
+    want = torch.stack([torch.arange(n, dtype=torch.float64) * (r + 1) for r in range(rows)])
+    ok = bool(torch.equal(full, want))
+    if rank == 0:
+        print(json.dumps({"dist_selftest": True, "n_gpus": world, "backend": "gloo" if world > 1 else "none",
+                          "gather_verified": ok, "shards": sharding.column_shards(n, world, tn)}))
+    if world > 1:
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
 
-    import paper_2006_13486_b200 as ks
-    from paper_2006_13486_b200 import _native
-    from paper_2006_13486_b200.device import device_format
-    from paper_2006_13486_b200.sdmm import launch_sdmm
 
-    compute = args.compute
-    tc = compute in ("bf16", "tf32")
-    op_dt = torch.bfloat16 if compute == "bf16" else torch.float32
-    out_dt = torch.bfloat16 if compute == "bf16" else torch.float32
-    s_in = 2 if compute == "bf16" else 4
-    s_out = s_in
+# ----------------------------------------------------------------- GPU legs
+class Bench:
+    """Shared state of the GPU arm: device, stream, rank/world, peaks."""
 
-    def setup(fact):
-        layers = build_layers(args.sparsity, args.batch, fact)
-        # every rank gets its own batch shard: same W (replicated), distinct inputs
-        for lay in layers:
-            lay["rng"] = ks.make_rng(
-                np.random.SeedSequence([lay["cfg"].seed, 1, rank]).generate_state(1)[0])
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist, self.args = torch, dist, args
+        self.rank, self.world, local = dist_env()
+        if self.world > 1:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        self.dev = torch.device("cuda", local if self.world > 1 else 0)
+        torch.cuda.set_device(self.dev)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.peaks = load_peaks()
+
+    def max_over_ranks(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    # -- a set of layers resident on the device, one CUDA graph per layer and one per step
+    def setup(self, layers, compute):
+        import paper_2006_13486_b200 as ks
+        from paper_2006_13486_b200.device import device_format
+        from paper_2006_13486_b200.sdmm import launch_sdmm
+        torch = self.torch
+        op_dt = torch.bfloat16 if compute == "bf16" else torch.float32
+        out_dt = op_dt
+        for lay in layers:   # every rank its own batch: same W (replicated), distinct inputs
+            lay["rng"] = ks.make_rng(np.random.SeedSequence([lay["cfg"].seed, 1, self.rank]).generate_state(1)[0])
         host_in, dev_in, dev_out, fmts = [], [], [], []
         for lay in layers:
-            x32 = torch.from_numpy(make_input(lay))
-            xh = x32.to(op_dt).pin_memory()
+            xh = torch.from_numpy(make_input(lay)).to(op_dt).pin_memory()
             host_in.append(xh)
-            dev_in.append(xh.to(dev))
-            dev_out.append(torch.empty((lay["m"], lay["n"]), dtype=out_dt, device=dev))
-            fmts.append(device_format(lay["w"], dev, op_dt))
+            dev_in.append(xh.to(self.dev))
+            dev_out.append(torch.empty((lay["m"], lay["n"]), dtype=out_dt, device=self.dev))
+            fmts.append(device_format(lay["w"], self.dev, op_dt))
         torch.cuda.synchronize()
-        # one CUDA graph per layer: the launch is captured once, replays cost ~us
         graphs = []
-        with torch.cuda.stream(stream):
+        with torch.cuda.stream(self.stream):
             for fmt, x, o in zip(fmts, dev_in, dev_out):
-                launch_sdmm(fmt, compute, x, o, dev)  # eager warm-up (attributes, prep)
-            stream.synchronize()
+                launch_sdmm(fmt, compute, x, o, self.dev)  # eager warm-up (attributes, prep)
+            self.stream.synchronize()
             for fmt, x, o in zip(fmts, dev_in, dev_out):
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g, stream=stream):
-                    launch_sdmm(fmt, compute, x, o, dev)
+                with torch.cuda.graph(g, stream=self.stream):
+                    launch_sdmm(fmt, compute, x, o, self.dev)
                 graphs.append(g)
             # the whole step as one graph: consecutive launches carry programmatic-dependent-launch
             # edges (each kernel's setup overlaps the previous one's tail)
             step_graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(step_graph, stream=stream):
+            with torch.cuda.graph(step_graph, stream=self.stream):
                 for fmt, x, o in zip(fmts, dev_in, dev_out):
-                    launch_sdmm(fmt, compute, x, o, dev)
+                    launch_sdmm(fmt, compute, x, o, self.dev)
         torch.cuda.synchronize()
-        return layers, host_in, dev_out, graphs, step_graph
+        return dict(layers=layers, host_in=host_in, dev_in=dev_in, dev_out=dev_out, graphs=graphs,
+                    step=step_graph, compute=compute, flops=sum(lay["flops"] for lay in layers))
 
-    def timed(graphs, dom, steps, warmup, sampler=None):
-        # events bracket only the dominant layers' launches inside the timed region (the
-        # roofline kernel); the other launches run back to back as in a plain step
-        ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
-        ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(steps * len(dom))]
-
-        def step(record=None):
-            for i, g in enumerate(graphs):
-                if record is not None and i in dom:
-                    ev_s[record[0]].record(stream)
-                    g.replay()
-                    ev_e[record[0]].record(stream)
-                    record[0] += 1
-                else:
-                    g.replay()
-
-        with torch.cuda.stream(stream):
+    def time_step(self, st, steps, warmup, sampler=None, flush=None):
+        """`steps` replays of the one-graph step between CUDA events, barrier + synchronize on both
+        sides, max over ranks.  With `flush`, a 256 MB buffer is overwritten before every step
+        and only the step itself is timed (events around each replay)."""
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
             for _ in range(warmup):
-                step()
+                st["step"].replay()
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        self.barrier()
         if sampler is not None:
             sampler.start()
-            time.sleep(0.3)  # sampler warm-up (first samples land before the timed region)
-        _native.reset_launch_count()
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
+            time.sleep(0.3)
+        self.barrier()
         torch.cuda.synchronize()
-        with torch.cuda.stream(stream):
-            t_start.record(stream)
-            cursor = [0]
-            for _ in range(steps):
-                step(cursor)
-            t_end.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        if flush is None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(self.stream):
+                a.record(self.stream)
+                for _ in range(steps):
+                    st["step"].replay()
+                b.record(self.stream)
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / steps
+        else:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(steps)]
+            with torch.cuda.stream(self.stream):
+                for a, b in evs:
+                    flush.add_(1)
+                    a.record(self.stream)
+                    st["step"].replay()
+                    b.record(self.stream)
+            torch.cuda.synchronize()
+            ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+        self.barrier()
         clocks = sampler.stop() if sampler is not None else None
-        elapsed_ms = t_start.elapsed_time(t_end)
-        if world > 1:
-            t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            elapsed_ms = float(t.item())
-        dom_ms = [a.elapsed_time(b) for a, b in zip(ev_s, ev_e)]
-        return elapsed_ms, (statistics.mean(dom_ms) if dom_ms else float("nan")), clocks
+        return self.max_over_ranks(ms), clocks
 
-    def timed_step(step_graph, steps, warmup, sampler):
-        """Headline region: `steps` replays of the one-graph step, barrier + sync on both sides."""
-        with torch.cuda.stream(stream):
-            for _ in range(warmup):
-                step_graph.replay()
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        sampler.start()
-        time.sleep(0.3)
-        _native.reset_launch_count()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        with torch.cuda.stream(stream):
-            a.record(stream)
-            for _ in range(steps):
-                step_graph.replay()
-            b.record(stream)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        clocks = sampler.stop()
-        ms = a.elapsed_time(b)
-        if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, clocks
-
-    def per_layer(graphs, steps):
-        """Mean event-timed duration of every layer's launch (separate pass, for the report)."""
+    def per_layer(self, st, reps, warm_layer=None):
+        """Mean event-timed duration of every layer's launch (its own graph, in step order), or
+        of one layer replayed back to back (`warm_layer`: its operands stay in L2)."""
+        torch = self.torch
+        graphs = st["graphs"]
+        idx = [warm_layer] * len(graphs) if warm_layer is not None else list(range(len(graphs)))
         evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in graphs] for _ in range(steps)]
-        with torch.cuda.stream(stream):
-            for k in range(steps):
-                for i, g in enumerate(graphs):
-                    evs[k][i][0].record(stream)
-                    g.replay()
-                    evs[k][i][1].record(stream)
+                for _ in idx] for _ in range(reps)]
+        with torch.cuda.stream(self.stream):
+            for _ in range(2):
+                for i in idx:
+                    graphs[i].replay()
+            for k in range(reps):
+                for j, i in enumerate(idx):
+                    evs[k][j][0].record(self.stream)
+                    graphs[i].replay()
+                    evs[k][j][1].record(self.stream)
         torch.cuda.synchronize()
-        return [statistics.mean(evs[k][i][0].elapsed_time(evs[k][i][1]) for k in range(steps))
-                for i in range(len(graphs))]
+        out = [statistics.mean(evs[k][j][0].elapsed_time(evs[k][j][1]) for k in range(reps))
+               for j in range(len(idx))]
+        return [self.max_over_ranks(v) for v in out]
 
-    stream = torch.cuda.Stream(device=dev)
-    layers, host_in, dev_out, graphs, step_graph = setup(args.factorisation)
-    flops_step = sum(lay["flops"] for lay in layers)
+    def leg_value(self, layers, compute, reps):
+        """(TFLOP/s whole job, ms per step, per-layer ms) of a set of layers."""
+        st = self.setup(layers, compute)
+        ms, _ = self.time_step(st, reps, 3)
+        lay_ms = self.per_layer(st, max(5, reps // 4))
+        return st, ms, lay_ms
+
+
+def run_ours(args):
+    B = Bench(args)
+    torch, rank, world = B.torch, B.rank, B.world
+    import paper_2006_13486_b200 as ks
+    from paper_2006_13486_b200 import _native
+    compute = args.compute
+    s_in = 2 if compute == "bf16" else 4
+    s_out = s_in
+
+    layers = build_layers(args.sparsity, args.batch, args.factorisation)
+    st = B.setup(layers, compute)
     dom = [i for i, lay in enumerate(layers) if lay["k"] == 4608 and lay["n"] == 16 * args.batch]
-    # headline: the one-graph step; roofline: events around each dominant launch in a second
-    # timed region of per-layer graph replays (same kernels, same inputs)
-    elapsed_ms, clocks = timed_step(step_graph, args.steps, args.warmup, ClockSampler(dev.index))
-    _, dom_avg_ms, _ = timed(graphs, dom, max(20, args.steps // 2), args.warmup)
-    layer_ms = per_layer(graphs, max(10, args.steps // 4))
-    ms_per_step = elapsed_ms / args.steps
-    value = flops_step * world / (ms_per_step * 1e-3) / 1e12
-    launches_in_region = len(graphs) * args.steps  # kernels in the timed step-graph replays
-
-    # roofline of the dominant kernel (HBM-bound at this shape)
+    _native.reset_launch_count()
+    ms_per_step, clocks = B.time_step(st, args.steps, args.warmup, ClockSampler(B.dev.index))
+    value = st["flops"] * world / (ms_per_step * 1e-3) / 1e12
+    launches_in_region = len(layers) * args.steps
+    layer_ms = B.per_layer(st, max(20, args.steps // 4))
+    dom_ms = statistics.mean(layer_ms[i] for i in dom)
     dom_layer = layers[dom[0]]
-    bytes_launch = algorithmic_bytes(dom_layer, s_in, s_out)
-    peak, peak_src = load_peak_hbm()
-    achieved = bytes_launch / (dom_avg_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": load_traffic(),
-                "kernel": f"{'gather_persistent_kernel (K4, TC16 relayout)' if args.factorisation == 'tc16' else 'tc_kernel (K2)'}"
-                          f"<bf16> conv10-12 ({args.factorisation} factorisation) "
-                          f"(M,K,N)=({dom_layer['m']},{dom_layer['k']},"
-                          f"{dom_layer['n']})", "algorithmic_bytes_per_launch": bytes_launch,
-                "avg_launch_us": dom_avg_ms * 1e3, "peak_source": peak_src,
-                "tflops_eff": dom_layer["flops"] / (dom_avg_ms * 1e-3) / 1e12}
+    rl = roofline(dom_layer, dom_ms, s_in, s_out, compute, B.peaks)
+    traffic, traffic_src = load_traffic()
+    rl.update({"traffic": traffic, "traffic_source": traffic_src,
+               "kernel": (f"{'gather_persistent_kernel (K4)' if args.factorisation == 'tc16' else 'tc_kernel (K2)'}"
+                          f" conv10-12 ({args.factorisation}) (M,K,N)=({dom_layer['m']},{dom_layer['k']},"
+                          f"{dom_layer['n']})"),
+               "avg_launch_us": dom_ms * 1e3,
+               "tflops_eff": dom_layer["flops"] / (dom_ms * 1e-3) / 1e12,
+               "timing": "events around each conv10-12 graph replay, layers in step order, max over ranks"})
+    layers_rl = {lay["name"]: {"us": round(ms * 1e3, 2),
+                               "frac": round(roofline(lay, ms, s_in, s_out, compute, B.peaks)["frac"], 3)}
+                 for lay, ms in zip(layers, layer_ms)}
 
-    # end-to-end through the public API with pinned host buffers
+    # ---- end to end through the public API: pinned host operands, every copy in the region
     e2e = None
     if not args.no_e2e:
+        host_out = [torch.empty((lay["m"], lay["n"]), dtype=o.dtype).pin_memory()
+                    for lay, o in zip(layers, st["dev_out"])]
+
         def e2e_step():
-            outs = []
-            for lay, xh in zip(layers, host_in):
-                o, _ = ks.rbgp4mm(lay["w"], xh, lay["params"], compute=compute)
-                outs.append(o)
-            return outs
+            with torch.cuda.stream(B.stream):
+                for lay, xh, oh in zip(layers, st["host_in"], host_out):
+                    ks.rbgp4mm(lay["w"], xh, lay["params"], compute=compute, out=oh, non_blocking=True)
         e2e_step()
         torch.cuda.synchronize()
         reps = max(3, min(20, args.steps // 10))
+        B.barrier()
         t0 = time.perf_counter()
         for _ in range(reps):
             e2e_step()
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / reps
-        if world > 1:
-            t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": flops_step * world / e2e_s / 1e12, "unit": UNIT,
-               "h2d_bytes_per_step": int(sum(x.numel() * x.element_size() for x in host_in)),
-               "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in dev_out)),
-               "ms_per_step": e2e_s * 1e3,
-               "path": "paper_2006_13486_b200.rbgp4mm(w, pinned host bf16 tensor, params, "
-                       "compute='bf16') per layer"}
+        e2e_s = B.max_over_ranks((time.perf_counter() - t0) / reps)
+        h2d = int(sum(x.numel() * x.element_size() for x in st["host_in"]))
+        d2h = int(sum(o.numel() * o.element_size() for o in host_out))
+        e2e = {"value": st["flops"] * world / e2e_s / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+               "pcie_gbs": (h2d + d2h) / e2e_s / 1e9,
+               "path": ("paper_2006_13486_b200.rbgp4mm(w, pinned host bf16 tensor, params, compute=, "
+                        "out=pinned host tensor, non_blocking=True) per layer: H2D on a copy-in stream, "
+                        "kernel on the compute stream, D2H on a copy-out stream, one sync per step"),
+               "matches_device_path": all(torch.equal(oh, o.cpu()) for oh, o in zip(host_out, st["dev_out"]))}
 
-    conv_leg = None if args.no_conv else run_conv_leg(args, dev, stream, rank, world, dist)
-    vgg_leg = None if args.vgg_batch <= 0 else run_vgg_leg(args, dev, stream, rank, world, dist)
-    wrn_leg = None if args.wrn_batch <= 0 else run_wrn_leg(args, dev, stream, rank, world, dist)
+    # ---- multi-GPU: one NCCL all-gather of conv10's output shards vs the single-GPU product
+    multi = None
+    if world > 1:
+        multi = verify_gather(B, st, dom[0])
 
-    cpu = None
+    legs = {}
+    if not args.no_l2:
+        flush = torch.empty(64 << 20, dtype=torch.float32, device=B.dev)  # 256 MB
+        cold_ms, _ = B.time_step(st, max(10, args.steps // 4), 3, flush=flush)
+        warm_us = B.per_layer(st, max(20, args.steps // 4), warm_layer=dom[0])[0] * 1e3
+        del flush
+        legs["l2"] = {"cold_step": {"value": st["flops"] * world / (cold_ms * 1e-3) / 1e12, "unit": UNIT,
+                                    "ms_per_step": cold_ms, "how": "256 MB overwrite before every step, "
+                                    "events around the step only"},
+                      "warm_conv10": {"us": warm_us, "tflops_eff": dom_layer["flops"] / (warm_us * 1e-6) / 1e12,
+                                      "frac_hbm": roofline(dom_layer, warm_us * 1e-3, s_in, s_out, compute,
+                                                           B.peaks)["frac"],
+                                      "how": "conv10 replayed back to back (its 38 MB stay in L2)"}}
+    if not args.no_sweep and compute == "bf16":
+        sweep = {}
+        for sp, fact in ((0.75, "tc16"), (0.875, "tc"), (0.9375, "tc")):
+            lays = build_layers(sp, args.batch, fact)
+            s2, ms, lms = B.leg_value(lays, compute, max(20, args.steps // 4))
+            sweep[f"{sp * 100:g}%-{fact}"] = {
+                "value": s2["flops"] * world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+                "factorisation": FACTORISATIONS[fact],
+                "conv10_us": lms[1] * 1e3, "conv10_frac": roofline(lays[1], lms[1], s_in, s_out, compute,
+                                                                   B.peaks)["frac"]}
+            del s2
+        sweep["87.5%-tc16"] = {"value": value, "unit": UNIT, "ms_per_step": ms_per_step, "headline": True}
+        from paper_2006_13486_b200 import workloads as wl
+        cfg = wl.SweepConfig("vgg19tc16-standin8x8-sp87.5", (4, 36), 0.5, (1, 1), (8, 8), 0.75, (16, 16),
+                             n_cols=args.batch * 64, seed=20)
+        lays = build_layers(0.875, args.batch, configs=[cfg])
+        s2, ms, lms = B.leg_value(lays, compute, max(20, args.steps // 4))
+        legs["standin_512x4608x16384"] = {
+            "what": "synthetic 512-ch layer at 8x8 maps (SURVEY §8(d) config 2 stand-in), tc16 87.5%",
+            "us": lms[0] * 1e3, "tflops_eff": lays[0]["flops"] / (lms[0] * 1e-3) / 1e12,
+            "roofline": roofline(lays[0], lms[0], s_in, s_out, compute, B.peaks)}
+        del s2
+        legs["sparsity"] = sweep
+    if not args.no_alt:
+        lays = build_layers(args.sparsity, args.batch, "paper")
+        s2, ms, lms = B.leg_value(lays, compute, max(10, args.steps // 8))
+        legs["paper_family"] = {"factorisation": FACTORISATIONS["paper"],
+                                "value": s2["flops"] * world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+                                "conv10_us": lms[1] * 1e3,
+                                "conv10_frac": roofline(lays[1], lms[1], s_in, s_out, compute, B.peaks)["frac"]}
+        del s2
+    if not args.no_precision and compute == "bf16":
+        prec = {}
+        for cm in ("tf32", "ffma"):
+            fact = "tc" if cm == "tf32" else args.factorisation
+            lays = build_layers(args.sparsity, args.batch, fact)
+            s2, ms, lms = B.leg_value(lays, cm, max(5, args.steps // 20))
+            prec[cm] = {"value": s2["flops"] * world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+                        "dtype": "f32 operands" + (" (tf32 tensor cores)" if cm == "tf32" else " (fp32 FFMA, SIMT)"),
+                        "factorisation": fact, "conv10_us": lms[1] * 1e3,
+                        "roofline_conv10": roofline(lays[1], lms[1], 4, 4, cm, B.peaks)}
+            del s2
+        legs["precision"] = prec
+    if not args.no_conv:
+        legs["conv_fused"] = run_conv_leg(B, args)
+    if args.vgg_batch > 0:
+        legs["vgg19"] = run_vgg_leg(B, args)
+    if args.wrn_batch > 0:
+        legs["wrn40_4"] = run_wrn_leg(B, args)
+
+    cpu, check = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        v, desc, _ = cpu_sample(layers, args.cpu_seconds, threads)
+        v, desc = cpu_sample(layers, args.cpu_seconds, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc}
-
-    alt = None
-    if not args.no_alt:
-        other = "tc" if args.factorisation == "tc16" else "tc16"
-        a_layers, _, _, a_graphs, _ = setup(other)
-        a_elapsed, a_dom, _ = timed(a_graphs, dom, max(10, args.steps // 4), args.warmup)
-        a_ms = a_elapsed / max(10, args.steps // 4)
-        a_flops = sum(lay["flops"] for lay in a_layers)
-        alt = {"factorisation": FACTORISATIONS[other],
-               "value": a_flops * world / (a_ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": a_ms,
-               "dominant_kernel_us": a_dom * 1e3,
-               "dominant_frac_hbm": algorithmic_bytes(a_layers[dom[0]], s_in, s_out)
-               / (a_dom * 1e-3) / 1e9 / load_peak_hbm()[0]}
+        check = output_check(layers, st["dev_out"], st["host_in"], threads=threads)
 
     if rank == 0:
         print(json.dumps({
@@ -636,20 +675,189 @@ def run_ours(args):
             "dtype": "bf16" if compute == "bf16" else "f32",
             "data": "synthetic (reference bench recipe: Philox masks/values, U(-1,1) inputs)",
             "config": workload_config(args, world),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": rl, "cpu_baseline": cpu, "e2e": e2e, "output_check": check,
             "gpu_launches": launches_in_region, "clocks": clocks,
-            "layers_us": {lay["cfg"].config_id.split("-")[1]: round(ms * 1e3, 2)
-                          for lay, ms in zip(layers, layer_ms)},
-            "conv_fused": conv_leg, "vgg19": vgg_leg, "wrn40_4": wrn_leg,
-            "alt_factorisation": alt,
+            "layers": layers_rl, "multi_gpu": multi, "legs": legs,
+            "peaks": {k: {"value": v[0], "source": v[1]} for k, v in B.peaks.items()},
         }))
     if world > 1:
-        dist.destroy_process_group()
+        B.dist.destroy_process_group()
+
+
+def verify_gather(B, st, li):
+    """NCCL all-gather of every rank's output shard of layer `li` (verification only, after the
+    timed region), compared on rank 0 with the same product of the concatenated inputs on ONE
+    GPU: reference sdmm.py:18-20 (bit-identical for any worker count) becomes "identical for
+    any GPU count".  Reports bit-exactness and rel-L2."""
+    import paper_2006_13486_b200 as ks
+    from paper_2006_13486_b200 import sharding
+    torch = B.torch
+    lay = st["layers"][li]
+    n_local = lay["n"]
+    full = sharding.gather_columns(st["dev_out"][li], n_local * B.world, lay["params"].tn)
+    res = {"layer": lay["name"], "collective": "all_gather (NCCL)", "n_gpus": B.world}
+    if B.rank == 0:
+        xs = [torch.empty_like(st["dev_in"][li]) for _ in range(B.world)]
+        xs[0].copy_(st["dev_in"][li])
+        for r in range(1, B.world):   # regenerate the other ranks' inputs from their seeds
+            rng = ks.make_rng(np.random.SeedSequence([lay["cfg"].seed, 1, r]).generate_state(1)[0])
+            xr = rng.uniform(-1.0, 1.0, size=(lay["k"], n_local)).astype(np.float32)
+            xs[r].copy_(torch.from_numpy(xr).to(xs[r].dtype))
+        x_all = torch.cat(xs, dim=1).contiguous()
+        one, _ = ks.rbgp4mm(lay["w"], x_all, lay["params"], compute=st["compute"])
+        torch.cuda.synchronize()
+        a, b = full.float(), one.float()
+        res.update(bit_exact=bool(torch.equal(full, one)),
+                   rel_l2=float(torch.linalg.norm(a - b) / torch.linalg.norm(b)),
+                   columns=int(full.shape[1]))
+        res["ok"] = res["bit_exact"] or res["rel_l2"] < 1e-6
+    B.barrier()
+    return res
+
+
+def run_conv_leg(B, args):
+    """The same eight layers as convolutions on NHWC activations (implicit im2col, no
+    materialised I): SparseConv2d with the layer's RBGP4 weight, batch `args.batch` per rank,
+    bf16, ReLU fused.  Same FLOP count as the SDMM step; L2 flushed between steps."""
+    torch = B.torch
+    from paper_2006_13486_b200 import conv as kconv
+    layers = build_layers(args.sparsity, args.batch, args.factorisation)
+    convs, xs = [], []
+    gen = torch.Generator(device=B.dev).manual_seed(11 + B.rank)
+    for lay in layers:
+        c_in = lay["k"] // 9
+        hw = 4 if lay["n"] == 16 * args.batch else 2
+        convs.append(kconv.SparseConv2d(lay["w"], 3, relu=True))
+        xs.append((torch.rand((args.batch, hw, hw, c_in), device=B.dev, generator=gen) * 2 - 1)
+                  .to(torch.bfloat16))
+    flops = sum(lay["flops"] for lay in layers)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=B.dev)  # 256 MB
+    with torch.cuda.stream(B.stream):
+        outs = [c(x) for c, x in zip(convs, xs)]  # warm-up: prepared formats, tensor maps
+        B.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=B.stream):
+            outs = [c(x) for c, x in zip(convs, xs)]
+    torch.cuda.synchronize()
+    steps = max(10, args.steps // 4)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    with torch.cuda.stream(B.stream):
+        for _ in range(args.warmup):
+            g.replay()
+        for a, b in evs:
+            flush.add_(1)
+            a.record(B.stream)
+            g.replay()
+            b.record(B.stream)
+    torch.cuda.synchronize()
+    ms = B.max_over_ranks(statistics.mean(a.elapsed_time(b) for a, b in evs))
+    act_bytes = sum(x.numel() * 2 for x in xs) + sum(o.numel() * 2 for o in outs) + \
+        sum(lay["nnz"] * 2 for lay in layers)
+    t_star = max(act_bytes / (B.peaks["hbm_gbs"][0] * 1e9), flops / (B.peaks["bf16_tflops"][0] * 1e12))
+    return {"value": flops * B.world / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+            "path": "paper_2006_13486_b200.conv.SparseConv2d (implicit im2col, NHWC bf16, ReLU fused)",
+            "hbm_bytes_per_step": act_bytes, "roofline_frac": t_star / (ms * 1e-3),
+            "l2": "256 MB overwrite between steps"}
+
+
+def run_vgg_leg(B, args):
+    """BASELINE config 5: full VGG19-CIFAR-100 RBGP4 inference (dense conv1 + classifier,
+    15 RBGP4 convs at `--sparsity`, 5 pools), synthetic global batch sharded over ranks; after
+    the timed region the logits are all-gathered and compared with one GPU's forward of a
+    slice of the global batch."""
+    torch = B.torch
+    from paper_2006_13486_b200.vgg import VGG19Sparse
+    batch = max(1, args.vgg_batch // B.world)
+    net = VGG19Sparse(sparsity=args.sparsity, num_classes=100, seed=0, device=str(B.dev))
+    gen = torch.Generator(device=B.dev).manual_seed(5 + B.rank)
+    x = torch.randn(batch, 32, 32, 3, device=B.dev, generator=gen).to(torch.bfloat16)
+    with torch.cuda.stream(B.stream):
+        net(x)
+        B.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=B.stream):
+            y = net(x)
+    torch.cuda.synchronize()
+    reps = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(B.stream):
+        for _ in range(2):
+            g.replay()
+        B.barrier()
+        a.record(B.stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(B.stream)
+    torch.cuda.synchronize()
+    ms = B.max_over_ranks(a.elapsed_time(b) / reps)
+    res = {"value": batch * B.world / (ms * 1e-3), "unit": "img/s", "ms_per_forward": ms,
+           "global_batch": batch * B.world, "sparsity": args.sparsity,
+           "sparse_tflops": net.sparse_flops_per_image * batch * B.world / (ms * 1e-3) / 1e12,
+           "model": "VGG19-CIFAR-100, RBGP4 convs 2-16 (bf16, NHWC), dense conv1 + classifier",
+           "data": "synthetic images, random-init weights"}
+    if B.world > 1:
+        logits = y.float().contiguous()
+        parts = [torch.empty_like(logits) for _ in range(B.world)]
+        B.dist.all_gather(parts, logits)
+        if B.rank == 0:
+            # rank 1's images, regenerated and run through rank 0's copy of the network
+            gen1 = torch.Generator(device=B.dev).manual_seed(5 + 1)
+            x1 = torch.randn(batch, 32, 32, 3, device=B.dev, generator=gen1).to(torch.bfloat16)
+            y1 = net(x1).float()
+            err = float(torch.linalg.norm(parts[1] - y1) / torch.linalg.norm(y1))
+            res["gather_check"] = {"collective": "all_gather (NCCL) of logits", "rank1_rel_l2": err,
+                                   "ok": err < 1e-2}
+        B.barrier()
+    del y
+    return res
+
+
+def run_wrn_leg(B, args):
+    """BASELINE config 3: WideResNet-40-4 CIFAR-10, all 39 non-first convs RBGP4 sparse,
+    synthetic batch `--wrn-batch` per rank; the bf16 tcgen05 path against the fp32 FFMA path,
+    each with its roofline (compulsory activation + weight bytes vs the binding peak)."""
+    torch = B.torch
+    from paper_2006_13486_b200.wrn import WRN40_4Sparse
+    batch = args.wrn_batch
+    net = WRN40_4Sparse(sparsity=args.sparsity, seed=0, device=str(B.dev))
+    gen = torch.Generator(device=B.dev).manual_seed(7 + B.rank)
+    x = torch.randn(batch, 32, 32, 3, device=B.dev, generator=gen)
+    flops = net.sparse_flops(batch)
+    res = {"global_batch": batch * B.world, "sparsity": args.sparsity,
+           "model": "WideResNet-40-4 CIFAR-10: dense conv1 + FC, 39 RBGP4 convs (36 3x3 + 3 1x1 shortcuts)",
+           "data": "synthetic images, random-init weights", "sparse_gflop_per_forward": flops / 1e9}
+    for compute in ("bf16", "ffma"):
+        with torch.cuda.stream(B.stream):
+            net(x, compute=compute)  # warm-up: prepared formats, tensor maps
+            reps = 3
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(B.stream)
+            for _ in range(reps):
+                net(x, compute=compute)
+            b.record(B.stream)
+        torch.cuda.synchronize()
+        ms = B.max_over_ranks(a.elapsed_time(b) / reps)
+        elt = 2 if compute == "bf16" else 4
+        nbytes = net.compulsory_bytes(batch, elt)
+        peak = B.peaks["bf16_tflops" if compute == "bf16" else "ffma_tflops"][0]
+        t_star = max(nbytes / (B.peaks["hbm_gbs"][0] * 1e9), flops / (peak * 1e12))
+        res[compute] = {"ms_per_forward": ms, "img_s": batch * B.world / (ms * 1e-3),
+                        "sparse_tflops": flops * B.world / (ms * 1e-3) / 1e12,
+                        "compulsory_bytes": nbytes, "roofline_frac": t_star / (ms * 1e-3),
+                        "bound": "hbm" if nbytes / (B.peaks["hbm_gbs"][0] * 1e9) >= flops / (peak * 1e12)
+                        else ("tensor" if compute == "bf16" else "ffma")}
+    return res
 
 
 def main():
-    args = parse_args()
-    if args.impl == "reference":
+    argv = sys.argv[1:]
+    args = parse_args(argv)
+    if maybe_spawn(args, argv):
+        return
+    if args.dist_selftest:
+        run_dist_selftest(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

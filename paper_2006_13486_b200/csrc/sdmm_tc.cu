@@ -65,6 +65,7 @@ constexpr int kBlockM = 128;
 
 struct TcParams {
     int64_t n_cols, ld_out, row_nnz;
+    int64_t ws_ld;           // split-K workspace row pitch: n_cols rounded up to 4 floats (16 B)
     int32_t tm, tk, d_o, d_t, u_i, v_i, d_i, rk, bm, bk;
     int32_t tn;              // MMA N (columns per CTA), multiple of 16, <= 256
     int32_t rows_valid;      // 128, or 64 when tm == 64 (upper half of A is zero)
@@ -476,7 +477,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             const int row = warp * 32 + lane;
             const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
             float *dst = wsp + (int64_t(kslice - 1) * (int64_t(gridDim.y) * p.rows_valid) + m0 + row) *
-                                   p.n_cols;
+                                   p.ws_ld;
             for (int c = 0; c < p.tn; c += 32) {
                 uint32_t r[32];
                 TMEM_LD_32x32b_X32(lane_base + uint32_t(c), r);
@@ -509,7 +510,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
         const int row = warp * 32 + lane;
         const bool row_ok = row < p.rows_valid;
         const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16);
-        const int64_t slice_stride = int64_t(gridDim.y) * p.rows_valid * p.n_cols;
+        const int64_t slice_stride = int64_t(gridDim.y) * p.rows_valid * p.ws_ld;
         unsigned char *stage_buf = p.pstage_bytes ? pstage : a_buf;  // idle rings unless persistent
         const uint32_t stage = smem_u32(stage_buf);
         for (int c = 0; c < p.tn; c += 32) {
@@ -521,7 +522,7 @@ tc_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUte
             if (!p.ostore && col >= p.n_cols) continue;
             const bool full = col + 32 <= p.n_cols;
             if (p.ksplit > 1 && col < p.n_cols) {
-                const float *part = wsp + (m0 + row) * p.n_cols + col;
+                const float *part = wsp + (m0 + row) * p.ws_ld + col;
                 for (int k = 1; k < p.ksplit; ++k, part += slice_stride) {
                     if (full) {
 #pragma unroll
@@ -692,6 +693,7 @@ int plan_tc(const ChainDims &c, int compute, TcPlan *out, int force_tn = 0) {
     }
     TcParams p{};
     p.n_cols = c.n_cols; p.ld_out = c.ld_out; p.row_nnz = c.row_nnz;
+    p.ws_ld = (c.n_cols + 3) & ~int64_t(3);
     p.tm = c.tm; p.tk = c.tk; p.d_o = c.d_o; p.d_t = c.d_t; p.u_i = c.u_i; p.v_i = c.v_i;
     p.d_i = c.d_i; p.rk = c.rk; p.bm = c.bm; p.bk = c.bk;
     p.rows_valid = c.tm == 64 ? 64 : kBlockM;
@@ -1094,8 +1096,8 @@ size_t tc_workspace_size(const ChainDims &c, int compute) {
         return 0;
     TcPlan pl;
     if (!plan_tc(c, compute, &pl) || pl.p.ksplit <= 1) return 0;
-    // (ksplit - 1) fp32 partial copies of the output, row-major (rows, n_cols)
-    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(c.n_cols) * 4;
+    // (ksplit - 1) fp32 partial copies of the output, row-major (rows, ws_ld)
+    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(pl.p.ws_ld) * 4;
 }
 
 int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values,
@@ -1285,7 +1287,7 @@ size_t conv_workspace_size(const ChainDims &c, const rbgp4_conv_desc *cv) {
         return 0;
     TcPlan pl;
     if (!conv_plan(c, cv, &pl) || pl.p.ksplit <= 1) return 0;
-    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(c.n_cols) * 4;
+    return size_t(pl.p.ksplit - 1) * size_t(pl.blocks_m) * pl.p.rows_valid * size_t(pl.p.ws_ld) * 4;
 }
 
 int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *values,

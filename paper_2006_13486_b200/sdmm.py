@@ -169,8 +169,15 @@ def _np_to_torch_dtype(dt):
 
 
 def rbgp4mm(w: RcubsMatrix, inp, params: TilingParams, *, compute: str = "exact",
-            out=None, out_dtype=None, device=None):
-    """O = W x I on the B200; returns (out, WorkReport) like reference `sdmm.py:235-294`."""
+            out=None, out_dtype=None, device=None, non_blocking: bool = False):
+    """O = W x I on the B200; returns (out, WorkReport) like reference `sdmm.py:235-294`.
+
+    Host operands: with a pinned CPU torch input, a pinned CPU `out` and non_blocking=True the
+    call only queues work -- the H2D copy on a per-device copy-in stream, the product on the
+    current stream, the D2H copy into `out` on a copy-out stream -- and returns at once, so
+    consecutive products overlap their copies with each other's kernels (both PCIe directions
+    and the SMs busy at the same time).  The caller synchronises (torch.cuda.synchronize()).
+    """
     if w.chain.k != 4:
         raise UnsupportedChainError(
             f"tiled multiply needs a 4-factor chain, got {w.chain.k}; "
@@ -201,10 +208,24 @@ def rbgp4mm(w: RcubsMatrix, inp, params: TilingParams, *, compute: str = "exact"
     if not is_tensor and out is None and out_dtype == t.bfloat16:
         raise InvalidArgumentError("numpy operands cannot hold a bfloat16 result; pass torch "
                                    "tensors or out_dtype=torch.float32")
+    host_out = isinstance(out, t.Tensor) and not out.is_cuda
+    if host_out and not (is_tensor and not inp.is_cuda and out.is_pinned()):
+        raise InvalidArgumentError("a host `out` must be a pinned CPU tensor, with a CPU torch input")
+    pipelined = non_blocking and host_out and inp.is_pinned()
     dev = resolve_device(device if device is not None else (inp.device if is_tensor and inp.is_cuda else None))
     with t.cuda.device(dev):
-        staged = Staged(inp, dev)
-        x = staged.tensor
+        stream = t.cuda.current_stream(dev)
+        if pipelined:
+            copy_in, copy_out = _copy_streams(dev)
+            with t.cuda.stream(copy_in):
+                x = t.empty(tuple(inp.shape), dtype=inp.dtype, device=dev)
+                x.copy_(inp, non_blocking=True)
+            stream.wait_stream(copy_in)
+            x.record_stream(stream)
+            staged = None
+        else:
+            staged = Staged(inp, dev)
+            x = staged.tensor
         if compute == "bf16":
             op_dt = t.bfloat16
             if x.dtype != t.bfloat16:
@@ -222,17 +243,41 @@ def rbgp4mm(w: RcubsMatrix, inp, params: TilingParams, *, compute: str = "exact"
             if out_dtype is not None and out_dtype != w_tdt:
                 raise InvalidArgumentError("SIMT modes return the operand dtype")
         fmt = device_format(w, dev, op_dt)
-        if out is None:
+        if out is None or host_out:
             res = t.empty((w.rows, n_cols), dtype=res_dt, device=dev)
         else:
             res = out
-            if (not isinstance(res, t.Tensor) or res.device != dev or res.dtype != res_dt
-                    or tuple(res.shape) != (w.rows, n_cols) or res.stride(1) != 1):
-                raise ShapeError(f"out must be a ({w.rows}, {n_cols}) {res_dt} tensor with unit "
-                                 f"column stride on {dev}")
+        if out is not None and (not isinstance(out, t.Tensor) or (not host_out and out.device != dev)
+                                or out.dtype != res_dt or tuple(out.shape) != (w.rows, n_cols)
+                                or out.stride(1) != 1):
+            raise ShapeError(f"out must be a ({w.rows}, {n_cols}) {res_dt} tensor with unit "
+                             f"column stride on {dev} (or pinned host memory)")
         launch_sdmm(fmt, compute, x, res, dev)
-        result = staged.give_back(res) if out is None else res
+        if host_out:
+            copy_out = _copy_streams(dev)[1]
+            copy_out.wait_stream(stream)
+            with t.cuda.stream(copy_out):
+                out.copy_(res, non_blocking=True)
+            res.record_stream(copy_out)
+            if not non_blocking:
+                copy_out.synchronize()
+            result = out
+        else:
+            result = staged.give_back(res) if out is None else res
     return result, work_report(w, n_cols, params)
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_streams(dev):
+    """(copy-in, copy-out) streams of a device for the pipelined host path (created once)."""
+    t = torch()
+    key = str(dev)
+    with _WS_LOCK:
+        if key not in _COPY_STREAMS:
+            _COPY_STREAMS[key] = (t.cuda.Stream(device=dev), t.cuda.Stream(device=dev))
+    return _COPY_STREAMS[key]
 
 
 def make_desc(fields: dict, n_cols: int, ld_in: int, ld_out: int) -> _native.Desc:
@@ -292,6 +337,14 @@ def prepared(fmt, compute: str, dev, desc):
 def launch_sdmm(fmt, compute: str, x, res, dev) -> None:
     """Queue one rbgp4_sdmm on the current stream of `dev` (no sync)."""
     lib = _native.lib()
+    if compute in ("tf32", "bf16") and x.shape[1] and (
+            x.data_ptr() % 16 or (x.stride(0) * x.element_size()) % 16):
+        # the tensor-core kernels read I by TMA: 16-byte aligned base and row pitch.  Any legal
+        # operand (e.g. N = 5 with tn = 1) is staged into a padded copy; n_cols stays N
+        per = 16 // x.element_size()
+        xp = torch().empty((x.shape[0], -(-x.shape[1] // per) * per), dtype=x.dtype, device=x.device)
+        xp[:, :x.shape[1]].copy_(x)
+        x = xp[:, :x.shape[1]]
     desc = make_desc(fmt.desc_fields, x.shape[1], x.stride(0), res.stride(0))
     code = _native.COMPUTE[compute]
     in_code, out_code = dtype_code(x.dtype), dtype_code(res.dtype)

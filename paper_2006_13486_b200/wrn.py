@@ -184,6 +184,20 @@ class WRN40_4Sparse:
         x = t.relu(x).mean(dim=(2, 3))
         return x @ self.fc.t()
 
+    def compulsory_bytes(self, batch: int, elt: int) -> float:
+        """Roofline bytes of the 39 RBGP4 convolutions: each layer reads its input activation
+        (batch * H * W * c_in) and its stored values once and writes its output once, in the
+        activation element size `elt` (implicit im2col: no 9x inflation)."""
+        total, hw = 0.0, 32
+        for conv_a, conv_b, short in self.blocks:
+            out = hw // conv_a.stride
+            for layer, h_in in ((conv_a, hw), (conv_b, out), (short, hw)):
+                if layer is not None:
+                    total += elt * (batch * h_in * h_in * layer.c_in + layer.w.nnz
+                                    + batch * out * out * layer.c_out)
+            hw = out
+        return total
+
     def sparse_flops(self, batch: int) -> float:
         """2 * nnz * output pixels over the 39 RBGP4 convolutions (the BASELINE metric)."""
         total, hw = 0.0, 32

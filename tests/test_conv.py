@@ -140,3 +140,17 @@ def test_strided_and_pointwise_conv_match_oracle(c_out, c_in, k, stride, hw, bat
     assert got.shape == ref.shape
     assert oracle.rel_l2(got, ref) < 1e-5
 
+
+
+@pytest.mark.gpu
+def test_sparse_conv_out_checked_before_launch():
+    """A caller-provided `out` on the wrong device or of an unsupported dtype is refused with
+    ShapeError before its pointer reaches the TMA-store kernel."""
+    import torch
+    chain = conv_chain(128, 128, seed=3)
+    w = ks.init_random(chain, 7, precision="f32")
+    x = torch.zeros((2, 4, 4, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ks.ShapeError):
+        conv.sparse_conv2d(w, x, 3, out=torch.empty((2, 4, 4, 128), dtype=torch.bfloat16))
+    with pytest.raises(ks.ShapeError):
+        conv.sparse_conv2d(w, x, 3, out=torch.empty((2, 4, 4, 128), dtype=torch.float16, device="cuda"))

@@ -148,3 +148,21 @@ def test_tensor_core_modes(golden, compute, tol, persistent, plan_options):
         out, _ = ks.rbgp4mm(w, inp, p, compute=compute)
         err = oracle.rel_l2(out, f64_oracle(w, inp))
         assert err <= tol, (cid, compute, err)
+
+
+@pytest.mark.parametrize("compute", ["bf16", "tf32"])
+@pytest.mark.parametrize("n_cols", [5, 13, 67])
+def test_tensor_core_modes_stage_unaligned_operands(compute, n_cols):
+    """Any legal reference operand runs on the tensor cores: N not a multiple of the 16-byte
+    TMA granule (tn = 1, reference sdmm.py:257-261 only needs N % tn == 0) is staged, not refused."""
+    import torch
+    chain, w, _ = wl.make_operands(wl.C1B)
+    inp = np.random.default_rng(n_cols).uniform(-1, 1, (w.cols, n_cols)).astype(np.float32)
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    x = torch.from_numpy(inp)
+    if compute == "bf16":
+        x = x.to(torch.bfloat16)
+    out, _ = ks.rbgp4mm(w, x.cuda(), p, compute=compute, out_dtype=torch.float32)
+    ref = f64_oracle(w, x.double().numpy())
+    assert out.shape == (w.rows, n_cols)
+    assert oracle.rel_l2(out.cpu().numpy(), ref) < 1e-2

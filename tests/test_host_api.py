@@ -168,6 +168,10 @@ class TestTilingAndErrors:
             ks.rbgp4mm(w, np.zeros((w.cols, 128), np.float32), replace(p, tm=p.tm + 1))
         with pytest.raises(ks.InvalidArgumentError):
             ks.rbgp4mm(w, np.zeros((w.cols, 128), np.float32), p, compute="fp8")
+        import torch
+        with pytest.raises(ks.InvalidArgumentError, match="bfloat16"):  # numpy cannot hold bf16
+            ks.rbgp4mm(w, np.zeros((w.cols, 128), np.float32), p, compute="bf16",
+                       out_dtype=torch.bfloat16)
 
     def test_general_chain_unsupported_by_tiled_product(self):
         chain = ks.RbgpChain((ks.complete_graph(4, 4), ks.complete_graph(2, 2)))

@@ -18,6 +18,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
+from conftest import ROOT
 import paper_2006_13486_b200 as ks
 from paper_2006_13486_b200 import sharding
 from paper_2006_13486_b200 import workloads as wl
@@ -75,3 +76,19 @@ def test_two_rank_gather_equals_single_process(tmp_path):
     # and that is the reference's own output (golden hash)
     import hashlib
     assert hashlib.sha256(got.tobytes()).hexdigest()[:16] == "9fe440861f6f8868"
+
+
+def test_bench_spawns_ranks_and_verifies_the_gather():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (torch.distributed.run
+    on 127.0.0.1); the self-test mode runs the same shard -> all-gather -> reassembly plumbing as
+    the GPU run's verification, over gloo on the CPU, and must report n_gpus 2 and a verified
+    gather."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-selftest"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert res.returncode == 0, res.stderr[-2000:]
+    line = json.loads([ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["gather_verified"] is True and line["backend"] == "gloo"

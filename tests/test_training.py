@@ -71,3 +71,16 @@ def test_autograd_trainable_layer():
     with torch.no_grad():
         layer.values -= 0.1 * layer.values.grad
     assert layer.values.shape == (w.rows, w.row_nnz)
+
+
+@pytest.mark.gpu
+def test_trainable_layer_rejects_mixed_dtypes():
+    """The kernel reads values and activations in one element type: f32 activations against
+    f64 trainable values (init_random's default) must raise, not reinterpret bytes."""
+    import torch
+    chain = wl.build_chain(CHAINS[2])
+    w = ks.init_random(chain, 2, precision="f64")
+    layer = training.TrainableSparseLinear(w, compute="ffma")
+    x = torch.randn(8, w.cols, dtype=torch.float32).cuda()
+    with pytest.raises(ks.ShapeError, match="dtype"):
+        layer(x)
