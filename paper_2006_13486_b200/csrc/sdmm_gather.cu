@@ -662,6 +662,8 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
     const int kk_n = p.bk / 16;
     const int n_mma = p.u_i * p.d_i * kk_n;
     const int u_o = p.u_o;
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 0);
+    cta_stamp(DBG(p.debug), 0, int(blockIdx.x));
 
     if (warp == 4 && lane == 0) {
         for (int i = 0; i < p.ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -692,6 +694,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
     tc_fence_after();
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const uint32_t tmem_d = *tmem_slot;
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 1);
 
     if (warp == 4) {
         // ================= producer: I slab + W tile of every step of every tile =================
@@ -725,6 +728,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                         tma_load_2d(dst + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * p.w_rows);
                     else
                         tma_load_2d(dst + p.i_bytes, &wmap, &full[st], j * p.d_t, tbm * p.tm);
+                    gtrace(DBG(p.debug), 0, int(g));
                 }
                 __syncwarp();
             }
@@ -757,6 +761,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                 mbar_wait(&full[st], uint32_t((g / p.ns) & 1));
                 tc_fence_after();
                 if (elect_one()) {
+                    gtrace(DBG(p.debug), 1, int(g));
                     const uint32_t st16 = uint32_t(st * stage_bytes) >> 4;
                     const uint64_t a_st = a_desc0 + st16, b_st = b_desc0 + st16;
                     if constexpr (MMA_N == 32) {
@@ -789,6 +794,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
                     }
                     tc_commit(&empty[st]);
                     if (s == p.d_o - 1) tc_commit(&acc_full[b]);
+                    gtrace(DBG(p.debug), 2, int(g));
                 }
                 __syncwarp();
             }
@@ -805,6 +811,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             if (DBG(p.debug) & 4096) mbar_wait_sleep(&acc_full[b], uint32_t((it >> 1) & 1), 64);
             else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
             tc_fence_after();
+            if (threadIdx.x == 0 && it < 4) gtrace(DBG(p.debug), 3, int(2 + 2 * it));
             const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * acc_cols);
             const int64_t col = n0 + t;
             const bool ok = col < p.n_cols;
@@ -868,6 +875,7 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
             }
             tc_fence_before();
             __syncwarp();
+            if (threadIdx.x == 0 && it < 4) gtrace(DBG(p.debug), 3, int(3 + 2 * it));
             if (lane == 0) mbar_arrive(&acc_empty[b]);
         }
     }
@@ -877,6 +885,8 @@ gather_persistent_kernel(const __grid_constant__ CUtensorMap imap, const __grid_
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(uint32_t(p.tmem_cols)));
     }
+    if (threadIdx.x == 0) gtrace(DBG(p.debug), 3, 11);
+    cta_stamp(DBG(p.debug), 1, int(blockIdx.x));
 }
 
 constexpr size_t kGSmemCap = 227 * 1024;
