@@ -69,6 +69,8 @@ struct Options {
     int32_t i3d = 1;          // K2 3-D I boxes
     int32_t promo = -1;       // K2 I-map L2 promotion bytes: -1 auto (256), 0 / 64 / 128 / 256
     int32_t conv_wide = 1;    // K2 conv: 256-pixel tiles for many-wave grids
+    int32_t stream = -1;      // K5 (sdmm_stream.cu) for the TC16 SDMM: -1 auto, 0 off (K4)
+    int32_t stream_g = 0;     // K5 row blocks per unit: 0 auto, else 1 / 2 / 4 / 8 (whole tiles)
     int32_t debug = 0;        // trace / ablation bits (debug builds only)
 };
 Options &opts();
@@ -116,6 +118,16 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
                        const int32_t *adj_o, const int32_t *adj_i, const int32_t *sched, const int32_t *pair,
                        const void *k4, const void *x, void *out, cudaStream_t stream);
 size_t gather_prep_bytes(const ChainDims &c);
+void gather_prep_views(const ChainDims &c, const void *k4, const int32_t **cols, const void **vals);
+
+// K5: streamed TC16 SDMM (sdmm_stream.cu); `k5` = its prepared tables (step words, row groups)
+int stream_shape_ok(const ChainDims &c);
+size_t stream_prep_bytes(const ChainDims &c);
+int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
+                   const int32_t *adj_i_host, void *k5, cudaStream_t stream);
+int stream_supported(const ChainDims &c, int out_dtype);
+int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void *k5, const void *inp, void *out,
+                  cudaStream_t stream);
 int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_host, void *k4,
                    cudaStream_t stream);
 

@@ -33,6 +33,7 @@ constexpr OptionSlot kOptionSlots[] = {
     {"wswz", &Options::wswz, 0, 1},              {"ostore", &Options::ostore, 0, 1},
     {"sched", &Options::sched, 0, 1},            {"i3d", &Options::i3d, 0, 1},
     {"promo", &Options::promo, -1, 256},         {"conv_wide", &Options::conv_wide, 0, 1},
+    {"stream", &Options::stream, -1, 0},         {"stream_g", &Options::stream_g, 0, 8},
     {"debug", &Options::debug, 0, 1 << 30},
 };
 const OptionSlot *find_option(const char *name) {

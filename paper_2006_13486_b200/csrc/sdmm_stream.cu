@@ -1,0 +1,860 @@
+// sdmm_stream.cu -- K5: the RBGP4 SDMM streamed through tcgen05 at the HBM rate.
+//
+// Replaces kronsparse.sdmm._tile_worker (reference sdmm.py:148-205) for compute="bf16" on
+// the tensor-core factorisation with 16 x 16 dense element blocks (g_r = (1,1), g_i (8,8) of
+// degree 2, g_b = (16,16): SURVEY §8(d) "TC16"), the shape the VGG19 512-channel layers, the
+// bench headline and the config-4 sweep run.  Same transposed product as K4
+// (sdmm_gather.cu) per output tile (tile-row tbm, 128 batch columns n0..):
+//     D^T (128 x rows) += I^T (128 x 16) * W^T (16 x rows)   per g_i column block,
+// M = 128 batch columns (MN-major I, as TMA lands it), the gather being the A descriptor's
+// start address.  K5 changes everything around the MMAs, from B200 measurements
+// (tools/stream_bench.cu, tools/epi_bench.cu, tools/tma_issue_bench.cu):
+//
+// * TMA issue is the producer's cost, not bandwidth: one thread spends ~265-310 cycles per
+//   3-D box and ~140-155 per 2-D box whatever its size.  So the loads of a step are spread
+//   over THREE producer warps, and a step is as few boxes as possible (whole tiles: one I
+//   slab + one W tile; row groups: the group's W rows are ONE box of a row-permuted copy).
+// * Setup.  K4 spent ~6k cycles before its first I request.  Here the W producer requests
+//   the W tiles of the first ring's worth of steps before griddepcontrol.wait (weights are
+//   never the previous grid's output); the I producers wait only for the barrier init.
+// * Work units.  Many tiles: whole tiles (the K4 TC16 relayout: 8 MMAs of N = 32 per step)
+//   in a persistent loop.  Few tiles (small N): ROW GROUPS -- a unit owns G row blocks of a
+//   tile and loads only the 16-row pieces of each slab those row blocks read (the union of
+//   their g_i neighbours), so the grid fills the SMs with NO split-K partial exchange (DSMEM
+//   measured 15 B/clk per SM).
+// * Epilogue.  Each epilogue warp owns 32 batch columns: it packs column pairs into 32-bit
+//   words with one shuffle (sub-word shared stores from different lanes measured ~60 cycles
+//   each), and stores its own rows: direct global stores under the next unit's main loop, or
+//   -- for a CTA's last unit, the only exposed one -- staging in the then idle ring and its
+//   own TMA tensor store (no cross-warp barrier).
+//
+// Warps (256 threads): 0-3 epilogue (TMEM lane = batch column), 4 / 7 I producers, 6 W
+// producer (+ I pieces), 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
+// output rows; fixed step order.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <vector>
+
+namespace rbgp4 {
+namespace {
+
+constexpr int kSBatch = 128;                  // MMA M: batch columns per unit
+constexpr int kMaxDo = 64;                    // steps per tile-row held in producer registers
+constexpr int kRgWords = 48;                  // one row-group record (int32 words)
+constexpr int kMaxRg = 8;                     // row groups per tile (G = 1)
+constexpr int kPieceBytes = 16 * kSBatch * 2; // one slab piece: 16 rows x 128 batch columns, bf16
+// record: [0] first g_i column block `lo` of the group's range, [1] range length L (the
+// group's row blocks read column blocks lo .. lo+L-1 only), [17 + r * d_i + ink] piece (column
+// block - lo) read by MMA (r, ink), [33 + r] output row block of the group's r-th row block
+constexpr int kRgLo = 0, kRgLen = 1, kRgMma = 17, kRgRows = 33;
+
+// row groups: one I tensor map per range length L = 1..8 (box = 16 L slab rows x 128 columns)
+struct IMaps {
+    CUtensorMap m[8];
+};
+
+#if RBGP4_DEBUG
+// debug builds (option debug bit 512): per-CTA %globaltimer at entry / exit, CTA-0 marks and
+// per-step trace (clock64 from entry)
+constexpr int kK5Stamps = 4096;
+__device__ unsigned long long g_k5_stamp[2][kK5Stamps];
+__device__ unsigned long long g_k5_mark[16];
+// bit 2048: launch slots (host counter mod 16) -- every CTA's entry / exit %globaltimer and CTA 0's
+// marks [first I issued, first full, last accumulator ready, last stores issued], for a whole
+// graph of launches (tools/step_timeline.py)
+__device__ unsigned long long g_k5_seq[16][2][160];
+__device__ unsigned long long g_k5_smark[16][4];
+__device__ unsigned long long g_k5_trace[3][64];  // [0] I producer issued, [1] MMA saw full, [2] MMAs issued
+__device__ unsigned long long g_k5_epi[16];       // CTA 0 warp 0, last unit: after each epilogue step
+__device__ __forceinline__ unsigned long long k5_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define K5_SMARK(i) do { if (p.slot >= 0 && blockIdx.x == 0) g_k5_smark[p.slot][i] = k5_gtimer(); } while (0)
+#else
+#define K5_SMARK(i) do { } while (0)
+#endif
+
+struct SParams {
+    int64_t n_cols, ld_out, n_units;
+    int32_t u_o, d_o, tm, tk, u_i, d_i, d_t;
+    int32_t ns, stage_bytes, i_bytes;  // ring stages; bytes per stage; I part of a stage
+    int32_t wres_bytes, ring_bytes;    // row groups: resident W of a unit; ring size
+    int32_t g, n_rg;                   // row-group mode: row blocks per unit, groups per tile
+    int32_t acc_cols, tmem_cols;       // TMEM columns per accumulator buffer / allocated
+    const int32_t *steps;              // [tbm][s] = adjacency slot j << 16 | K-block
+    const int32_t *cols;               // whole tiles: TMEM column of row block ui's ink-th partial
+    const int32_t *rg;                 // row groups: n_rg records of kRgWords
+    int32_t debug, slot;
+};
+
+__device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src) : "memory");
+}
+
+template <bool OUT_BF16, bool RG>
+__global__ void __launch_bounds__(256, 1)
+stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
+              const __grid_constant__ CUtensorMap omap, const __grid_constant__ IMaps imaps, const SParams p,
+              void *__restrict__ out) {
+    extern __shared__ unsigned char smem_raw[];
+    __shared__ int32_t s_rg[RG ? kMaxRg * kRgWords : 1];
+    __shared__ int32_t s_cols[RG ? 1 : 64];
+    // 1024-byte aligned ring (swizzle atoms); pointer arithmetic on smem_raw keeps the shared
+    // address space visible to the compiler (plain C++ stores to the staging area stay STS)
+    unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    // [barriers, 1 KB][row groups: the unit's resident W][ring]
+    uint64_t *full = reinterpret_cast<uint64_t *>(base);
+    uint64_t *empty = full + 16;
+    uint64_t *acc_full = empty + 16;     // [2] last MMA of a unit committed
+    uint64_t *acc_empty = acc_full + 2;  // [2] the epilogue has read the buffer
+    uint64_t *wfull = acc_empty + 2;     // row groups: the unit's W landed
+    uint64_t *wempty = wfull + 1;        // row groups: the unit's MMAs are done with W
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wempty + 1);
+    unsigned char *wres = base + 1024;   // row groups: d_o steps x G*16 rows x d_t slots
+    unsigned char *ring = wres + p.wres_bytes;
+    // ring geometry: whole tiles -- planned on the host; row groups -- a stage holds the
+    // longest column-block range among the groups (the records), so typical ranges (~4 of 8
+    // pieces) get twice the stages of a worst-case ring.  Every warp derives the same values.
+    int NS = p.ns, SB = p.stage_bytes;
+    if constexpr (RG) {
+        int l = threadIdx.x % 32 < p.n_rg ? __ldg(p.rg + (threadIdx.x % 32) * kRgWords + kRgLen) : 1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+        SB = l * kPieceBytes;
+        NS = min(16, p.ring_bytes / SB);
+    }
+    constexpr int kThreads = 256;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int upt = RG ? p.n_rg : 1;  // units per tile
+#if RBGP4_DEBUG
+    const unsigned long long c_entry = clock64();
+    const bool trace = (p.debug & 512) && blockIdx.x == 0;
+    if ((p.debug & 512) && threadIdx.x == 0 && blockIdx.x < kK5Stamps) g_k5_stamp[0][blockIdx.x] = k5_gtimer();
+    if (p.slot >= 0 && threadIdx.x == 0 && blockIdx.x < 160) g_k5_seq[p.slot][0][blockIdx.x] = k5_gtimer();
+#define K5_MARK(i) do { if (trace) g_k5_mark[i] = clock64() - c_entry; } while (0)
+#else
+#define K5_MARK(i) do { } while (0)
+#endif
+
+    if (warp == 7) {
+        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");  // idle
+    } else if (warp == 4 || warp == 6) {
+        // ========================== TMA producers ==========================
+        // warp 6: expect_tx + the W box of every step (before griddepcontrol.wait for the first
+        // ring's worth: weights are never the previous grid's output); warp 4: barrier init, then
+        // after griddepcontrol.wait the I box of every step -- a whole slab, or (row groups) the
+        // 16 L rows of the group's column-block range.  Two boxes per step: a TMA box costs its
+        // engine ~150-300 cycles whatever its size (tools/tma_issue_bench.cu).
+        const bool wprod = warp == 6;
+        // lane l holds the step words l and l + 32 of the current tile-row (shuffled out)
+        int32_t e0 = 0, e1 = 0, rl = 0;
+        auto load_steps = [&](int tbm) {
+            const int32_t *row = p.steps + int64_t(tbm) * p.d_o;
+            e0 = lane < p.d_o ? __ldg(row + lane) : 0;
+            e1 = lane + 32 < p.d_o ? __ldg(row + lane + 32) : 0;
+        };
+        // row groups: lanes 0 / 1 hold the record's lo / L
+        auto load_rec = [&](int rgi) { rl = lane < 2 ? __ldg(p.rg + rgi * kRgWords + lane) : 0; };
+        int tbm_cur = int((first / upt) % p.u_o);
+        int rg_cur = RG ? int(first % p.n_rg) : 0;
+        load_steps(tbm_cur);
+        if (RG) load_rec(rg_cur);
+        if (!wprod && lane == 0) {
+            for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+            for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+            mbar_init(wfull, 1);
+            mbar_init(wempty, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(wprod ? &wmap : &imap)) : "memory");
+        }
+        __syncwarp();
+        // barrier 3 (warps 4 and 6): the barrier init is visible to the W producer; barrier 1
+        // (setup, all warps): arrive only -- producers never wait for TMEM or the tables
+        if (!wprod) asm volatile("bar.arrive 3, 64;" ::: "memory");
+        else asm volatile("bar.sync 3, 64;" ::: "memory");
+        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        auto step_word = [&](int s) -> int32_t {
+            const int32_t a = __shfl_sync(0xffffffffu, e0, s & 31);
+            const int32_t b = __shfl_sync(0xffffffffu, e1, s & 31);
+            return s < 32 ? a : b;
+        };
+        const int w_rows = p.tm * p.d_i;  // whole tiles: relayout W tile of a step
+        // whole tiles: expect_tx (I slab + W tile) and the W box of a step, by warp 6
+        auto issue_w = [&](int st, int tbm, int32_t word) {
+            const int j = word >> 16;
+            if (elect_one()) {
+                mbar_expect_tx(&full[st], uint32_t(SB));
+                tma_load_2d(ring + size_t(st) * SB + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * w_rows);
+            }
+            __syncwarp();
+        };
+        // row groups: the unit's whole W (group rgi's rows of the d_o tiles (tbm, j)), one 3-D box
+        auto issue_wres = [&](int tbm, int rgi, int64_t it) {
+            mbar_wait(wempty, uint32_t(it & 1) ^ 1u);
+            if (elect_one()) {
+                mbar_expect_tx(wfull, uint32_t(p.wres_bytes));
+                tma_load_3d(wres, &wmap, wfull, 0, rgi * p.g * 16, tbm * p.d_o);
+            }
+            __syncwarp();
+        };
+        const int pre = min(NS, p.d_o);
+        if (wprod && first < p.n_units) {
+            if constexpr (RG) issue_wres(tbm_cur, rg_cur, 0);
+            else for (int s = 0; s < pre; ++s) issue_w(s, tbm_cur, step_word(s));
+            K5_MARK(0);
+        }
+        if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");
+        int64_t g = 0, it = 0;
+        int rs_st = 0;
+        uint32_t rs_ph = 0;
+        for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+            const int64_t tile = u / upt;
+            const int tbm = int(tile % p.u_o);
+            const int rgi = RG ? int(u % p.n_rg) : 0;
+            const int64_t n0 = (tile / p.u_o) * kSBatch;
+            if (tbm != tbm_cur) { load_steps(tbm); tbm_cur = tbm; }
+            if (RG && rgi != rg_cur) { load_rec(rgi); rg_cur = rgi; }
+            const int lo = RG ? __shfl_sync(0xffffffffu, rl, kRgLo) : 0;
+            const int len = RG ? __shfl_sync(0xffffffffu, rl, kRgLen) : 8;
+            if (RG && wprod) {
+                if (it > 0) issue_wres(tbm, rgi, it);
+                continue;  // row groups: W is resident, warp 6 has nothing per step
+            }
+            for (int s = 0; s < p.d_o; ++s, ++g) {
+                // ring position by increments (a 64-bit g % NS is a software division per step)
+                const int st = rs_st;
+                const uint32_t ph = rs_ph;
+                if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
+                const int32_t word = step_word(s);
+                if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
+                if (wprod) {
+                    if (g >= pre) issue_w(st, tbm, word);
+                } else {
+                    const int32_t krow = (word & 0xFFFF) * p.tk;
+                    if (elect_one()) {
+                        if constexpr (RG) {
+                            mbar_expect_tx(&full[st], uint32_t(len * kPieceBytes));
+                            tma_load_3d(ring + size_t(st) * SB, &imaps.m[len - 1], &full[st], 0,
+                                        krow + lo * 16, int32_t(n0 / 64));
+                        } else {
+                            tma_load_3d(ring + size_t(st) * SB, &imap, &full[st], 0, krow, int32_t(n0 / 64));
+                        }
+                    }
+                    __syncwarp();
+#if RBGP4_DEBUG
+                    if (trace && lane == 0 && g < 64) g_k5_trace[0][g] = clock64() - c_entry;
+#endif
+                    if (g == 0 && lane == 0) { K5_MARK(1); K5_SMARK(0); }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ========================= TMEM allocation + MMA issue =========================
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        tc_fence_after();
+        const uint32_t tmem_d = *tmem_slot;
+        constexpr uint32_t kN = RG ? 16u : 32u;
+        // D f32, A/B bf16, A MN-major (I slab), B K-major (W rows), N, M = 128
+        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (0u << 16) |
+                                   ((kN >> 3) << 17) | (uint32_t(kSBatch >> 4) << 24);
+        const uint32_t ring_a = smem_u32(ring);
+        // A: MN-major, 128B swizzle: 64-column atoms spaced by the rows staged per atom (a
+        // whole slab, or one 16-row piece), 8-row groups 1024 B apart
+        const uint64_t a_desc_t = smem_desc(ring_a, uint32_t(p.tk) * 128u, 1024, 2u);
+        // B: K-major W rows (row groups: d_t slots per row; whole tiles: 16-slot relayout rows)
+        const uint32_t w_row = RG ? uint32_t(p.d_t * 2) : 32u;
+        const uint64_t b_desc0 = RG ? smem_desc(smem_u32(wres), 0, 8 * w_row, swizzle_layout_code(int(w_row)))
+                                    : smem_desc(ring_a + uint32_t(p.i_bytes), 0, 8 * w_row, swizzle_layout_code(int(w_row)));
+        // row groups: the adjacency slot j of each step picks the step's W in the resident copy
+        int32_t e0 = 0, e1 = 0;
+        int tbm_cur = -1;
+        int64_t g = 0, it = 0;
+        int rs_st = 0;
+        uint32_t rs_ph = 0;
+        for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+            const int b = int(it & 1);
+            const int32_t *rec = RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr;
+            // row groups: the staged range holds L pieces of 16 rows per 64-column atom
+            const uint64_t a_desc0 = RG ? smem_desc(ring_a, uint32_t(rec[kRgLen]) * 2048u, 1024, 2u) : a_desc_t;
+            if constexpr (RG) {
+                const int tbm = int((u / upt) % p.u_o);
+                if (tbm != tbm_cur) {
+                    const int32_t *row = p.steps + int64_t(tbm) * p.d_o;
+                    e0 = lane < p.d_o ? __ldg(row + lane) : 0;
+                    e1 = lane + 32 < p.d_o ? __ldg(row + lane + 32) : 0;
+                    tbm_cur = tbm;
+                }
+                mbar_wait(wfull, uint32_t(it & 1));
+            }
+            mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
+            tc_fence_after();
+            const uint32_t d_base = tmem_d + uint32_t(b * p.acc_cols);
+            for (int s = 0; s < p.d_o; ++s, ++g) {
+                const int st = rs_st;
+                const uint32_t ph = rs_ph;
+                if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
+                int32_t wj = 0;
+                if constexpr (RG) {
+                    const int32_t a = __shfl_sync(0xffffffffu, e0, s & 31), bb = __shfl_sync(0xffffffffu, e1, s & 31);
+                    wj = (s < 32 ? a : bb) >> 16;
+                }
+                mbar_wait(&full[st], ph);
+                tc_fence_after();
+#if RBGP4_DEBUG
+                if (trace && lane == 0 && g < 64) g_k5_trace[1][g] = clock64() - c_entry;
+#endif
+                if (g == 0 && lane == 0) { K5_MARK(2); K5_SMARK(1); }
+                if (elect_one()) {
+                    const uint32_t st16 = uint32_t(st * SB) >> 4;
+                    const uint64_t a_st = a_desc0 + st16;
+                    const uint64_t b_st = RG ? b_desc0 + uint32_t((wj * p.g * 16 * int(w_row)) >> 4) : b_desc0 + st16;
+                    if constexpr (RG) {
+                        for (int r = 0; r < p.g; ++r)
+#pragma unroll
+                            for (int ink = 0; ink < 2; ++ink) {
+                                const uint32_t piece = uint32_t(rec[kRgMma + r * 2 + ink]);
+                                tc_mma<false>(d_base + uint32_t(r * 16), a_st + piece * uint32_t(2048 >> 4),
+                                              b_st + uint32_t(r * ((16 * w_row) >> 4) + ink * 2), idesc,
+                                              (s > 0 || ink > 0) ? 1u : 0u);
+                            }
+                    } else {
+                        // TC16 relayout: 8 column blocks of 16 slab rows, one N = 32 MMA each
+                        const uint32_t acc = s > 0 ? 1u : 0u;
+#pragma unroll
+                        for (int kb = 0; kb < 8; ++kb)
+                            tc_mma<false>(d_base + uint32_t(kb * 32), a_st + uint32_t(kb * 16 * 8),
+                                          b_st + uint32_t(kb * ((32 * 32) >> 4)), idesc, acc);
+                    }
+                    tc_commit(&empty[st]);
+                    if (s == p.d_o - 1) {
+                        tc_commit(&acc_full[b]);
+                        if (RG) tc_commit(wempty);
+                    }
+#if RBGP4_DEBUG
+                    if (trace && g < 64) g_k5_trace[2][g] = clock64() - c_entry;
+#endif
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        // ============================ epilogue (warps 0-3) ============================
+        if constexpr (RG) {
+            for (int i = threadIdx.x; i < p.n_rg * kRgWords; i += 128) s_rg[i] = p.rg[i];
+        } else {
+            for (int i = threadIdx.x; i < p.u_i * p.d_i; i += 128) s_cols[i] = p.cols[i];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        tc_fence_after();
+        const uint32_t tmem_d = *tmem_slot;
+        // this warp's 32 batch columns; staged rows of 64 B (bf16) / 128 B (f32)
+        constexpr int kRowBytes = OUT_BF16 ? 64 : 128;
+        const int nrows = RG ? p.g * 16 : p.tm;
+        unsigned char *wstage_p = ring + warp * nrows * kRowBytes;
+        const uint32_t wstage = smem_u32(wstage_p);
+        // bf16: lane pair (2k, 2k+1) stores columns 2k, 2k+1 of row m (even lane) / m+1 (odd)
+        const int k2 = lane >> 1, odd = lane & 1;
+        int64_t it = 0;
+        for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+            const int b = int(it & 1);
+            const int64_t tile = u / upt;
+            const int32_t *rec = RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr;
+            const int tbm = int(tile % p.u_o);
+            const int64_t n0 = (tile / p.u_o) * kSBatch;
+            const int64_t m0 = int64_t(tbm) * p.tm;
+            const bool last = u + stride >= p.n_units;
+            const int64_t c0 = n0 + warp * 32;  // this warp's first column
+            const bool ok = c0 < p.n_cols;      // n_cols % 64 == 0: a warp's 32 columns are all in or out
+            mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
+            tc_fence_after();
+            if (last && threadIdx.x == 0) { K5_MARK(3); K5_SMARK(2); }
+            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * p.acc_cols);
+            // 16 fp32 rows (row block rb, staging slot rs) of this lane's column -> bf16 pairs
+            // packed across the lane pair / f32 as is; staged (last unit) or stored directly.
+            // Kept compact (a loop over row blocks, not unrolled): the epilogue runs once per
+            // unit, cold in the instruction cache.
+            auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two) {
+                const int64_t grow0 = m0 + int64_t(rb) * 16;
+                if constexpr (OUT_BF16) {
+                    // all 8 shuffles first, then the stores (plain C++ stores: a volatile asm store
+                    // with a memory clobber serialised every pair behind its shuffle, ~90 cycles each)
+                    uint32_t words[8];
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+                        const int m = 2 * h;
+                        const float x0 = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
+                        const float x1 = __uint_as_float(va[m + 1]) + (two ? __uint_as_float(vb[m + 1]) : 0.0f);
+                        // even lane sends row m+1, odd lane row m; each gets its pair's other column
+                        const float recv = __shfl_xor_sync(0xffffffffu, odd ? x0 : x1, 1);
+                        const __nv_bfloat162 v2 = odd ? __floats2bfloat162_rn(recv, x1) : __floats2bfloat162_rn(x0, recv);
+                        words[h] = *reinterpret_cast<const uint32_t *>(&v2);
+                    }
+                    if (last) {
+                        // [row][64 B], 64B swizzle: 16-byte chunk ^ (row / 2) % 4 (row = m + odd)
+                        unsigned char *sb = wstage_p + rs * 16 * 64 + (k2 & 3) * 4 + odd * 64;
+#pragma unroll
+                        for (int h = 0; h < 8; ++h)
+                            *reinterpret_cast<uint32_t *>(sb + h * 128 + ((((k2 >> 2) ^ (h & 3))) << 4)) = words[h];
+                    } else if (ok) {
+                        uint32_t *gbase = reinterpret_cast<uint32_t *>(static_cast<__nv_bfloat16 *>(out) +
+                                                                      (grow0 + odd) * p.ld_out + c0 + 2 * k2);
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) gbase[int64_t(2 * h) * (p.ld_out / 2)] = words[h];
+                    }
+                } else {
+                    float x[16];
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
+                    if (last) {
+                        // [row][128 B], 128B swizzle: chunk ^ row % 8
+                        unsigned char *sb = wstage_p + rs * 16 * 128 + (lane & 3) * 4;
+#pragma unroll
+                        for (int m = 0; m < 16; ++m)
+                            *reinterpret_cast<float *>(sb + m * 128 + ((((lane >> 2) ^ (m & 7))) << 4)) = x[m];
+                    } else if (ok) {
+                        float *gbase = static_cast<float *>(out) + grow0 * p.ld_out + c0 + lane;
+#pragma unroll
+                        for (int m = 0; m < 16; ++m) gbase[int64_t(m) * p.ld_out] = x[m];
+                    }
+                }
+            };
+            // row block i's TMEM columns: row groups -> column 16 i (one partial); whole tiles ->
+            // its two d_i partials s_cols[2 i], s_cols[2 i + 1] (TC16 relayout)
+            const int nrb = RG ? p.g : p.u_i;
+            auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16]) {
+                if constexpr (RG) {
+                    TMEM_LD_32x32b_X16(lane_base + uint32_t(i * 16), va);
+                } else {
+                    TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[2 * i]), va);
+                    TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[2 * i + 1]), vb);
+                }
+            };
+            // software pipeline over row blocks: row block i+1's TMEM loads are in flight while
+            // row block i is converted and stored (tcgen05.wait::ld waits for all of them)
+            uint32_t a0[16], b0[16], a1[16], b1[16];
+#if RBGP4_DEBUG
+#define K5_EPI(i) do { if (trace && last && threadIdx.x == 0 && (i) < 16) g_k5_epi[i] = clock64() - c_entry; } while (0)
+#else
+#define K5_EPI(i) do { } while (0)
+#endif
+            tload(0, a0, b0);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            K5_EPI(0);
+#pragma unroll 1
+            for (int i = 0; i < nrb; i += 2) {
+                if (i + 1 < nrb) tload(i + 1, a1, b1);
+                put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG);
+                K5_EPI(1 + 2 * i);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                K5_EPI(2 + 2 * i);
+                if (i + 1 >= nrb) break;
+                if (i + 2 < nrb) tload(i + 2, a0, b0);
+                put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG);
+                K5_EPI(3 + 2 * i);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                K5_EPI(4 + 2 * i);
+            }
+#undef K5_EPI
+            // all TMEM reads of this buffer are done: the MMA warp may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+            if (last) {
+                // the ring is idle (this CTA's last MMA has completed): this warp's rows go out
+                // by its own TMA stores (boxes of 32 columns x 16 rows (groups) / x tm rows)
+                fence_async_smem();
+                __syncwarp();
+                if (threadIdx.x == 0) K5_MARK(11);
+                if (ok && elect_one()) {
+                    if constexpr (RG) {
+                        for (int r = 0; r < p.g; ++r)
+                            tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0),
+                                           int32_t(m0) + rec[kRgRows + r] * 16);
+                    } else {
+                        tma_store_2d_g(&omap, wstage, int32_t(c0), int32_t(m0));
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    if (warp == 0) { K5_MARK(4); K5_SMARK(3); }
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                }
+                __syncwarp();
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tmem_slot),
+                     "r"(uint32_t(p.tmem_cols)));
+    }
+#if RBGP4_DEBUG
+    if (threadIdx.x == 0) K5_MARK(5);
+    if ((p.debug & 512) && threadIdx.x == 0 && blockIdx.x < kK5Stamps) g_k5_stamp[1][blockIdx.x] = k5_gtimer();
+    if (p.slot >= 0 && threadIdx.x == 0 && blockIdx.x < 160) g_k5_seq[p.slot][1][blockIdx.x] = k5_gtimer();
+#endif
+#undef K5_MARK
+#undef K5_SMARK
+}
+
+// row-permuted copy of the values for the row-group mode: tile (tbm, j) of W (tm rows x d_t
+// slots, sorted-column order, reference rcubs.py:79-98) with its row blocks in group order
+// perm[k] -- the same bytes, so a group's rows of a step are one contiguous box
+__global__ void rg_values_kernel(const __nv_bfloat16 *__restrict__ values, int64_t row_nnz, int tm, int d_t,
+                                 int d_o, const int32_t *__restrict__ perm, int64_t total,
+                                 __nv_bfloat16 *__restrict__ outv) {
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int slot = int(idx % d_t);
+        const int64_t row = idx / d_t;  // row of the permuted copy: ((tbm * d_o + j) * tm + k * 16 + m)
+        const int m = int(row % 16), k = int((row / 16) % (tm / 16));
+        const int64_t tj = row / tm;
+        const int64_t tbm = tj / d_o, j = tj % d_o;
+        outv[idx] = values[(tbm * tm + perm[k] * 16 + m) * row_nnz + j * d_t + slot];
+    }
+}
+
+// K5 section of the prepared buffer: [steps i32 u_o x d_o][records: G = 1, 2, 4][perm i32 8]
+// [row-permuted values bf16 (rows x row_nnz)]
+int rg_groups(int g) { return 8 / g; }
+size_t rg_offset_words(int g) { return g == 1 ? 0 : g == 2 ? size_t(8) * kRgWords : size_t(12) * kRgWords; }
+size_t a16w(size_t words) { return (words + 3) & ~size_t(3); }
+size_t tables_words(const ChainDims &c) { return a16w(size_t(c.u_o) * c.d_o) + a16w(size_t(14) * kRgWords + 8); }
+
+}  // namespace
+
+// TC16 shape (the one K5 covers): g_r (1,1), 16 x 16 element blocks, g_i (8,8) of degree 2
+// (its relayout exists, sdmm_gather.cu), 128 x 128 tiles, at most 64 steps per tile-row.
+int stream_shape_ok(const ChainDims &c) {
+    return c.rm == 1 && c.rk == 1 && c.bm == 16 && c.bk == 16 && c.u_i == 8 && c.v_i == 8 && c.d_i == 2 &&
+           c.tm == 128 && c.tk == 128 && c.d_t == 32 && c.d_o <= kMaxDo && c.v_o < (1 << 16) &&
+           gather_relayout_ok(c);
+}
+
+size_t stream_prep_bytes(const ChainDims &c) {
+    if (!stream_shape_ok(c)) return 0;
+    return 4 * tables_words(c) + size_t(c.rows) * c.row_nnz * 2;
+}
+
+int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
+                   const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
+    const size_t n_steps = size_t(c.u_o) * c.d_o;
+    std::vector<int32_t> tab(tables_words(c), 0);
+    for (int u = 0; u < c.u_o; ++u)
+        for (int s = 0; s < c.d_o; ++s) {
+            const int j = sched_host ? sched_host[size_t(u) * c.d_o + s] : s;
+            tab[size_t(u) * c.d_o + s] = (j << 16) | adj_o_host[size_t(u) * c.d_o + j];
+        }
+    // Row-block order for the row groups: a unit of G row blocks loads the contiguous range of
+    // g_i column blocks its row blocks read (one TMA box per step), so the pairs (G = 2) are the
+    // perfect matching of the 8 row blocks with the smallest total range (all 105 matchings
+    // tried), the quads (G = 4) the best pairing of those pairs; every group is a run of `perm`.
+    auto nb = [&](int r, int ink) { return adj_i_host[r * c.d_i + ink]; };
+    auto range_of = [&](const std::vector<int> &rows, int *lo) {
+        int a = c.v_i, b = -1;
+        for (int r : rows)
+            for (int ink = 0; ink < c.d_i; ++ink) { a = std::min(a, nb(r, ink)); b = std::max(b, nb(r, ink)); }
+        if (lo) *lo = a;
+        return b - a + 1;
+    };
+    std::vector<std::pair<int, int>> best_pairs, cur;
+    int best_cost = 1 << 30;
+    std::vector<char> used(c.u_i, 0);
+    std::function<void(int)> match = [&](int cost) {
+        int a = 0;
+        while (a < c.u_i && used[a]) ++a;
+        if (a == c.u_i) {
+            if (cost < best_cost) { best_cost = cost; best_pairs = cur; }
+            return;
+        }
+        used[a] = 1;
+        for (int b = a + 1; b < c.u_i; ++b) {
+            if (used[b]) continue;
+            used[b] = 1;
+            cur.push_back({a, b});
+            match(cost + range_of({a, b}, nullptr));
+            cur.pop_back();
+            used[b] = 0;
+        }
+        used[a] = 0;
+    };
+    match(0);
+    // pairs of pairs: 3 ways to split 4 pairs into 2 quads
+    const int split[3][4] = {{0, 1, 2, 3}, {0, 2, 1, 3}, {0, 3, 1, 2}};
+    int bs = 0, bcost = 1 << 30;
+    for (int k = 0; k < 3; ++k) {
+        int cost = 0;
+        for (int h = 0; h < 2; ++h) {
+            const auto &x = best_pairs[split[k][2 * h]], &y = best_pairs[split[k][2 * h + 1]];
+            cost += range_of({x.first, x.second, y.first, y.second}, nullptr);
+        }
+        if (cost < bcost) { bcost = cost; bs = k; }
+    }
+    std::vector<int32_t> perm;
+    for (int k = 0; k < 4; ++k) {
+        const auto &x = best_pairs[split[bs][k]];
+        perm.push_back(x.first);
+        perm.push_back(x.second);
+    }
+    int32_t *recs = tab.data() + a16w(n_steps);
+    for (int g : {1, 2, 4}) {
+        for (int gi = 0; gi < rg_groups(g); ++gi) {
+            int32_t *rec = recs + rg_offset_words(g) + size_t(gi) * kRgWords;
+            std::vector<int> rows(perm.begin() + gi * g, perm.begin() + (gi + 1) * g);
+            int lo = 0;
+            const int len = range_of(rows, &lo);
+            rec[kRgLo] = lo;
+            rec[kRgLen] = len;
+            for (int r = 0; r < g; ++r) {
+                rec[kRgRows + r] = rows[r];
+                for (int ink = 0; ink < c.d_i; ++ink) rec[kRgMma + r * c.d_i + ink] = nb(rows[r], ink) - lo;
+            }
+        }
+    }
+    int32_t *perm_t = recs + size_t(14) * kRgWords;
+    std::copy(perm.begin(), perm.end(), perm_t);
+    cudaError_t e = cudaMemcpyAsync(k5, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) {
+        const int32_t *perm_d = static_cast<const int32_t *>(k5) + a16w(n_steps) + size_t(14) * kRgWords;
+        __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + 4 * tables_words(c));
+        const int64_t total = c.rows * c.row_nnz;
+        rg_values_kernel<<<int(std::min<int64_t>((total + 255) / 256, 4 * kNumSMs)), 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, perm_d, total, outv);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) note_launch();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // `tab` is a host temporary
+    if (e != cudaSuccess) {
+        set_error("rbgp4_prepare: writing the K5 tables: %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    return RBGP4_OK;
+}
+
+namespace {
+struct SPlan {
+    SParams p;
+    size_t smem;
+    unsigned grid;
+    bool rg;
+};
+
+constexpr size_t kSSmemCap = 227 * 1024;
+
+int stream_plan(const ChainDims &c, int out_dtype, SPlan *pl) {
+    if (!stream_shape_ok(c) || c.n_cols % 64 != 0) return 0;
+    if (opts().stream == 0) return 0;
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    SParams p{};
+    p.n_cols = c.n_cols;
+    p.ld_out = c.ld_out;
+    p.u_o = c.u_o; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.u_i = c.u_i; p.d_i = c.d_i; p.d_t = c.d_t;
+    const int64_t tiles = c.u_o * ((c.n_cols + kSBatch - 1) / kSBatch);
+    // whole tiles when they fill ~2/3 of the SMs, else the largest row group that does
+    int g = 8;
+    if (opts().stream_g > 0) g = opts().stream_g;
+    else if (tiles < 96) g = tiles * 2 >= 96 ? 4 : tiles * 4 >= 96 ? 2 : 1;
+    if (g != 1 && g != 2 && g != 4 && g != 8) return 0;
+    const bool rg = g < 8;
+    p.g = rg ? g : c.u_i;
+    p.n_rg = rg ? 8 / g : 1;
+    p.n_units = tiles * p.n_rg;
+    // row groups: stage = the longest possible column-block range (8 pieces) + the group's W rows
+    p.i_bytes = rg ? 8 * kPieceBytes : c.tk * kSBatch * 2;
+    // whole tiles: a stage = I slab + the step's relayout W tile; row groups: the I range only,
+    // the unit's W resident (d_o steps x G*16 rows x d_t slots)
+    const int w_bytes = rg ? 0 : c.tm * c.d_i * 32;
+    p.stage_bytes = int((size_t(p.i_bytes) + w_bytes + 1023) & ~size_t(1023));
+    p.wres_bytes = rg ? int((size_t(c.d_o) * g * 16 * c.d_t * 2 + 1023) & ~size_t(1023)) : 0;
+    p.acc_cols = rg ? g * 16 : c.tm * c.d_i;
+    const unsigned grid = unsigned(std::min<int64_t>(p.n_units, kNumSMs));
+    const bool multi = p.n_units > int64_t(grid);
+    int tcols = 32;
+    while (tcols < p.acc_cols * (multi ? 2 : 1)) tcols *= 2;
+    if (tcols > 512) return 0;
+    p.tmem_cols = tcols;
+    // the last unit is staged in the ring: 4 warps x nrows x 32 columns of the output
+    const size_t staging = size_t(rg ? g * 16 : c.tm) * kSBatch * oelt;
+    const size_t statics = (rg ? size_t(kMaxRg) * kRgWords * 4 : 256) + 64;
+    const size_t fixed = 1024 + 1024;  // alignment slack + barrier block
+    if (fixed + statics + p.wres_bytes + 2 * size_t(p.stage_bytes) > kSSmemCap) return 0;
+    int ns = int(std::min<size_t>(16, (kSSmemCap - fixed - statics - p.wres_bytes) / p.stage_bytes));
+    // row groups: the kernel re-cuts the ring into stages of the longest range actually used
+    p.ring_bytes = int(kSSmemCap - fixed - statics - p.wres_bytes) & ~1023;
+    if (opts().stages > 0) ns = std::max(2, std::min(ns, int(opts().stages)));
+    if (ns < 2 || size_t(ns) * p.stage_bytes < staging) return 0;
+    p.ns = ns;
+    p.debug = DBG(opts().debug);
+    p.slot = -1;
+    pl->p = p;
+    pl->smem = rg ? fixed + size_t(p.ring_bytes) + p.wres_bytes : fixed + size_t(ns) * p.stage_bytes;
+    pl->grid = grid;
+    pl->rg = rg;
+    return 1;
+}
+}  // namespace
+
+int stream_supported(const ChainDims &c, int out_dtype) {
+    SPlan pl;
+    return stream_plan(c, out_dtype, &pl);
+}
+
+int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void *k5, const void *inp, void *out,
+                  cudaStream_t stream) {
+    SPlan pl;
+    if (!stream_plan(c, out_dtype, &pl) || k4 == nullptr || k5 == nullptr) return RBGP4_EUNSUPPORTED;
+    if (c.n_cols == 0) return RBGP4_OK;
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    const int32_t *cols;
+    const void *rvals;
+    gather_prep_views(c, k4, &cols, &rvals);
+    SParams &p = pl.p;
+    static int launch_seq = 0;  // debug builds: launch slots for tools/step_timeline.py
+    if (p.debug & 2048) p.slot = launch_seq++ & 15;
+    p.cols = cols;
+    p.steps = static_cast<const int32_t *>(k5);
+    p.rg = p.steps + a16w(size_t(c.u_o) * c.d_o) + rg_offset_words(pl.rg ? p.g : 1);
+    const void *rgvals = static_cast<const char *>(k5) + 4 * tables_words(c);
+    RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(inp) % 16 == 0 && (c.ld_in * 2) % 16 == 0 &&
+                      reinterpret_cast<uintptr_t>(out) % 16 == 0 && (c.ld_out * oelt) % 16 == 0,
+                  "K5 needs 16-byte aligned I / O rows");
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return RBGP4_ECUDA;
+    }
+    CUtensorMap imap, wmap, omap;
+    IMaps imaps;
+    memset(&imaps, 0, sizeof(imaps));
+    // I as (64 cols, K rows, N/64 atoms): a whole slab (tk rows) per box; row groups: one map
+    // per column-block range length L (16 L rows per box)
+    for (int len = pl.rg ? 1 : 8; len <= 8; ++len) {
+        cuuint64_t dims[3] = {64, cuuint64_t(c.cols), cuuint64_t(c.n_cols / 64)};
+        cuuint64_t strides[2] = {cuuint64_t(c.ld_in) * 2, 128};
+        cuuint32_t box[3] = {64, cuuint32_t(16 * len), 2};
+        cuuint32_t e3[3] = {1, 1, 1};
+        CUtensorMap *m = pl.rg ? &imaps.m[len - 1] : &imap;
+        CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(inp), dims, strides, box,
+                         e3, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K5 I) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    if (pl.rg) imap = imaps.m[7];
+    {
+        cuuint64_t wdims[2], wstrides[1];
+        cuuint32_t wbox[2];
+        const void *wbase;
+        CUtensorMapSwizzle swz;
+        if (pl.rg) {
+            // row-permuted values as (d_t slots, tm rows, u_o * d_o tiles (tbm, j)); box = a
+            // group's G*16 rows of all d_o tiles of its tile-row: the unit's whole W, one load
+            cuuint64_t d3[3] = {cuuint64_t(c.d_t), cuuint64_t(c.tm), cuuint64_t(c.u_o) * c.d_o};
+            cuuint64_t s3[2] = {cuuint64_t(c.d_t) * 2, cuuint64_t(c.tm) * c.d_t * 2};
+            cuuint32_t b3[3] = {cuuint32_t(c.d_t), cuuint32_t(pl.p.g * 16), cuuint32_t(c.d_o)};
+            cuuint32_t e3[3] = {1, 1, 1};
+            CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(rgvals), d3, s3, b3, e3,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,  // d_t = 32: 64-byte rows
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
+                return RBGP4_ECUDA;
+            }
+            wbase = nullptr;
+        } else {      // relayout tiles: (16, u_o * d_o * tm * d_i), box (16, tm * d_i)
+            wbase = rvals;
+            wdims[0] = 16; wdims[1] = cuuint64_t(c.u_o) * c.d_o * c.tm * c.d_i;
+            wstrides[0] = 32;
+            wbox[0] = 16; wbox[1] = cuuint32_t(c.tm * c.d_i);
+            swz = CU_TENSOR_MAP_SWIZZLE_32B;
+        }
+        if (wbase) {
+            cuuint32_t e2[2] = {1, 1};
+            CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(wbase), wdims, wstrides,
+                             wbox, e2, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) {
+                set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
+                return RBGP4_ECUDA;
+            }
+        }
+    }
+    {
+        // O (n_cols, rows) row-major; box = one epilogue warp's 32 columns x (16 | tm) rows
+        cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
+        cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
+        cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : c.tm)};
+        cuuint32_t e2[2] = {1, 1};
+        CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out,
+                         odims, ostrides, obox, e2, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         oelt == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K5 O) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, IMaps, SParams, void *) =
+        oelt == 2 ? (pl.rg ? stream_kernel<true, true> : stream_kernel<true, false>)
+                  : (pl.rg ? stream_kernel<false, true> : stream_kernel<false, false>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(K5): %s", cudaGetErrorString(e));
+        (void)cudaGetLastError();
+        return RBGP4_ECUDA;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = opts().pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
+    if (e != cudaSuccess) {
+        set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    RBGP4_CHECK_LAUNCH("stream_kernel launch");
+    return RBGP4_OK;
+}
+
+}  // namespace rbgp4
+
+#if RBGP4_DEBUG
+// debug builds only (not part of include/rbgp4.h): K5 per-CTA stamps, CTA-0 marks and trace
+extern "C" int rbgp4_debug_k5(unsigned long long *stamps, int n, unsigned long long *marks) {
+    if (n > 2 * rbgp4::kK5Stamps) n = 2 * rbgp4::kK5Stamps;
+    if (cudaMemcpyFromSymbol(stamps, rbgp4::g_k5_stamp, sizeof(unsigned long long) * n) != cudaSuccess) return -3;
+    return cudaMemcpyFromSymbol(marks, rbgp4::g_k5_mark, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -3;
+}
+extern "C" int rbgp4_debug_k5_seq(unsigned long long *stamps, unsigned long long *marks) {
+    if (cudaMemcpyFromSymbol(stamps, rbgp4::g_k5_seq, sizeof(unsigned long long) * 16 * 2 * 160) != cudaSuccess)
+        return -3;
+    return cudaMemcpyFromSymbol(marks, rbgp4::g_k5_smark, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : -3;
+}
+extern "C" int rbgp4_debug_k5_trace(unsigned long long *host) {
+    if (cudaMemcpyFromSymbol(host, rbgp4::g_k5_trace, sizeof(unsigned long long) * 192) != cudaSuccess) return -3;
+    return cudaMemcpyFromSymbol(host + 192, rbgp4::g_k5_epi, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -3;
+}
+#endif  // RBGP4_DEBUG

@@ -997,12 +997,15 @@ size_t sched_end(const ChainDims &c, const TcPlan &pl) {
 size_t k4_bytes(const ChainDims &c, int compute) {
     return compute == RBGP4_COMPUTE_BF16 ? gather_prep_bytes(c) : 0;
 }
+size_t k5_bytes(const ChainDims &c, int compute) {
+    return compute == RBGP4_COMPUTE_BF16 && k4_bytes(c, compute) ? stream_prep_bytes(c) : 0;
+}
 }  // namespace
 
 size_t tc_prep_size(const ChainDims &c, int compute) {
     TcPlan pl;
     if (!plan_tc(c, compute, &pl)) return 0;
-    return sched_end(c, pl) + k4_bytes(c, compute);
+    return sched_end(c, pl) + ((k4_bytes(c, compute) + 15) & ~size_t(15)) + k5_bytes(c, compute);
 }
 
 const int32_t *tc_prep_schedule(const ChainDims &c, const TcPlan &pl, const void *prep) {
@@ -1016,6 +1019,13 @@ const int32_t *tc_prep_pair(const ChainDims &c, const TcPlan &pl, const void *pr
 
 const void *tc_prep_k4(const ChainDims &c, const TcPlan &pl, int compute, const void *prep) {
     return prep && k4_bytes(c, compute) ? static_cast<const char *>(prep) + sched_end(c, pl) : nullptr;
+}
+
+// K5 tables (sdmm_stream.cu) after the K4 section
+const void *tc_prep_k5(const ChainDims &c, const TcPlan &pl, int compute, const void *prep) {
+    return prep && k5_bytes(c, compute)
+               ? static_cast<const char *>(prep) + sched_end(c, pl) + ((k4_bytes(c, compute) + 15) & ~size_t(15))
+               : nullptr;
 }
 
 int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_t *adj_o,
@@ -1071,6 +1081,14 @@ int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_
         set_error("rbgp4_prepare: writing the schedule: %s", cudaGetErrorString(e));
         return RBGP4_ECUDA;
     }
+    if (const void *k5 = tc_prep_k5(c, pl, compute, prep)) {
+        if (values == nullptr) {
+            set_error("rbgp4_prepare: values needed for the bf16 relayout");
+            return RBGP4_EINVAL;
+        }
+        if (int rc = stream_prepare(c, values, adj.data(), sched.data(), adji.data(), const_cast<void *>(k5), stream))
+            return rc;
+    }
     if (const void *k4 = tc_prep_k4(c, pl, compute, prep)) {
         if (values == nullptr) {
             set_error("rbgp4_prepare: values needed for the bf16 relayout");
@@ -1108,6 +1126,12 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
     pl.p.prep = static_cast<const uint16_t *>(prep);
     pl.p.sched = tc_prep_schedule(c, pl, prep);
+    // TC16 shape, prepared: the streamed kernel (K5)
+    {
+        const void *k4 = tc_prep_k4(c, pl, compute, prep), *k5 = tc_prep_k5(c, pl, compute, prep);
+        if (compute == RBGP4_COMPUTE_BF16 && k4 && k5 && stream_supported(c, out_dtype))
+            return launch_stream(c, out_dtype, k4, k5, inp, out, stream);
+    }
     // g_b blocks >= 16 x 16: the gathered-block kernel (K4), no densification
     {
         const void *k4 = tc_prep_k4(c, pl, compute, prep);

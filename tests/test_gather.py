@@ -35,7 +35,7 @@ def run(w, x, compute="bf16", out_dtype=None, dense=False, relayout=False, persi
     The prepared buffer is cached per matrix and its layout follows the mode, so non-default
     modes run on a fresh RcubsMatrix copy."""
     p = ks.tiling_for_chain(w.chain, tn=1, rn=1, bn=1)
-    opt = {}
+    opt = {"stream": 0}  # K4 itself (K5 would take the prepared TC16 shape; tests/test_stream.py)
     if dense:
         opt["dense"] = 1
     if relayout:
