@@ -116,7 +116,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     uint64_t *acc_empty = acc_full + 2;  // [2] the epilogue has read the buffer
     uint64_t *wfull = acc_empty + 2;     // row groups: the unit's W landed
     uint64_t *wempty = wfull + 1;        // row groups: the unit's MMAs are done with W
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wempty + 1);
+    uint64_t *last_full = wempty + 1;    // the CTA's last unit accumulated (one phase: warps 4-7)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(last_full + 1);
     unsigned char *wres = base + 1024;   // row groups: d_o steps x G*16 rows x d_t slots
     unsigned char *ring = wres + p.wres_bytes;
     // ring geometry: whole tiles -- planned on the host; row groups -- a stage holds the
@@ -144,8 +145,141 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 #define K5_MARK(i) do { } while (0)
 #endif
 
+
+    // ---- epilogue of one unit, row blocks [rb0, rb1), TMEM lane quarter = warp % 4 ----
+    // (TMEM lane = batch column).  Run by warps 0-3 for every unit and, for the CTA's last unit,
+    // split with warps 4-7.  `cols` / `rec`: the TMEM column table (whole tiles) / the unit's
+    // row-group record, in shared or global memory.
+    constexpr int kRowBytes = OUT_BF16 ? 64 : 128;  // staged row of one warp's 32 columns
+    auto drain = [&](int64_t u, int64_t it, int rb0, int rb1, const int32_t *cols, const int32_t *rec,
+                     bool helper) {
+        const int q = warp & 3;
+        const int b = int(it & 1);
+        const int64_t tile = u / upt;
+        const int tbm = int(tile % p.u_o);
+        const int64_t n0 = (tile / p.u_o) * kSBatch;
+        const int64_t m0 = int64_t(tbm) * p.tm;
+        const bool last = u + stride >= p.n_units;
+        const int64_t c0 = n0 + q * 32;     // this warp's first column
+        const bool ok = c0 < p.n_cols;      // n_cols % 64 == 0: a warp's 32 columns are all in or out
+        const int nrows = RG ? p.g * 16 : p.tm;
+        unsigned char *wstage_p = ring + q * nrows * kRowBytes;  // [row][kRowBytes] for columns c0..
+        const uint32_t wstage = smem_u32(wstage_p);
+        const int k2 = lane >> 1, odd = lane & 1;  // bf16: lane pair (2k, 2k+1) -> columns 2k, 2k+1
+        // warps 0-3 follow acc_full[b] unit by unit; the helpers (warps 4-7) may be many phases
+        // behind it, so they wait on the single-phase last_full instead
+        if (helper) mbar_wait_parked(last_full, 0u);
+        else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
+        tc_fence_after();
+        if (last && threadIdx.x == 0) { K5_MARK(3); K5_SMARK(2); }
+        const uint32_t tmem_d = *tmem_slot;
+        const uint32_t lane_base = tmem_d + (uint32_t(q * 32) << 16) + uint32_t(b * p.acc_cols);
+        // 16 fp32 rows (row block rb, staging slot rs) of this lane's column -> bf16 pairs packed
+        // across the lane pair / f32 as is; staged (last unit) or stored directly.  Kept compact
+        // (a loop over row blocks, not unrolled): the epilogue runs cold in the instruction cache.
+        auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two) {
+            const int64_t grow0 = m0 + int64_t(rb) * 16;
+            if constexpr (OUT_BF16) {
+                // all 8 shuffles first, then the stores (plain C++ stores: a volatile asm store with
+                // a memory clobber serialised every pair behind its shuffle, ~90 cycles each)
+                uint32_t words[8];
+#pragma unroll
+                for (int h = 0; h < 8; ++h) {
+                    const int m = 2 * h;
+                    const float x0 = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
+                    const float x1 = __uint_as_float(va[m + 1]) + (two ? __uint_as_float(vb[m + 1]) : 0.0f);
+                    // even lane sends row m+1, odd lane row m; each gets its pair's other column
+                    const float recv = __shfl_xor_sync(0xffffffffu, odd ? x0 : x1, 1);
+                    const __nv_bfloat162 v2 = odd ? __floats2bfloat162_rn(recv, x1) : __floats2bfloat162_rn(x0, recv);
+                    words[h] = *reinterpret_cast<const uint32_t *>(&v2);
+                }
+                if (last) {
+                    // [row][64 B], 64B swizzle: 16-byte chunk ^ (row / 2) % 4 (row = m + odd)
+                    unsigned char *sb = wstage_p + rs * 16 * 64 + (k2 & 3) * 4 + odd * 64;
+#pragma unroll
+                    for (int h = 0; h < 8; ++h)
+                        *reinterpret_cast<uint32_t *>(sb + h * 128 + ((((k2 >> 2) ^ (h & 3))) << 4)) = words[h];
+                } else if (ok) {
+                    uint32_t *gbase = reinterpret_cast<uint32_t *>(static_cast<__nv_bfloat16 *>(out) +
+                                                                  (grow0 + odd) * p.ld_out + c0 + 2 * k2);
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) gbase[int64_t(2 * h) * (p.ld_out / 2)] = words[h];
+                }
+            } else {
+                float x[16];
+#pragma unroll
+                for (int m = 0; m < 16; ++m) x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
+                if (last) {
+                    // [row][128 B], 128B swizzle: chunk ^ row % 8
+                    unsigned char *sb = wstage_p + rs * 16 * 128 + (lane & 3) * 4;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m)
+                        *reinterpret_cast<float *>(sb + m * 128 + ((((lane >> 2) ^ (m & 7))) << 4)) = x[m];
+                } else if (ok) {
+                    float *gbase = static_cast<float *>(out) + grow0 * p.ld_out + c0 + lane;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) gbase[int64_t(m) * p.ld_out] = x[m];
+                }
+            }
+        };
+        // row block i's TMEM columns: row groups -> column 16 i (one partial); whole tiles -> its
+        // two d_i partials cols[2 i], cols[2 i + 1] (TC16 relayout)
+        auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16]) {
+            if constexpr (RG) {
+                TMEM_LD_32x32b_X16(lane_base + uint32_t(i * 16), va);
+            } else {
+                TMEM_LD_32x32b_X16(lane_base + uint32_t(cols[2 * i]), va);
+                TMEM_LD_32x32b_X16(lane_base + uint32_t(cols[2 * i + 1]), vb);
+            }
+        };
+        // software pipeline over row blocks: row block i+1's TMEM loads are in flight while row
+        // block i is converted and stored (tcgen05.wait::ld waits for all of them)
+        uint32_t a0[16], b0[16], a1[16], b1[16];
+        tload(rb0, a0, b0);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll 1
+        for (int i = rb0; i < rb1; i += 2) {
+            if (i + 1 < rb1) tload(i + 1, a1, b1);
+            put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (i + 1 >= rb1) break;
+            if (i + 2 < rb1) tload(i + 2, a0, b0);
+            put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
+        if (!helper) {
+            // all TMEM reads of this buffer are done: the MMA warp may reuse it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[b]);
+        }
+        if (last) {
+            // the ring is idle (this CTA's last MMA has completed): this warp's rows go out by its
+            // own TMA stores (32 columns x 16 rows per row block (groups) / x 64 rows (tiles))
+            fence_async_smem();
+            __syncwarp();
+            if (threadIdx.x == 0) K5_MARK(11);
+            if (ok && elect_one()) {
+                if constexpr (RG) {
+                    for (int r = rb0; r < rb1; ++r)
+                        tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0),
+                                       int32_t(m0) + rec[kRgRows + r] * 16);
+                } else {
+                    for (int r = rb0; r < rb1; r += 4)
+                        tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0), int32_t(m0) + r * 16);
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                if (warp == 0) { K5_MARK(4); K5_SMARK(3); }
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncwarp();
+        }
+    };
+
     if (warp == 7) {
-        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");  // idle
+        // idle until the last unit's epilogue (below); it waits on barriers warp 4 initialises
+        asm volatile("bar.sync 3, 96;" ::: "memory");
+        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
     } else if (warp == 4 || warp == 6) {
         // ========================== TMA producers ==========================
         // warp 6: expect_tx + the W box of every step (before griddepcontrol.wait for the first
@@ -172,16 +306,17 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
             mbar_init(wfull, 1);
             mbar_init(wempty, 1);
+            mbar_init(last_full, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(wprod ? &wmap : &imap)) : "memory");
         }
         __syncwarp();
-        // barrier 3 (warps 4 and 6): the barrier init is visible to the W producer; barrier 1
+        // barrier 3 (warps 4, 6, 7): the barrier init is visible to warps 6 and 7; barrier 1
         // (setup, all warps): arrive only -- producers never wait for TMEM or the tables
-        if (!wprod) asm volatile("bar.arrive 3, 64;" ::: "memory");
-        else asm volatile("bar.sync 3, 64;" ::: "memory");
+        if (!wprod) asm volatile("bar.arrive 3, 96;" ::: "memory");
+        else asm volatile("bar.sync 3, 96;" ::: "memory");
         asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         auto step_word = [&](int s) -> int32_t {
@@ -344,6 +479,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     if (s == p.d_o - 1) {
                         tc_commit(&acc_full[b]);
                         if (RG) tc_commit(wempty);
+                        if (u + stride >= p.n_units) tc_commit(last_full);
                     }
 #if RBGP4_DEBUG
                     if (trace && g < 64) g_k5_trace[2][g] = clock64() - c_entry;
@@ -361,139 +497,24 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
-        const uint32_t tmem_d = *tmem_slot;
-        // this warp's 32 batch columns; staged rows of 64 B (bf16) / 128 B (f32)
-        constexpr int kRowBytes = OUT_BF16 ? 64 : 128;
-        const int nrows = RG ? p.g * 16 : p.tm;
-        unsigned char *wstage_p = ring + warp * nrows * kRowBytes;
-        const uint32_t wstage = smem_u32(wstage_p);
-        // bf16: lane pair (2k, 2k+1) stores columns 2k, 2k+1 of row m (even lane) / m+1 (odd)
-        const int k2 = lane >> 1, odd = lane & 1;
         int64_t it = 0;
         for (int64_t u = first; u < p.n_units; u += stride, ++it) {
-            const int b = int(it & 1);
-            const int64_t tile = u / upt;
-            const int32_t *rec = RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr;
-            const int tbm = int(tile % p.u_o);
-            const int64_t n0 = (tile / p.u_o) * kSBatch;
-            const int64_t m0 = int64_t(tbm) * p.tm;
+            // the CTA's last unit is the only exposed epilogue: warps 4-7 (idle by then) take
+            // the second half of its row blocks
             const bool last = u + stride >= p.n_units;
-            const int64_t c0 = n0 + warp * 32;  // this warp's first column
-            const bool ok = c0 < p.n_cols;      // n_cols % 64 == 0: a warp's 32 columns are all in or out
-            mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
-            tc_fence_after();
-            if (last && threadIdx.x == 0) { K5_MARK(3); K5_SMARK(2); }
-            const uint32_t lane_base = tmem_d + (uint32_t(warp * 32) << 16) + uint32_t(b * p.acc_cols);
-            // 16 fp32 rows (row block rb, staging slot rs) of this lane's column -> bf16 pairs
-            // packed across the lane pair / f32 as is; staged (last unit) or stored directly.
-            // Kept compact (a loop over row blocks, not unrolled): the epilogue runs once per
-            // unit, cold in the instruction cache.
-            auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two) {
-                const int64_t grow0 = m0 + int64_t(rb) * 16;
-                if constexpr (OUT_BF16) {
-                    // all 8 shuffles first, then the stores (plain C++ stores: a volatile asm store
-                    // with a memory clobber serialised every pair behind its shuffle, ~90 cycles each)
-                    uint32_t words[8];
-#pragma unroll
-                    for (int h = 0; h < 8; ++h) {
-                        const int m = 2 * h;
-                        const float x0 = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
-                        const float x1 = __uint_as_float(va[m + 1]) + (two ? __uint_as_float(vb[m + 1]) : 0.0f);
-                        // even lane sends row m+1, odd lane row m; each gets its pair's other column
-                        const float recv = __shfl_xor_sync(0xffffffffu, odd ? x0 : x1, 1);
-                        const __nv_bfloat162 v2 = odd ? __floats2bfloat162_rn(recv, x1) : __floats2bfloat162_rn(x0, recv);
-                        words[h] = *reinterpret_cast<const uint32_t *>(&v2);
-                    }
-                    if (last) {
-                        // [row][64 B], 64B swizzle: 16-byte chunk ^ (row / 2) % 4 (row = m + odd)
-                        unsigned char *sb = wstage_p + rs * 16 * 64 + (k2 & 3) * 4 + odd * 64;
-#pragma unroll
-                        for (int h = 0; h < 8; ++h)
-                            *reinterpret_cast<uint32_t *>(sb + h * 128 + ((((k2 >> 2) ^ (h & 3))) << 4)) = words[h];
-                    } else if (ok) {
-                        uint32_t *gbase = reinterpret_cast<uint32_t *>(static_cast<__nv_bfloat16 *>(out) +
-                                                                      (grow0 + odd) * p.ld_out + c0 + 2 * k2);
-#pragma unroll
-                        for (int h = 0; h < 8; ++h) gbase[int64_t(2 * h) * (p.ld_out / 2)] = words[h];
-                    }
-                } else {
-                    float x[16];
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
-                    if (last) {
-                        // [row][128 B], 128B swizzle: chunk ^ row % 8
-                        unsigned char *sb = wstage_p + rs * 16 * 128 + (lane & 3) * 4;
-#pragma unroll
-                        for (int m = 0; m < 16; ++m)
-                            *reinterpret_cast<float *>(sb + m * 128 + ((((lane >> 2) ^ (m & 7))) << 4)) = x[m];
-                    } else if (ok) {
-                        float *gbase = static_cast<float *>(out) + grow0 * p.ld_out + c0 + lane;
-#pragma unroll
-                        for (int m = 0; m < 16; ++m) gbase[int64_t(m) * p.ld_out] = x[m];
-                    }
-                }
-            };
-            // row block i's TMEM columns: row groups -> column 16 i (one partial); whole tiles ->
-            // its two d_i partials s_cols[2 i], s_cols[2 i + 1] (TC16 relayout)
             const int nrb = RG ? p.g : p.u_i;
-            auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16]) {
-                if constexpr (RG) {
-                    TMEM_LD_32x32b_X16(lane_base + uint32_t(i * 16), va);
-                } else {
-                    TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[2 * i]), va);
-                    TMEM_LD_32x32b_X16(lane_base + uint32_t(s_cols[2 * i + 1]), vb);
-                }
-            };
-            // software pipeline over row blocks: row block i+1's TMEM loads are in flight while
-            // row block i is converted and stored (tcgen05.wait::ld waits for all of them)
-            uint32_t a0[16], b0[16], a1[16], b1[16];
-#if RBGP4_DEBUG
-#define K5_EPI(i) do { if (trace && last && threadIdx.x == 0 && (i) < 16) g_k5_epi[i] = clock64() - c_entry; } while (0)
-#else
-#define K5_EPI(i) do { } while (0)
-#endif
-            tload(0, a0, b0);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            K5_EPI(0);
-#pragma unroll 1
-            for (int i = 0; i < nrb; i += 2) {
-                if (i + 1 < nrb) tload(i + 1, a1, b1);
-                put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG);
-                K5_EPI(1 + 2 * i);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                K5_EPI(2 + 2 * i);
-                if (i + 1 >= nrb) break;
-                if (i + 2 < nrb) tload(i + 2, a0, b0);
-                put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG);
-                K5_EPI(3 + 2 * i);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                K5_EPI(4 + 2 * i);
-            }
-#undef K5_EPI
-            // all TMEM reads of this buffer are done: the MMA warp may reuse it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[b]);
-            if (last) {
-                // the ring is idle (this CTA's last MMA has completed): this warp's rows go out
-                // by its own TMA stores (boxes of 32 columns x 16 rows (groups) / x tm rows)
-                fence_async_smem();
-                __syncwarp();
-                if (threadIdx.x == 0) K5_MARK(11);
-                if (ok && elect_one()) {
-                    if constexpr (RG) {
-                        for (int r = 0; r < p.g; ++r)
-                            tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0),
-                                           int32_t(m0) + rec[kRgRows + r] * 16);
-                    } else {
-                        tma_store_2d_g(&omap, wstage, int32_t(c0), int32_t(m0));
-                    }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                    if (warp == 0) { K5_MARK(4); K5_SMARK(3); }
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                }
-                __syncwarp();
-            }
+            const int split = (last && nrb >= 2) ? nrb / 2 : nrb;
+            drain(u, it, 0, split, s_cols, RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr, false);
+        }
+    }
+    if (warp >= 4) {
+        // warps 4-7 after their roles: the second half of the last unit's row blocks (tables
+        // read from global memory: these warps never synchronised on the epilogue's copies)
+        const int64_t n_mine = (p.n_units - first + stride - 1) / stride;
+        const int64_t u = first + (n_mine - 1) * stride;
+        const int nrb = RG ? p.g : p.u_i;
+        if (n_mine > 0 && nrb >= 2) {
+            drain(u, n_mine - 1, nrb / 2, nrb, p.cols, RG ? p.rg + int(u % p.n_rg) * kRgWords : nullptr, true);
         }
     }
     tc_fence_before();
@@ -800,7 +821,7 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
         // O (n_cols, rows) row-major; box = one epilogue warp's 32 columns x (16 | tm) rows
         cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
         cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
-        cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : c.tm)};
+        cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : c.tm / 2)};
         cuuint32_t e2[2] = {1, 1};
         CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out,
                          odims, ostrides, obox, e2, CU_TENSOR_MAP_INTERLEAVE_NONE,
