@@ -278,8 +278,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 
     if (warp == 7) {
         // idle until the last unit's epilogue (below); it waits on barriers warp 4 initialises
-        asm volatile("bar.sync 3, 96;" ::: "memory");
-        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("barrier.sync 3, 96;" ::: "memory");
+        asm volatile("barrier.arrive 1, %0;" ::"n"(kThreads) : "memory");
     } else if (warp == 4 || warp == 6) {
         // ========================== TMA producers ==========================
         // warp 6: expect_tx + the W box of every step (before griddepcontrol.wait for the first
@@ -315,9 +315,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         __syncwarp();
         // barrier 3 (warps 4, 6, 7): the barrier init is visible to warps 6 and 7; barrier 1
         // (setup, all warps): arrive only -- producers never wait for TMEM or the tables
-        if (!wprod) asm volatile("bar.arrive 3, 96;" ::: "memory");
-        else asm volatile("bar.sync 3, 96;" ::: "memory");
-        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
+        if (!wprod) asm volatile("barrier.arrive 3, 96;" ::: "memory");
+        else asm volatile("barrier.sync 3, 96;" ::: "memory");
+        asm volatile("barrier.arrive 1, %0;" ::"n"(kThreads) : "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         auto step_word = [&](int s) -> int32_t {
             const int32_t a = __shfl_sync(0xffffffffu, e0, s & 31);
@@ -400,7 +400,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                          smem_u32(tmem_slot)), "r"(uint32_t(p.tmem_cols)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
         const uint32_t tmem_d = *tmem_slot;
         constexpr uint32_t kN = RG ? 16u : 32u;
@@ -495,7 +495,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         } else {
             for (int i = threadIdx.x; i < p.u_i * p.d_i; i += 128) s_cols[i] = p.cols[i];
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
         int64_t it = 0;
         for (int64_t u = first; u < p.n_units; u += stride, ++it) {
