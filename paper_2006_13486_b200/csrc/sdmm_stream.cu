@@ -28,8 +28,8 @@
 //   -- for a CTA's last unit, the only exposed one -- staging in the then idle ring and its
 //   own TMA tensor store (no cross-warp barrier).
 //
-// Warps (256 threads): 0-3 epilogue (TMEM lane = batch column), 4 / 7 I producers, 6 W
-// producer (+ I pieces), 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
+// Warps (256 threads): 0-3 epilogue (TMEM lane = batch column), 4 / 7 I producers (even /
+// odd steps), 6 W producer, 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
 // output rows; fixed step order.
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <type_traits>
 #include <vector>
 
 namespace rbgp4 {
@@ -66,7 +67,7 @@ __device__ unsigned long long g_k5_mark[16];
 // bit 2048: launch slots (host counter mod 16) -- every CTA's entry / exit %globaltimer and CTA 0's
 // marks [first I issued, first full, last accumulator ready, last stores issued], for a whole
 // graph of launches (tools/step_timeline.py)
-__device__ unsigned long long g_k5_seq[16][2][160];
+__device__ unsigned long long g_k5_seq[16][3][160];  // [slot][entry | exit | first I issued][CTA]
 __device__ unsigned long long g_k5_smark[16][4];
 __device__ unsigned long long g_k5_trace[3][64];  // [0] I producer issued, [1] MMA saw full, [2] MMAs issued
 __device__ unsigned long long g_k5_epi[16];       // CTA 0 warp 0, last unit: after each epilogue step
@@ -121,11 +122,15 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     unsigned char *wres = base + 1024;   // row groups: d_o steps x G*16 rows x d_t slots
     unsigned char *ring = wres + p.wres_bytes;
     // ring geometry: whole tiles -- planned on the host; row groups -- a stage holds the
-    // longest column-block range among the groups (the records), so typical ranges (~4 of 8
-    // pieces) get twice the stages of a worst-case ring.  Every warp derives the same values.
+    // longest column-block range among the groups THIS CTA visits (units first, first + grid,
+    // ...: the group index cycles with period n_rg), so a CTA whose units are all one group of
+    // range L gets ring / (L pieces) stages (~11 for L = 4 instead of ~5 for the worst group).
+    // Every warp derives the same values.
     int NS = p.ns, SB = p.stage_bytes;
     if constexpr (RG) {
-        int l = threadIdx.x % 32 < p.n_rg ? __ldg(p.rg + (threadIdx.x % 32) * kRgWords + kRgLen) : 1;
+        const int li = threadIdx.x % 32;
+        const int64_t u_l = int64_t(blockIdx.x) + int64_t(li) * gridDim.x;
+        int l = (li < p.n_rg && u_l < p.n_units) ? __ldg(p.rg + int(u_l % p.n_rg) * kRgWords + kRgLen) : 1;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
         SB = l * kPieceBytes;
@@ -276,11 +281,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
     };
 
-    if (warp == 7) {
-        // idle until the last unit's epilogue (below); it waits on barriers warp 4 initialises
-        asm volatile("barrier.sync 3, 96;" ::: "memory");
-        asm volatile("barrier.arrive 1, %0;" ::"n"(kThreads) : "memory");
-    } else if (warp == 4 || warp == 6) {
+    if (warp == 4 || warp == 6 || warp == 7) {
         // ========================== TMA producers ==========================
         // warp 6: expect_tx + the W box of every step (before griddepcontrol.wait for the first
         // ring's worth: weights are never the previous grid's output); warp 4: barrier init, then
@@ -288,6 +289,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // 16 L rows of the group's column-block range.  Two boxes per step: a TMA box costs its
         // engine ~150-300 cycles whatever its size (tools/tma_issue_bench.cu).
         const bool wprod = warp == 6;
+        // the I boxes of consecutive steps alternate between warps 4 and 7: a box costs its
+        // issuing thread ~300-450 cycles, which bounds one issuer at ~35-60 B/clk
+        // (tools/stream_bench.cu); two issuers keep the row-group ranges (~16 KB boxes) and
+        // the whole slabs ahead of the MMAs
+        const int64_t iparity = warp == 7 ? 1 : 0;
         // lane l holds the step words l and l + 32 of the current tile-row (shuffled out)
         int32_t e0 = 0, e1 = 0, rl = 0;
         auto load_steps = [&](int tbm) {
@@ -301,13 +307,18 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         int rg_cur = RG ? int(first % p.n_rg) : 0;
         load_steps(tbm_cur);
         if (RG) load_rec(rg_cur);
-        if (!wprod && lane == 0) {
+#if RBGP4_DEBUG
+        if (trace && warp == 4 && (e0 == 0x7fffffff || rl == 0x7fffffff)) g_k5_mark[15] = 1;  // wait for the loads
+        if (warp == 4 && lane == 0) K5_MARK(6);
+#endif
+        if (warp == 4 && lane == 0) {
             for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
             for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
             mbar_init(wfull, 1);
             mbar_init(wempty, 1);
             mbar_init(last_full, 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            K5_MARK(7);
         }
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(wprod ? &wmap : &imap)) : "memory");
@@ -315,7 +326,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         __syncwarp();
         // barrier 3 (warps 4, 6, 7): the barrier init is visible to warps 6 and 7; barrier 1
         // (setup, all warps): arrive only -- producers never wait for TMEM or the tables
-        if (!wprod) asm volatile("barrier.arrive 3, 96;" ::: "memory");
+        if (warp == 4) asm volatile("barrier.arrive 3, 96;" ::: "memory");
         else asm volatile("barrier.sync 3, 96;" ::: "memory");
         asm volatile("barrier.arrive 1, %0;" ::"n"(kThreads) : "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -350,6 +361,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             K5_MARK(0);
         }
         if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (warp == 4 && lane == 0) K5_MARK(8);
         int64_t g = 0, it = 0;
         int rs_st = 0;
         uint32_t rs_ph = 0;
@@ -372,10 +384,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 const uint32_t ph = rs_ph;
                 if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
                 const int32_t word = step_word(s);
-                if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                 if (wprod) {
+                    if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                     if (g >= pre) issue_w(st, tbm, word);
-                } else {
+                } else if ((g & 1) == iparity) {
+                    if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                     const int32_t krow = (word & 0xFFFF) * p.tk;
                     if (elect_one()) {
                         if constexpr (RG) {
@@ -390,7 +403,13 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 #if RBGP4_DEBUG
                     if (trace && lane == 0 && g < 64) g_k5_trace[0][g] = clock64() - c_entry;
 #endif
-                    if (g == 0 && lane == 0) { K5_MARK(1); K5_SMARK(0); }
+                    if (g == 0 && lane == 0) {
+                        K5_MARK(1);
+                        K5_SMARK(0);
+#if RBGP4_DEBUG
+                        if (p.slot >= 0 && blockIdx.x < 160) g_k5_seq[p.slot][2][blockIdx.x] = k5_gtimer();
+#endif
+                    }
                 }
             }
         }
@@ -412,81 +431,98 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // whole slab, or one 16-row piece), 8-row groups 1024 B apart
         const uint64_t a_desc_t = smem_desc(ring_a, uint32_t(p.tk) * 128u, 1024, 2u);
         // B: K-major W rows (row groups: d_t slots per row; whole tiles: 16-slot relayout rows)
-        const uint32_t w_row = RG ? uint32_t(p.d_t * 2) : 32u;
+        constexpr uint32_t w_row = RG ? 64u : 32u;  // d_t = 32 slots (stream_shape_ok)
         const uint64_t b_desc0 = RG ? smem_desc(smem_u32(wres), 0, 8 * w_row, swizzle_layout_code(int(w_row)))
                                     : smem_desc(ring_a + uint32_t(p.i_bytes), 0, 8 * w_row, swizzle_layout_code(int(w_row)));
-        // row groups: the adjacency slot j of each step picks the step's W in the resident copy
-        int32_t e0 = 0, e1 = 0;
-        int tbm_cur = -1;
-        int64_t g = 0, it = 0;
-        int rs_st = 0;
-        uint32_t rs_ph = 0;
-        for (int64_t u = first; u < p.n_units; u += stride, ++it) {
-            const int b = int(it & 1);
-            const int32_t *rec = RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr;
-            // row groups: the staged range holds L pieces of 16 rows per 64-column atom
-            const uint64_t a_desc0 = RG ? smem_desc(ring_a, uint32_t(rec[kRgLen]) * 2048u, 1024, 2u) : a_desc_t;
-            if constexpr (RG) {
-                const int tbm = int((u / upt) % p.u_o);
-                if (tbm != tbm_cur) {
-                    const int32_t *row = p.steps + int64_t(tbm) * p.d_o;
-                    e0 = lane < p.d_o ? __ldg(row + lane) : 0;
-                    e1 = lane + 32 < p.d_o ? __ldg(row + lane + 32) : 0;
-                    tbm_cur = tbm;
+        // row groups: the adjacency slot j of each step picks the step's W in the resident copy.
+        // The group size is a compile-time constant of the loop (G = 1, 2, 4) so a unit's piece
+        // offsets are hoisted into registers and a step is 2G back-to-back UTCHMMA after uniform
+        // adds (loading them from the record every step cost ~200 cycles per step).
+        auto mma_loop = [&](auto gc) {
+            constexpr int G = decltype(gc)::value;  // 0: whole tiles
+            int32_t e0 = 0, e1 = 0;
+            int tbm_cur = -1;
+            int64_t g = 0, it = 0;
+            int rs_st = 0;
+            uint32_t rs_ph = 0;
+            for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+                const int b = int(it & 1);
+                uint64_t a_desc0 = a_desc_t;
+                uint32_t aoff[G > 0 ? 2 * G : 1];
+                if constexpr (G > 0) {
+                    const int32_t *rec = s_rg + int(u % p.n_rg) * kRgWords;
+                    // the staged range holds L pieces of 16 rows per 64-column atom
+                    a_desc0 = smem_desc(ring_a, uint32_t(rec[kRgLen]) * 2048u, 1024, 2u);
+#pragma unroll
+                    for (int i = 0; i < 2 * G; ++i) aoff[i] = uint32_t(rec[kRgMma + i]) * uint32_t(2048 >> 4);
+                    const int tbm = int((u / upt) % p.u_o);
+                    if (tbm != tbm_cur) {
+                        const int32_t *row = p.steps + int64_t(tbm) * p.d_o;
+                        e0 = lane < p.d_o ? __ldg(row + lane) : 0;
+                        e1 = lane + 32 < p.d_o ? __ldg(row + lane + 32) : 0;
+                        tbm_cur = tbm;
+                    }
+                    mbar_wait(wfull, uint32_t(it & 1));
                 }
-                mbar_wait(wfull, uint32_t(it & 1));
-            }
-            mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
-            tc_fence_after();
-            const uint32_t d_base = tmem_d + uint32_t(b * p.acc_cols);
-            for (int s = 0; s < p.d_o; ++s, ++g) {
-                const int st = rs_st;
-                const uint32_t ph = rs_ph;
-                if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
-                int32_t wj = 0;
-                if constexpr (RG) {
-                    const int32_t a = __shfl_sync(0xffffffffu, e0, s & 31), bb = __shfl_sync(0xffffffffu, e1, s & 31);
-                    wj = (s < 32 ? a : bb) >> 16;
-                }
-                mbar_wait(&full[st], ph);
+                mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
                 tc_fence_after();
-#if RBGP4_DEBUG
-                if (trace && lane == 0 && g < 64) g_k5_trace[1][g] = clock64() - c_entry;
-#endif
-                if (g == 0 && lane == 0) { K5_MARK(2); K5_SMARK(1); }
-                if (elect_one()) {
-                    const uint32_t st16 = uint32_t(st * SB) >> 4;
-                    const uint64_t a_st = a_desc0 + st16;
-                    const uint64_t b_st = RG ? b_desc0 + uint32_t((wj * p.g * 16 * int(w_row)) >> 4) : b_desc0 + st16;
-                    if constexpr (RG) {
-                        for (int r = 0; r < p.g; ++r)
-#pragma unroll
-                            for (int ink = 0; ink < 2; ++ink) {
-                                const uint32_t piece = uint32_t(rec[kRgMma + r * 2 + ink]);
-                                tc_mma<false>(d_base + uint32_t(r * 16), a_st + piece * uint32_t(2048 >> 4),
-                                              b_st + uint32_t(r * ((16 * w_row) >> 4) + ink * 2), idesc,
-                                              (s > 0 || ink > 0) ? 1u : 0u);
-                            }
-                    } else {
-                        // TC16 relayout: 8 column blocks of 16 slab rows, one N = 32 MMA each
-                        const uint32_t acc = s > 0 ? 1u : 0u;
-#pragma unroll
-                        for (int kb = 0; kb < 8; ++kb)
-                            tc_mma<false>(d_base + uint32_t(kb * 32), a_st + uint32_t(kb * 16 * 8),
-                                          b_st + uint32_t(kb * ((32 * 32) >> 4)), idesc, acc);
+                const uint32_t d_base = tmem_d + uint32_t(b * p.acc_cols);
+                for (int s = 0; s < p.d_o; ++s, ++g) {
+                    const int st = rs_st;
+                    const uint32_t ph = rs_ph;
+                    if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
+                    int32_t wj = 0;
+                    if constexpr (G > 0) {
+                        const int32_t a = __shfl_sync(0xffffffffu, e0, s & 31), bb = __shfl_sync(0xffffffffu, e1, s & 31);
+                        wj = (s < 32 ? a : bb) >> 16;
                     }
-                    tc_commit(&empty[st]);
-                    if (s == p.d_o - 1) {
-                        tc_commit(&acc_full[b]);
-                        if (RG) tc_commit(wempty);
-                        if (u + stride >= p.n_units) tc_commit(last_full);
-                    }
+                    mbar_wait(&full[st], ph);
+                    tc_fence_after();
 #if RBGP4_DEBUG
-                    if (trace && g < 64) g_k5_trace[2][g] = clock64() - c_entry;
+                    if (trace && lane == 0 && g < 64) g_k5_trace[1][g] = clock64() - c_entry;
 #endif
+                    if (g == 0 && lane == 0) { K5_MARK(2); K5_SMARK(1); }
+                    if (elect_one()) {
+                        const uint32_t st16 = uint32_t(st * SB) >> 4;
+                        const uint64_t a_st = a_desc0 + st16;
+                        if constexpr (G > 0) {
+                            const uint64_t b_st = b_desc0 + uint32_t(wj * ((G * 16 * int(w_row)) >> 4));
+#pragma unroll
+                            for (int r = 0; r < G; ++r)
+#pragma unroll
+                                for (int ink = 0; ink < 2; ++ink)
+                                    tc_mma<false>(d_base + uint32_t(r * 16), a_st + aoff[r * 2 + ink],
+                                                  b_st + uint32_t(r * ((16 * w_row) >> 4) + ink * 2), idesc,
+                                                  (s > 0 || ink > 0) ? 1u : 0u);
+                        } else {
+                            // TC16 relayout: 8 column blocks of 16 slab rows, one N = 32 MMA each
+                            const uint64_t b_st = b_desc0 + st16;
+                            const uint32_t acc = s > 0 ? 1u : 0u;
+#pragma unroll
+                            for (int kb = 0; kb < 8; ++kb)
+                                tc_mma<false>(d_base + uint32_t(kb * 32), a_st + uint32_t(kb * 16 * 8),
+                                              b_st + uint32_t(kb * ((32 * 32) >> 4)), idesc, acc);
+                        }
+                        tc_commit(&empty[st]);
+                        if (s == p.d_o - 1) {
+                            tc_commit(&acc_full[b]);
+                            if (G > 0) tc_commit(wempty);
+                            if (u + stride >= p.n_units) tc_commit(last_full);
+                        }
+#if RBGP4_DEBUG
+                        if (trace && g < 64) g_k5_trace[2][g] = clock64() - c_entry;
+#endif
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
+        };
+        if constexpr (RG) {
+            if (p.g == 1) mma_loop(std::integral_constant<int, 1>{});
+            else if (p.g == 2) mma_loop(std::integral_constant<int, 2>{});
+            else mma_loop(std::integral_constant<int, 4>{});
+        } else {
+            mma_loop(std::integral_constant<int, 0>{});
         }
     } else {
         // ============================ epilogue (warps 0-3) ============================
@@ -870,7 +906,7 @@ extern "C" int rbgp4_debug_k5(unsigned long long *stamps, int n, unsigned long l
     return cudaMemcpyFromSymbol(marks, rbgp4::g_k5_mark, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -3;
 }
 extern "C" int rbgp4_debug_k5_seq(unsigned long long *stamps, unsigned long long *marks) {
-    if (cudaMemcpyFromSymbol(stamps, rbgp4::g_k5_seq, sizeof(unsigned long long) * 16 * 2 * 160) != cudaSuccess)
+    if (cudaMemcpyFromSymbol(stamps, rbgp4::g_k5_seq, sizeof(unsigned long long) * 16 * 3 * 160) != cudaSuccess)
         return -3;
     return cudaMemcpyFromSymbol(marks, rbgp4::g_k5_smark, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : -3;
 }

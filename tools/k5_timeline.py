@@ -76,9 +76,9 @@ print(f"CTAs {used.size}: entry skew {(ent.max() - t0) / 1e3:.2f} us, span {(ext
       f"lifetime p10/p50/p90 {np.percentile(ext - ent, 10) / 1e3:.2f}/{np.percentile(ext - ent, 50) / 1e3:.2f}/"
       f"{np.percentile(ext - ent, 90) / 1e3:.2f} us, exit p10/p90 {(np.percentile(ext, 10) - t0) / 1e3:.2f}/"
       f"{(np.percentile(ext, 90) - t0) / 1e3:.2f} us")
-names = {0: "first W issued", 1: "first I issued", 2: "first full (MMA warp)", 3: "last acc ready",
-         6: "warp0 wake", 7: "warp1 wake", 8: "warp2 wake", 9: "warp3 wake", 10: "warp0 first TMEM chunk",
-         11: "warp0 staged", 12: "epilogue barrier", 4: "last stores issued", 5: "exit"}
+names = {6: "steps loaded (I prod)", 7: "barriers init", 8: "after griddepcontrol.wait", 0: "first W issued",
+         1: "first I issued", 2: "first full (MMA warp)", 3: "last acc ready", 11: "warp0 staged",
+         4: "last stores issued", 5: "exit"}
 print("CTA0 marks (cycles from entry): " + ", ".join(f"{nm} {int(mk[i])}" for i, nm in names.items()))
 tr = np.zeros(208, dtype=np.uint64)
 lib.rbgp4_debug_k5_trace.argtypes = [ctypes.c_void_p]

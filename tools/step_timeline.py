@@ -37,10 +37,10 @@ with torch.cuda.stream(B.stream):
 torch.cuda.synchronize()
 lib = _native.lib()
 lib.rbgp4_debug_k5_seq.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
-stamps = np.zeros(16 * 2 * 160, dtype=np.uint64)
+stamps = np.zeros(16 * 3 * 160, dtype=np.uint64)
 marks = np.zeros(64, dtype=np.uint64)
 assert lib.rbgp4_debug_k5_seq(stamps.ctypes.data, marks.ctypes.data) == 0
-stamps = stamps.reshape(16, 2, 160).astype(np.int64)
+stamps = stamps.reshape(16, 3, 160).astype(np.int64)
 marks = marks.reshape(16, 4).astype(np.int64)
 # the step replay's launches: the n slots with the latest entries, in time order
 n = len(layers)
@@ -56,3 +56,8 @@ for i, s in enumerate(slots):
     print(f"  {layers[i]['name']:>6} CTAs {ent.size:3d}: entry {ent.min() / 1e3:6.2f}..{ent.max() / 1e3:6.2f}  "
           f"exit {ext.min() / 1e3:6.2f}..{ext.max() / 1e3:6.2f} | CTA0 first-I {mk[0]:6.2f} first-full {mk[1]:6.2f} "
           f"acc-ready {mk[2]:6.2f} stores {mk[3]:6.2f}")
+    fi = stamps[s][2][: ent.size] - t0
+    ok = stamps[s][2][: ent.size] > 0
+    d = (fi[ok] - ent[ok]) / 1e3
+    print(f"         first-I - entry p10/p50/p90 {np.percentile(d, 10):.2f}/{np.percentile(d, 50):.2f}/{np.percentile(d, 90):.2f} us; "
+          f"first-I min/max {fi[ok].min() / 1e3:6.2f}/{fi[ok].max() / 1e3:6.2f}")
