@@ -206,6 +206,11 @@ int rbgp4_abi_version(void);
 int64_t rbgp4_launch_count(void);
 void rbgp4_reset_launch_count(void);
 
+/* Name of the kernel family this thread's last product / convolution launched ("K1 simt",
+ * "K2 tc", "K2 conv", "K4 gather", "K4 conv", "K5 stream", "K5 rows", "K5 conv", "csr", ...):
+ * which device path a call took, for tests and the benchmark. */
+const char *rbgp4_last_kernel(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ EXPORTED = (
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
     "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
-    "rbgp4_reset_launch_count", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
+    "rbgp4_reset_launch_count", "rbgp4_last_kernel", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
     "rbgp4_reset_options", "rbgp4_debug_build",
 )
 
@@ -106,6 +106,7 @@ def lib():
     h.rbgp4_abi_version.restype = i32
     h.rbgp4_launch_count.restype = i64
     h.rbgp4_reset_launch_count.restype = None
+    h.rbgp4_last_kernel.restype = ctypes.c_char_p
     h.rbgp4_set_option.argtypes = [ctypes.c_char_p, i64]
     h.rbgp4_set_option.restype = i32
     h.rbgp4_get_option.argtypes = [ctypes.c_char_p, ctypes.POINTER(i64)]
@@ -147,6 +148,11 @@ def options(**kw):
     finally:
         for k, v in old.items():
             set_option(k, v)
+
+
+def last_kernel() -> str:
+    """Kernel family of this thread's last launch through the ABI (e.g. "K5 conv")."""
+    return lib().rbgp4_last_kernel().decode()
 
 
 def launch_count() -> int:

@@ -112,6 +112,7 @@ extern "C" int rbgp4_chain_sdmm(int k, const int32_t *num_left, const int32_t *n
                   (long long)p.row_nnz);
     dim3 grid(unsigned(p.rows), unsigned((n_cols + kThreads - 1) / kThreads));
     auto s = static_cast<cudaStream_t>(stream);
+    note_kernel("chain");
     if (dtype == RBGP4_F32) {
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(chain_row_kernel<float>,
@@ -162,6 +163,7 @@ extern "C" int rbgp4_csr_sdmm(int64_t rows, const int64_t *indptr, const int32_t
     if (rows == 0 || n_cols == 0) return RBGP4_OK;
     dim3 grid(unsigned(rows), unsigned((n_cols + kThreads - 1) / kThreads));
     auto s = static_cast<cudaStream_t>(stream);
+    note_kernel("csr");
     if (dtype == RBGP4_F32)
         csr_row_kernel<float><<<grid, kThreads, 0, s>>>(
             indptr, indices, static_cast<const float *>(values), static_cast<const float *>(inp),

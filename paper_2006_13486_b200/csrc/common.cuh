@@ -16,6 +16,8 @@ namespace rbgp4 {
 void set_error(const char *fmt, ...);
 // count a kernel launch for rbgp4_launch_count()
 void note_launch(int n = 1);
+// record the kernel family of the current launch for rbgp4_last_kernel() (static string)
+void note_kernel(const char *name);
 
 #define RBGP4_CHECK_LAUNCH(what)                                                   \
     do {                                                                           \
@@ -120,7 +122,8 @@ int launch_gather_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
 size_t gather_prep_bytes(const ChainDims &c);
 void gather_prep_views(const ChainDims &c, const void *k4, const int32_t **cols, const void **vals);
 
-// K5: streamed TC16 SDMM (sdmm_stream.cu); `k5` = its prepared tables (step words, row groups)
+// K5: streamed tcgen05 SDMM / conv (sdmm_stream.cu); `k5` = its prepared tables (step words, row
+// groups for TC16; slice relayout for other block shapes)
 int stream_shape_ok(const ChainDims &c);
 size_t stream_prep_bytes(const ChainDims &c);
 int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
@@ -128,6 +131,9 @@ int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_
 int stream_supported(const ChainDims &c, int out_dtype);
 int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void *k5, const void *inp, void *out,
                   cudaStream_t stream);
+int stream_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype);
+int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *k4, const void *k5,
+                       const void *x, void *out, cudaStream_t stream);
 int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_host, void *k4,
                    cudaStream_t stream);
 

@@ -54,6 +54,10 @@ void set_error(const char *fmt, ...) {
 }
 
 void note_launch(int n) { g_launches += n; }
+namespace {
+thread_local const char *g_last_kernel = "";
+}
+void note_kernel(const char *name) { g_last_kernel = name; }
 
 int validate_desc(const rbgp4_desc *d, ChainDims *c) {
     RBGP4_REQUIRE(d != nullptr, "null descriptor");
@@ -149,6 +153,8 @@ void rbgp4_reset_options(void) { g_opts = Options(); }
 int64_t rbgp4_launch_count(void) { return g_launches; }
 
 void rbgp4_reset_launch_count(void) { g_launches = 0; }
+
+const char *rbgp4_last_kernel(void) { return rbgp4::g_last_kernel; }
 
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype) {
     ChainDims c;

@@ -1135,6 +1135,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
         at[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = at;
         cfg.numAttrs = opts().pdl ? 1 : 0;
+        note_kernel(pl.p.conv ? "K4 conv" : "K4 gather");
         e = cudaLaunchKernelEx(&cfg, pk, imap, wmap, pl.p, adj_o, adj_i, out, pl.n_tiles);
         if (e != cudaSuccess) {
             set_error("gather_persistent_kernel launch (%u CTAs, smem %zu): %s", pl.grid.x, pl.smem,
@@ -1181,6 +1182,7 @@ int gather_launch_typed(const GPlan &pl, const CUtensorMap &imap, const CUtensor
     }
     cfg.attrs = attrs;
     cfg.numAttrs = unsigned(na);
+    note_kernel(pl.p.conv ? "K4 conv" : "K4 gather");
     e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, pl.p, adj_o, adj_i);
     if (e != cudaSuccess) {
         set_error("gather_kernel launch (grid %u x %u x %u, smem %zu): %s", pl.grid.x, pl.grid.y,

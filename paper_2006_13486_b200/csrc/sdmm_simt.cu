@@ -302,6 +302,7 @@ int launch_one(const ChainDims &c, const SimtPlan &pl, const T *values, const in
         }
     }
     dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm));
+    note_kernel("K1 simt");
     kern<<<grid, kThreads, pl.smem, stream>>>(p, values, adj_o, adj_i, inp, out);
     RBGP4_CHECK_LAUNCH("simt_kernel launch");
     return RBGP4_OK;

@@ -91,6 +91,11 @@ struct SParams {
     const int32_t *steps;              // [tbm][s] = adjacency slot j << 16 | K-block
     const int32_t *cols;               // whole tiles: TMEM column of row block ui's ink-th partial
     const int32_t *rg;                 // row groups: n_rg records of kRgWords
+    // whole tiles (slice relayout): K16 slices per step, MMA N (rows of a slice's union, padded),
+    // W rows per step (nsl * mma_n), entries of the cols table (row blocks x 2 partials)
+    int32_t nsl, mma_n, w_rows, n_cols_tab;
+    // implicit-im2col convolution (NHWC): input channels, OUTPUT map, kernel width, pad, stride
+    int32_t c_in, img_h, img_w, kw, pad, stride, relu;
     int32_t debug, slot;
 };
 
@@ -99,14 +104,17 @@ __device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t 
                      reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src) : "memory");
 }
 
-template <bool OUT_BF16, bool RG>
+// RG: row-group units (TC16 only); CONV: A = tap-shifted NHWC boxes (K-major), O = NHWC;
+// BM: element-block rows of the chain (16 / 8 / 4) -- the granularity of the epilogue's
+// TMEM partial loads
+template <bool OUT_BF16, bool RG, bool CONV, int BM>
 __global__ void __launch_bounds__(256, 1)
 stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
               const __grid_constant__ CUtensorMap omap, const __grid_constant__ IMaps imaps, const SParams p,
               void *__restrict__ out) {
     extern __shared__ unsigned char smem_raw[];
     __shared__ int32_t s_rg[RG ? kMaxRg * kRgWords : 1];
-    __shared__ int32_t s_cols[RG ? 1 : 64];
+    __shared__ int32_t s_cols[RG ? 1 : 128];
     // 1024-byte aligned ring (swizzle atoms); pointer arithmetic on smem_raw keeps the shared
     // address space visible to the compiler (plain C++ stores to the staging area stay STS)
     unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -165,6 +173,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         const int64_t n0 = (tile / p.u_o) * kSBatch;
         const int64_t m0 = int64_t(tbm) * p.tm;
         const bool last = u + stride >= p.n_units;
+        const bool stage_last = last && !CONV;  // conv: direct NHWC stores for every unit
         const int64_t c0 = n0 + q * 32;     // this warp's first column
         const bool ok = c0 < p.n_cols;      // n_cols % 64 == 0: a warp's 32 columns are all in or out
         const int nrows = RG ? p.g * 16 : p.tm;
@@ -184,7 +193,32 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // (a loop over row blocks, not unrolled): the epilogue runs cold in the instruction cache.
         auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two) {
             const int64_t grow0 = m0 + int64_t(rb) * 16;
-            if constexpr (OUT_BF16) {
+            if constexpr (CONV) {
+                // NHWC: this lane's pixel c0 + lane holds output channels grow0 .. grow0 + 15
+                // contiguously -> 32 (bf16) / 64 (f32) bytes of 16-byte stores, ReLU fused
+                float x[16];
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
+                    if (p.relu) x[m] = fmaxf(x[m], 0.0f);
+                }
+                if (!ok) return;
+                if constexpr (OUT_BF16) {
+                    uint32_t w[8];
+#pragma unroll
+                    for (int h = 0; h < 8; ++h) {
+                        const __nv_bfloat162 v2 = __floats2bfloat162_rn(x[2 * h], x[2 * h + 1]);
+                        w[h] = *reinterpret_cast<const uint32_t *>(&v2);
+                    }
+                    uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + (c0 + lane) * p.ld_out + grow0);
+                    g[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                    g[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                } else {
+                    float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + (c0 + lane) * p.ld_out + grow0);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) g[h] = make_float4(x[4 * h], x[4 * h + 1], x[4 * h + 2], x[4 * h + 3]);
+                }
+            } else if constexpr (OUT_BF16) {
                 // all 8 shuffles first, then the stores (plain C++ stores: a volatile asm store with
                 // a memory clobber serialised every pair behind its shuffle, ~90 cycles each)
                 uint32_t words[8];
@@ -198,7 +232,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     const __nv_bfloat162 v2 = odd ? __floats2bfloat162_rn(recv, x1) : __floats2bfloat162_rn(x0, recv);
                     words[h] = *reinterpret_cast<const uint32_t *>(&v2);
                 }
-                if (last) {
+                if (stage_last) {
                     // [row][64 B], 64B swizzle: 16-byte chunk ^ (row / 2) % 4 (row = m + odd)
                     unsigned char *sb = wstage_p + rs * 16 * 64 + (k2 & 3) * 4 + odd * 64;
 #pragma unroll
@@ -214,7 +248,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 float x[16];
 #pragma unroll
                 for (int m = 0; m < 16; ++m) x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
-                if (last) {
+                if (stage_last) {
                     // [row][128 B], 128B swizzle: chunk ^ row % 8
                     unsigned char *sb = wstage_p + rs * 16 * 128 + (lane & 3) * 4;
 #pragma unroll
@@ -227,14 +261,33 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
         };
-        // row block i's TMEM columns: row groups -> column 16 i (one partial); whole tiles -> its
-        // two d_i partials cols[2 i], cols[2 i + 1] (TC16 relayout)
+        // rows 16 i .. 16 i + 15: row groups -> TMEM columns 16 i (one partial); whole tiles ->
+        // per element-row block rb of BM rows inside them, its (up to) two partials at TMEM
+        // columns cols[2 rb], cols[2 rb + 1] of the slice relayout (-1: no such partial)
         auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16]) {
             if constexpr (RG) {
                 TMEM_LD_32x32b_X16(lane_base + uint32_t(i * 16), va);
             } else {
-                TMEM_LD_32x32b_X16(lane_base + uint32_t(cols[2 * i]), va);
-                TMEM_LD_32x32b_X16(lane_base + uint32_t(cols[2 * i + 1]), vb);
+#pragma unroll
+                for (int j = 0; j < 16 / BM; ++j) {
+                    const int rb = i * (16 / BM) + j;
+                    const int ca = cols[2 * rb], cb = cols[2 * rb + 1];
+                    uint32_t *pa = va + j * BM, *pb = vb + j * BM;
+                    if constexpr (BM == 16) {
+                        TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
+                        if (cb >= 0) TMEM_LD_32x32b_X16(lane_base + uint32_t(cb), vb);
+                    } else if constexpr (BM == 8) {
+                        TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
+                        if (cb >= 0) TMEM_LD_32x32b_X8(lane_base + uint32_t(cb), pb);
+                    } else {
+                        TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
+                        if (cb >= 0) TMEM_LD_32x32b_X4(lane_base + uint32_t(cb), pb);
+                    }
+                    if (cb < 0) {
+#pragma unroll
+                        for (int m = 0; m < BM; ++m) pb[m] = 0u;
+                    }
+                }
             }
         };
         // software pipeline over row blocks: row block i+1's TMEM loads are in flight while row
@@ -258,9 +311,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
         }
-        if (last) {
+        if (stage_last) {
             // the ring is idle (this CTA's last MMA has completed): this warp's rows go out by its
-            // own TMA stores (32 columns x 16 rows per row block (groups) / x 64 rows (tiles))
+            // own TMA stores (32 columns x 16 rows per row block (groups) / x tm/2 rows (tiles))
             fence_async_smem();
             __syncwarp();
             if (threadIdx.x == 0) K5_MARK(11);
@@ -270,7 +323,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0),
                                        int32_t(m0) + rec[kRgRows + r] * 16);
                 } else {
-                    for (int r = rb0; r < rb1; r += 4)
+                    for (int r = rb0; r < rb1; r += p.tm / 32)
                         tma_store_2d_g(&omap, wstage + uint32_t(r * 16 * kRowBytes), int32_t(c0), int32_t(m0) + r * 16);
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -335,7 +388,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int32_t b = __shfl_sync(0xffffffffu, e1, s & 31);
             return s < 32 ? a : b;
         };
-        const int w_rows = p.tm * p.d_i;  // whole tiles: relayout W tile of a step
+        const int w_rows = p.w_rows;  // whole tiles: slice-relayout W tile of a step (nsl x mma_n rows)
         // whole tiles: expect_tx (I slab + W tile) and the W box of a step, by warp 6
         auto issue_w = [&](int st, int tbm, int32_t word) {
             const int j = word >> 16;
@@ -370,6 +423,13 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int tbm = int(tile % p.u_o);
             const int rgi = RG ? int(u % p.n_rg) : 0;
             const int64_t n0 = (tile / p.u_o) * kSBatch;
+            // conv: the unit's 128 output pixels = image b0, output rows h0.. (or whole images)
+            int cb0 = 0, ch0 = 0;
+            if constexpr (CONV) {
+                const int64_t hw = int64_t(p.img_h) * p.img_w;
+                cb0 = int(n0 / hw);
+                ch0 = int(n0 - int64_t(cb0) * hw) / p.img_w;
+            }
             if (tbm != tbm_cur) { load_steps(tbm); tbm_cur = tbm; }
             if (RG && rgi != rg_cur) { load_rec(rgi); rg_cur = rgi; }
             const int lo = RG ? __shfl_sync(0xffffffffu, rl, kRgLo) : 0;
@@ -395,6 +455,14 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                             mbar_expect_tx(&full[st], uint32_t(len * kPieceBytes));
                             tma_load_3d(ring + size_t(st) * SB, &imaps.m[len - 1], &full[st], 0,
                                         krow + lo * 16, int32_t(n0 / 64));
+                        } else if constexpr (CONV) {
+                            // K rows [krow, krow + tk) = tap (ti, tj), channels [c0, c0 + tk): per
+                            // 64-channel atom one 4-D box of the 128 tap-shifted pixels (OOB = padding)
+                            const int tap = krow / p.c_in, c0 = krow - tap * p.c_in;
+                            const int ti = tap / p.kw, tj = tap - ti * p.kw;
+                            for (int a = 0; a < p.tk / 64; ++a)
+                                tma_load_4d(ring + size_t(st) * SB + a * (kSBatch * 128), &imap, &full[st], c0 + 64 * a,
+                                            tj - p.pad, ch0 * p.stride + ti - p.pad, cb0);
                         } else {
                             tma_load_3d(ring + size_t(st) * SB, &imap, &full[st], 0, krow, int32_t(n0 / 64));
                         }
@@ -422,14 +490,19 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
         const uint32_t tmem_d = *tmem_slot;
-        constexpr uint32_t kN = RG ? 16u : 32u;
-        // D f32, A/B bf16, A MN-major (I slab), B K-major (W rows), N, M = 128
-        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (0u << 16) |
-                                   ((kN >> 3) << 17) | (uint32_t(kSBatch >> 4) << 24);
+        // D f32, A/B bf16, A MN-major (SDMM: I slab) or K-major (conv: NHWC pixel x channel
+        // box), B K-major (W rows), N = 16 (row groups) / the slice union (whole tiles), M = 128
+        const uint32_t kN = RG ? 16u : uint32_t(p.mma_n);
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((CONV ? 0u : 1u) << 15) | (0u << 16) |
+                               ((kN >> 3) << 17) | (uint32_t(kSBatch >> 4) << 24);
         const uint32_t ring_a = smem_u32(ring);
-        // A: MN-major, 128B swizzle: 64-column atoms spaced by the rows staged per atom (a
-        // whole slab, or one 16-row piece), 8-row groups 1024 B apart
-        const uint64_t a_desc_t = smem_desc(ring_a, uint32_t(p.tk) * 128u, 1024, 2u);
+        // A: SDMM -- MN-major, 128B swizzle: 64-column atoms spaced by the rows staged per atom (a
+        // whole slab, or one 16-row piece), 8-row groups 1024 B apart; conv -- K-major, 128B
+        // swizzle, [64-channel atom][128 pixels][128 B]
+        const uint64_t a_desc_t = CONV ? smem_desc(ring_a, 0, 1024, 2u) : smem_desc(ring_a, uint32_t(p.tk) * 128u, 1024, 2u);
+        // whole tiles: B offset of slice kb (mma_n rows of 32 B), D column of slice kb
+        const uint32_t b_slice16 = uint32_t(p.mma_n * 32) >> 4, d_slice = uint32_t(p.mma_n);
+        const int nsl = p.nsl;
         // B: K-major W rows (row groups: d_t slots per row; whole tiles: 16-slot relayout rows)
         constexpr uint32_t w_row = RG ? 64u : 32u;  // d_t = 32 slots (stream_shape_ok)
         const uint64_t b_desc0 = RG ? smem_desc(smem_u32(wres), 0, 8 * w_row, swizzle_layout_code(int(w_row)))
@@ -495,13 +568,19 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                                                   b_st + uint32_t(r * ((16 * w_row) >> 4) + ink * 2), idesc,
                                                   (s > 0 || ink > 0) ? 1u : 0u);
                         } else {
-                            // TC16 relayout: 8 column blocks of 16 slab rows, one N = 32 MMA each
+                            // slice relayout: K16 slice kb of the step (16 slab rows / 16 channels)
+                            // times the union of the rows reading it, one N = mma_n MMA each (TC16:
+                            // 8 column blocks of 16, N = 32)
                             const uint64_t b_st = b_desc0 + st16;
                             const uint32_t acc = s > 0 ? 1u : 0u;
 #pragma unroll
-                            for (int kb = 0; kb < 8; ++kb)
-                                tc_mma<false>(d_base + uint32_t(kb * 32), a_st + uint32_t(kb * 16 * 8),
-                                              b_st + uint32_t(kb * ((32 * 32) >> 4)), idesc, acc);
+                            for (int kb = 0; kb < 8; ++kb) {
+                                if (kb >= nsl) break;
+                                const uint32_t a16 = CONV ? uint32_t(kb / 4) * uint32_t(kSBatch * 128 / 16) + uint32_t(kb % 4) * 2u
+                                                          : uint32_t(kb * 16 * 8);
+                                tc_mma<false>(d_base + uint32_t(kb) * d_slice, a_st + a16,
+                                              b_st + uint32_t(kb) * b_slice16, idesc, acc);
+                            }
                         }
                         tc_commit(&empty[st]);
                         if (s == p.d_o - 1) {
@@ -529,7 +608,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         if constexpr (RG) {
             for (int i = threadIdx.x; i < p.n_rg * kRgWords; i += 128) s_rg[i] = p.rg[i];
         } else {
-            for (int i = threadIdx.x; i < p.u_i * p.d_i; i += 128) s_cols[i] = p.cols[i];
+            for (int i = threadIdx.x; i < p.n_cols_tab; i += 128) s_cols[i] = p.cols[i];
         }
         asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
@@ -538,7 +617,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             // the CTA's last unit is the only exposed epilogue: warps 4-7 (idle by then) take
             // the second half of its row blocks
             const bool last = u + stride >= p.n_units;
-            const int nrb = RG ? p.g : p.u_i;
+            const int nrb = RG ? p.g : p.tm / 16;
             const int split = (last && nrb >= 2) ? nrb / 2 : nrb;
             drain(u, it, 0, split, s_cols, RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr, false);
         }
@@ -548,7 +627,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // read from global memory: these warps never synchronised on the epilogue's copies)
         const int64_t n_mine = (p.n_units - first + stride - 1) / stride;
         const int64_t u = first + (n_mine - 1) * stride;
-        const int nrb = RG ? p.g : p.u_i;
+        const int nrb = RG ? p.g : p.tm / 16;
         if (n_mine > 0 && nrb >= 2) {
             drain(u, n_mine - 1, nrb / 2, nrb, p.cols, RG ? p.rg + int(u % p.n_rg) * kRgWords : nullptr, true);
         }
@@ -595,21 +674,169 @@ size_t tables_words(const ChainDims &c) { return a16w(size_t(c.u_o) * c.d_o) + a
 
 }  // namespace
 
-// TC16 shape (the one K5 covers): g_r (1,1), 16 x 16 element blocks, g_i (8,8) of degree 2
-// (its relayout exists, sdmm_gather.cu), 128 x 128 tiles, at most 64 steps per tile-row.
+// TC16 shape: g_r (1,1), 16 x 16 element blocks, g_i (8,8) of degree 2 (its relayout exists,
+// sdmm_gather.cu), 128 x 128 tiles, at most 64 steps per tile-row -- whole tiles on K4's
+// relayout, or row groups.
 int stream_shape_ok(const ChainDims &c) {
     return c.rm == 1 && c.rk == 1 && c.bm == 16 && c.bk == 16 && c.u_i == 8 && c.v_i == 8 && c.d_i == 2 &&
            c.tm == 128 && c.tk == 128 && c.d_t == 32 && c.d_o <= kMaxDo && c.v_o < (1 << 16) &&
            gather_relayout_ok(c);
 }
 
-size_t stream_prep_bytes(const ChainDims &c) {
-    if (!stream_shape_ok(c)) return 0;
-    return 4 * tables_words(c) + size_t(c.rows) * c.row_nnz * 2;
+namespace {
+// Slice relayout (any other g_b that tiles K16, e.g. the 8 x 8 / 4 x 4 element blocks of the
+// small-channel VGG / WRN layers and the `tc` factorisation): a step's K range is cut into
+// K16 slices; slice kb multiplies the 16 slab rows (channels) [16 kb, 16 kb + 16) by the union
+// of the tile's rows that have a nonzero there -- a per-matrix constant, since g_r (x) g_i (x)
+// g_b repeats in every tile -- padded to `mma_n` rows with zeros.  The prepared values hold,
+// per W tile (tbm, j), the [slice][union row][16 k] dense K-major operand (zeros where a union
+// row's block does not cover a k); each output row has at most two partials (the slices its
+// d_i column blocks fall in), summed in the epilogue.  MMA work per step is tk/16 MMAs of
+// N = mma_n, whatever the block size (TC16 is the special case union = d_r blocks of 16).
+struct SliceDims {
+    int nsl, mma_n, d_r;
+};
+bool slice_dims(const ChainDims &c, SliceDims *sd) {
+    if (c.rm != 1 || c.rk != 1) return false;
+    if ((c.tm != 64 && c.tm != 128) || (c.tk != 64 && c.tk != 128)) return false;
+    if (c.bm != 4 && c.bm != 8 && c.bm != 16) return false;
+    if (!(c.bk <= 16 ? 16 % c.bk == 0 : c.bk % 16 == 0)) return false;
+    if (c.d_i * std::max(1, c.bk / 16) > 2) return false;  // <= 2 partials per row
+    if (c.d_t != c.d_i * c.bk || c.d_o > kMaxDo || c.v_o >= (1 << 16)) return false;
+    if ((int64_t(c.u_i) * c.d_i) % c.v_i) return false;
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    const int per = (c.bk < 16 ? 16 / c.bk : 1) * d_r * c.bm;
+    const int n = (std::min(per, c.tm) + 15) & ~15;
+    if (n > 256 || (c.tk / 16) * n > 256) return false;
+    if (c.tm / c.bm * 2 > 128) return false;  // cols table
+    sd->nsl = c.tk / 16;
+    sd->mma_n = n;
+    sd->d_r = d_r;
+    return true;
+}
+// slice section of the prepared buffer: [steps i32 u_o x d_o][cols i32 (tm/bm) x 2][map rows i32
+// nsl x mma_n][map k-offsets i16 nsl x mma_n x 16][values bf16 u_o x d_o x nsl x mma_n x 16]
+struct SliceLayout {
+    size_t steps, cols, rows, offs, vals, total;  // word offsets (vals: byte offset), bytes
+};
+SliceLayout slice_layout(const ChainDims &c, const SliceDims &sd) {
+    SliceLayout l;
+    const size_t w = size_t(sd.nsl) * sd.mma_n;
+    l.steps = 0;
+    l.cols = a16w(size_t(c.u_o) * c.d_o);
+    l.rows = l.cols + a16w(size_t(c.tm / c.bm) * 2);
+    l.offs = l.rows + a16w(w);
+    l.vals = 4 * (l.offs + a16w(w * 8));
+    l.total = l.vals + size_t(c.u_o) * c.d_o * w * 16 * 2;
+    return l;
 }
 
-int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
-                   const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
+__global__ void slice_values_kernel(const __nv_bfloat16 *__restrict__ values, int64_t row_nnz, int tm, int d_t,
+                                    int d_o, int nsl, int mma_n, const int32_t *__restrict__ mrows,
+                                    const int16_t *__restrict__ moffs, int64_t total,
+                                    __nv_bfloat16 *__restrict__ outv) {
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int kk = int(idx % 16);
+        const int64_t r = idx / 16;                  // (tile, slice, union row)
+        const int n = int(r % (int64_t(nsl) * mma_n));  // slice * mma_n + union row
+        const int64_t tj = r / (int64_t(nsl) * mma_n);  // W tile (tbm, j)
+        const int64_t tbm = tj / d_o, j = tj % d_o;
+        const int row = mrows[n], off = moffs[n * 16 + kk];
+        __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
+        if (row >= 0 && off >= 0) v = values[(tbm * tm + row) * row_nnz + j * d_t + off];
+        outv[idx] = v;
+    }
+}
+
+// step words [tbm][s] = adjacency slot j << 16 | K-block (the schedule order of the steps)
+void step_words(const ChainDims &c, const int32_t *adj_o_host, const int32_t *sched_host, int32_t *tab) {
+    for (int u = 0; u < c.u_o; ++u)
+        for (int s = 0; s < c.d_o; ++s) {
+            const int j = sched_host ? sched_host[size_t(u) * c.d_o + s] : s;
+            tab[size_t(u) * c.d_o + s] = (j << 16) | adj_o_host[size_t(u) * c.d_o + j];
+        }
+}
+
+int slice_prepare(const ChainDims &c, const SliceDims &sd, const void *values, const int32_t *adj_o_host,
+                  const int32_t *sched_host, const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
+    const SliceLayout l = slice_layout(c, sd);
+    std::vector<int32_t> tab(l.vals / 4, -1);
+    step_words(c, adj_o_host, sched_host, tab.data());
+    const int n_rb = c.tm / c.bm, w = sd.nsl * sd.mma_n;
+    // does row block rb read slab column k (relative to the tile)?  -> its slot offset, else -1
+    auto offset_of = [&](int rb, int k) {
+        const int cb = k / c.bk;
+        int rank = 0;
+        bool hit = false;
+        for (int ink = 0; ink < c.d_i; ++ink) {
+            const int nb = adj_i_host[rb * c.d_i + ink];
+            if (nb == cb) hit = true;
+            else if (nb < cb) ++rank;
+        }
+        return hit ? rank * c.bk + k % c.bk : -1;
+    };
+    int32_t *cols = tab.data() + l.cols, *mrows = tab.data() + l.rows;
+    int16_t *moffs = reinterpret_cast<int16_t *>(tab.data() + l.offs);
+    std::vector<int> nparts(n_rb, 0);
+    for (int kb = 0; kb < sd.nsl; ++kb) {
+        int pos = 0;
+        for (int rb = 0; rb < n_rb; ++rb) {
+            bool touches = false;
+            for (int k = 16 * kb; k < 16 * kb + 16 && !touches; ++k) touches = offset_of(rb, k) >= 0;
+            if (!touches) continue;
+            if ((pos + 1) * c.bm > sd.mma_n || nparts[rb] >= 2) {
+                set_error("rbgp4_prepare: slice %d needs more than %d rows / row block %d more than 2 partials", kb,
+                          sd.mma_n, rb);
+                return RBGP4_EUNSUPPORTED;
+            }
+            cols[rb * 2 + nparts[rb]++] = kb * sd.mma_n + pos * c.bm;
+            for (int m = 0; m < c.bm; ++m) {
+                const int n = kb * sd.mma_n + pos * c.bm + m;
+                mrows[n] = rb * c.bm + m;
+                for (int kk = 0; kk < 16; ++kk) moffs[n * 16 + kk] = int16_t(offset_of(rb, 16 * kb + kk));
+            }
+            ++pos;
+        }
+        for (int n = kb * sd.mma_n + pos * c.bm; n < (kb + 1) * sd.mma_n; ++n)
+            for (int kk = 0; kk < 16; ++kk) moffs[n * 16 + kk] = -1;
+    }
+    for (int rb = 0; rb < n_rb; ++rb)
+        if (nparts[rb] == 0) {
+            set_error("rbgp4_prepare: row block %d has no nonzero", rb);
+            return RBGP4_EUNSUPPORTED;
+        }
+    (void)w;
+    cudaError_t e = cudaMemcpyAsync(k5, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) {
+        const int32_t *mr = static_cast<const int32_t *>(k5) + l.rows;
+        const int16_t *mo = reinterpret_cast<const int16_t *>(static_cast<const int32_t *>(k5) + l.offs);
+        __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + l.vals);
+        const int64_t total = int64_t(c.u_o) * c.d_o * sd.nsl * sd.mma_n * 16;
+        slice_values_kernel<<<int(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs)), 256, 0, stream>>>(
+            static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, sd.nsl, sd.mma_n, mr, mo,
+            total, outv);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) note_launch();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);  // `tab` is a host temporary
+    if (e != cudaSuccess) {
+        set_error("rbgp4_prepare: writing the K5 slice relayout: %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    return RBGP4_OK;
+}
+}  // namespace
+
+size_t stream_prep_bytes(const ChainDims &c) {
+    if (stream_shape_ok(c)) return 4 * tables_words(c) + size_t(c.rows) * c.row_nnz * 2;
+    SliceDims sd;
+    if (slice_dims(c, &sd)) return slice_layout(c, sd).total;
+    return 0;
+}
+
+static int tc16_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
+                        const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
     const size_t n_steps = size_t(c.u_o) * c.d_o;
     std::vector<int32_t> tab(tables_words(c), 0);
     for (int u = 0; u < c.u_o; ++u)
@@ -703,6 +930,14 @@ int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_
     return RBGP4_OK;
 }
 
+int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
+                   const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
+    if (stream_shape_ok(c)) return tc16_prepare(c, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+    SliceDims sd;
+    if (!slice_dims(c, &sd)) return RBGP4_EUNSUPPORTED;
+    return slice_prepare(c, sd, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+}
+
 namespace {
 struct SPlan {
     SParams p;
@@ -713,41 +948,52 @@ struct SPlan {
 
 constexpr size_t kSSmemCap = 227 * 1024;
 
-int stream_plan(const ChainDims &c, int out_dtype, SPlan *pl) {
-    if (!stream_shape_ok(c) || c.n_cols % 64 != 0) return 0;
+int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl) {
     if (opts().stream == 0) return 0;
+    const bool tc16 = stream_shape_ok(c);
+    SliceDims sd{};
+    if (tc16) sd = SliceDims{8, 32, 2};
+    else if (!slice_dims(c, &sd)) return 0;
+    // (a warp's 32 columns / pixels are all in or out; conv: OOB images of the last tile load as zeros)
+    if (c.n_cols % (conv ? 32 : 64) != 0) return 0;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
     SParams p{};
     p.n_cols = c.n_cols;
     p.ld_out = c.ld_out;
     p.u_o = c.u_o; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.u_i = c.u_i; p.d_i = c.d_i; p.d_t = c.d_t;
+    p.nsl = sd.nsl;
+    p.mma_n = sd.mma_n;
+    p.w_rows = sd.nsl * sd.mma_n;
+    p.n_cols_tab = c.tm / c.bm * 2;
     const int64_t tiles = c.u_o * ((c.n_cols + kSBatch - 1) / kSBatch);
-    // whole tiles when they fill ~2/3 of the SMs, else the largest row group that does
+    // whole tiles when they fill ~2/3 of the SMs, else (TC16 SDMM) the largest row group that does
     int g = 8;
-    if (opts().stream_g > 0) g = opts().stream_g;
-    else if (tiles < 96) g = tiles * 2 >= 96 ? 4 : tiles * 4 >= 96 ? 2 : 1;
-    if (g != 1 && g != 2 && g != 4 && g != 8) return 0;
+    if (tc16 && !conv) {
+        if (opts().stream_g > 0) g = opts().stream_g;
+        else if (tiles < 96) g = tiles * 2 >= 96 ? 4 : tiles * 4 >= 96 ? 2 : 1;
+        if (g != 1 && g != 2 && g != 4 && g != 8) return 0;
+    }
     const bool rg = g < 8;
-    p.g = rg ? g : c.u_i;
+    p.g = rg ? g : c.tm / 16;
     p.n_rg = rg ? 8 / g : 1;
     p.n_units = tiles * p.n_rg;
     // row groups: stage = the longest possible column-block range (8 pieces) + the group's W rows
     p.i_bytes = rg ? 8 * kPieceBytes : c.tk * kSBatch * 2;
-    // whole tiles: a stage = I slab + the step's relayout W tile; row groups: the I range only,
-    // the unit's W resident (d_o steps x G*16 rows x d_t slots)
-    const int w_bytes = rg ? 0 : c.tm * c.d_i * 32;
+    // whole tiles: a stage = I slab (conv: pixel x channel box) + the step's relayout W tile;
+    // row groups: the I range only, the unit's W resident (d_o steps x G*16 rows x d_t slots)
+    const int w_bytes = rg ? 0 : p.w_rows * 32;
     p.stage_bytes = int((size_t(p.i_bytes) + w_bytes + 1023) & ~size_t(1023));
     p.wres_bytes = rg ? int((size_t(c.d_o) * g * 16 * c.d_t * 2 + 1023) & ~size_t(1023)) : 0;
-    p.acc_cols = rg ? g * 16 : c.tm * c.d_i;
+    p.acc_cols = rg ? g * 16 : p.w_rows;
     const unsigned grid = unsigned(std::min<int64_t>(p.n_units, kNumSMs));
     const bool multi = p.n_units > int64_t(grid);
     int tcols = 32;
     while (tcols < p.acc_cols * (multi ? 2 : 1)) tcols *= 2;
     if (tcols > 512) return 0;
     p.tmem_cols = tcols;
-    // the last unit is staged in the ring: 4 warps x nrows x 32 columns of the output
-    const size_t staging = size_t(rg ? g * 16 : c.tm) * kSBatch * oelt;
-    const size_t statics = (rg ? size_t(kMaxRg) * kRgWords * 4 : 256) + 64;
+    // the last unit is staged in the ring (SDMM): 4 warps x nrows x 32 columns of the output
+    const size_t staging = conv ? 0 : size_t(rg ? g * 16 : c.tm) * kSBatch * oelt;
+    const size_t statics = (rg ? size_t(kMaxRg) * kRgWords * 4 : 512) + 64;
     const size_t fixed = 1024 + 1024;  // alignment slack + barrier block
     if (fixed + statics + p.wres_bytes + 2 * size_t(p.stage_bytes) > kSSmemCap) return 0;
     int ns = int(std::min<size_t>(16, (kSSmemCap - fixed - statics - p.wres_bytes) / p.stage_bytes));
@@ -764,22 +1010,93 @@ int stream_plan(const ChainDims &c, int out_dtype, SPlan *pl) {
     pl->rg = rg;
     return 1;
 }
+
+using StreamKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, IMaps, SParams, void *);
+
+template <bool OB>
+StreamKernel pick_kernel(bool rg, bool conv, int bm) {
+    if (rg) return stream_kernel<OB, true, false, 16>;
+    if (conv) return bm == 16 ? stream_kernel<OB, false, true, 16> : bm == 8 ? stream_kernel<OB, false, true, 8>
+                                                                             : stream_kernel<OB, false, true, 4>;
+    return bm == 16 ? stream_kernel<OB, false, false, 16> : bm == 8 ? stream_kernel<OB, false, false, 8>
+                                                                    : stream_kernel<OB, false, false, 4>;
+}
+
+// the whole-tile W map: slice-relayout rows of 16 k (32 B), box = one step's nsl x mma_n rows
+int encode_slice_w(CUtensorMap *wmap, const ChainDims &c, const SParams &p, const void *vals) {
+    auto enc = encode_fn();
+    cuuint64_t wdims[2] = {16, cuuint64_t(c.u_o) * c.d_o * p.w_rows};
+    cuuint64_t wstrides[1] = {32};
+    cuuint32_t wbox[2] = {16, cuuint32_t(p.w_rows)};
+    cuuint32_t e2[2] = {1, 1};
+    CUresult r = enc(wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(vals), wdims, wstrides, wbox, e2,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
+        return RBGP4_ECUDA;
+    }
+    return RBGP4_OK;
+}
+
+// (cols table, relayout values) of the whole-tile path: K4's relayout for TC16, else the slices
+void whole_tile_views(const ChainDims &c, const void *k4, const void *k5, const int32_t **cols, const void **vals) {
+    if (stream_shape_ok(c)) {
+        gather_prep_views(c, k4, cols, vals);
+        return;
+    }
+    SliceDims sd;
+    slice_dims(c, &sd);
+    const SliceLayout l = slice_layout(c, sd);
+    *cols = static_cast<const int32_t *>(k5) + l.cols;
+    *vals = static_cast<const char *>(k5) + l.vals;
+}
+
+int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &imap, const CUtensorMap &wmap,
+                   const CUtensorMap &omap, const IMaps &imaps, void *out, cudaStream_t stream) {
+    StreamKernel kern = oelt == 2 ? pick_kernel<true>(pl.rg, conv, bm) : pick_kernel<false>(pl.rg, conv, bm);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(K5): %s", cudaGetErrorString(e));
+        (void)cudaGetLastError();
+        return RBGP4_ECUDA;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = pl.smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = opts().pdl ? 1 : 0;
+    note_kernel(conv ? "K5 conv" : pl.rg ? "K5 rows" : "K5 stream");
+    e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
+    if (e != cudaSuccess) {
+        set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
+    RBGP4_CHECK_LAUNCH("stream_kernel launch");
+    return RBGP4_OK;
+}
 }  // namespace
 
 int stream_supported(const ChainDims &c, int out_dtype) {
     SPlan pl;
-    return stream_plan(c, out_dtype, &pl);
+    return stream_plan(c, out_dtype, false, &pl);
 }
 
 int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void *k5, const void *inp, void *out,
                   cudaStream_t stream) {
     SPlan pl;
-    if (!stream_plan(c, out_dtype, &pl) || k4 == nullptr || k5 == nullptr) return RBGP4_EUNSUPPORTED;
+    if (!stream_plan(c, out_dtype, false, &pl) || k5 == nullptr || (stream_shape_ok(c) && k4 == nullptr))
+        return RBGP4_EUNSUPPORTED;
     if (c.n_cols == 0) return RBGP4_OK;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
     const int32_t *cols;
     const void *rvals;
-    gather_prep_views(c, k4, &cols, &rvals);
+    whole_tile_views(c, k4, k5, &cols, &rvals);
     SParams &p = pl.p;
     static int launch_seq = 0;  // debug builds: launch slots for tools/step_timeline.py
     if (p.debug & 2048) p.slot = launch_seq++ & 15;
@@ -803,7 +1120,7 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
     for (int len = pl.rg ? 1 : 8; len <= 8; ++len) {
         cuuint64_t dims[3] = {64, cuuint64_t(c.cols), cuuint64_t(c.n_cols / 64)};
         cuuint64_t strides[2] = {cuuint64_t(c.ld_in) * 2, 128};
-        cuuint32_t box[3] = {64, cuuint32_t(16 * len), 2};
+        cuuint32_t box[3] = {64, cuuint32_t(pl.rg ? 16 * len : c.tk), 2};
         cuuint32_t e3[3] = {1, 1, 1};
         CUtensorMap *m = pl.rg ? &imaps.m[len - 1] : &imap;
         CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(inp), dims, strides, box,
@@ -815,46 +1132,25 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
         }
     }
     if (pl.rg) imap = imaps.m[7];
-    {
-        cuuint64_t wdims[2], wstrides[1];
-        cuuint32_t wbox[2];
-        const void *wbase;
-        CUtensorMapSwizzle swz;
-        if (pl.rg) {
-            // row-permuted values as (d_t slots, tm rows, u_o * d_o tiles (tbm, j)); box = a
-            // group's G*16 rows of all d_o tiles of its tile-row: the unit's whole W, one load
-            cuuint64_t d3[3] = {cuuint64_t(c.d_t), cuuint64_t(c.tm), cuuint64_t(c.u_o) * c.d_o};
-            cuuint64_t s3[2] = {cuuint64_t(c.d_t) * 2, cuuint64_t(c.tm) * c.d_t * 2};
-            cuuint32_t b3[3] = {cuuint32_t(c.d_t), cuuint32_t(pl.p.g * 16), cuuint32_t(c.d_o)};
-            cuuint32_t e3[3] = {1, 1, 1};
-            CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(rgvals), d3, s3, b3, e3,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,  // d_t = 32: 64-byte rows
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
-                return RBGP4_ECUDA;
-            }
-            wbase = nullptr;
-        } else {      // relayout tiles: (16, u_o * d_o * tm * d_i), box (16, tm * d_i)
-            wbase = rvals;
-            wdims[0] = 16; wdims[1] = cuuint64_t(c.u_o) * c.d_o * c.tm * c.d_i;
-            wstrides[0] = 32;
-            wbox[0] = 16; wbox[1] = cuuint32_t(c.tm * c.d_i);
-            swz = CU_TENSOR_MAP_SWIZZLE_32B;
+    if (pl.rg) {
+        // row-permuted values as (d_t slots, tm rows, u_o * d_o tiles (tbm, j)); box = a
+        // group's G*16 rows of all d_o tiles of its tile-row: the unit's whole W, one load
+        cuuint64_t d3[3] = {cuuint64_t(c.d_t), cuuint64_t(c.tm), cuuint64_t(c.u_o) * c.d_o};
+        cuuint64_t s3[2] = {cuuint64_t(c.d_t) * 2, cuuint64_t(c.tm) * c.d_t * 2};
+        cuuint32_t b3[3] = {cuuint32_t(c.d_t), cuuint32_t(pl.p.g * 16), cuuint32_t(c.d_o)};
+        cuuint32_t e3[3] = {1, 1, 1};
+        CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(rgvals), d3, s3, b3, e3,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,  // d_t = 32: 64-byte rows
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
+            return RBGP4_ECUDA;
         }
-        if (wbase) {
-            cuuint32_t e2[2] = {1, 1};
-            CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(wbase), wdims, wstrides,
-                             wbox, e2, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-            if (r != CUDA_SUCCESS) {
-                set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
-                return RBGP4_ECUDA;
-            }
-        }
+    } else if (int rc = encode_slice_w(&wmap, c, p, rvals)) {
+        return rc;
     }
     {
-        // O (n_cols, rows) row-major; box = one epilogue warp's 32 columns x (16 | tm) rows
+        // O (n_cols, rows) row-major; box = one epilogue warp's 32 columns x (16 | tm/2) rows
         cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
         cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
         cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : c.tm / 2)};
@@ -868,32 +1164,91 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
             return RBGP4_ECUDA;
         }
     }
-    void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, IMaps, SParams, void *) =
-        oelt == 2 ? (pl.rg ? stream_kernel<true, true> : stream_kernel<true, false>)
-                  : (pl.rg ? stream_kernel<false, true> : stream_kernel<false, false>);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
-    if (e != cudaSuccess) {
-        set_error("cudaFuncSetAttribute(K5): %s", cudaGetErrorString(e));
-        (void)cudaGetLastError();
+    return launch_planned(pl, oelt, false, c.bm, imap, wmap, omap, imaps, out, stream);
+}
+
+// Implicit-im2col convolution on K5 (whole tiles): a unit = 128 output pixels (whole output
+// rows of one image, or whole images) x one tile-row of output channels; the I slab of a step
+// is the tap-shifted NHWC box of those pixels (one 4-D TMA box per 64-channel atom, OOB =
+// zero padding, element strides for stride 2), O is NHWC with ReLU fused.
+namespace {
+bool conv_tiles_ok(const ChainDims &c, const rbgp4_conv_desc *cv, int oelt) {
+    const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
+    const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
+    const int64_t hw = int64_t(oh) * ow;
+    const bool tiles = (kSBatch <= hw) ? (hw % kSBatch == 0 && kSBatch % ow == 0) : (kSBatch % hw == 0);
+    const int th = kSBatch <= hw ? kSBatch / ow : oh;
+    const int tb = kSBatch <= hw ? 1 : int(kSBatch / hw);
+    return tiles && cv->c_in % 64 == 0 && cv->c_in % c.tk == 0 && (cv->stride == 1 || cv->stride == 2) &&
+           ow * cv->stride <= 256 && th * cv->stride <= 256 && tb <= 256 && cv->kh == cv->kw &&
+           c.n_cols % 32 == 0 && (int64_t(c.rows) * oelt) % 16 == 0;
+}
+}  // namespace
+
+int stream_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype) {
+    SPlan pl;
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    return cv != nullptr && stream_plan(c, out_dtype, true, &pl) && conv_tiles_ok(c, cv, oelt);
+}
+
+int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *k4, const void *k5,
+                       const void *x, void *out, cudaStream_t stream) {
+    SPlan pl;
+    const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
+    if (!stream_plan(c, out_dtype, true, &pl) || !conv_tiles_ok(c, cv, oelt) || k5 == nullptr ||
+        (stream_shape_ok(c) && k4 == nullptr))
+        return RBGP4_EUNSUPPORTED;
+    if (c.n_cols == 0) return RBGP4_OK;
+    const int32_t *cols;
+    const void *rvals;
+    whole_tile_views(c, k4, k5, &cols, &rvals);
+    SParams &p = pl.p;
+    p.cols = cols;
+    p.steps = static_cast<const int32_t *>(k5);
+    p.rg = nullptr;
+    p.ld_out = int64_t(c.rows);  // NHWC: a pixel row holds c_out channels
+    const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
+    const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
+    p.c_in = cv->c_in;
+    p.img_h = oh;
+    p.img_w = ow;
+    p.kw = cv->kw;
+    p.pad = cv->pad;
+    p.stride = cv->stride;
+    p.relu = cv->relu;
+    RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0,
+                  "conv input / output must be 16-byte aligned");
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
         return RBGP4_ECUDA;
     }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(pl.grid);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = pl.smem;
-    cfg.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = opts().pdl ? 1 : 0;
-    e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
-    if (e != cudaSuccess) {
-        set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
-        return RBGP4_ECUDA;
+    const int64_t hw = int64_t(oh) * ow;
+    const int th = kSBatch <= hw ? int(kSBatch / ow) : oh;
+    const int tb = kSBatch <= hw ? 1 : int(kSBatch / hw);
+    CUtensorMap imap, wmap, omap;
+    memset(&omap, 0, sizeof(omap));
+    IMaps imaps;
+    memset(&imaps, 0, sizeof(imaps));
+    {
+        const cuuint32_t sd = cuuint32_t(cv->stride);
+        cuuint32_t estr[4] = {1, sd, sd, 1};  // strided conv: every stride-th input pixel
+        const int64_t ihw = int64_t(cv->height) * cv->width;
+        cuuint64_t dims[4] = {cuuint64_t(cv->c_in), cuuint64_t(cv->width), cuuint64_t(cv->height),
+                              cuuint64_t(cv->batch)};
+        cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
+                                 cuuint64_t(ihw) * cv->c_in * 2};
+        cuuint32_t box[4] = {64, cuuint32_t(ow) * sd, cuuint32_t(th) * sd, cuuint32_t(tb)};
+        CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K5 conv input) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
     }
-    RBGP4_CHECK_LAUNCH("stream_kernel launch");
-    return RBGP4_OK;
+    if (int rc = encode_slice_w(&wmap, c, p, rvals)) return rc;
+    return launch_planned(pl, oelt, true, c.bm, imap, wmap, omap, imaps, out, stream);
 }
 
 }  // namespace rbgp4

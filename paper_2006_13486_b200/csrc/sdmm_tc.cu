@@ -858,6 +858,7 @@ int launch_typed(const TcPlan &pl, const CUtensorMap &map, const CUtensorMap &wm
     }
     cfg.attrs = attrs;
     cfg.numAttrs = na;
+    note_kernel(pl.p.conv ? "K2 conv" : "K2 tc");
     e = cudaLaunchKernelEx(&cfg, kern, map, wmap, omap, pl.p, static_cast<const E *>(values), adj_o, adj_i,
                            out, wsp);
     if (e != cudaSuccess) {
@@ -998,7 +999,7 @@ size_t k4_bytes(const ChainDims &c, int compute) {
     return compute == RBGP4_COMPUTE_BF16 ? gather_prep_bytes(c) : 0;
 }
 size_t k5_bytes(const ChainDims &c, int compute) {
-    return compute == RBGP4_COMPUTE_BF16 && k4_bytes(c, compute) ? stream_prep_bytes(c) : 0;
+    return compute == RBGP4_COMPUTE_BF16 ? stream_prep_bytes(c) : 0;
 }
 }  // namespace
 
@@ -1126,10 +1127,10 @@ int launch_tc(const ChainDims &c, int compute, int out_dtype, const void *values
     if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
     pl.p.prep = static_cast<const uint16_t *>(prep);
     pl.p.sched = tc_prep_schedule(c, pl, prep);
-    // TC16 shape, prepared: the streamed kernel (K5)
+    // prepared bf16 with a K5 section (TC16 or slice relayout): the streamed kernel (K5)
     {
         const void *k4 = tc_prep_k4(c, pl, compute, prep), *k5 = tc_prep_k5(c, pl, compute, prep);
-        if (compute == RBGP4_COMPUTE_BF16 && k4 && k5 && stream_supported(c, out_dtype))
+        if (compute == RBGP4_COMPUTE_BF16 && k5 && (k4 || !stream_shape_ok(c)) && stream_supported(c, out_dtype))
             return launch_stream(c, out_dtype, k4, k5, inp, out, stream);
     }
     // g_b blocks >= 16 x 16: the gathered-block kernel (K4), no densification
@@ -1322,6 +1323,11 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
     if (c.n_cols == 0) return RBGP4_OK;
     pl.p.prep = static_cast<const uint16_t *>(prep);
     pl.p.sched = tc_prep_schedule(c, pl, prep);
+    {
+        const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep), *k5 = tc_prep_k5(c, pl, RBGP4_COMPUTE_BF16, prep);
+        if (k5 && (k4 || !stream_shape_ok(c)) && stream_conv_supported(c, cv, out_dtype))
+            return launch_stream_conv(c, cv, out_dtype, k4, k5, x, out, stream);
+    }
     {
         const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep);
         if (gather_conv_supported(c, cv, out_dtype, k4 != nullptr))

@@ -209,6 +209,15 @@ __device__ __forceinline__ uint32_t swz(uint32_t off, int span) {
     return off ^ (((off >> 7) & mask) << 4);
 }
 
+#define TMEM_LD_32x32b_X8(taddr, r)                                                        \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"     \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),  \
+                   "=r"(r[6]), "=r"(r[7])                                                   \
+                 : "r"(taddr))
+#define TMEM_LD_32x32b_X4(taddr, r)                                                        \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"                 \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])                           \
+                 : "r"(taddr))
 #define TMEM_LD_32x32b_X16(taddr, r)                                                       \
     asm volatile(                                                                          \
         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"    \
