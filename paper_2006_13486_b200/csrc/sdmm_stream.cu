@@ -28,8 +28,8 @@
 //   -- for a CTA's last unit, the only exposed one -- staging in the then idle ring and its
 //   own TMA tensor store (no cross-warp barrier).
 //
-// Warps (256 threads): 0-3 epilogue (TMEM lane = batch column), 4 / 7 I producers (even /
-// odd steps), 6 W producer, 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
+// Warps (384 threads): 0-3 epilogue (TMEM lane = batch column), 4 and 7-11 I producers (steps
+// round-robin), 6 W producer, 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
 // output rows; fixed step order.
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -44,6 +44,12 @@ namespace rbgp4 {
 namespace {
 
 constexpr int kSBatch = 128;                  // MMA M: batch columns per unit
+// 12 warps: 0-3 epilogue, 4 and 7-11 I producers (steps round-robin: a TMA box costs its
+// issuing thread ~450 cycles, tools/tma_par_bench.cu), 5 MMA, 6 W producer
+constexpr int kSThreads = 384;
+constexpr int kHaloAtom = (180 * 128 + 1023) & ~1023;  // halo conv: 18 x 10 pixels x 128 B, 1024-aligned
+constexpr int kIProd = 6;
+constexpr int kProdThreads = 32 * (kIProd + 1);  // the producer warps 4, 6, 7..11 (barrier 3)
 constexpr int kMaxDo = 64;                    // steps per tile-row held in producer registers
 constexpr int kRgWords = 48;                  // one row-group record (int32 words)
 constexpr int kMaxRg = 8;                     // row groups per tile (G = 1)
@@ -70,7 +76,7 @@ __device__ unsigned long long g_k5_mark[16];
 __device__ unsigned long long g_k5_seq[16][3][160];  // [slot][entry | exit | first I issued][CTA]
 __device__ unsigned long long g_k5_smark[16][4];
 __device__ unsigned long long g_k5_trace[3][64];  // [0] I producer issued, [1] MMA saw full, [2] MMAs issued
-__device__ unsigned long long g_k5_epi[16];       // CTA 0 warp 0, last unit: after each epilogue step
+__device__ unsigned long long g_k5_epi[16];       // CTA 0: units 0-3 [epilogue start, end (warp 0), MMA acc_empty wait start, end]
 __device__ __forceinline__ unsigned long long k5_gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -96,6 +102,8 @@ struct SParams {
     int32_t nsl, mma_n, w_rows, n_cols_tab;
     // implicit-im2col convolution (NHWC): input channels, OUTPUT map, kernel width, pad, stride
     int32_t c_in, img_h, img_w, kw, pad, stride, relu;
+    // halo conv: stride of a staged 64-channel halo atom (bytes), strips per image (rows, columns)
+    int32_t halo_atom, strips_y, strips_x, epi2;  // epi2: warps 8-11 are a second epilogue group
     int32_t debug, slot;
 };
 
@@ -105,16 +113,21 @@ __device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t 
 }
 
 // RG: row-group units (TC16 only); CONV: A = tap-shifted NHWC boxes (K-major), O = NHWC;
+// HALO (conv, one channel block, 3x3 stride 1): a unit is a strip of 16 output rows x 8 output
+// columns of one image; its 18 x 10 halo is staged ONCE (one 4-D box per 64-channel atom) and
+// the nine taps are A-descriptor row offsets into it (SBO = 10 halo pixels), the unit's W (all
+// taps) stays resident -- the taps no longer re-read the input from L2 (9x -> 1.4x);
 // BM: element-block rows of the chain (16 / 8 / 4) -- the granularity of the epilogue's
 // TMEM partial loads
-template <bool OUT_BF16, bool RG, bool CONV, int BM>
-__global__ void __launch_bounds__(256, 1)
+template <bool OUT_BF16, bool RG, bool CONV, int BM, bool HALO = false>
+__global__ void __launch_bounds__(kSThreads, 1)
 stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
               const __grid_constant__ CUtensorMap omap, const __grid_constant__ IMaps imaps, const SParams p,
               void *__restrict__ out) {
     extern __shared__ unsigned char smem_raw[];
     __shared__ int32_t s_rg[RG ? kMaxRg * kRgWords : 1];
     __shared__ int32_t s_cols[RG ? 1 : 128];
+    __shared__ uint32_t s_tap[HALO ? 18 : 1];  // halo: per tap, A row offset / B tile offset (16-byte units)
     // 1024-byte aligned ring (swizzle atoms); pointer arithmetic on smem_raw keeps the shared
     // address space visible to the compiler (plain C++ stores to the staging area stay STS)
     unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -144,7 +157,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         SB = l * kPieceBytes;
         NS = min(16, p.ring_bytes / SB);
     }
-    constexpr int kThreads = 256;
+    constexpr int kThreads = kSThreads;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int64_t first = blockIdx.x, stride = gridDim.x;
     const int upt = RG ? p.n_rg : 1;  // units per tile
@@ -175,7 +188,17 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         const bool last = u + stride >= p.n_units;
         const bool stage_last = last && !CONV;  // conv: direct NHWC stores for every unit
         const int64_t c0 = n0 + q * 32;     // this warp's first column
-        const bool ok = c0 < p.n_cols;      // n_cols % 64 == 0: a warp's 32 columns are all in or out
+        const bool ok = HALO || c0 < p.n_cols;  // n_cols % 64 == 0: a warp's 32 columns are all in or out
+        // conv: this lane's output pixel (NHWC row); halo strips: (r, c) = (m / 8, m % 8) of the
+        // unit's 16 x 8 strip, m = TMEM lane
+        int64_t pix = c0 + lane;
+        if constexpr (HALO) {
+            const int64_t per_img = int64_t(p.strips_y) * p.strips_x;
+            const int64_t bimg = u / per_img;
+            const int sy = int((u - bimg * per_img) / p.strips_x), sx = int(u % p.strips_x);
+            const int m = q * 32 + lane;
+            pix = (bimg * p.img_h + sy * 16 + (m >> 3)) * p.img_w + sx * 8 + (m & 7);
+        }
         const int nrows = RG ? p.g * 16 : p.tm;
         unsigned char *wstage_p = ring + q * nrows * kRowBytes;  // [row][kRowBytes] for columns c0..
         const uint32_t wstage = smem_u32(wstage_p);
@@ -186,6 +209,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
         tc_fence_after();
         if (last && threadIdx.x == 0) { K5_MARK(3); K5_SMARK(2); }
+#if RBGP4_DEBUG
+        if (trace && threadIdx.x == 0 && !helper && it < 4) g_k5_epi[4 * it] = clock64() - c_entry;
+#endif
         const uint32_t tmem_d = *tmem_slot;
         const uint32_t lane_base = tmem_d + (uint32_t(q * 32) << 16) + uint32_t(b * p.acc_cols);
         // 16 fp32 rows (row block rb, staging slot rs) of this lane's column -> bf16 pairs packed
@@ -210,11 +236,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         const __nv_bfloat162 v2 = __floats2bfloat162_rn(x[2 * h], x[2 * h + 1]);
                         w[h] = *reinterpret_cast<const uint32_t *>(&v2);
                     }
-                    uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + (c0 + lane) * p.ld_out + grow0);
+                    uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + pix * p.ld_out + grow0);
                     g[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     g[1] = make_uint4(w[4], w[5], w[6], w[7]);
                 } else {
-                    float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + (c0 + lane) * p.ld_out + grow0);
+                    float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + pix * p.ld_out + grow0);
 #pragma unroll
                     for (int h = 0; h < 4; ++h) g[h] = make_float4(x[4 * h], x[4 * h + 1], x[4 * h + 2], x[4 * h + 3]);
                 }
@@ -310,6 +336,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[b]);
+#if RBGP4_DEBUG
+            if (trace && threadIdx.x == 0 && it < 4) g_k5_epi[4 * it + 1] = clock64() - c_entry;
+#endif
         }
         if (stage_last) {
             // the ring is idle (this CTA's last MMA has completed): this warp's rows go out by its
@@ -334,7 +363,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
     };
 
-    if (warp == 4 || warp == 6 || warp == 7) {
+    // halo conv with a heavy epilogue (p.epi2: 128 rows of 4 x 4 blocks, ~1.5x the unit's MMA
+    // time): warps 8-11 are a second epilogue group (the unit's second half of rows)
+    const bool kEpiB = HALO && p.epi2;
+    const bool epi_b = kEpiB && warp >= 8;
+    if (warp == 4 || (warp >= 6 && !epi_b)) {
         // ========================== TMA producers ==========================
         // warp 6: expect_tx + the W box of every step (before griddepcontrol.wait for the first
         // ring's worth: weights are never the previous grid's output); warp 4: barrier init, then
@@ -346,7 +379,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // issuing thread ~300-450 cycles, which bounds one issuer at ~35-60 B/clk
         // (tools/stream_bench.cu); two issuers keep the row-group ranges (~16 KB boxes) and
         // the whole slabs ahead of the MMAs
-        const int64_t iparity = warp == 7 ? 1 : 0;
+        // producer index of this warp among the I producers 4, 7, 8, .. (steps round-robin).  At
+        // most NS producers take part: a producer's next step must be at most one ring round
+        // ahead of its last, or its parity wait on `empty` could pass two phases early.
+        const int iparity = warp == 4 ? 0 : warp - 6;
+        const int n_ip = min(HALO ? 2 : kIProd, NS);
         // lane l holds the step words l and l + 32 of the current tile-row (shuffled out)
         int32_t e0 = 0, e1 = 0, rl = 0;
         auto load_steps = [&](int tbm) {
@@ -366,7 +403,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 #endif
         if (warp == 4 && lane == 0) {
             for (int i = 0; i < NS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-            for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+            for (int i = 0; i < 2; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], kEpiB ? 8 : 4); }
             mbar_init(wfull, 1);
             mbar_init(wempty, 1);
             mbar_init(last_full, 1);
@@ -379,8 +416,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         __syncwarp();
         // barrier 3 (warps 4, 6, 7): the barrier init is visible to warps 6 and 7; barrier 1
         // (setup, all warps): arrive only -- producers never wait for TMEM or the tables
-        if (warp == 4) asm volatile("barrier.arrive 3, 96;" ::: "memory");
-        else asm volatile("barrier.sync 3, 96;" ::: "memory");
+        const int bar3 = kEpiB ? 96 : kProdThreads;  // the producer warps
+        if (warp == 4) asm volatile("barrier.arrive 3, %0;" ::"r"(bar3) : "memory");
+        else asm volatile("barrier.sync 3, %0;" ::"r"(bar3) : "memory");
         asm volatile("barrier.arrive 1, %0;" ::"n"(kThreads) : "memory");
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         auto step_word = [&](int s) -> int32_t {
@@ -407,6 +445,46 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             }
             __syncwarp();
         };
+        if constexpr (HALO) {
+            // W: the tile-row's d_o tap tiles, resident, loaded once (never the previous grid's output)
+            if (wprod) {
+                if (first < p.n_units && elect_one()) {
+                    mbar_expect_tx(wfull, uint32_t(p.d_o * w_rows * 32));
+                    for (int j = 0; j < p.d_o; ++j)
+                        tma_load_2d(wres + size_t(j) * w_rows * 32, &wmap, wfull, 0, j * w_rows);
+                }
+                __syncwarp();
+            } else {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                // I: one halo box set per unit, units round-robin over the I producers
+                int st = 0, ipu = 0;
+                uint32_t ph = 0;
+                const int n_iu = min(2, NS);
+                const int64_t per_img = int64_t(p.strips_y) * p.strips_x;
+                const uint32_t hbytes = uint32_t(p.tk / 64) * 180u * 128u;
+                for (int64_t u = first, gu = 0; u < p.n_units; u += stride, ++gu) {
+                    const int cst = st;
+                    const uint32_t cph = ph;
+                    if (++st == NS) { st = 0; ph ^= 1u; }
+                    const int mine = ipu;
+                    if (++ipu == n_iu) ipu = 0;
+                    if (mine != iparity) continue;
+                    if (gu >= NS) mbar_wait(&empty[cst], cph ^ 1u);
+                    const int64_t bimg = u / per_img;
+                    const int sy = int((u - bimg * per_img) / p.strips_x), sx = int(u % p.strips_x);
+                    if (elect_one()) {
+                        mbar_expect_tx(&full[cst], hbytes);
+                        for (int a = 0; a < p.tk / 64; ++a)
+                            tma_load_4d(ring + size_t(cst) * SB + size_t(a) * p.halo_atom, &imap, &full[cst], 64 * a,
+                                        sx * 8 - 1, sy * 16 - 1, int32_t(bimg));
+                    }
+                    __syncwarp();
+#if RBGP4_DEBUG
+                    if (trace && lane == 0 && gu < 64) g_k5_trace[0][gu] = clock64() - c_entry;
+#endif
+                }
+            }
+        } else {
         const int pre = min(NS, p.d_o);
         if (wprod && first < p.n_units) {
             if constexpr (RG) issue_wres(tbm_cur, rg_cur, 0);
@@ -416,7 +494,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         if (!wprod) asm volatile("griddepcontrol.wait;" ::: "memory");
         if (warp == 4 && lane == 0) K5_MARK(8);
         int64_t g = 0, it = 0;
-        int rs_st = 0;
+        int rs_st = 0, ip = 0;  // ring slot, producer of the current step (g mod kIProd)
         uint32_t rs_ph = 0;
         for (int64_t u = first; u < p.n_units; u += stride, ++it) {
             const int64_t tile = u / upt;
@@ -443,11 +521,13 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 const int st = rs_st;
                 const uint32_t ph = rs_ph;
                 if (++rs_st == NS) { rs_st = 0; rs_ph ^= 1u; }
+                const int ipc = ip;
+                if (++ip == n_ip) ip = 0;
                 const int32_t word = step_word(s);
                 if (wprod) {
                     if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                     if (g >= pre) issue_w(st, tbm, word);
-                } else if ((g & 1) == iparity) {
+                } else if (ipc == iparity) {
                     if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                     const int32_t krow = (word & 0xFFFF) * p.tk;
                     if (elect_one()) {
@@ -481,6 +561,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
         }
+        }  // !HALO
     } else if (warp == 5) {
         // ========================= TMEM allocation + MMA issue =========================
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -537,7 +618,13 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     }
                     mbar_wait(wfull, uint32_t(it & 1));
                 }
+#if RBGP4_DEBUG
+                if (trace && lane == 0 && it < 4) g_k5_epi[4 * it + 2] = clock64() - c_entry;
+#endif
                 mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
+#if RBGP4_DEBUG
+                if (trace && lane == 0 && it < 4) g_k5_epi[4 * it + 3] = clock64() - c_entry;
+#endif
                 tc_fence_after();
                 const uint32_t d_base = tmem_d + uint32_t(b * p.acc_cols);
                 for (int s = 0; s < p.d_o; ++s, ++g) {
@@ -596,7 +683,70 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
             }
         };
-        if constexpr (RG) {
+        // halo conv: one ring stage per unit; the nine taps (step words: adjacency slot j << 16 | tap)
+        // are row offsets ti * 10 + tj into the staged 18 x 10 halo (SW128 K-major rows of 128 B,
+        // 8-pixel groups 10 rows apart), the tap's W tile the resident slot j
+        auto halo_loop = [&]() {
+            constexpr int kTaps = 9;
+            // per tap (in 16-byte units): the A start row ti * 10 + tj inside the halo, the B tile of
+            // its adjacency slot j in the resident W (kept in shared memory: 18 values held in
+            // registers across the unit loop were spilled and reloaded per MMA)
+            if (lane < kTaps) {
+                const int32_t w = __ldg(p.steps + lane);  // u_o = 1: tile-row 0
+                const int t = w & 0xFFFF;
+                s_tap[lane] = uint32_t((t / 3) * 10 + t % 3) * (128u >> 4);
+                s_tap[kTaps + lane] = uint32_t(w >> 16) * (uint32_t(p.w_rows * 32) >> 4);
+            }
+            __syncwarp();
+            const uint64_t a_halo = smem_desc(ring_a, 0, 10 * 128, 2u);
+            const uint64_t b_res = smem_desc(smem_u32(wres), 0, 8 * 32, swizzle_layout_code(32));
+            mbar_wait(wfull, 0u);
+            int st = 0;
+            uint32_t ph = 0;
+            int64_t it = 0;
+            for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+                const int b = int(it & 1);
+                const int cst = st;
+                const uint32_t cph = ph;
+                if (++st == NS) { st = 0; ph ^= 1u; }
+                mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
+                mbar_wait(&full[cst], cph);
+                tc_fence_after();
+#if RBGP4_DEBUG
+                if (trace && lane == 0 && it < 64) g_k5_trace[1][it] = clock64() - c_entry;
+#endif
+                if (elect_one()) {
+                    const uint32_t d_base = tmem_d + uint32_t(b * p.acc_cols);
+                    const uint32_t stage16 = uint32_t(cst * SB) >> 4;
+#pragma unroll 1
+                    for (int s = 0; s < kTaps; ++s) {
+                        const uint64_t a_s = a_halo + stage16 + s_tap[s];
+                        const uint64_t b_s = b_res + s_tap[kTaps + s];
+                        const uint32_t acc = s > 0 ? 1u : 0u;
+#pragma unroll
+                        for (int kb = 0; kb < 8; ++kb) {
+                            if (kb >= nsl) break;
+                            // (base offset 0: the 128B swizzle acts on the absolute address bits,
+                            // so a start shifted by any number of 128-byte rows reads the rows
+                            // exactly as TMA swizzled them -- tests/test_slices.py)
+                            tc_mma<false>(d_base + uint32_t(kb) * d_slice,
+                                          a_s + uint32_t((kb / 4) * (kHaloAtom >> 4) + (kb % 4) * 2),
+                                          b_s + uint32_t(kb) * b_slice16, idesc, acc);
+                        }
+                    }
+                    tc_commit(&empty[cst]);
+                    tc_commit(&acc_full[b]);
+                    if (u + stride >= p.n_units) tc_commit(last_full);
+#if RBGP4_DEBUG
+                    if (trace && it < 64) g_k5_trace[2][it] = clock64() - c_entry;
+#endif
+                }
+                __syncwarp();
+            }
+        };
+        if constexpr (HALO) {
+            halo_loop();
+        } else if constexpr (RG) {
             if (p.g == 1) mma_loop(std::integral_constant<int, 1>{});
             else if (p.g == 2) mma_loop(std::integral_constant<int, 2>{});
             else mma_loop(std::integral_constant<int, 4>{});
@@ -604,25 +754,32 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             mma_loop(std::integral_constant<int, 0>{});
         }
     } else {
-        // ============================ epilogue (warps 0-3) ============================
-        if constexpr (RG) {
-            for (int i = threadIdx.x; i < p.n_rg * kRgWords; i += 128) s_rg[i] = p.rg[i];
-        } else {
-            for (int i = threadIdx.x; i < p.n_cols_tab; i += 128) s_cols[i] = p.cols[i];
+        // ============================ epilogue (warps 0-3; halo: + 8-11) ============================
+        if (warp < 4) {
+            if constexpr (RG) {
+                for (int i = threadIdx.x; i < p.n_rg * kRgWords; i += 128) s_rg[i] = p.rg[i];
+            } else {
+                for (int i = threadIdx.x; i < p.n_cols_tab; i += 128) s_cols[i] = p.cols[i];
+            }
         }
         asm volatile("barrier.sync 1, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
         int64_t it = 0;
         for (int64_t u = first; u < p.n_units; u += stride, ++it) {
+            const int nrb = RG ? p.g : p.tm / 16;
+            if (kEpiB) {
+                // halo: two groups split every unit's rows (its epilogue is ~1.5x its MMA time)
+                drain(u, it, epi_b ? nrb / 2 : 0, epi_b ? nrb : nrb / 2, s_cols, nullptr, false);
+                continue;
+            }
             // the CTA's last unit is the only exposed epilogue: warps 4-7 (idle by then) take
             // the second half of its row blocks
             const bool last = u + stride >= p.n_units;
-            const int nrb = RG ? p.g : p.tm / 16;
             const int split = (last && nrb >= 2) ? nrb / 2 : nrb;
             drain(u, it, 0, split, s_cols, RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr, false);
         }
     }
-    if (warp >= 4) {
+    if (!kEpiB && warp >= 4 && warp < 8) {
         // warps 4-7 after their roles: the second half of the last unit's row blocks (tables
         // read from global memory: these warps never synchronised on the epilogue's copies)
         const int64_t n_mine = (p.n_units - first + stride - 1) / stride;
@@ -943,12 +1100,21 @@ struct SPlan {
     SParams p;
     size_t smem;
     unsigned grid;
-    bool rg;
+    bool rg, halo;
 };
+
+
+// the halo strip conv: 3 x 3 stride 1 'same', one channel block (c_in == tk), u_o = 1, output
+// maps cut into 16 x 8 strips
+bool halo_ok(const ChainDims &c, const rbgp4_conv_desc *cv) {
+    return cv != nullptr && opts().halo != 0 && c.u_o == 1 && c.d_o == 9 && cv->c_in == c.tk && cv->kh == 3 &&
+           cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->height % 16 == 0 && cv->width % 8 == 0 &&
+           c.n_cols == int64_t(cv->batch) * cv->height * cv->width;
+}
 
 constexpr size_t kSSmemCap = 227 * 1024;
 
-int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl) {
+int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl, const rbgp4_conv_desc *cv = nullptr) {
     if (opts().stream == 0) return 0;
     const bool tc16 = stream_shape_ok(c);
     SliceDims sd{};
@@ -974,16 +1140,29 @@ int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl) {
         if (g != 1 && g != 2 && g != 4 && g != 8) return 0;
     }
     const bool rg = g < 8;
+    const bool halo = conv && halo_ok(c, cv);
     p.g = rg ? g : c.tm / 16;
     p.n_rg = rg ? 8 / g : 1;
     p.n_units = tiles * p.n_rg;
+    if (halo) {
+        p.strips_y = cv->height / 16;
+        p.strips_x = cv->width / 8;
+        p.n_units = int64_t(cv->batch) * p.strips_y * p.strips_x;
+        p.halo_atom = kHaloAtom;
+        p.epi2 = c.tm / c.bm >= 32 ? 1 : 0;
+    }
     // row groups: stage = the longest possible column-block range (8 pieces) + the group's W rows
     p.i_bytes = rg ? 8 * kPieceBytes : c.tk * kSBatch * 2;
     // whole tiles: a stage = I slab (conv: pixel x channel box) + the step's relayout W tile;
     // row groups: the I range only, the unit's W resident (d_o steps x G*16 rows x d_t slots)
-    const int w_bytes = rg ? 0 : p.w_rows * 32;
+    const int w_bytes = rg || halo ? 0 : p.w_rows * 32;
     p.stage_bytes = int((size_t(p.i_bytes) + w_bytes + 1023) & ~size_t(1023));
     p.wres_bytes = rg ? int((size_t(c.d_o) * g * 16 * c.d_t * 2 + 1023) & ~size_t(1023)) : 0;
+    if (halo) {
+        // a stage = the unit's halo (one atom per 64 channels); W of all nine taps resident
+        p.stage_bytes = (c.tk / 64) * kHaloAtom;
+        p.wres_bytes = int((size_t(c.d_o) * p.w_rows * 32 + 1023) & ~size_t(1023));
+    }
     p.acc_cols = rg ? g * 16 : p.w_rows;
     const unsigned grid = unsigned(std::min<int64_t>(p.n_units, kNumSMs));
     const bool multi = p.n_units > int64_t(grid);
@@ -1005,17 +1184,20 @@ int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl) {
     p.debug = DBG(opts().debug);
     p.slot = -1;
     pl->p = p;
-    pl->smem = rg ? fixed + size_t(p.ring_bytes) + p.wres_bytes : fixed + size_t(ns) * p.stage_bytes;
+    pl->smem = (rg ? fixed + size_t(p.ring_bytes) : fixed + size_t(ns) * p.stage_bytes) + p.wres_bytes;
     pl->grid = grid;
     pl->rg = rg;
+    pl->halo = halo;
     return 1;
 }
 
 using StreamKernel = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, IMaps, SParams, void *);
 
 template <bool OB>
-StreamKernel pick_kernel(bool rg, bool conv, int bm) {
+StreamKernel pick_kernel(bool rg, bool conv, int bm, bool halo) {
     if (rg) return stream_kernel<OB, true, false, 16>;
+    if (halo) return bm == 16 ? stream_kernel<OB, false, true, 16, true> : bm == 8 ? stream_kernel<OB, false, true, 8, true>
+                                                                             : stream_kernel<OB, false, true, 4, true>;
     if (conv) return bm == 16 ? stream_kernel<OB, false, true, 16> : bm == 8 ? stream_kernel<OB, false, true, 8>
                                                                              : stream_kernel<OB, false, true, 4>;
     return bm == 16 ? stream_kernel<OB, false, false, 16> : bm == 8 ? stream_kernel<OB, false, false, 8>
@@ -1054,7 +1236,7 @@ void whole_tile_views(const ChainDims &c, const void *k4, const void *k5, const 
 
 int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &imap, const CUtensorMap &wmap,
                    const CUtensorMap &omap, const IMaps &imaps, void *out, cudaStream_t stream) {
-    StreamKernel kern = oelt == 2 ? pick_kernel<true>(pl.rg, conv, bm) : pick_kernel<false>(pl.rg, conv, bm);
+    StreamKernel kern = oelt == 2 ? pick_kernel<true>(pl.rg, conv, bm, pl.halo) : pick_kernel<false>(pl.rg, conv, bm, pl.halo);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(K5): %s", cudaGetErrorString(e));
@@ -1063,7 +1245,7 @@ int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &im
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(pl.grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(kSThreads);
     cfg.dynamicSmemBytes = pl.smem;
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
@@ -1071,7 +1253,7 @@ int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &im
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = opts().pdl ? 1 : 0;
-    note_kernel(conv ? "K5 conv" : pl.rg ? "K5 rows" : "K5 stream");
+    note_kernel(pl.halo ? "K5 halo" : conv ? "K5 conv" : pl.rg ? "K5 rows" : "K5 stream");
     e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
     if (e != cudaSuccess) {
         set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
@@ -1188,14 +1370,14 @@ bool conv_tiles_ok(const ChainDims &c, const rbgp4_conv_desc *cv, int oelt) {
 int stream_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype) {
     SPlan pl;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
-    return cv != nullptr && stream_plan(c, out_dtype, true, &pl) && conv_tiles_ok(c, cv, oelt);
+    return cv != nullptr && stream_plan(c, out_dtype, true, &pl, cv) && (pl.halo || conv_tiles_ok(c, cv, oelt));
 }
 
 int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *k4, const void *k5,
                        const void *x, void *out, cudaStream_t stream) {
     SPlan pl;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
-    if (!stream_plan(c, out_dtype, true, &pl) || !conv_tiles_ok(c, cv, oelt) || k5 == nullptr ||
+    if (!stream_plan(c, out_dtype, true, &pl, cv) || !(pl.halo || conv_tiles_ok(c, cv, oelt)) || k5 == nullptr ||
         (stream_shape_ok(c) && k4 == nullptr))
         return RBGP4_EUNSUPPORTED;
     if (c.n_cols == 0) return RBGP4_OK;
@@ -1239,6 +1421,11 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
         cuuint64_t strides[3] = {cuuint64_t(cv->c_in) * 2, cuuint64_t(cv->width) * cv->c_in * 2,
                                  cuuint64_t(ihw) * cv->c_in * 2};
         cuuint32_t box[4] = {64, cuuint32_t(ow) * sd, cuuint32_t(th) * sd, cuuint32_t(tb)};
+        if (pl.halo) {  // the 18 x 10 halo of a 16 x 8 output strip
+            box[1] = 10;
+            box[2] = 18;
+            box[3] = 1;
+        }
         CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(x), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -88,9 +88,10 @@ def test_slice_sdmm_deterministic():
 
 CONV_CASES = [
     # (c_out, c_in, hw, batch, stride, kernel, what)
-    (64, 64, 32, 2, 1, "K5 conv", "VGG conv0: 4x4 blocks, 64x64 tiles, 4 output rows per tile"),
-    (128, 64, 16, 3, 1, "K5 conv", "VGG conv2: 4x4 blocks, N = 64 slices"),
-    (128, 128, 16, 2, 1, "K5 conv", "VGG conv3: 8x8 blocks"),
+    (64, 64, 32, 2, 1, "K5 halo", "VGG conv0: 4x4 blocks, 64x64 tiles, halo strips"),
+    (128, 64, 16, 3, 1, "K5 halo", "VGG conv2: 4x4 blocks, N = 64 slices, halo strips"),
+    (128, 128, 16, 2, 1, "K5 halo", "VGG conv3: 8x8 blocks, halo strips"),
+    (64, 64, 16, 3, 1, "K5 halo", "one strip column per image row (16 x 16 map, 64 channels)"),
     (256, 128, 8, 5, 1, "K5 conv", "VGG conv5: two images per tile"),
     (512, 256, 4, 16, 1, "K5 conv", "VGG conv10: TC16, eight images per tile"),
     (512, 512, 2, 64, 1, "K5 conv", "VGG conv15: TC16, 32 images per tile"),
@@ -102,6 +103,17 @@ CONV_CASES = [
 @pytest.mark.parametrize("relu", [False, True])
 @pytest.mark.parametrize("out_dtype", ["bf16", "f32"])
 def test_slice_conv_matches_oracle(c_out, c_in, hw, batch, stride, kernel, what, relu, out_dtype):
+    _conv_case(c_out, c_in, hw, batch, stride, kernel, what, relu, out_dtype)
+
+
+@pytest.mark.parametrize("c_out,c_in,hw,batch,stride,kernel,what", CONV_CASES[:4], ids=[c[-1] for c in CONV_CASES[:4]])
+def test_tap_conv_matches_oracle(c_out, c_in, hw, batch, stride, kernel, what):
+    """The same layers with the halo strips off (option halo=0): tap-shifted boxes per step."""
+    with _native.options(halo=0):
+        _conv_case(c_out, c_in, hw, batch, stride, "K5 conv", what, True, "bf16")
+
+
+def _conv_case(c_out, c_in, hw, batch, stride, kernel, what, relu, out_dtype):
     chain = layer_chain(c_out, c_in, 0.875, seed=c_out + c_in + hw)
     w = ks.init_random(chain, 7, precision="f32")
     rng = np.random.default_rng(3)

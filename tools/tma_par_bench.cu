@@ -36,7 +36,10 @@ __global__ void par_kernel(const __grid_constant__ CUtensorMap m, Cfg c) {
         const uint32_t dst = su32(ring + size_t(st) * c.bytes);
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[st])), "r"(c.bytes) : "memory");
         const int2 e = L[s];
-        if (c.dims == 3)
+        if (c.dims == 4)
+            asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                         ::"r"(dst), "l"(&m), "r"(0), "r"((e.x & 3) - 1), "r"(e.x >> 2), "r"(e.y), "r"(su32(&full[st])) : "memory");
+        else if (c.dims == 3)
             asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
                          ::"r"(dst), "l"(&m), "r"(0), "r"(e.x), "r"(e.y), "r"(su32(&full[st])) : "memory");
         else
@@ -67,13 +70,26 @@ int main() {
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
     const double clk = clk_khz * 1e3;
     struct Shape { const char *name; int dims, rows, atoms; };
-    const Shape shapes[] = {{"3d 64x128x2 (32 KB)", 3, 128, 2}, {"3d 64x64x2 (16 KB)", 3, 64, 2},
+    // dims 4: NHWC conv boxes over a (64 ch, W, W, B) bf16 tensor: rows = W (map width), atoms =
+    // image rows per box (W x atoms x (128 / (W x atoms)) images = 128 pixels)
+    const Shape shapes[] = {{"4d conv 32x32 box 32x4x1", 4, 32, 4}, {"4d conv 8x8 box 8x8x2", 4, 8, 8},
+                            {"4d conv 4x4 box 4x4x8", 4, 4, 4},{"3d 64x128x2 (32 KB)", 3, 128, 2}, {"3d 64x64x2 (16 KB)", 3, 64, 2},
                             {"3d 64x32x2 (8 KB)", 3, 32, 2}, {"2d 64x128 (16 KB)", 2, 128, 1},
                             {"2d 64x256 (32 KB)", 2, 256, 1}};
     for (const Shape &sh : shapes) {
         CUtensorMap m;
-        const int bytes = sh.rows * 128 * sh.atoms;
-        if (sh.dims == 3) {
+        const int bytes = sh.dims == 4 ? 128 * 128 : sh.rows * 128 * sh.atoms;
+        int nimg = 0;
+        if (sh.dims == 4) {
+            const int W = sh.rows, hb = sh.atoms, tb = 128 / (W * hb);
+            nimg = int((size_t(K) * N * 2) / (size_t(W) * W * 128));
+            cuuint64_t d4[4] = {64, cuuint64_t(W), cuuint64_t(W), cuuint64_t(nimg)};
+            cuuint64_t s4[3] = {128, cuuint64_t(W) * 128, cuuint64_t(W) * W * 128};
+            cuuint32_t b4[4] = {64, cuuint32_t(W), cuuint32_t(hb > W ? W : hb), cuuint32_t(tb)};
+            cuuint32_t e4[4] = {1, 1, 1, 1};
+            enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, dI, d4, s4, b4, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else if (sh.dims == 3) {
             cuuint64_t d3[3] = {64, cuuint64_t(K), cuuint64_t(N / 64)};
             cuuint64_t s3[2] = {cuuint64_t(N) * 2, 128};
             cuuint32_t b3[3] = {64, cuuint32_t(sh.rows), cuuint32_t(sh.atoms)};
@@ -97,7 +113,15 @@ int main() {
                 const int grid = 148 * cps;
                 const int steps = int((size_t(768) << 20) / (size_t(grid) * nw * bytes));  // ~768 MB moved
                 std::vector<int2> L(size_t(grid) * nw * steps);
-                for (auto &e : L) e = make_int2(int(rng() % (K / sh.rows)) * sh.rows, int(rng() % (N / 64 / sh.atoms)) * sh.atoms);
+                if (sh.dims == 4) {
+                    const int W = sh.rows, hb = sh.atoms > W ? W : sh.atoms, tb = 128 / (W * hb);
+                    // e.x = (output row h0 + tap row) << 2 | tap col (0..2); e.y = first image
+                    for (auto &e : L)
+                        e = make_int2((int(rng() % (W / hb)) * hb + int(rng() % 3) - 1) * 4 + int(rng() % 3),
+                                      int(rng() % (nimg / tb)) * tb);
+                } else {
+                    for (auto &e : L) e = make_int2(int(rng() % (K / sh.rows)) * sh.rows, int(rng() % (N / 64 / sh.atoms)) * sh.atoms);
+                }
                 int2 *dl;
                 cudaMalloc(&dl, L.size() * sizeof(int2));
                 cudaMemcpy(dl, L.data(), L.size() * sizeof(int2), cudaMemcpyHostToDevice);
