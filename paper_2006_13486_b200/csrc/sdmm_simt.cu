@@ -227,6 +227,175 @@ simt_kernel(const SimtParams p, const T *__restrict__ values, const int32_t *__r
     }
 }
 
+// ---------------------------------------------------------------- wide f32 variant
+// The common f32 shape (repetition groups of >= 16 rows, d_t % 4 == 0, 16-byte aligned rows):
+// each thread owns 16 rows of one group x 4 columns, so an I vector (LDS.128) feeds 64 FMAs
+// and the W values of 4 consecutive j are one broadcast LDS.128 per row -- about one shared
+// wavefront per 8 FFMA instead of one per 2 (the generic kernel is shared-memory bound at
+// ~0.22 of the FFMA peak).  W is staged with 16-byte cp.async.  Same per-element order as the
+// reference (sdmm.py:178-204): c = 0; c += w*x over j ascending; acc += c per step.
+constexpr int kWideRows = 16;
+
+template <bool EXACT>
+__global__ void __launch_bounds__(kThreads)
+simt_wide_kernel(const SimtParams p, const float *__restrict__ values, const int32_t *__restrict__ adj_o,
+                 const int32_t *__restrict__ adj_i, const float *__restrict__ inp, float *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int64_t n0 = int64_t(blockIdx.x) * p.tnc;
+    const int64_t tbm = blockIdx.y;
+    const int tid = threadIdx.x;
+    float *wring = reinterpret_cast<float *>(smem_raw);
+    float *iring = wring + 2 * p.tm * p.wstride;
+    int32_t *rowidx = reinterpret_cast<int32_t *>(iring + 2 * p.tk * p.istride);
+    const int wslot = p.tm * p.wstride, islot = p.tk * p.istride;
+    for (int e = tid; e < p.u_i * p.d_t; e += int(blockDim.x)) {
+        int ui = e / p.d_t, j = e - ui * p.d_t;
+        int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
+        rowidx[e] = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;
+    }
+    const int tc = tid % p.cthreads;
+    const int slot0 = (tid / p.cthreads) * kWideRows;  // this thread's 16 group slots
+    const int ui = slot0 / p.g;
+    int urow[kWideRows];
+#pragma unroll
+    for (int i = 0; i < kWideRows; ++i) {
+        const int w = slot0 - ui * p.g + i, rm = w / p.bm, m = w - rm * p.bm;
+        urow[i] = (rm * p.u_i + ui) * p.bm + m;
+    }
+    float acc[kWideRows][4];
+#pragma unroll
+    for (int i = 0; i < kWideRows; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][e] = 0.0f;
+    const int32_t *orow = adj_o + tbm * p.d_o;
+    auto stage_w = [&](int s, float *ws, const float *is_unused) {
+        (void)is_unused;
+        const float *wsrc = values + tbm * p.tm * p.row_nnz + int64_t(s) * p.d_t;
+        const int chunks = p.d_t / 4;
+        for (int e = tid; e < p.tm * chunks; e += int(blockDim.x)) {
+            const int r = e / chunks, c4 = (e - r * chunks) * 4;
+            cp_async16(ws + r * p.wstride + c4, wsrc + r * p.row_nnz + c4, true);
+        }
+    };
+    auto stage_i = [&](int64_t oind, float *is) {
+        const float *isrc = inp + oind * p.tk * p.ld_in + n0;
+        const int chunks = p.tnc / 4;
+        for (int e = tid; e < p.tk * chunks; e += int(blockDim.x)) {
+            const int r = e / chunks, c = (e - r * chunks) * 4;
+            const bool ok = n0 + c < p.n_cols;
+            cp_async16(is + r * p.istride + c, ok ? isrc + r * p.ld_in + c : isrc, ok);
+        }
+    };
+    stage_w(0, wring, nullptr);
+    stage_i(orow[0], iring);
+    cp_async_commit();
+    const int32_t *ridx = rowidx + ui * p.d_t;
+    for (int s = 0; s < p.d_o; ++s) {
+        if (s + 1 < p.d_o) {
+            const int b = (s + 1) & 1;
+            stage_w(s + 1, wring + b * wslot, nullptr);
+            stage_i(orow[s + 1], iring + b * islot);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float *ws = wring + (s & 1) * wslot;
+        const float *is = iring + (s & 1) * islot + tc * 4;
+        float c[kWideRows][4];
+#pragma unroll
+        for (int i = 0; i < kWideRows; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[i][e] = 0.0f;
+#pragma unroll 1
+        for (int j = 0; j < p.d_t; j += 4) {
+            float x[4][4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) load4<float>(is + ridx[j + jj] * p.istride, x[jj]);
+#pragma unroll
+            for (int i = 0; i < kWideRows; ++i) {
+                const float4 w4 = *reinterpret_cast<const float4 *>(ws + urow[i] * p.wstride + j);
+                const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if constexpr (EXACT) c[i][e] = __fadd_rn(c[i][e], __fmul_rn(w[jj], x[jj][e]));
+                        else c[i][e] = __fmaf_rn(w[jj], x[jj][e], c[i][e]);
+                    }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kWideRows; ++i)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][e] = __fadd_rn(acc[i][e], c[i][e]);
+        __syncthreads();
+    }
+    const int64_t col = n0 + tc * 4;
+#pragma unroll
+    for (int i = 0; i < kWideRows; ++i) {
+        float *dst = out + (tbm * p.tm + urow[i]) * p.ld_out + col;
+        if (p.vec_out && col + 3 < p.n_cols) {
+            *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (col + e < p.n_cols) dst[e] = acc[i][e];
+        }
+    }
+}
+
+// wide-variant geometry: (tm / 16) row threads x cthreads column threads (<= 256 per CTA)
+bool wide_ok(const ChainDims &c, const void *values, const void *inp) {
+    if (opts().simt_wide == 0) return false;
+    return c.g % kWideRows == 0 && c.tm % kWideRows == 0 && c.tm / kWideRows * 8 <= kThreads &&
+           c.d_t % 4 == 0 && c.row_nnz % 4 == 0 &&
+           c.ld_in % 4 == 0 && c.n_cols % 4 == 0 && reinterpret_cast<uintptr_t>(values) % 16 == 0 &&
+           reinterpret_cast<uintptr_t>(inp) % 16 == 0;
+}
+
+template <bool EXACT>
+int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, const int32_t *adj_i,
+                const float *inp, float *out, cudaStream_t stream) {
+    SimtParams p{};
+    p.rows = c.rows; p.n_cols = c.n_cols; p.ld_in = c.ld_in; p.ld_out = c.ld_out;
+    p.row_nnz = c.row_nnz; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.rm = c.rm; p.rk = c.rk;
+    p.bm = c.bm; p.bk = c.bk; p.u_i = c.u_i; p.v_i = c.v_i; p.d_i = c.d_i; p.d_t = c.d_t; p.g = c.g;
+    // 16 column threads (64 columns): with ~255 registers per thread, two 128-thread CTAs share
+    // an SM, each with its own 2-stage ring (conv10 ffma: 104 us against 151 us at 32 column
+    // threads and 148 us on the generic kernel, tools/simt_ab.py); below one CTA per SM the
+    // generic kernel's narrower tiles win (conv13, N = 1024: 62 vs 69 us), so it takes those
+    const int rthreads = c.tm / kWideRows;
+    const int64_t row_blocks = c.rows / c.tm;
+    int ct = 16;
+    if (opts().simt_ct == 8 || opts().simt_ct == 16 || opts().simt_ct == 32) ct = opts().simt_ct;
+    else if ((c.n_cols + 4 * ct - 1) / (4 * ct) * row_blocks < kNumSMs) return RBGP4_EUNSUPPORTED;
+    if (ct * rthreads > kThreads) return RBGP4_EUNSUPPORTED;
+    p.cthreads = ct;
+    p.tnc = 4 * ct;
+    p.wstride = c.d_t + 4;
+    p.istride = p.tnc;
+    p.vec_in = 1;
+    p.vec_out = (c.ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    const size_t smem = (2 * (size_t(c.tm) * p.wstride + size_t(c.tk) * p.tnc) * 4 + 15) / 16 * 16 +
+                        size_t(c.u_i) * c.d_t * 4;
+    if (smem > 227 * 1024) return RBGP4_EUNSUPPORTED;
+    auto kern = simt_wide_kernel<EXACT>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) {
+            set_error("cudaFuncSetAttribute(simt wide): %s", cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+    }
+    dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm));
+    note_kernel("K1 simt wide");
+    kern<<<grid, unsigned(rthreads * ct), smem, stream>>>(p, values, adj_o, adj_i, inp, out);
+    RBGP4_CHECK_LAUNCH("simt_wide_kernel launch");
+    return RBGP4_OK;
+}
+
 struct SimtPlan {
     int rt, nch, cthreads;
     size_t smem;
@@ -343,6 +512,13 @@ int launch_simt(const ChainDims &c, int compute, int dtype, const void *values,
     SimtPlan pl;
     const bool exact = compute == RBGP4_COMPUTE_EXACT;
     if (dtype == RBGP4_F32) {
+        if (wide_ok(c, values, inp)) {
+            const int rc = exact ? launch_wide<true>(c, static_cast<const float *>(values), adj_o, adj_i,
+                                                     static_cast<const float *>(inp), static_cast<float *>(out), stream)
+                                 : launch_wide<false>(c, static_cast<const float *>(values), adj_o, adj_i,
+                                                      static_cast<const float *>(inp), static_cast<float *>(out), stream);
+            if (rc != RBGP4_EUNSUPPORTED) return rc;
+        }
         if (!plan_simt<float>(c, &pl)) return RBGP4_EUNSUPPORTED;
         return exact ? dispatch<float, true>(c, pl, values, adj_o, adj_i, inp, out, stream)
                      : dispatch<float, false>(c, pl, values, adj_o, adj_i, inp, out, stream);
