@@ -102,6 +102,12 @@ size_t rbgp4_prepare_size(const rbgp4_desc *desc, int compute);
 int rbgp4_prepare(const rbgp4_desc *desc, int compute, const void *values, const int32_t *adj_o,
                   const int32_t *adj_i, void *prep, size_t prep_bytes, void *stream);
 
+/* Training: rebuild only the value-dependent sections of a prepared buffer (the relayout
+ * copies of `values`) after the values changed; the pattern tables of rbgp4_prepare are kept.
+ * Stream-ordered device work only (no host synchronisation; CUDA-graph capturable). */
+int rbgp4_prepare_values(const rbgp4_desc *desc, int compute, const void *values, void *prep,
+                         size_t prep_bytes, void *stream);
+
 /* rbgp4_sdmm with the prepared buffer of rbgp4_prepare (prep may be NULL). */
 int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int out_dtype,
                         const void *values, const int32_t *adj_o, const int32_t *adj_i,
@@ -138,7 +144,9 @@ int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int wid
  *   grad_values[u, j] = sum_n d_out[u, n] * inp[c(u, j), n],
  * in the (rows, row_nnz) layout of `values` (c = the closed-form column map of the chain).
  * d_out is rows x n_cols (row stride ld_do), inp is cols x n_cols (row stride ld_in);
- * desc->n_cols = n_cols (desc->ld_in/ld_out are ignored).  F32 (fp32 FMA) or F64.
+ * desc->n_cols = n_cols (desc->ld_in/ld_out are ignored).  F32 (fp32 FMA), F64, or BF16:
+ * bf16 d_out / inp on the tensor cores (128 x 128 tiles, g_r = (1,1), bk in {4, 8, 16}) with an
+ * F32 grad_values (fp32 accumulation).
  * The input gradient W^T x dO is rbgp4_sdmm on the transposed chain (a valid RBGP4 chain
  * of the transposed factors; paper_2006_13486_b200.training.transpose builds it).
  */

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b2
 F32, F64, BF16 = 0, 1, 2
 COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
 EXPORTED = (
-    "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size",
+    "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size", "rbgp4_prepare_values",
     "rbgp4_workspace_size", "rbgp4_sdmm_supported", "rbgp4_chain_sdmm",
     "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
@@ -85,6 +85,8 @@ def lib():
     h.rbgp4_sddmm.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
     h.rbgp4_sddmm.restype = i32
     h.rbgp4_prepare.restype = i32
+    h.rbgp4_prepare_values.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, sz, vp]
+    h.rbgp4_prepare_values.restype = i32
     h.rbgp4_conv2d_workspace_size.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc)]
     h.rbgp4_conv2d_workspace_size.restype = sz
     h.rbgp4_conv2d.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc), i32, vp, vp, vp, vp,

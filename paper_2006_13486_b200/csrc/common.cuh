@@ -134,9 +134,17 @@ int stream_supported(const ChainDims &c, int out_dtype);
 int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void *k5, const void *inp, void *out,
                   cudaStream_t stream);
 int stream_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype);
+int stream_prepare_values(const ChainDims &c, const void *values, void *k5, cudaStream_t stream);
+int gather_prepare_values(const ChainDims &c, const void *values, void *k4, cudaStream_t stream);
+int tc_prepare_values(const ChainDims &c, int compute, const void *values, void *prep, size_t bytes,
+                      cudaStream_t stream);
 int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *k4, const void *k5,
                        const void *x, void *out, cudaStream_t stream);
 int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_host, void *k4,
                    cudaStream_t stream);
+// K7: tensor-core weight gradient (sddmm_tc.cu): bf16 dO / I, f32 gradient in the values layout
+int sddmm_tc_supported(const ChainDims &c);
+int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj_i, const void *d_out,
+                    int64_t ld_do, const void *inp, int64_t ld_in, float *grad, cudaStream_t stream);
 
 }  // namespace rbgp4

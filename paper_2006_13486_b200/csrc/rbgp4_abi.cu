@@ -234,6 +234,15 @@ int rbgp4_prepare(const rbgp4_desc *desc, int compute, const void *values, const
     return tc_prepare(c, compute, values, adj_o, adj_i, prep, prep_bytes, static_cast<cudaStream_t>(stream));
 }
 
+int rbgp4_prepare_values(const rbgp4_desc *desc, int compute, const void *values, void *prep, size_t prep_bytes,
+                         void *stream) {
+    ChainDims c;
+    int rc = validate_desc(desc, &c);
+    if (rc != RBGP4_OK) return rc;
+    if (compute != RBGP4_COMPUTE_TF32 && compute != RBGP4_COMPUTE_BF16) return RBGP4_OK;
+    return tc_prepare_values(c, compute, values, prep, prep_bytes, static_cast<cudaStream_t>(stream));
+}
+
 size_t rbgp4_conv2d_workspace_size(const rbgp4_desc *desc, const rbgp4_conv_desc *conv) {
     ChainDims c;
     if (validate_desc(desc, &c) != RBGP4_OK) return 0;

@@ -74,10 +74,14 @@ extern "C" int rbgp4_sddmm(const rbgp4_desc *desc, int dtype, const int32_t *adj
     d.ld_in = d.ld_out = d.n_cols;
     int rc = validate_desc(&d, &c);
     if (rc != RBGP4_OK) return rc;
-    RBGP4_REQUIRE(dtype == RBGP4_F32 || dtype == RBGP4_F64, "rbgp4_sddmm: F32 or F64 operands");
+    RBGP4_REQUIRE(dtype == RBGP4_F32 || dtype == RBGP4_F64 || dtype == RBGP4_BF16,
+                  "rbgp4_sddmm: F32, F64 or BF16 operands");
     RBGP4_REQUIRE(ld_do >= c.n_cols && ld_in >= c.n_cols, "rbgp4_sddmm: leading dimensions < n_cols");
     RBGP4_REQUIRE(adj_o && adj_i && grad_values && (c.n_cols == 0 || (d_out && inp)), "rbgp4_sddmm: null pointer");
     if (c.rows == 0) return RBGP4_OK;
+    if (dtype == RBGP4_BF16)  // tensor cores (sddmm_tc.cu): bf16 dO / I, f32 gradient
+        return launch_sddmm_tc(c, adj_o, adj_i, d_out, ld_do, inp, ld_in, static_cast<float *>(grad_values),
+                               static_cast<cudaStream_t>(stream));
     const int esz = dtype == RBGP4_F32 ? 4 : 8;
     const int64_t n_chunk = std::max<int64_t>(1, std::min<int64_t>(c.n_cols, (32 * 1024) / esz));
     const size_t smem = size_t(n_chunk) * esz;

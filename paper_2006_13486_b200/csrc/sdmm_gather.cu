@@ -1049,6 +1049,22 @@ __global__ void relayout_kernel(const __nv_bfloat16 *__restrict__ values, int64_
 }
 }  // namespace
 
+// values-only refresh of the relayout (training: new values, same pattern): the users table
+// written by gather_prepare stays in the prepared buffer; stream-ordered, no host work
+int gather_prepare_values(const ChainDims &c, const void *values, void *k4, cudaStream_t stream) {
+    const int d_r = c.u_i * c.d_i / c.v_i;
+    const int32_t *cols_d;
+    const void *vals_d;
+    gather_prep_views(c, k4, &cols_d, &vals_d);
+    const int32_t *users_d = reinterpret_cast<const int32_t *>(static_cast<char *>(k4) + a16(size_t(c.u_i) * c.d_i * 4));
+    const int64_t total = c.rows * c.row_nnz;
+    relayout_kernel<<<int(std::min<int64_t>((total + 255) / 256, 4 * kNumSMs)), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, c.bm, c.bk, d_r, users_d, total,
+        static_cast<__nv_bfloat16 *>(const_cast<void *>(vals_d)));
+    RBGP4_CHECK_LAUNCH("relayout_kernel launch");
+    return RBGP4_OK;
+}
+
 size_t gather_prep_bytes(const ChainDims &c) {
     if (!gather_relayout_ok(c)) return 0;
     const int d_r = c.u_i * c.d_i / c.v_i;

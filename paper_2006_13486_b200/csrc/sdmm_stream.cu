@@ -1087,6 +1087,32 @@ static int tc16_prepare(const ChainDims &c, const void *values, const int32_t *a
     return RBGP4_OK;
 }
 
+// values-only refresh (training): the tables of stream_prepare stay; the value copies are
+// rebuilt on the device from the new values (stream-ordered, no host work, graph-capturable)
+int stream_prepare_values(const ChainDims &c, const void *values, void *k5, cudaStream_t stream) {
+    const int64_t total = c.rows * c.row_nnz;
+    const int blocks = int(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
+    if (stream_shape_ok(c)) {
+        const int32_t *perm_d = static_cast<const int32_t *>(k5) + a16w(size_t(c.u_o) * c.d_o) + size_t(14) * kRgWords;
+        __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + 4 * tables_words(c));
+        rg_values_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm,
+                                                     c.d_t, c.d_o, perm_d, total, outv);
+        RBGP4_CHECK_LAUNCH("rg_values_kernel launch");
+        return RBGP4_OK;
+    }
+    SliceDims sd;
+    if (!slice_dims(c, &sd)) return RBGP4_OK;  // no K5 section
+    const SliceLayout l = slice_layout(c, sd);
+    const int32_t *mr = static_cast<const int32_t *>(k5) + l.rows;
+    const int16_t *mo = reinterpret_cast<const int16_t *>(static_cast<const int32_t *>(k5) + l.offs);
+    __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + l.vals);
+    const int64_t tot = int64_t(c.u_o) * c.d_o * sd.nsl * sd.mma_n * 16;
+    slice_values_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 8 * kNumSMs)), 256, 0, stream>>>(
+        static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, sd.nsl, sd.mma_n, mr, mo, tot, outv);
+    RBGP4_CHECK_LAUNCH("slice_values_kernel launch");
+    return RBGP4_OK;
+}
+
 int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
                    const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
     if (stream_shape_ok(c)) return tc16_prepare(c, values, adj_o_host, sched_host, adj_i_host, k5, stream);

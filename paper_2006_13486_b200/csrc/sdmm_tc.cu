@@ -1100,6 +1100,22 @@ int tc_prepare(const ChainDims &c, int compute, const void *values, const int32_
     return RBGP4_OK;
 }
 
+int tc_prepare_values(const ChainDims &c, int compute, const void *values, void *prep, size_t bytes,
+                      cudaStream_t stream) {
+    TcPlan pl;
+    if (!plan_tc(c, compute, &pl)) return RBGP4_EUNSUPPORTED;
+    if (prep == nullptr || bytes < tc_prep_size(c, compute)) {
+        set_error("rbgp4_prepare_values needs the %zu-byte buffer of rbgp4_prepare", tc_prep_size(c, compute));
+        return RBGP4_EWORKSPACE;
+    }
+    RBGP4_REQUIRE(values != nullptr, "rbgp4_prepare_values: null values");
+    if (const void *k5 = tc_prep_k5(c, pl, compute, prep))
+        if (int rc = stream_prepare_values(c, values, const_cast<void *>(k5), stream)) return rc;
+    if (const void *k4 = tc_prep_k4(c, pl, compute, prep))
+        return gather_prepare_values(c, values, const_cast<void *>(k4), stream);
+    return RBGP4_OK;
+}
+
 int tc_supported(const ChainDims &c, int compute, int out_dtype) {
     if (out_dtype != RBGP4_F32 && out_dtype != RBGP4_BF16) {
         set_error("tensor-core modes write f32 or bf16 outputs");

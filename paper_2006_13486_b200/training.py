@@ -9,6 +9,11 @@ masks).  For O = W x I with W an RBGP4 chain matrix:
 
 `SparseLinearFunction` wires both into torch.autograd for a layer y = x W^T whose values are a
 trainable fp32 / fp64 tensor (the pattern stays fixed).
+
+compute="bf16" runs all three products on the tensor cores: the forward and W^T x dO on the
+streamed / gathered kernels (K5 / K4) of the bf16 values (fp32 master values cast per step; the
+layer owns its prepared buffers and refreshes only their value copies, `rbgp4_prepare_values`),
+and dW on K7 (`rbgp4_sddmm` with bf16 operands, fp32 gradient), fp32 accumulation throughout.
 """
 
 from __future__ import annotations
@@ -62,13 +67,17 @@ def sddmm(w, d_out, inp, values_out=None):
             or d_out.shape[1] != inp.shape[1]:
         raise ShapeError(f"sddmm: d_out {tuple(d_out.shape)} / inp {tuple(inp.shape)} do not match "
                          f"W ({w.rows} x {w.cols})")
-    if d_out.dtype != inp.dtype or d_out.dtype not in (t.float32, t.float64):
-        raise ShapeError("sddmm: d_out and inp must share an f32 / f64 dtype")
+    if d_out.dtype != inp.dtype or d_out.dtype not in (t.float32, t.float64, t.bfloat16):
+        raise ShapeError("sddmm: d_out and inp must share an f32 / f64 / bf16 dtype")
     dev = resolve_device(d_out.device)
     d_out = d_out if d_out.stride(1) == 1 else d_out.contiguous()
     inp = inp if inp.stride(1) == 1 else inp.contiguous()
     fmt = device_format(w, dev, d_out.dtype)
-    res = values_out if values_out is not None else t.empty((w.rows, w.row_nnz), dtype=d_out.dtype, device=dev)
+    # bf16 operands: tensor cores, f32 gradient
+    gdt = t.float32 if d_out.dtype == t.bfloat16 else d_out.dtype
+    res = values_out if values_out is not None else t.empty((w.rows, w.row_nnz), dtype=gdt, device=dev)
+    if res.dtype != gdt or tuple(res.shape) != (w.rows, w.row_nnz) or not res.is_contiguous() or res.device != dev:
+        raise ShapeError(f"sddmm: values_out must be a contiguous ({w.rows}, {w.row_nnz}) {gdt} tensor on {dev}")
     desc = make_desc(fmt.desc_fields, d_out.shape[1], d_out.shape[1], d_out.shape[1])
     _native.check(_native.lib().rbgp4_sddmm(
         ctypes.byref(desc), dtype_code(d_out.dtype), fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(),
@@ -110,6 +119,84 @@ def _product(fmt, values, inp, compute):
     return out
 
 
+class _PatternBF16:
+    """Fixed pattern of a bf16 (tensor-core) trainable layer: device formats of W and W^T, and
+    prepared buffers OWNED by the layer (their relayout copies follow the trainable values; the
+    matrix's shared cached buffers are never mutated)."""
+
+    def __init__(self, w, device):
+        t = torch()
+        self.w, self.wt = w, transpose(w)
+        self.perm = t.from_numpy(transpose_permutation(w)).to(device)
+        self.fmt = device_format(w, device, t.bfloat16)
+        self.fmt_t = device_format(self.wt, device, t.bfloat16)
+        self._prep = {}
+
+    def product(self, fmt, values, inp, out_dtype):
+        """O = W x I on the tensor cores with the given bf16 values (the layer's own prep)."""
+        t = torch()
+        lib = _native.lib()
+        out = t.empty((fmt.desc_fields["rows"], inp.shape[1]), dtype=out_dtype, device=inp.device)
+        if inp.shape[1] == 0:
+            return out
+        desc = make_desc(fmt.desc_fields, inp.shape[1], inp.stride(0), out.stride(0))
+        code = _native.COMPUTE["bf16"]
+        stream = stream_handle(inp.device)
+        nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
+        prep = None
+        if nbytes:
+            key = (id(fmt), nbytes)
+            prep = self._prep.get(key)
+            if prep is None:
+                prep = t.empty(nbytes, dtype=t.uint8, device=inp.device)
+                _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, values.data_ptr(), fmt.adj_o.data_ptr(),
+                                                fmt.adj_i.data_ptr(), prep.data_ptr(), nbytes, stream),
+                              "rbgp4_prepare")
+                self._prep[key] = prep
+            else:
+                _native.check(lib.rbgp4_prepare_values(ctypes.byref(desc), code, values.data_ptr(),
+                                                       prep.data_ptr(), nbytes, stream), "rbgp4_prepare_values")
+        need = lib.rbgp4_workspace_size(ctypes.byref(desc), code, _native.BF16)
+        from .sdmm import workspace
+        ws = workspace(inp.device, need, stream) if need else None
+        _native.check(lib.rbgp4_sdmm_prepared(
+            ctypes.byref(desc), code, _native.BF16, dtype_code(out_dtype), values.data_ptr(), fmt.adj_o.data_ptr(),
+            fmt.adj_i.data_ptr(), prep.data_ptr() if prep is not None else None, inp.data_ptr(), out.data_ptr(),
+            ws.data_ptr() if ws is not None else None, need, stream), "rbgp4_sdmm(compute=bf16)")
+        return out
+
+
+def make_sparse_linear_function_bf16():
+    t = torch()
+
+    class SparseLinearBF16(t.autograd.Function):
+        """y = x W^T on the tensor cores: bf16 operands, fp32 accumulation, fp32 outputs and
+        gradients; W = (pattern, fp32 master values)."""
+
+        @staticmethod
+        def forward(ctx, x, values, pattern):
+            vb = values.detach().to(t.bfloat16).contiguous()
+            xt = x.detach().t().to(t.bfloat16).contiguous()
+            ctx.save_for_backward(xt, vb)
+            ctx.pattern = pattern
+            return pattern.product(pattern.fmt, vb, xt, t.float32).t()
+
+        @staticmethod
+        def backward(ctx, dy):
+            xt, vb = ctx.saved_tensors
+            pat = ctx.pattern
+            d_out = dy.t().to(t.bfloat16).contiguous()        # dO (rows x N), bf16
+            grad_x = grad_v = None
+            if ctx.needs_input_grad[0]:
+                vt = vb.reshape(-1)[pat.perm].reshape(pat.wt.rows, pat.wt.row_nnz).contiguous()
+                grad_x = pat.product(pat.fmt_t, vt, d_out, t.float32).t()   # (W^T dO)^T
+            if ctx.needs_input_grad[1]:
+                grad_v = sddmm(pat.w, d_out, xt)                              # K7, f32
+            return grad_x, grad_v, None
+
+    return SparseLinearBF16
+
+
 def make_sparse_linear_function():
     t = torch()
 
@@ -140,17 +227,28 @@ def make_sparse_linear_function():
 
 
 class TrainableSparseLinear:
-    """y = x W^T with a fixed RBGP4 pattern and trainable stored values (fp32 or fp64)."""
+    """y = x W^T with a fixed RBGP4 pattern and trainable stored values.
+
+    compute "exact" / "ffma": SIMT kernels in the values' dtype (fp32 or fp64).  compute "bf16":
+    tensor cores (K5/K4 products, K7 gradient) with fp32 master values, bf16 operands, fp32
+    accumulation and fp32 outputs / gradients."""
 
     def __init__(self, w, device="cuda", compute="ffma"):
         t = torch()
-        if compute not in ("exact", "ffma"):
-            raise InvalidArgumentError("trainable layer computes in 'exact' or 'ffma' (f32 / f64)")
+        if compute not in ("exact", "ffma", "bf16"):
+            raise InvalidArgumentError("trainable layer computes in 'exact', 'ffma' (f32 / f64) or 'bf16'")
         dev = resolve_device(device)
-        self.pattern = _Pattern(w, dev)
-        self.values = t.nn.Parameter(t.from_numpy(np.array(w.values)).to(dev))
         self.compute = compute
-        self._fn = make_sparse_linear_function()
+        if compute == "bf16":
+            self.pattern = _PatternBF16(w, dev)
+            self.values = t.nn.Parameter(t.from_numpy(np.asarray(w.values, dtype=np.float32)).to(dev))
+            self._fn = make_sparse_linear_function_bf16()
+        else:
+            self.pattern = _Pattern(w, dev)
+            self.values = t.nn.Parameter(t.from_numpy(np.array(w.values)).to(dev))
+            self._fn = make_sparse_linear_function()
 
     def __call__(self, x):
+        if self.compute == "bf16":
+            return self._fn.apply(x, self.values, self.pattern)
         return self._fn.apply(x, self.values, self.pattern, self.compute)

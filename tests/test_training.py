@@ -84,3 +84,69 @@ def test_trainable_layer_rejects_mixed_dtypes():
     x = torch.randn(8, w.cols, dtype=torch.float32).cuda()
     with pytest.raises(ks.ShapeError, match="dtype"):
         layer(x)
+
+
+# ---------------------------------------------------------------- tensor-core training (bf16)
+TC_CHAINS = [
+    wl.SweepConfig("tc16", (4, 8), 0.5, (1, 1), (8, 8), 0.75, (16, 16), n_cols=1, seed=4),        # K5 TC16
+    wl.SweepConfig("slice8", (4, 8), 0.5, (1, 1), (16, 16), 0.875, (8, 8), n_cols=1, seed=5),     # K5 slices
+    wl.SweepConfig("tc", (4, 6), 0.5, (1, 1), (16, 16), 0.75, (8, 8), n_cols=1, seed=3),          # K2
+]
+
+
+def _bf16_round(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(torch.bfloat16).double().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", TC_CHAINS, ids=[c.config_id for c in TC_CHAINS])
+@pytest.mark.parametrize("n", [256, 200])
+def test_sddmm_bf16_tensor_cores(cfg, n):
+    """K7: bf16 dO / I, f32 gradient == the f64 pattern gradient of the same bf16-rounded
+    operands (fp32 accumulation: rel-L2 <= 1e-5)."""
+    import torch
+    import oracle
+    from paper_2006_13486_b200 import _native
+    chain = wl.build_chain(cfg)
+    w = ks.init_random(chain, 1, precision="f32")
+    rng = np.random.default_rng(9)
+    d_out = rng.standard_normal((w.rows, n)).astype(np.float32)
+    inp = rng.standard_normal((w.cols, n)).astype(np.float32)
+    db, ib = torch.from_numpy(d_out).to(torch.bfloat16), torch.from_numpy(inp).to(torch.bfloat16)
+    got = training.sddmm(w, db.cuda(), ib.cuda())
+    torch.cuda.synchronize()
+    assert got.dtype == torch.float32 and _native.last_kernel() == "K7 sddmm"
+    ref = _pattern_grad(w, db.double().numpy(), ib.double().numpy())
+    assert oracle.rel_l2(got.cpu().numpy(), ref) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", TC_CHAINS, ids=[c.config_id for c in TC_CHAINS])
+def test_autograd_trainable_layer_bf16(cfg):
+    """Forward, input gradient and weight gradient of a bf16 tensor-core layer against f64
+    references on the same bf16-rounded operands; then two SGD steps (the layer's prepared value
+    copies follow the trainable values) still match."""
+    import torch
+    chain = wl.build_chain(cfg)
+    w = ks.init_random(chain, 2, precision="f32")
+    layer = training.TrainableSparseLinear(w, compute="bf16")
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(256, w.cols, generator=g).cuda().requires_grad_(True)
+    gy = torch.randn(256, w.rows, generator=g).cuda()
+    for step in range(3):
+        x.grad = None
+        layer.values.grad = None
+        y = layer(x)
+        (y * gy).sum().backward()
+        wb = _bf16_round(layer.values.detach().cpu().numpy())
+        dense = ks.RcubsMatrix(w.chain, wb).to_dense()
+        xb = _bf16_round(x.detach().cpu().numpy())
+        gb = _bf16_round(gy.cpu().numpy())
+        rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)  # noqa: E731
+        assert rel(y.detach().cpu().numpy(), xb @ dense.T) < 1e-5, step
+        assert rel(x.grad.cpu().numpy(), gb @ dense) < 1e-5, step
+        want = _pattern_grad(ks.RcubsMatrix(w.chain, wb), gb.T, xb.T)
+        assert rel(layer.values.grad.cpu().numpy(), want) < 1e-5, step
+        with torch.no_grad():
+            layer.values -= 0.05 * layer.values.grad
