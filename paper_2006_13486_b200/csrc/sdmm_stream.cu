@@ -854,6 +854,7 @@ struct SliceDims {
     int nsl, mma_n, d_r;
 };
 bool slice_dims(const ChainDims &c, SliceDims *sd) {
+    if (opts().relayout == 0) return false;  // option relayout=0: no value relayout of any kind
     if (c.rm != 1 || c.rk != 1) return false;
     if ((c.tm != 64 && c.tm != 128) || (c.tk != 64 && c.tk != 128)) return false;
     if (c.bm != 4 && c.bm != 8 && c.bm != 16) return false;
