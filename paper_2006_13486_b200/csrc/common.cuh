@@ -75,6 +75,7 @@ struct Options {
     int32_t stream_g = 0;     // K5 row blocks per unit: 0 auto, else 1 / 2 / 4 / 8 (whole tiles)
     int32_t halo = -1;        // K5 halo-strip conv where admissible: -1 auto, 0 off
     int32_t simt_wide = -1;   // K1 wide f32 kernel (16 rows x 4 columns per thread): -1 auto, 0 off
+    int32_t merge = -1;       // K5: two tile-rows per unit when g_o is complete: -1 auto, 0 off
     int32_t debug = 0;        // trace / ablation bits (debug builds only)
 };
 Options &opts();

@@ -35,6 +35,7 @@ constexpr OptionSlot kOptionSlots[] = {
     {"promo", &Options::promo, -1, 256},         {"conv_wide", &Options::conv_wide, 0, 1},
     {"stream", &Options::stream, -1, 0},         {"stream_g", &Options::stream_g, 0, 8},
     {"halo", &Options::halo, -1, 0},             {"simt_wide", &Options::simt_wide, -1, 0},
+    {"merge", &Options::merge, -1, 0},
     {"debug", &Options::debug, 0, 1 << 30},
 };
 const OptionSlot *find_option(const char *name) {

@@ -104,6 +104,7 @@ struct SParams {
     int32_t c_in, img_h, img_w, kw, pad, stride, relu;
     // halo conv: stride of a staged 64-channel halo atom (bytes), strips per image (rows, columns)
     int32_t halo_atom, strips_y, strips_x, epi2;  // epi2: warps 8-11 are a second epilogue group
+    int32_t nbuf;                      // TMEM accumulator buffers (2: epilogue overlapped; 1: 512 columns)
     int32_t debug, slot;
 };
 
@@ -180,7 +181,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
     auto drain = [&](int64_t u, int64_t it, int rb0, int rb1, const int32_t *cols, const int32_t *rec,
                      bool helper) {
         const int q = warp & 3;
-        const int b = int(it & 1);
+        const int b = p.nbuf == 2 ? int(it & 1) : 0;
+        const uint32_t bph = uint32_t((p.nbuf == 2 ? (it >> 1) : it) & 1);  // use count of buffer b
         const int64_t tile = u / upt;
         const int tbm = int(tile % p.u_o);
         const int64_t n0 = (tile / p.u_o) * kSBatch;
@@ -206,7 +208,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // warps 0-3 follow acc_full[b] unit by unit; the helpers (warps 4-7) may be many phases
         // behind it, so they wait on the single-phase last_full instead
         if (helper) mbar_wait_parked(last_full, 0u);
-        else mbar_wait_parked(&acc_full[b], uint32_t((it >> 1) & 1));
+        else mbar_wait_parked(&acc_full[b], bph);
         tc_fence_after();
         if (last && threadIdx.x == 0) { K5_MARK(3); K5_SMARK(2); }
 #if RBGP4_DEBUG
@@ -363,9 +365,10 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         }
     };
 
-    // halo conv with a heavy epilogue (p.epi2: 128 rows of 4 x 4 blocks, ~1.5x the unit's MMA
-    // time): warps 8-11 are a second epilogue group (the unit's second half of rows)
-    const bool kEpiB = HALO && p.epi2;
+    // a heavy epilogue (p.epi2: the halo conv's 128 rows of 4 x 4 blocks, ~1.5x the unit's MMA
+    // time; a single-buffered accumulator, whose epilogue is not overlapped): warps 8-11 are a
+    // second epilogue group (the unit's second half of rows) and 4 / 7 the only I producers
+    const bool kEpiB = p.epi2 != 0;
     const bool epi_b = kEpiB && warp >= 8;
     if (warp == 4 || (warp >= 6 && !epi_b)) {
         // ========================== TMA producers ==========================
@@ -383,7 +386,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // most NS producers take part: a producer's next step must be at most one ring round
         // ahead of its last, or its parity wait on `empty` could pass two phases early.
         const int iparity = warp == 4 ? 0 : warp - 6;
-        const int n_ip = min(HALO ? 2 : kIProd, NS);
+        const int n_ip = min(kEpiB ? 2 : kIProd, NS);
         // lane l holds the step words l and l + 32 of the current tile-row (shuffled out)
         int32_t e0 = 0, e1 = 0, rl = 0;
         auto load_steps = [&](int tbm) {
@@ -432,7 +435,10 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int j = word >> 16;
             if (elect_one()) {
                 mbar_expect_tx(&full[st], uint32_t(SB));
-                tma_load_2d(ring + size_t(st) * SB + p.i_bytes, &wmap, &full[st], 0, (tbm * p.d_o + j) * w_rows);
+                // (merged tile-rows: 512 rows = two boxes; a TMA box spans at most 256 rows)
+                for (int r0 = 0; r0 < w_rows; r0 += 256)
+                    tma_load_2d(ring + size_t(st) * SB + p.i_bytes + r0 * 32, &wmap, &full[st], 0,
+                                (tbm * p.d_o + j) * w_rows + r0);
             }
             __syncwarp();
         };
@@ -451,7 +457,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 if (first < p.n_units && elect_one()) {
                     mbar_expect_tx(wfull, uint32_t(p.d_o * w_rows * 32));
                     for (int j = 0; j < p.d_o; ++j)
-                        tma_load_2d(wres + size_t(j) * w_rows * 32, &wmap, wfull, 0, j * w_rows);
+                        for (int r0 = 0; r0 < w_rows; r0 += 256)
+                            tma_load_2d(wres + (size_t(j) * w_rows + r0) * 32, &wmap, wfull, 0, j * w_rows + r0);
                 }
                 __syncwarp();
             } else {
@@ -600,7 +607,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             int rs_st = 0;
             uint32_t rs_ph = 0;
             for (int64_t u = first; u < p.n_units; u += stride, ++it) {
-                const int b = int(it & 1);
+                const int b = p.nbuf == 2 ? int(it & 1) : 0;
+                const uint32_t bph = uint32_t((p.nbuf == 2 ? (it >> 1) : it) & 1);
                 uint64_t a_desc0 = a_desc_t;
                 uint32_t aoff[G > 0 ? 2 * G : 1];
                 if constexpr (G > 0) {
@@ -621,7 +629,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 #if RBGP4_DEBUG
                 if (trace && lane == 0 && it < 4) g_k5_epi[4 * it + 2] = clock64() - c_entry;
 #endif
-                mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
+                mbar_wait(&acc_empty[b], bph ^ 1u);
 #if RBGP4_DEBUG
                 if (trace && lane == 0 && it < 4) g_k5_epi[4 * it + 3] = clock64() - c_entry;
 #endif
@@ -705,11 +713,12 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             uint32_t ph = 0;
             int64_t it = 0;
             for (int64_t u = first; u < p.n_units; u += stride, ++it) {
-                const int b = int(it & 1);
+                const int b = p.nbuf == 2 ? int(it & 1) : 0;
+                const uint32_t bph = uint32_t((p.nbuf == 2 ? (it >> 1) : it) & 1);
                 const int cst = st;
                 const uint32_t cph = ph;
                 if (++st == NS) { st = 0; ph ^= 1u; }
-                mbar_wait(&acc_empty[b], uint32_t((it >> 1) & 1) ^ 1u);
+                mbar_wait(&acc_empty[b], bph ^ 1u);
                 mbar_wait(&full[cst], cph);
                 tc_fence_after();
 #if RBGP4_DEBUG
@@ -851,12 +860,12 @@ namespace {
 // d_i column blocks fall in), summed in the epilogue.  MMA work per step is tk/16 MMAs of
 // N = mma_n, whatever the block size (TC16 is the special case union = d_r blocks of 16).
 struct SliceDims {
-    int nsl, mma_n, d_r;
+    int nsl, mma_n, d_r, r;  // r: tile-rows merged into one unit (see merged())
 };
-bool slice_dims(const ChainDims &c, SliceDims *sd) {
+bool slice_dims(const ChainDims &c, SliceDims *sd, int max_cols = 256) {
     if (opts().relayout == 0) return false;  // option relayout=0: no value relayout of any kind
     if (c.rm != 1 || c.rk != 1) return false;
-    if ((c.tm != 64 && c.tm != 128) || (c.tk != 64 && c.tk != 128)) return false;
+    if ((c.tm != 64 && c.tm != 128 && c.tm != 256) || (c.tk != 64 && c.tk != 128)) return false;
     if (c.bm != 4 && c.bm != 8 && c.bm != 16) return false;
     if (!(c.bk <= 16 ? 16 % c.bk == 0 : c.bk % 16 == 0)) return false;
     if (c.d_i * std::max(1, c.bk / 16) > 2) return false;  // <= 2 partials per row
@@ -865,12 +874,49 @@ bool slice_dims(const ChainDims &c, SliceDims *sd) {
     const int d_r = c.u_i * c.d_i / c.v_i;
     const int per = (c.bk < 16 ? 16 / c.bk : 1) * d_r * c.bm;
     const int n = (std::min(per, c.tm) + 15) & ~15;
-    if (n > 256 || (c.tk / 16) * n > 256) return false;
+    if (n > 256 || (c.tk / 16) * n > max_cols) return false;
     if (c.tm / c.bm * 2 > 128) return false;  // cols table
     sd->nsl = c.tk / 16;
     sd->mma_n = n;
     sd->d_r = d_r;
+    sd->r = 1;
     return true;
+}
+
+// Tile-row merging: when g_o is complete (every tile-row reads every K-block, in the same
+// order), R = 2 consecutive tile-rows form one unit -- a virtual tile of 2 tm rows whose slice
+// unions are twice as wide (N = 64 for TC16 / 8 x 8 blocks).  Each I slab is then loaded once
+// for both tile-rows (half the L2 -> SM bytes) and a step is tk/16 MMAs of twice the N (an
+// M128 K16 MMA costs ~82 cycles up to N = 64 and ~95 at N = 128: tools/umma_bench3.cu), for a
+// single-buffered 512-column accumulator (the epilogue is no longer overlapped).
+ChainDims merged(const ChainDims &c, int r) {
+    ChainDims m = c;
+    m.tm = c.tm * r;
+    m.u_i = c.u_i * r;
+    m.u_o = c.u_o / r;
+    return m;
+}
+int merge_factor(const ChainDims &c) {
+    if (opts().merge == 0 || c.tm != 128 || c.u_o % 2 || c.d_o != c.v_o) return 1;
+    SliceDims sd;
+    return slice_dims(merged(c, 2), &sd, 512) ? 2 : 1;
+}
+// K5 mode of a chain: 0 none, 1 TC16 on K4's relayout (row groups possible), 2 slice relayout
+// on the effective (possibly merged) dims `eff`
+int k5_mode(const ChainDims &c, ChainDims *eff, SliceDims *sd) {
+    *eff = c;
+    const int r = merge_factor(c);
+    if (r > 1) {
+        *eff = merged(c, r);
+        slice_dims(*eff, sd, 512);
+        sd->r = r;
+        return 2;
+    }
+    if (stream_shape_ok(c)) {
+        *sd = SliceDims{8, 32, 2, 1};
+        return 1;
+    }
+    return slice_dims(c, sd) ? 2 : 0;
 }
 // slice section of the prepared buffer: [steps i32 u_o x d_o][cols i32 (tm/bm) x 2][map rows i32
 // nsl x mma_n][map k-offsets i16 nsl x mma_n x 16][values bf16 u_o x d_o x nsl x mma_n x 16]
@@ -987,9 +1033,11 @@ int slice_prepare(const ChainDims &c, const SliceDims &sd, const void *values, c
 }  // namespace
 
 size_t stream_prep_bytes(const ChainDims &c) {
-    if (stream_shape_ok(c)) return 4 * tables_words(c) + size_t(c.rows) * c.row_nnz * 2;
+    ChainDims e;
     SliceDims sd;
-    if (slice_dims(c, &sd)) return slice_layout(c, sd).total;
+    const int mode = k5_mode(c, &e, &sd);
+    if (mode == 1) return 4 * tables_words(c) + size_t(c.rows) * c.row_nnz * 2;
+    if (mode == 2) return slice_layout(e, sd).total;
     return 0;
 }
 
@@ -1093,7 +1141,10 @@ static int tc16_prepare(const ChainDims &c, const void *values, const int32_t *a
 int stream_prepare_values(const ChainDims &c, const void *values, void *k5, cudaStream_t stream) {
     const int64_t total = c.rows * c.row_nnz;
     const int blocks = int(std::min<int64_t>((total + 255) / 256, 8 * kNumSMs));
-    if (stream_shape_ok(c)) {
+    ChainDims e;
+    SliceDims sd;
+    const int mode = k5_mode(c, &e, &sd);
+    if (mode == 1) {
         const int32_t *perm_d = static_cast<const int32_t *>(k5) + a16w(size_t(c.u_o) * c.d_o) + size_t(14) * kRgWords;
         __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + 4 * tables_words(c));
         rg_values_kernel<<<blocks, 256, 0, stream>>>(static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm,
@@ -1101,25 +1152,37 @@ int stream_prepare_values(const ChainDims &c, const void *values, void *k5, cuda
         RBGP4_CHECK_LAUNCH("rg_values_kernel launch");
         return RBGP4_OK;
     }
-    SliceDims sd;
-    if (!slice_dims(c, &sd)) return RBGP4_OK;  // no K5 section
-    const SliceLayout l = slice_layout(c, sd);
+    if (mode != 2) return RBGP4_OK;  // no K5 section
+    const SliceLayout l = slice_layout(e, sd);
     const int32_t *mr = static_cast<const int32_t *>(k5) + l.rows;
     const int16_t *mo = reinterpret_cast<const int16_t *>(static_cast<const int32_t *>(k5) + l.offs);
     __nv_bfloat16 *outv = reinterpret_cast<__nv_bfloat16 *>(static_cast<char *>(k5) + l.vals);
-    const int64_t tot = int64_t(c.u_o) * c.d_o * sd.nsl * sd.mma_n * 16;
+    const int64_t tot = int64_t(e.u_o) * e.d_o * sd.nsl * sd.mma_n * 16;
     slice_values_kernel<<<int(std::min<int64_t>((tot + 255) / 256, 8 * kNumSMs)), 256, 0, stream>>>(
-        static_cast<const __nv_bfloat16 *>(values), c.row_nnz, c.tm, c.d_t, c.d_o, sd.nsl, sd.mma_n, mr, mo, tot, outv);
+        static_cast<const __nv_bfloat16 *>(values), e.row_nnz, e.tm, e.d_t, e.d_o, sd.nsl, sd.mma_n, mr, mo, tot, outv);
     RBGP4_CHECK_LAUNCH("slice_values_kernel launch");
     return RBGP4_OK;
 }
 
 int stream_prepare(const ChainDims &c, const void *values, const int32_t *adj_o_host, const int32_t *sched_host,
                    const int32_t *adj_i_host, void *k5, cudaStream_t stream) {
-    if (stream_shape_ok(c)) return tc16_prepare(c, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+    ChainDims e;
     SliceDims sd;
-    if (!slice_dims(c, &sd)) return RBGP4_EUNSUPPORTED;
-    return slice_prepare(c, sd, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+    const int mode = k5_mode(c, &e, &sd);
+    if (mode == 1) return tc16_prepare(c, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+    if (mode != 2) return RBGP4_EUNSUPPORTED;
+    if (sd.r == 1) return slice_prepare(c, sd, values, adj_o_host, sched_host, adj_i_host, k5, stream);
+    // merged tile-rows: the virtual tile-row t is tile-row t * r (g_o complete: every tile-row has
+    // the same adjacency and slot j <-> K-block j); its row blocks repeat g_i r times
+    std::vector<int32_t> ao(size_t(e.u_o) * c.d_o), sc(ao.size()), ai(size_t(e.u_i) * c.d_i);
+    for (int t = 0; t < e.u_o; ++t)
+        for (int s2 = 0; s2 < c.d_o; ++s2) {
+            ao[size_t(t) * c.d_o + s2] = adj_o_host[size_t(t) * sd.r * c.d_o + s2];
+            sc[size_t(t) * c.d_o + s2] = sched_host ? sched_host[size_t(t) * sd.r * c.d_o + s2] : s2;
+        }
+    for (int rb = 0; rb < e.u_i; ++rb)
+        for (int ink = 0; ink < c.d_i; ++ink) ai[size_t(rb) * c.d_i + ink] = adj_i_host[(rb % c.u_i) * c.d_i + ink];
+    return slice_prepare(e, sd, values, ao.data(), sc.data(), ai.data(), k5, stream);
 }
 
 namespace {
@@ -1128,6 +1191,7 @@ struct SPlan {
     size_t smem;
     unsigned grid;
     bool rg, halo;
+    ChainDims eff;  // effective dims (merged tile-rows)
 };
 
 
@@ -1141,12 +1205,13 @@ bool halo_ok(const ChainDims &c, const rbgp4_conv_desc *cv) {
 
 constexpr size_t kSSmemCap = 227 * 1024;
 
-int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl, const rbgp4_conv_desc *cv = nullptr) {
+int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, const rbgp4_conv_desc *cv = nullptr) {
     if (opts().stream == 0) return 0;
-    const bool tc16 = stream_shape_ok(c);
+    ChainDims c;  // the effective dims: merged tile-rows count as one tile-row of 2 tm rows
     SliceDims sd{};
-    if (tc16) sd = SliceDims{8, 32, 2};
-    else if (!slice_dims(c, &sd)) return 0;
+    const int mode = k5_mode(c_in, &c, &sd);
+    if (mode == 0) return 0;
+    const bool tc16 = mode == 1;
     // (a warp's 32 columns / pixels are all in or out; conv: OOB images of the last tile load as zeros)
     if (c.n_cols % (conv ? 32 : 64) != 0) return 0;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
@@ -1167,7 +1232,7 @@ int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl, const r
         if (g != 1 && g != 2 && g != 4 && g != 8) return 0;
     }
     const bool rg = g < 8;
-    const bool halo = conv && halo_ok(c, cv);
+    const bool halo = conv && sd.r == 1 && halo_ok(c, cv);
     p.g = rg ? g : c.tm / 16;
     p.n_rg = rg ? 8 / g : 1;
     p.n_units = tiles * p.n_rg;
@@ -1193,8 +1258,11 @@ int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl, const r
     p.acc_cols = rg ? g * 16 : p.w_rows;
     const unsigned grid = unsigned(std::min<int64_t>(p.n_units, kNumSMs));
     const bool multi = p.n_units > int64_t(grid);
+    // two accumulator buffers when they fit (epilogue of unit i under the MMAs of unit i+1)
+    p.nbuf = (multi && p.acc_cols * 2 <= 512) ? 2 : 1;
+    if (p.nbuf == 1 && multi && !rg) p.epi2 = 1;
     int tcols = 32;
-    while (tcols < p.acc_cols * (multi ? 2 : 1)) tcols *= 2;
+    while (tcols < p.acc_cols * p.nbuf) tcols *= 2;
     if (tcols > 512) return 0;
     p.tmem_cols = tcols;
     // the last unit is staged in the ring (SDMM): 4 warps x nrows x 32 columns of the output
@@ -1215,6 +1283,7 @@ int stream_plan(const ChainDims &c, int out_dtype, bool conv, SPlan *pl, const r
     pl->grid = grid;
     pl->rg = rg;
     pl->halo = halo;
+    pl->eff = c;
     return 1;
 }
 
@@ -1236,7 +1305,7 @@ int encode_slice_w(CUtensorMap *wmap, const ChainDims &c, const SParams &p, cons
     auto enc = encode_fn();
     cuuint64_t wdims[2] = {16, cuuint64_t(c.u_o) * c.d_o * p.w_rows};
     cuuint64_t wstrides[1] = {32};
-    cuuint32_t wbox[2] = {16, cuuint32_t(p.w_rows)};
+    cuuint32_t wbox[2] = {16, cuuint32_t(std::min(p.w_rows, 256))};
     cuuint32_t e2[2] = {1, 1};
     CUresult r = enc(wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(vals), wdims, wstrides, wbox, e2,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1250,13 +1319,13 @@ int encode_slice_w(CUtensorMap *wmap, const ChainDims &c, const SParams &p, cons
 
 // (cols table, relayout values) of the whole-tile path: K4's relayout for TC16, else the slices
 void whole_tile_views(const ChainDims &c, const void *k4, const void *k5, const int32_t **cols, const void **vals) {
-    if (stream_shape_ok(c)) {
+    ChainDims e;
+    SliceDims sd;
+    if (k5_mode(c, &e, &sd) == 1) {
         gather_prep_views(c, k4, cols, vals);
         return;
     }
-    SliceDims sd;
-    slice_dims(c, &sd);
-    const SliceLayout l = slice_layout(c, sd);
+    const SliceLayout l = slice_layout(e, sd);
     *cols = static_cast<const int32_t *>(k5) + l.cols;
     *vals = static_cast<const char *>(k5) + l.vals;
 }
@@ -1301,6 +1370,7 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
     SPlan pl;
     if (!stream_plan(c, out_dtype, false, &pl) || k5 == nullptr || (stream_shape_ok(c) && k4 == nullptr))
         return RBGP4_EUNSUPPORTED;
+    const ChainDims &e = pl.eff;
     if (c.n_cols == 0) return RBGP4_OK;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
     const int32_t *cols;
@@ -1355,14 +1425,14 @@ int launch_stream(const ChainDims &c, int out_dtype, const void *k4, const void 
             set_error("cuTensorMapEncodeTiled(K5 W) failed (%d)", int(r));
             return RBGP4_ECUDA;
         }
-    } else if (int rc = encode_slice_w(&wmap, c, p, rvals)) {
+    } else if (int rc = encode_slice_w(&wmap, e, p, rvals)) {
         return rc;
     }
     {
         // O (n_cols, rows) row-major; box = one epilogue warp's 32 columns x (16 | tm/2) rows
         cuuint64_t odims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.rows)};
         cuuint64_t ostrides[1] = {cuuint64_t(c.ld_out) * oelt};
-        cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : c.tm / 2)};
+        cuuint32_t obox[2] = {32, cuuint32_t(pl.rg ? 16 : e.tm / 2)};
         cuuint32_t e2[2] = {1, 1};
         CUresult r = enc(&omap, oelt == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out,
                          odims, ostrides, obox, e2, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1461,7 +1531,7 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
             return RBGP4_ECUDA;
         }
     }
-    if (int rc = encode_slice_w(&wmap, c, p, rvals)) return rc;
+    if (int rc = encode_slice_w(&wmap, pl.eff, p, rvals)) return rc;
     return launch_planned(pl, oelt, true, c.bm, imap, wmap, omap, imaps, out, stream);
 }
 

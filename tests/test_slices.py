@@ -46,7 +46,9 @@ SDMM_CASES = [
     ((4, 36), 0.5, (16, 16), 0.875, (8, 8), 1024, "K5 stream", "8x8 blocks, fewer tiles than SMs"),
     ((1, 9), 0.0, (16, 16), 0.875, (4, 4), 4096, "K5 stream", "4x4 blocks, 64x64 tiles (VGG conv0 shape)"),
     ((1, 9), 0.0, (32, 16), 0.875, (4, 4), 2048, "K5 stream", "4x4 blocks, 128x64 tiles, N = 64 slices"),
-    ((2, 18), 0.0, (16, 16), 0.875, (8, 8), 65536, "K5 stream", "persistent: many units per CTA"),
+    ((2, 18), 0.0, (16, 16), 0.875, (8, 8), 65536, "K5 stream", "persistent, merged tile-row pairs (g_o complete)"),
+    ((4, 18), 0.0, (8, 8), 0.75, (16, 16), 8192, "K5 stream", "TC16 with g_o complete: merged pairs, N = 64"),
+    ((2, 9), 0.0, (16, 16), 0.875, (8, 8), 1024, "K5 stream", "merged pairs, one unit per CTA"),
     ((4, 36), 0.5, (16, 16), 0.75, (8, 8), 1024, "K2 tc", "g_i degree 4: four partials -> densify K2"),
 ]
 
@@ -71,6 +73,23 @@ def test_slice_sdmm_matches_oracle(g_o, sp_o, g_i, sp_i, g_b, n, kernel, what, o
     ref = oracle.reference_product(_w64(w), np.ascontiguousarray(xb.double().numpy()[:, cols]), threads=8)
     tol = 1e-2 if out_dtype == "bf16" else 1e-5
     assert _rel(got[:, cols], ref) <= tol, what
+
+
+@pytest.mark.parametrize("g_i,sp_i,g_b", [((8, 8), 0.75, (16, 16)), ((16, 16), 0.875, (8, 8))])
+def test_merged_pairs_match_unmerged(g_i, sp_i, g_b):
+    """Tile-row merging (option merge) changes only which MMA computes a partial: f32 outputs
+    agree with the unmerged kernel to fp32 rounding."""
+    cfg = wl.SweepConfig("merge", (2, 18), 0.0, (1, 1), g_i, sp_i, g_b, n_cols=4096, seed=21)
+    chain = wl.build_chain(cfg)
+    rng = ks.make_rng(4)
+    w = ks.init_random(chain, rng, precision="f32")
+    xb = _bf16(rng.uniform(-1.0, 1.0, size=(w.cols, 4096))).cuda()
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    a, _ = ks.rbgp4mm(w, xb, p, compute="bf16", out_dtype=torch.float32)
+    with _native.options(merge=0):
+        b, _ = ks.rbgp4mm(w, xb, p, compute="bf16", out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert _rel(a.cpu().numpy(), b.cpu().numpy()) < 1e-6
 
 
 def test_slice_sdmm_deterministic():

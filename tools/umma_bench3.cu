@@ -82,6 +82,9 @@ int main() {
     const int steps = 256;
     struct C { int n, nmma, amn, grid, smem_kb, wait, dspan = 128, seqa = 0, dpair = 0; };
     std::vector<C> cs;
+    // MMA cost vs N at 1 CTA/SM (8 MMAs per step, MN-major A, D over 512 TMEM columns)
+    for (int n : {16, 32, 64, 128, 256}) cs.push_back({n, 8, 1, 148, 150, 0, 512, 1, 0});
+    for (int n : {32, 64, 128, 256}) cs.push_back({n, 8, 0, 148, 150, 0, 512, 1, 0});
     // in-kernel patterns at 2 CTAs/SM, issue only: direct mode (16 x N16, pairs into one D),
     // relayout (8 x N32 over 256 D columns, sequential A)
     for (int dspan : {128, 256})
