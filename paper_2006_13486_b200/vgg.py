@@ -66,6 +66,17 @@ def layer_chain(c_out: int, c_in: int, sparsity: float, seed: int = 0, k: int = 
     raise InvalidArgumentError(f"no RBGP4 factorisation for {c_out}x{c_in} at {sparsity}: {last}")
 
 
+def _dense_conv_relu(x, w):
+    """The dense first conv (3 -> 64, a library call as in the paper) with its ReLU fused by cuDNN
+    (conv + separate relu_ measured 4.72 ms at batch 32768, fused 3.40 ms: the ReLU pass re-read
+    and re-wrote the 4.3 GB activation)."""
+    t = torch()
+    fused = getattr(t.ops.aten, "cudnn_convolution_relu", None)
+    if fused is not None and x.is_cuda:
+        return fused(x, w, None, [1, 1], [1, 1], [1, 1], 1)
+    return t.nn.functional.conv2d(x, w, padding=1).relu_()
+
+
 def maxpool2x2(x):
     t = torch()
     b, h, w, c = x.shape
@@ -108,8 +119,8 @@ class VGG19Sparse:
         """x: (batch, 32, 32, 3) bf16 CUDA tensor -> (batch, num_classes) logits."""
         t = torch()
         x = x_nhwc.permute(0, 3, 1, 2)  # NCHW view of channels-last memory
-        x = t.nn.functional.conv2d(x, self.conv1, padding=1).relu_()
-        x = x.permute(0, 2, 3, 1).contiguous()  # NHWC
+        x = _dense_conv_relu(x, self.conv1)
+        x = x.permute(0, 2, 3, 1).contiguous()  # NHWC (a view: cuDNN wrote channels-last)
         for kind, layer in self.layers:
             x = maxpool2x2(x) if kind == "pool" else layer(x)
         return x.reshape(x.shape[0], -1) @ self.fc.t()
