@@ -120,9 +120,15 @@ int rbgp4_sdmm_prepared(const rbgp4_desc *desc, int compute, int in_dtype, int o
  * (batch, height, width, rows) in bf16 or f32, stride 1, "same" padding (pad = (k-1)/2).
  * W is the chain matrix of the layer with rows = c_out and columns in tap-major im2col
  * order, column = (i*kw + j)*c_in + c  (conv weight[c_out, c, i, j]); desc->n_cols must be
- * batch*height*width (ld_in/ld_out are ignored).  relu != 0 fuses max(0, .) into the store.
+ * batch*height*width (ld_in/ld_out are ignored).  `relu` is a flags word: bit 0
+ * (RBGP4_CONV_RELU) fuses max(0, .) into the store; bit 1 (RBGP4_CONV_POOL2) fuses the 2x2 /
+ * stride-2 max pool that follows a VGG stage, so O is (batch, H'/2, W'/2, rows) -- bf16 output,
+ * taken by the streamed kernel where its pixel tiles hold whole 2x2 windows (halo strips, or
+ * output maps up to 16 wide); otherwise RBGP4_EUNSUPPORTED (pool separately).
  * Tensor-core bf16 path only (compute = RBGP4_COMPUTE_BF16).
  */
+#define RBGP4_CONV_RELU 1
+#define RBGP4_CONV_POOL2 2
 typedef struct rbgp4_conv_desc {
     int32_t batch, height, width, c_in;
     int32_t kh, kw, pad, stride;

@@ -16,6 +16,8 @@ from .errors import DeviceError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "librbgp4_b200.so")
 
 F32, F64, BF16 = 0, 1, 2
+EUNSUPPORTED = -2       # RBGP4_EUNSUPPORTED
+CONV_POOL2 = 2          # RBGP4_CONV_POOL2 (rbgp4_conv_desc.relu flags)
 COMPUTE = {"exact": 0, "ffma": 1, "tf32": 2, "bf16": 3}
 EXPORTED = (
     "rbgp4_sdmm", "rbgp4_sdmm_prepared", "rbgp4_prepare", "rbgp4_prepare_size", "rbgp4_prepare_values",

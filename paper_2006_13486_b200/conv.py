@@ -43,12 +43,15 @@ def conv_out_hw(height: int, width: int, k: int, stride: int):
 
 
 def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = False, out=None,
-                  out_dtype=None):
+                  out_dtype=None, pool: bool = False):
     """NHWC conv of `x` (batch, H, W, c_in) with chain matrix `w`, 'same' padding, stride 1 or 2.
 
     Returns an NHWC (batch, H', W', c_out) CUDA tensor.  `x` must be a CUDA bf16 tensor
     (contiguous NHWC); the weight values are converted to bf16 once and cached.  Stride 2 is
     read by strided TMA boxes (every other input pixel); 1 x 1 kernels have no padding.
+    pool=True also applies the 2x2 / stride-2 max pool (bf16 output (batch, H'/2, W'/2, c_out)):
+    fused into the streamed kernel's epilogue where its pixel tiles hold whole windows, else
+    the separate NHWC pool kernel.
     """
     t = torch()
     if w.chain.k != 4:
@@ -71,12 +74,20 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
     if res_dt not in (t.bfloat16, t.float32):
         raise InvalidArgumentError(f"conv writes bf16 or f32, got {res_dt}")
     oh, ow = conv_out_hw(height, width, kh, stride)
+    if pool:
+        if res_dt != t.bfloat16 or oh % 2 or ow % 2:
+            raise InvalidArgumentError("pool=True needs a bf16 output with an even output map")
+        if out is not None:
+            raise InvalidArgumentError("pool=True allocates its own output")
     with t.cuda.device(dev):
         fmt = device_format(w, dev, t.bfloat16)
         n_cols = batch * oh * ow
         desc = make_desc(fmt.desc_fields, n_cols, n_cols, n_cols)
-        cv = _native.ConvDesc(batch, height, width, c_in, kh, kw, (kh - 1) // 2, stride, int(bool(relu)))
-        if out is None:
+        cv = _native.ConvDesc(batch, height, width, c_in, kh, kw, (kh - 1) // 2, stride,
+                              int(bool(relu)) | (_native.CONV_POOL2 if pool else 0))
+        if pool:
+            res = t.empty((batch, oh // 2, ow // 2, w.rows), dtype=res_dt, device=dev)
+        elif out is None:
             res = t.empty((batch, oh, ow, w.rows), dtype=res_dt, device=dev)
         else:
             res = out
@@ -92,11 +103,15 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
         need = lib.rbgp4_conv2d_workspace_size(ctypes.byref(desc), ctypes.byref(cv))
         ws = workspace(dev, need, stream_handle(dev)) if need else None
         code = {t.bfloat16: _native.BF16, t.float32: _native.F32}[res.dtype]
-        _native.check(lib.rbgp4_conv2d(
+        rc = lib.rbgp4_conv2d(
             ctypes.byref(desc), ctypes.byref(cv), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),
             fmt.adj_i.data_ptr(), prep.data_ptr() if prep is not None else None, x.data_ptr(),
-            res.data_ptr(), ws.data_ptr() if ws is not None else None, need, stream_handle(dev)),
-            "rbgp4_conv2d")
+            res.data_ptr(), ws.data_ptr() if ws is not None else None, need, stream_handle(dev))
+        if pool and rc == _native.EUNSUPPORTED:
+            # no fused window layout for this shape: conv, then the NHWC pool kernel
+            from .vgg import maxpool2x2
+            return maxpool2x2(sparse_conv2d(w, x, kernel_size, stride=stride, relu=relu))
+        _native.check(rc, "rbgp4_conv2d")
     return res
 
 
@@ -106,8 +121,8 @@ class SparseConv2d:
     def __init__(self, w, kernel_size: int = 3, relu: bool = True, stride: int = 1):
         self.w, self.kernel_size, self.relu, self.stride = w, kernel_size, relu, stride
 
-    def __call__(self, x):
-        return sparse_conv2d(self.w, x, self.kernel_size, stride=self.stride, relu=self.relu)
+    def __call__(self, x, pool: bool = False):
+        return sparse_conv2d(self.w, x, self.kernel_size, stride=self.stride, relu=self.relu, pool=pool)
 
 
 class SparseLinear:

@@ -194,12 +194,29 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // conv: this lane's output pixel (NHWC row); halo strips: (r, c) = (m / 8, m % 8) of the
         // unit's 16 x 8 strip, m = TMEM lane
         int64_t pix = c0 + lane;
+        // fused 2x2 max pool (conv flag bit 1): window partners are lanes ^1 (x) and ^ystr (y);
+        // the (even x, even y) lane stores the pooled pixel `pix` of the (H/2, W/2) map
+        const bool pool = CONV && (p.relu & 2);
+        int ystr = 1;
+        bool leader = true;
         if constexpr (HALO) {
             const int64_t per_img = int64_t(p.strips_y) * p.strips_x;
             const int64_t bimg = u / per_img;
             const int sy = int((u - bimg * per_img) / p.strips_x), sx = int(u % p.strips_x);
             const int m = q * 32 + lane;
             pix = (bimg * p.img_h + sy * 16 + (m >> 3)) * p.img_w + sx * 8 + (m & 7);
+            if (pool) {
+                ystr = 8;
+                leader = !(m & 1) && !(m & 8);
+                pix = (bimg * (p.img_h / 2) + (sy * 16 + (m >> 3)) / 2) * (p.img_w / 2) + (sx * 8 + (m & 7)) / 2;
+            }
+        } else if (pool) {
+            const int64_t hw = int64_t(p.img_h) * p.img_w;
+            const int64_t bimg = pix / hw;
+            const int rem = int(pix - bimg * hw), y = rem / p.img_w, x = rem - y * p.img_w;
+            ystr = p.img_w;
+            leader = !(x & 1) && !(y & 1);
+            pix = (bimg * (p.img_h / 2) + y / 2) * (p.img_w / 2) + x / 2;
         }
         const int nrows = RG ? p.g * 16 : p.tm;
         unsigned char *wstage_p = ring + q * nrows * kRowBytes;  // [row][kRowBytes] for columns c0..
@@ -228,7 +245,15 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
 #pragma unroll
                 for (int m = 0; m < 16; ++m) {
                     x[m] = __uint_as_float(va[m]) + (two ? __uint_as_float(vb[m]) : 0.0f);
-                    if (p.relu) x[m] = fmaxf(x[m], 0.0f);
+                    if (p.relu & 1) x[m] = fmaxf(x[m], 0.0f);
+                }
+                if (pool) {
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) {
+                        x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], 1));
+                        x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], ystr));
+                    }
+                    if (!leader) return;
                 }
                 if (!ok) return;
                 if constexpr (OUT_BF16) {
@@ -1349,7 +1374,8 @@ int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &im
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = opts().pdl ? 1 : 0;
-    note_kernel(pl.halo ? "K5 halo" : conv ? "K5 conv" : pl.rg ? "K5 rows" : "K5 stream");
+    if (!conv) note_kernel(pl.rg ? "K5 rows" : "K5 stream");
+    else if (pl.halo) note_kernel((pl.p.relu & 2) ? "K5 halo+pool" : "K5 halo");
     e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
     if (e != cudaSuccess) {
         set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
@@ -1464,17 +1490,30 @@ bool conv_tiles_ok(const ChainDims &c, const rbgp4_conv_desc *cv, int oelt) {
 }
 }  // namespace
 
+// the fused 2x2 pool needs whole windows inside a warp's 32 pixels: halo strips (rows ^8), or
+// output maps of width 2..16 (a power of two; rows ^ow) with an even height
+bool pool_ok(const SPlan &pl, const rbgp4_conv_desc *cv, int out_dtype) {
+    if (!(cv->relu & 2)) return true;
+    if (out_dtype != RBGP4_BF16) return false;
+    const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
+    const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
+    if (oh % 2 || ow % 2) return false;
+    return pl.halo || (ow <= 16 && (ow & (ow - 1)) == 0);
+}
+
 int stream_conv_supported(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype) {
     SPlan pl;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
-    return cv != nullptr && stream_plan(c, out_dtype, true, &pl, cv) && (pl.halo || conv_tiles_ok(c, cv, oelt));
+    return cv != nullptr && stream_plan(c, out_dtype, true, &pl, cv) && (pl.halo || conv_tiles_ok(c, cv, oelt)) &&
+           pool_ok(pl, cv, out_dtype);
 }
 
 int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, const void *k4, const void *k5,
                        const void *x, void *out, cudaStream_t stream) {
     SPlan pl;
     const int oelt = out_dtype == RBGP4_BF16 ? 2 : 4;
-    if (!stream_plan(c, out_dtype, true, &pl, cv) || !(pl.halo || conv_tiles_ok(c, cv, oelt)) || k5 == nullptr ||
+    if (!stream_plan(c, out_dtype, true, &pl, cv) || !(pl.halo || conv_tiles_ok(c, cv, oelt)) ||
+        !pool_ok(pl, cv, out_dtype) || k5 == nullptr ||
         (stream_shape_ok(c) && k4 == nullptr))
         return RBGP4_EUNSUPPORTED;
     if (c.n_cols == 0) return RBGP4_OK;
@@ -1486,6 +1525,7 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     p.steps = static_cast<const int32_t *>(k5);
     p.rg = nullptr;
     p.ld_out = int64_t(c.rows);  // NHWC: a pixel row holds c_out channels
+    note_kernel((cv->relu & 2) ? "K5 conv+pool" : "K5 conv");
     const int oh = (cv->height + 2 * cv->pad - cv->kh) / cv->stride + 1;
     const int ow = (cv->width + 2 * cv->pad - cv->kw) / cv->stride + 1;
     p.c_in = cv->c_in;

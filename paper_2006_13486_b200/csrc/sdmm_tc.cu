@@ -1344,6 +1344,10 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
         if (k5 && (k4 || !stream_shape_ok(c)) && stream_conv_supported(c, cv, out_dtype))
             return launch_stream_conv(c, cv, out_dtype, k4, k5, x, out, stream);
     }
+    if (cv->relu & RBGP4_CONV_POOL2) {
+        set_error("rbgp4_conv2d: the fused 2x2 pool runs on the streamed kernel only (this shape: pool separately)");
+        return RBGP4_EUNSUPPORTED;
+    }
     {
         const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep);
         if (gather_conv_supported(c, cv, out_dtype, k4 != nullptr))

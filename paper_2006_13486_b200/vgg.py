@@ -121,8 +121,15 @@ class VGG19Sparse:
         x = x_nhwc.permute(0, 3, 1, 2)  # NCHW view of channels-last memory
         x = _dense_conv_relu(x, self.conv1)
         x = x.permute(0, 2, 3, 1).contiguous()  # NHWC (a view: cuDNN wrote channels-last)
-        for kind, layer in self.layers:
+        i = 0
+        while i < len(self.layers):
+            kind, layer = self.layers[i]
+            if kind == "conv" and i + 1 < len(self.layers) and self.layers[i + 1][0] == "pool":
+                x = layer(x, pool=True)  # conv + ReLU + 2x2 max pool in one epilogue
+                i += 2
+                continue
             x = maxpool2x2(x) if kind == "pool" else layer(x)
+            i += 1
         return x.reshape(x.shape[0], -1) @ self.fc.t()
 
     __call__ = forward

@@ -152,3 +152,32 @@ def _conv_case(c_out, c_in, hw, batch, stride, kernel, what, relu, out_dtype):
         ref = np.maximum(ref, 0.0)
     tol = 1e-2 if out_dtype == "bf16" else 1e-5
     assert _rel(got, ref) <= tol, what
+
+
+POOL_CASES = [
+    # (c_out, c_in, hw, batch, kernel)
+    (64, 64, 32, 2, "K5 halo+pool"),      # VGG conv0 -> pool1 (halo strips: window rows ^8)
+    (128, 128, 16, 2, "K5 halo+pool"),    # VGG conv3 -> pool4
+    (256, 256, 8, 5, "K5 conv+pool"),     # VGG conv8 -> pool9 (two images per tile: rows ^8)
+    (512, 512, 4, 16, "K5 conv+pool"),    # VGG conv13 -> pool14 (rows ^4)
+    (512, 512, 2, 64, "K5 conv+pool"),    # VGG conv18 -> pool19 (one window per image)
+    (256, 64, 32, 2, "K5 conv"),          # 32-wide non-halo map: no fused layout, separate pool
+]
+
+
+@pytest.mark.parametrize("c_out,c_in,hw,batch,kernel", POOL_CASES, ids=[f"{c[0]}x{c[1]}@{c[2]}" for c in POOL_CASES])
+def test_fused_pool_is_conv_then_pool(c_out, c_in, hw, batch, kernel):
+    """conv + ReLU + 2x2 max pool in one epilogue == the conv followed by the NHWC pool kernel,
+    bit for bit (rounding to bf16 is monotonic, so max and rounding commute)."""
+    from paper_2006_13486_b200.vgg import maxpool2x2
+    chain = layer_chain(c_out, c_in, 0.875, seed=c_out + 3 * c_in + hw)
+    w = ks.init_random(chain, 9, precision="f32")
+    x = _bf16(np.random.default_rng(4).uniform(-1, 1, (batch, hw, hw, c_in))).cuda()
+    fused = conv.sparse_conv2d(w, x, 3, relu=True, pool=True)
+    torch.cuda.synchronize()
+    got_kernel = _native.last_kernel()
+    ref = maxpool2x2(conv.sparse_conv2d(w, x, 3, relu=True))
+    torch.cuda.synchronize()
+    assert fused.shape == (batch, hw // 2, hw // 2, c_out)
+    assert got_kernel == kernel, got_kernel
+    assert torch.equal(fused, ref)
