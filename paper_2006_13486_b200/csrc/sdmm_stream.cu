@@ -99,7 +99,7 @@ struct SParams {
     const int32_t *rg;                 // row groups: n_rg records of kRgWords
     // whole tiles (slice relayout): K16 slices per step, MMA N (rows of a slice's union, padded),
     // W rows per step (nsl * mma_n), entries of the cols table (row blocks x 2 partials)
-    int32_t nsl, mma_n, w_rows, n_cols_tab;
+    int32_t nsl, mma_n, w_rows, n_cols_tab, parts;  // parts: TMEM partials per row block (2 or 4)
     // implicit-im2col convolution (NHWC): input channels, OUTPUT map, kernel width, pad, stride
     int32_t c_in, img_h, img_w, kw, pad, stride, relu;
     // halo conv: stride of a staged 64-channel halo atom (bytes), strips per image (rows, columns)
@@ -317,24 +317,30 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // rows 16 i .. 16 i + 15: row groups -> TMEM columns 16 i (one partial); whole tiles ->
         // per element-row block rb of BM rows inside them, its (up to) two partials at TMEM
         // columns cols[2 rb], cols[2 rb + 1] of the slice relayout (-1: no such partial)
-        auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16]) {
+        // (`pp` selects the pair of partials 2 pp, 2 pp + 1 of a row block: p.parts = 2 or 4)
+        const int nparts = RG ? 1 : p.parts;
+        auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16], int pp) {
             if constexpr (RG) {
                 TMEM_LD_32x32b_X16(lane_base + uint32_t(i * 16), va);
             } else {
 #pragma unroll
                 for (int j = 0; j < 16 / BM; ++j) {
                     const int rb = i * (16 / BM) + j;
-                    const int ca = cols[2 * rb], cb = cols[2 * rb + 1];
+                    const int ca = cols[rb * nparts + 2 * pp], cb = cols[rb * nparts + 2 * pp + 1];
                     uint32_t *pa = va + j * BM, *pb = vb + j * BM;
                     if constexpr (BM == 16) {
-                        TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
+                        if (ca >= 0) TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
                         if (cb >= 0) TMEM_LD_32x32b_X16(lane_base + uint32_t(cb), vb);
                     } else if constexpr (BM == 8) {
-                        TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
+                        if (ca >= 0) TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
                         if (cb >= 0) TMEM_LD_32x32b_X8(lane_base + uint32_t(cb), pb);
                     } else {
-                        TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
+                        if (ca >= 0) TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
                         if (cb >= 0) TMEM_LD_32x32b_X4(lane_base + uint32_t(cb), pb);
+                    }
+                    if (ca < 0) {
+#pragma unroll
+                        for (int m = 0; m < BM; ++m) pa[m] = 0u;
                     }
                     if (cb < 0) {
 #pragma unroll
@@ -346,17 +352,34 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // software pipeline over row blocks: row block i+1's TMEM loads are in flight while row
         // block i is converted and stored (tcgen05.wait::ld waits for all of them)
         uint32_t a0[16], b0[16], a1[16], b1[16];
-        tload(rb0, a0, b0);
+        if (nparts > 2) {
+            // four partials per row (g_i degree 4): both pairs of a row block, then
+            // (p0 + p2) + (p1 + p3) in a fixed order -- not pipelined across row blocks
+#pragma unroll 1
+            for (int i = rb0; i < rb1; ++i) {
+                tload(i, a0, b0, 0);
+                tload(i, a1, b1, 1);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    a0[m] = __float_as_uint(__uint_as_float(a0[m]) + __uint_as_float(a1[m]));
+                    b0[m] = __float_as_uint(__uint_as_float(b0[m]) + __uint_as_float(b1[m]));
+                }
+                put16(i, i, a0, b0, true);
+            }
+        } else {
+        tload(rb0, a0, b0, 0);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll 1
         for (int i = rb0; i < rb1; i += 2) {
-            if (i + 1 < rb1) tload(i + 1, a1, b1);
+            if (i + 1 < rb1) tload(i + 1, a1, b1, 0);
             put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (i + 1 >= rb1) break;
-            if (i + 2 < rb1) tload(i + 2, a0, b0);
+            if (i + 2 < rb1) tload(i + 2, a0, b0, 0);
             put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         }
         if (!helper) {
             // all TMEM reads of this buffer are done: the MMA warp may reuse it
@@ -886,6 +909,7 @@ namespace {
 // N = mma_n, whatever the block size (TC16 is the special case union = d_r blocks of 16).
 struct SliceDims {
     int nsl, mma_n, d_r, r;  // r: tile-rows merged into one unit (see merged())
+    int parts;               // partial accumulators per row block: 2, or 4 (g_i degree 4)
 };
 bool slice_dims(const ChainDims &c, SliceDims *sd, int max_cols = 256) {
     if (opts().relayout == 0) return false;  // option relayout=0: no value relayout of any kind
@@ -893,18 +917,20 @@ bool slice_dims(const ChainDims &c, SliceDims *sd, int max_cols = 256) {
     if ((c.tm != 64 && c.tm != 128 && c.tm != 256) || (c.tk != 64 && c.tk != 128)) return false;
     if (c.bm != 4 && c.bm != 8 && c.bm != 16) return false;
     if (!(c.bk <= 16 ? 16 % c.bk == 0 : c.bk % 16 == 0)) return false;
-    if (c.d_i * std::max(1, c.bk / 16) > 2) return false;  // <= 2 partials per row
+    const int parts = c.d_i * std::max(1, c.bk / 16) <= 2 ? 2 : 4;
+    if (c.d_i * std::max(1, c.bk / 16) > 4) return false;  // <= 4 partials per row
     if (c.d_t != c.d_i * c.bk || c.d_o > kMaxDo || c.v_o >= (1 << 16)) return false;
     if ((int64_t(c.u_i) * c.d_i) % c.v_i) return false;
     const int d_r = c.u_i * c.d_i / c.v_i;
     const int per = (c.bk < 16 ? 16 / c.bk : 1) * d_r * c.bm;
     const int n = (std::min(per, c.tm) + 15) & ~15;
     if (n > 256 || (c.tk / 16) * n > max_cols) return false;
-    if (c.tm / c.bm * 2 > 128) return false;  // cols table
+    if (c.tm / c.bm * parts > 128) return false;  // cols table
     sd->nsl = c.tk / 16;
     sd->mma_n = n;
     sd->d_r = d_r;
     sd->r = 1;
+    sd->parts = parts;
     return true;
 }
 
@@ -938,10 +964,11 @@ int k5_mode(const ChainDims &c, ChainDims *eff, SliceDims *sd) {
         return 2;
     }
     if (stream_shape_ok(c)) {
-        *sd = SliceDims{8, 32, 2, 1};
+        *sd = SliceDims{8, 32, 2, 1, 2};
         return 1;
     }
-    return slice_dims(c, sd) ? 2 : 0;
+    // (512 accumulator columns -- g_i degree 4 -- run single-buffered)
+    return slice_dims(c, sd, 512) ? 2 : 0;
 }
 // slice section of the prepared buffer: [steps i32 u_o x d_o][cols i32 (tm/bm) x 2][map rows i32
 // nsl x mma_n][map k-offsets i16 nsl x mma_n x 16][values bf16 u_o x d_o x nsl x mma_n x 16]
@@ -953,7 +980,7 @@ SliceLayout slice_layout(const ChainDims &c, const SliceDims &sd) {
     const size_t w = size_t(sd.nsl) * sd.mma_n;
     l.steps = 0;
     l.cols = a16w(size_t(c.u_o) * c.d_o);
-    l.rows = l.cols + a16w(size_t(c.tm / c.bm) * 2);
+    l.rows = l.cols + a16w(size_t(c.tm / c.bm) * sd.parts);
     l.offs = l.rows + a16w(w);
     l.vals = 4 * (l.offs + a16w(w * 8));
     l.total = l.vals + size_t(c.u_o) * c.d_o * w * 16 * 2;
@@ -1014,12 +1041,12 @@ int slice_prepare(const ChainDims &c, const SliceDims &sd, const void *values, c
             bool touches = false;
             for (int k = 16 * kb; k < 16 * kb + 16 && !touches; ++k) touches = offset_of(rb, k) >= 0;
             if (!touches) continue;
-            if ((pos + 1) * c.bm > sd.mma_n || nparts[rb] >= 2) {
-                set_error("rbgp4_prepare: slice %d needs more than %d rows / row block %d more than 2 partials", kb,
-                          sd.mma_n, rb);
+            if ((pos + 1) * c.bm > sd.mma_n || nparts[rb] >= sd.parts) {
+                set_error("rbgp4_prepare: slice %d needs more than %d rows / row block %d more than %d partials", kb,
+                          sd.mma_n, rb, sd.parts);
                 return RBGP4_EUNSUPPORTED;
             }
-            cols[rb * 2 + nparts[rb]++] = kb * sd.mma_n + pos * c.bm;
+            cols[rb * sd.parts + nparts[rb]++] = kb * sd.mma_n + pos * c.bm;
             for (int m = 0; m < c.bm; ++m) {
                 const int n = kb * sd.mma_n + pos * c.bm + m;
                 mrows[n] = rb * c.bm + m;
@@ -1247,7 +1274,8 @@ int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, cons
     p.nsl = sd.nsl;
     p.mma_n = sd.mma_n;
     p.w_rows = sd.nsl * sd.mma_n;
-    p.n_cols_tab = c.tm / c.bm * 2;
+    p.n_cols_tab = c.tm / c.bm * sd.parts;
+    p.parts = sd.parts;
     const int64_t tiles = c.u_o * ((c.n_cols + kSBatch - 1) / kSBatch);
     // whole tiles when they fill ~2/3 of the SMs, else (TC16 SDMM) the largest row group that does
     int g = 8;

@@ -7,7 +7,7 @@ the tile rows with a nonzero there (zero-padded to the MMA N); every output row 
 two partials.  Bar: rel-L2 <= 1e-2 with bf16 outputs (the output rounding is ~2e-3), <= 1e-5
 with f32 outputs, against the f64 oracle on the same bf16-rounded operands (north star), and
 the launch is the K5 kernel (rbgp4_last_kernel).  Shapes the slices cannot take (more than two
-partials per row: g_i degree 4 with 8 x 8 blocks) still run, on the densify kernel K2.
+partials per row: g_i degree 8 with 8 x 8 blocks) still run, on the densify kernel K2.
 """
 
 from __future__ import annotations
@@ -49,7 +49,9 @@ SDMM_CASES = [
     ((2, 18), 0.0, (16, 16), 0.875, (8, 8), 65536, "K5 stream", "persistent, merged tile-row pairs (g_o complete)"),
     ((4, 18), 0.0, (8, 8), 0.75, (16, 16), 8192, "K5 stream", "TC16 with g_o complete: merged pairs, N = 64"),
     ((2, 9), 0.0, (16, 16), 0.875, (8, 8), 1024, "K5 stream", "merged pairs, one unit per CTA"),
-    ((4, 36), 0.5, (16, 16), 0.75, (8, 8), 1024, "K2 tc", "g_i degree 4: four partials -> densify K2"),
+    ((4, 36), 0.5, (16, 16), 0.75, (8, 8), 4096, "K5 stream", "g_i degree 4 (8x8 blocks): four partials, N = 64"),
+    ((2, 18), 0.0, (8, 8), 0.5, (16, 16), 8192, "K5 stream", "TC16 blocks, g_i degree 4 (50 %): four partials"),
+    ((4, 36), 0.5, (16, 16), 0.5, (8, 8), 1024, "K2 tc", "g_i degree 8: too many partials -> densify K2"),
 ]
 
 
