@@ -145,6 +145,15 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
 int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int width, int channels,
                           void *stream);
 
+/* Materialised im2col of an NHWC tensor (F32 or BF16) into the chain's tap-major operand
+ * cols (k*k*channels, batch*H'*W') ('same' padding, stride 1 or 2), for the layers the
+ * implicit-im2col conv does not take (the fp32 FFMA path); one pass, zero padding. */
+int rbgp4_im2col_nhwc(int dtype, const void *x, void *cols, int batch, int height, int width, int channels,
+                      int k, int stride, void *stream);
+
+/* dst (n, rows) = src (rows, n) transposed (the product's O back to NHWC), ReLU fused if relu. */
+int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, void *stream);
+
 /*
  * Training direction: the weight gradient restricted to the pattern,
  *   grad_values[u, j] = sum_n d_out[u, n] * inp[c(u, j), n],

@@ -25,7 +25,7 @@ EXPORTED = (
     "rbgp4_conv2d", "rbgp4_conv2d_workspace_size", "rbgp4_maxpool2x2_nhwc",
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count", "rbgp4_last_kernel", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
-    "rbgp4_reset_options", "rbgp4_debug_build",
+    "rbgp4_reset_options", "rbgp4_debug_build", "rbgp4_im2col_nhwc", "rbgp4_nc_to_nhwc",
 )
 
 
@@ -96,6 +96,10 @@ def lib():
     h.rbgp4_conv2d.restype = i32
     h.rbgp4_maxpool2x2_nhwc.argtypes = [vp, vp, i32, i32, i32, i32, vp]
     h.rbgp4_maxpool2x2_nhwc.restype = i32
+    h.rbgp4_im2col_nhwc.argtypes = [i32, vp, vp, i32, i32, i32, i32, i32, i32, vp]
+    h.rbgp4_im2col_nhwc.restype = i32
+    h.rbgp4_nc_to_nhwc.argtypes = [i32, vp, vp, i32, ctypes.c_int64, i32, vp]
+    h.rbgp4_nc_to_nhwc.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

@@ -58,3 +58,137 @@ extern "C" int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int heig
     RBGP4_CHECK_LAUNCH("maxpool2x2_nhwc launch");
     return RBGP4_OK;
 }
+
+// ---------------------------------------------------------------- im2col / layout transposes
+// For the layers the implicit-im2col conv does not take (the fp32 FFMA path of WRN-40-4 and its
+// 16-channel bf16 layers): im2col of an NHWC tensor into the chain's tap-major (k*k*C, B*H'*W')
+// operand in ONE pass (32 x 32 shared-memory transposes per tap: coalesced channel reads, coalesced
+// pixel writes; OOB taps = the zero padding), and the (C, N) -> NHWC (N, C) transpose of the
+// product's output with the ReLU fused.  (torch's pad / stack / permute / contiguous chain took
+// ~3 ms per 64-channel 32x32 layer at batch 512; the product itself 0.42 ms.)
+namespace rbgp4 {
+namespace {
+
+constexpr int kColPix = 128;  // output pixels per im2col block (32 channels x 128 pixels)
+
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_nhwc_kernel(const T *__restrict__ x, T *__restrict__ cols, int b,
+                                                          int h, int w, int c, int k, int stride, int oh, int ow) {
+    __shared__ T tile[kColPix][33];
+    const int64_t n_pix = int64_t(b) * oh * ow;
+    const int tap = blockIdx.z, ti = tap / k, tj = tap % k, pad = (k - 1) / 2;
+    const int64_t p0 = int64_t(blockIdx.x) * kColPix;  // first output pixel
+    const int c0 = blockIdx.y * 32;                     // first channel
+    const int ch = c0 + threadIdx.x;
+    // read: kColPix pixels x 32 channels, lanes along channels (coalesced NHWC rows); the
+    // pixel coordinates are decomposed once and stepped (64-bit divisions per element made
+    // this kernel integer-bound)
+    int64_t pix = p0 + threadIdx.y;
+    int ox = int(pix % ow), oy, bi;
+    {
+        const int64_t t = pix / ow;
+        oy = int(t % oh);
+        bi = int(t / oh);
+    }
+    for (int r = threadIdx.y; r < kColPix; r += blockDim.y) {
+        T v = T(0.0f);
+        if (pix < n_pix && ch < c) {
+            const int iy = oy * stride + ti - pad, ix = ox * stride + tj - pad;
+            if (iy >= 0 && iy < h && ix >= 0 && ix < w) v = x[((int64_t(bi) * h + iy) * w + ix) * c + ch];
+        }
+        tile[r][threadIdx.x] = v;
+        pix += blockDim.y;
+        ox += blockDim.y;
+        while (ox >= ow) {
+            ox -= ow;
+            if (++oy == oh) { oy = 0; ++bi; }
+        }
+    }
+    __syncthreads();
+    // write: 32 channel rows x kColPix pixels, each lane 4 consecutive pixels (one row of cols
+    // per warp instruction when the rows are 16-byte aligned)
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int chr = c0 + r;
+        if (chr >= c) break;
+        T *dst = cols + (int64_t(tap) * c + chr) * n_pix + p0;
+        const int px = threadIdx.x * 4;
+        if (sizeof(T) == 4 && n_pix % 4 == 0 && p0 + px + 3 < n_pix) {
+            float4 v;
+            v.x = float(tile[px][r]); v.y = float(tile[px + 1][r]); v.z = float(tile[px + 2][r]); v.w = float(tile[px + 3][r]);
+            *reinterpret_cast<float4 *>(dst + px) = v;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (p0 + px + j < n_pix) dst[px + j] = tile[px + j][r];
+        }
+    }
+}
+
+template <typename T>
+__global__ void nc_to_nhwc_kernel(const T *__restrict__ src, T *__restrict__ dst, int rows, int64_t n, int relu) {
+    __shared__ T tile[32][33];
+    const int64_t n0 = int64_t(blockIdx.x) * 32;
+    const int r0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int row = r0 + r;
+        const int64_t col = n0 + threadIdx.x;
+        T v = T(0.0f);
+        if (row < rows && col < n) v = src[int64_t(row) * n + col];
+        tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t col = n0 + r;
+        const int row = r0 + threadIdx.x;
+        if (row < rows && col < n) {
+            T v = tile[threadIdx.x][r];
+            if (relu && float(v) < 0.0f) v = T(0.0f);
+            dst[col * rows + row] = v;
+        }
+    }
+}
+
+}  // namespace
+}  // namespace rbgp4
+
+extern "C" int rbgp4_im2col_nhwc(int dtype, const void *x, void *cols, int batch, int height, int width,
+                                 int channels, int k, int stride, void *stream) {
+    using namespace rbgp4;
+    RBGP4_REQUIRE(dtype == RBGP4_F32 || dtype == RBGP4_BF16, "im2col: F32 or BF16");
+    RBGP4_REQUIRE(batch >= 0 && height > 0 && width > 0 && channels > 0 && k % 2 == 1 && (stride == 1 || stride == 2),
+                  "im2col: bad geometry");
+    const int pad = (k - 1) / 2;
+    const int oh = (height + 2 * pad - k) / stride + 1, ow = (width + 2 * pad - k) / stride + 1;
+    const int64_t n_pix = int64_t(batch) * oh * ow;
+    if (n_pix == 0) return RBGP4_OK;
+    dim3 grid(unsigned((n_pix + kColPix - 1) / kColPix), unsigned((channels + 31) / 32), unsigned(k * k));
+    dim3 block(32, 8);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (dtype == RBGP4_F32)
+        im2col_nhwc_kernel<float><<<grid, block, 0, s>>>(static_cast<const float *>(x), static_cast<float *>(cols),
+                                                         batch, height, width, channels, k, stride, oh, ow);
+    else
+        im2col_nhwc_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16 *>(x),
+                                                                 static_cast<__nv_bfloat16 *>(cols), batch, height,
+                                                                 width, channels, k, stride, oh, ow);
+    RBGP4_CHECK_LAUNCH("im2col_nhwc launch");
+    return RBGP4_OK;
+}
+
+extern "C" int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, void *stream) {
+    using namespace rbgp4;
+    RBGP4_REQUIRE(dtype == RBGP4_F32 || dtype == RBGP4_BF16, "nc_to_nhwc: F32 or BF16");
+    RBGP4_REQUIRE(rows >= 0 && n >= 0, "nc_to_nhwc: bad sizes");
+    if (rows == 0 || n == 0) return RBGP4_OK;
+    dim3 grid(unsigned((n + 31) / 32), unsigned((rows + 31) / 32));
+    dim3 block(32, 8);
+    auto s = static_cast<cudaStream_t>(stream);
+    if (dtype == RBGP4_F32)
+        nc_to_nhwc_kernel<float><<<grid, block, 0, s>>>(static_cast<const float *>(src), static_cast<float *>(dst),
+                                                        rows, n, relu);
+    else
+        nc_to_nhwc_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16 *>(src),
+                                                                static_cast<__nv_bfloat16 *>(dst), rows, n, relu);
+    RBGP4_CHECK_LAUNCH("nc_to_nhwc launch");
+    return RBGP4_OK;
+}

@@ -58,3 +58,23 @@ def test_wrn_forward_bf16_and_ffma():
     finally:
         torch.backends.cudnn.allow_tf32 = tf32
     assert float((y32 - ref32).norm() / ref32.norm()) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("b,h,w,c,k,stride", [(2, 5, 7, 16, 3, 1), (3, 8, 8, 64, 3, 2), (2, 6, 6, 48, 1, 2),
+                                              (1, 32, 32, 16, 3, 1)])
+def test_native_im2col_and_transpose_are_exact(dtype, b, h, w, c, k, stride):
+    """rbgp4_im2col_nhwc == the numpy im2col oracle and rbgp4_nc_to_nhwc == transpose + ReLU, bit for
+    bit (pure data movement)."""
+    import torch
+    from test_conv import im2col_nhwc
+    from paper_2006_13486_b200 import wrn
+    tdt = torch.float32 if dtype == "f32" else torch.bfloat16
+    x = torch.randn(b, h, w, c).to(tdt)
+    cols, (bb, oh, ow) = wrn.im2col(x.cuda(), k, stride)
+    want = im2col_nhwc(x.float().numpy(), k, stride)
+    assert cols.shape == want.shape and np.array_equal(cols.float().cpu().numpy(), want)
+    y = torch.randn(24, bb * oh * ow).to(tdt)
+    got = wrn.to_nhwc(y.cuda(), bb, oh, ow, relu=True).cpu()
+    assert torch.equal(got, y.t().reshape(bb, oh, ow, 24).relu())
