@@ -102,7 +102,8 @@ def test_product_path_fails_loudly_without_gpu():
 def test_prepared_section_carries_the_tc16_relayout(plan_options):
     """rbgp4_prepare_size (host-only arithmetic): the TC16 shape (16x16 blocks, g_i (8,8) of degree
     2) gets the column-block relayout of its values (same byte count as the values) in its prepared
-    section; g_i of degree 4 does not, and option relayout=0 removes it."""
+    section; g_i of degree 4 gets the K5 slice relayout (the values plus zero padding); option
+    relayout=0 removes every value relayout."""
     lib = _native.lib()
 
     def prep_bytes(sp_i):
@@ -114,9 +115,10 @@ def test_prepared_section_carries_the_tc16_relayout(plan_options):
     size, values = prep_bytes(0.75)
     assert size >= values
     size4, values4 = prep_bytes(0.5)
-    assert size4 < values4
+    assert size4 >= values4
     plan_options("relayout", 0)
     assert prep_bytes(0.75)[0] < values
+    assert prep_bytes(0.5)[0] < values4
 
 
 def test_plan_options_are_explicit_and_thread_local():
