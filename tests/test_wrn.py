@@ -32,14 +32,6 @@ def test_layer_factorisations(sparsity):
     assert n == 39
 
 
-@pytest.mark.parametrize("k,stride", [(3, 1), (3, 2), (1, 2)])
-def test_torch_im2col_matches_oracle_order(k, stride):
-    x = np.random.default_rng(0).standard_normal((2, 8, 8, 16)).astype(np.float32)
-    cols, (b, oh, ow) = im2col(torch.from_numpy(x), k, stride)
-    assert (b, oh, ow) == (2, (8 + 2 * (k // 2) - k) // stride + 1, (8 + 2 * (k // 2) - k) // stride + 1)
-    assert np.array_equal(cols.numpy(), im2col_nhwc(x, k, stride))
-
-
 @pytest.mark.gpu
 def test_wrn_forward_bf16_and_ffma():
     from paper_2006_13486_b200.wrn import WRN40_4Sparse
