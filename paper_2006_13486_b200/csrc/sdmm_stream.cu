@@ -317,7 +317,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // rows 16 i .. 16 i + 15: row groups -> TMEM columns 16 i (one partial); whole tiles ->
         // per element-row block rb of BM rows inside them, its (up to) two partials at TMEM
         // columns cols[2 rb], cols[2 rb + 1] of the slice relayout (-1: no such partial)
-        // (`pp` selects the pair of partials 2 pp, 2 pp + 1 of a row block: p.parts = 2 or 4)
+        // rows 16 i .. 16 i + 15 of partial pair pp (p.parts = 2: pp = 0; 4: pp = 0, 1).  The first
+        // partial of a row block always exists; only the others may be -1.  (The two-partial
+        // path keeps the unconditional first load: guarding it doubled the halo conv epilogue.)
         const int nparts = RG ? 1 : p.parts;
         auto tload = [&](int i, uint32_t (&va)[16], uint32_t (&vb)[16], int pp) {
             if constexpr (RG) {
@@ -328,21 +330,23 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     const int rb = i * (16 / BM) + j;
                     const int ca = cols[rb * nparts + 2 * pp], cb = cols[rb * nparts + 2 * pp + 1];
                     uint32_t *pa = va + j * BM, *pb = vb + j * BM;
-                    if constexpr (BM == 16) {
-                        if (ca >= 0) TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
-                        if (cb >= 0) TMEM_LD_32x32b_X16(lane_base + uint32_t(cb), vb);
-                    } else if constexpr (BM == 8) {
-                        if (ca >= 0) TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
-                        if (cb >= 0) TMEM_LD_32x32b_X8(lane_base + uint32_t(cb), pb);
+                    if (pp == 0) {
+                        if constexpr (BM == 16) TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
+                        else if constexpr (BM == 8) TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
+                        else TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
+                    } else if (ca >= 0) {
+                        if constexpr (BM == 16) TMEM_LD_32x32b_X16(lane_base + uint32_t(ca), va);
+                        else if constexpr (BM == 8) TMEM_LD_32x32b_X8(lane_base + uint32_t(ca), pa);
+                        else TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
                     } else {
-                        if (ca >= 0) TMEM_LD_32x32b_X4(lane_base + uint32_t(ca), pa);
-                        if (cb >= 0) TMEM_LD_32x32b_X4(lane_base + uint32_t(cb), pb);
-                    }
-                    if (ca < 0) {
 #pragma unroll
                         for (int m = 0; m < BM; ++m) pa[m] = 0u;
                     }
-                    if (cb < 0) {
+                    if (cb >= 0) {
+                        if constexpr (BM == 16) TMEM_LD_32x32b_X16(lane_base + uint32_t(cb), vb);
+                        else if constexpr (BM == 8) TMEM_LD_32x32b_X8(lane_base + uint32_t(cb), pb);
+                        else TMEM_LD_32x32b_X4(lane_base + uint32_t(cb), pb);
+                    } else {
 #pragma unroll
                         for (int m = 0; m < BM; ++m) pb[m] = 0u;
                     }
