@@ -80,6 +80,27 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const T *__restrict__ 
     const int64_t p0 = int64_t(blockIdx.x) * kColPix;  // first output pixel
     const int c0 = blockIdx.y * 32;                     // first channel
     const int ch = c0 + threadIdx.x;
+    if (sizeof(T) == 4 && c % 4 == 0 && n_pix < (int64_t(1) << 31)) {
+        // f32: 16-byte loads, 8 lanes x 4 channels per pixel, 4 pixels per warp instruction
+        // (the scalar loop below was instruction-bound: 69 % issue, 2.8 TB/s)
+        const int tid = threadIdx.y * 32 + threadIdx.x;
+        const int cq = tid & 7, pr = tid >> 3;  // channel quad, pixel row (0..31)
+        const int chq = c0 + 4 * cq;
+        for (int r = pr; r < kColPix; r += 32) {
+            const int pix = int(p0) + r;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (pix < n_pix && chq < c) {
+                const int ox = pix % ow, t = pix / ow, oy = t % oh, bi = t / oh;
+                const int iy = oy * stride + ti - pad, ix = ox * stride + tj - pad;
+                if (iy >= 0 && iy < h && ix >= 0 && ix < w)
+                    v = *reinterpret_cast<const float4 *>(x + ((int64_t(bi) * h + iy) * w + ix) * c + chq);
+            }
+            tile[r][4 * cq] = T(v.x);
+            tile[r][4 * cq + 1] = T(v.y);
+            tile[r][4 * cq + 2] = T(v.z);
+            tile[r][4 * cq + 3] = T(v.w);
+        }
+    } else {
     // read: kColPix pixels x 32 channels, lanes along channels (coalesced NHWC rows); the
     // pixel coordinates are decomposed once and stepped (64-bit divisions per element made
     // this kernel integer-bound)
@@ -104,6 +125,7 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const T *__restrict__ 
             if (++oy == oh) { oy = 0; ++bi; }
         }
     }
+    }
     __syncthreads();
     // write: 32 channel rows x kColPix pixels, each lane 4 consecutive pixels (one row of cols
     // per warp instruction when the rows are 16-byte aligned)
@@ -111,15 +133,18 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const T *__restrict__ 
         const int chr = c0 + r;
         if (chr >= c) break;
         T *dst = cols + (int64_t(tap) * c + chr) * n_pix + p0;
-        const int px = threadIdx.x * 4;
-        if (sizeof(T) == 4 && n_pix % 4 == 0 && p0 + px + 3 < n_pix) {
-            float4 v;
-            v.x = float(tile[px][r]); v.y = float(tile[px + 1][r]); v.z = float(tile[px + 2][r]); v.w = float(tile[px + 3][r]);
-            *reinterpret_cast<float4 *>(dst + px) = v;
-        } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (p0 + px + j < n_pix) dst[px + j] = tile[px + j][r];
+        for (int half = 0; half < kColPix / 128; ++half) {
+            const int px = half * 128 + threadIdx.x * 4;
+            if (sizeof(T) == 4 && n_pix % 4 == 0 && p0 + px + 3 < n_pix) {
+                float4 v;
+                v.x = float(tile[px][r]); v.y = float(tile[px + 1][r]); v.z = float(tile[px + 2][r]); v.w = float(tile[px + 3][r]);
+                *reinterpret_cast<float4 *>(dst + px) = v;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (p0 + px + j < n_pix) dst[px + j] = tile[px + j][r];
+            }
         }
     }
 }
