@@ -151,3 +151,28 @@ def test_no_environment_reads_in_the_library_sources():
     import glob
     for path in glob.glob(os.path.join(ROOT, "paper_2006_13486_b200", "csrc", "*.c*")):
         assert "getenv" not in open(path).read(), path
+
+
+def test_prepared_section_sizes_follow_the_k5_modes(plan_options):
+    """rbgp4_prepare_size (host-only): the K5 slice section of a chain with a complete g_o holds the
+    MERGED tile-row pairs -- per virtual tile-row (2 x 128 rows) and step, 8 K16 slices x 64 union
+    rows x 16 k of bf16 (zero-padded) -- and option merge=0 falls back to unmerged 128-row tiles
+    (the TC16 path, K4's relayout plus the row-group copy); 4x4 blocks get 4 slices per 64-row step."""
+    lib = _native.lib()
+
+    def size(g_o, sp_o, g_i, sp_i, g_b):
+        cfg = wl.SweepConfig("p", g_o, sp_o, (1, 1), g_i, sp_i, g_b, n_cols=1, seed=0)
+        chain = wl.build_chain(cfg)
+        d = make_desc(chain_fields(chain), 4096, 4096, 4096)
+        return lib.rbgp4_prepare_size(ctypes.byref(d), 3), chain
+
+    merged, chain = size((4, 18), 0.0, (8, 8), 0.75, (16, 16))
+    vals_merged = (4 // 2) * 18 * 8 * 64 * 16 * 2
+    assert merged >= vals_merged
+    plan_options("merge", 0)
+    unmerged, _ = size((4, 18), 0.0, (8, 8), 0.75, (16, 16))
+    assert unmerged != merged
+    assert unmerged >= 2 * chain.num_left * chain.row_nnz * 2  # K4 relayout + row-group copy
+    plan_options("merge", -1)
+    small, chain4 = size((1, 9), 0.0, (16, 16), 0.875, (4, 4))
+    assert small >= 9 * 4 * 32 * 16 * 2  # 9 steps x 4 slices x 32 union rows x 16 k
