@@ -861,8 +861,9 @@ def run_train_leg(B, args):
     layer as a TrainableSparseLinear(compute="bf16") on the headline operands (N = 16 * batch
     pixels x K = 4608 inputs): forward O = W x I (K5), input gradient W^T x dO (K5 on the
     transposed chain), weight gradient restricted to the pattern (K7), fp32 master values.
-    Reports the autograd step (incl. the torch layout casts / transposes of the nn.Linear-style
-    API) and the three products alone on pre-laid-out bf16 operands; FLOPs = 3 x 2 nnz N."""
+    Reports the autograd step (eager, incl. the torch layout casts / transposes of the
+    nn.Linear-style API and the Python launch overhead) and the three products alone on
+    pre-laid-out bf16 operands, each a CUDA graph; FLOPs = 3 x 2 nnz N."""
     torch = B.torch
     from paper_2006_13486_b200 import training
     lay = build_layers(args.sparsity, args.batch, args.factorisation)[1]
@@ -903,14 +904,22 @@ def run_train_leg(B, args):
                "input_grad_K5_transposed": lambda: pat.product(pat.fmt_t, vt, dout, torch.float32),
                "weight_grad_K7": lambda: training.sddmm(pat.w, dout, xt)}
         for name, op in ops.items():
-            op()
+            op()  # prepared buffers (host-synchronising) before capture
+            B.stream.synchronize()
+            # each product as a CUDA graph of `reps` launches: device time, not the Python launch
+            # overhead of the per-call API (which the event-timed eager loop measured)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=B.stream):
+                for _ in range(reps):
+                    op()
+            g.replay()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(B.stream)
-            for _ in range(reps):
-                op()
+            g.replay()
             b.record(B.stream)
             torch.cuda.synchronize()
             kerns[name] = B.max_over_ranks(a.elapsed_time(b) / reps) * 1e3
+            del g
     k_ms = sum(kerns.values()) / 1e3
     return {"layer": lay["name"], "shape": {"rows": w.rows, "cols": w.cols, "n": n}, "sparsity": args.sparsity,
             "step_ms": ms_step, "step_tflops": flops * B.world / (ms_step * 1e-3) / 1e12,

@@ -29,6 +29,7 @@ constexpr int kStage = 2 * kHalf;
 struct TParams {
     int64_t n_cols, row_nnz;
     int32_t d_o, tm, tk, u_i, d_i, bm, bk, d_t, ns, n_chunks;
+    int32_t split;  // 2: two CTAs per tile, each half of the batch chunks, added into a zeroed grad
 };
 
 template <int BK>
@@ -44,7 +45,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(acc_full + 1);
     unsigned char *ring = base + 1024;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tbm = int(blockIdx.x / p.d_o), j = int(blockIdx.x % p.d_o);
+    const int tile = int(blockIdx.x / p.split), half = int(blockIdx.x % p.split);
+    const int tbm = tile / p.d_o, j = tile % p.d_o;
+    // this CTA's batch chunks [c_lo, c_hi)
+    const int c_lo = p.split == 1 ? 0 : (half == 0 ? 0 : p.n_chunks / 2);
+    const int c_hi = p.split == 1 ? p.n_chunks : (half == 0 ? p.n_chunks / 2 : p.n_chunks);
+    const int n_my = c_hi - c_lo;
     const int kblk = __ldg(adj_o + int64_t(tbm) * p.d_o + j);
     if (warp == 4) {
         if (lane == 0) {
@@ -54,13 +60,13 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
         }
         __syncwarp();
         asm volatile("barrier.sync 1, %0;" ::"n"(kTThreads) : "memory");
-        for (int c = 0; c < p.n_chunks; ++c) {
+        for (int c = 0; c < n_my; ++c) {
             const int st = c % p.ns;
             if (c >= p.ns) mbar_wait(&empty[st], uint32_t((c / p.ns - 1) & 1));
             if (elect_one()) {
                 mbar_expect_tx(&full[st], uint32_t(kStage));
-                tma_load_2d(ring + size_t(st) * kStage, &dmap, &full[st], c * kChunk, tbm * p.tm);
-                tma_load_2d(ring + size_t(st) * kStage + kHalf, &imap, &full[st], c * kChunk, kblk * p.tk);
+                tma_load_2d(ring + size_t(st) * kStage, &dmap, &full[st], (c_lo + c) * kChunk, tbm * p.tm);
+                tma_load_2d(ring + size_t(st) * kStage + kHalf, &imap, &full[st], (c_lo + c) * kChunk, kblk * p.tk);
             }
             __syncwarp();
         }
@@ -77,7 +83,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
                                    ((128u >> 3) << 17) | ((128u >> 4) << 24);
         const uint64_t a0 = smem_desc(smem_u32(ring), 0, 1024, 2u);
         const uint64_t b0 = smem_desc(smem_u32(ring) + kHalf, 0, 1024, 2u);
-        for (int c = 0; c < p.n_chunks; ++c) {
+        for (int c = 0; c < n_my; ++c) {
             const int st = c % p.ns;
             mbar_wait(&full[st], uint32_t((c / p.ns) & 1));
             tc_fence_after();
@@ -88,7 +94,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
                     tc_mma<false>(tmem_d, a0 + off + uint32_t(k * 2), b0 + off + uint32_t(k * 2), idesc,
                                   (c > 0 || k > 0) ? 1u : 0u);
                 tc_commit(&empty[st]);
-                if (c == p.n_chunks - 1) tc_commit(acc_full);
+                if (c == n_my - 1) tc_commit(acc_full);
             }
             __syncwarp();
         }
@@ -110,12 +116,17 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
                 else if constexpr (BK == 8) TMEM_LD_32x32b_X8(lane_base + col, v);
                 else TMEM_LD_32x32b_X4(lane_base + col, v);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (mine) {
+                if (mine && p.split == 1) {
                     float4 *g = reinterpret_cast<float4 *>(grow + ink * BK);
 #pragma unroll
                     for (int q = 0; q < BK / 4; ++q)
                         g[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                            __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                } else if (mine) {
+                    // two halves into a zeroed gradient: 0 + a + b == 0 + b + a exactly (fp32 addition
+                    // commutes), so the result is deterministic whichever half lands first
+#pragma unroll
+                    for (int q = 0; q < BK; ++q) atomicAdd(grow + ink * BK + q, __uint_as_float(v[q]));
                 }
             }
         }
@@ -170,6 +181,9 @@ int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj
     p.d_i = c.d_i; p.bm = c.bm; p.bk = c.bk; p.d_t = c.d_t;
     p.n_chunks = int((c.n_cols + kChunk - 1) / kChunk);
     p.ns = 6;
+    // fewer tiles than SMs: split each tile's batch over two CTAs (deterministic, see the epilogue)
+    const int64_t tiles = int64_t(c.u_o) * c.d_o;
+    p.split = (tiles <= kNumSMs && p.n_chunks >= 8) ? 2 : 1;
     const size_t smem = 1024 + 1024 + size_t(p.ns) * kStage;
     void (*kern)(CUtensorMap, CUtensorMap, TParams, const int32_t *, const int32_t *, float *) =
         c.bk == 16 ? sddmm_tc_kernel<16> : c.bk == 8 ? sddmm_tc_kernel<8> : sddmm_tc_kernel<4>;
@@ -183,8 +197,15 @@ int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj
         e = cudaMemsetAsync(grad, 0, size_t(c.rows) * c.row_nnz * 4, stream);
         return e == cudaSuccess ? RBGP4_OK : RBGP4_ECUDA;
     }
+    if (p.split == 2) {
+        e = cudaMemsetAsync(grad, 0, size_t(c.rows) * c.row_nnz * 4, stream);
+        if (e != cudaSuccess) {
+            set_error("sddmm_tc: zeroing the gradient: %s", cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+    }
     note_kernel("K7 sddmm");
-    kern<<<unsigned(c.u_o * c.d_o), kTThreads, smem, stream>>>(dmap, imap, p, adj_o, adj_i, grad);
+    kern<<<unsigned(tiles * p.split), kTThreads, smem, stream>>>(dmap, imap, p, adj_o, adj_i, grad);
     RBGP4_CHECK_LAUNCH("sddmm_tc_kernel launch");
     return RBGP4_OK;
 }
