@@ -892,6 +892,27 @@ def run_train_leg(B, args):
         b.record(B.stream)
     torch.cuda.synchronize()
     ms_step = B.max_over_ranks(a.elapsed_time(b) / reps)
+    # the whole SGD step (forward, autograd backward, update) captured as one CUDA graph: device
+    # time without the per-op Python launch overhead
+    ms_graph, graph_note = None, None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(B.stream):
+            B.stream.synchronize()
+            with torch.cuda.graph(g, stream=B.stream):
+                step()
+            g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(B.stream)
+            for _ in range(reps):
+                g.replay()
+            b.record(B.stream)
+        torch.cuda.synchronize()
+        ms_graph = B.max_over_ranks(a.elapsed_time(b) / reps)
+        del g
+    except Exception as exc:  # noqa: BLE001 -- report, the eager figure stands
+        graph_note = f"graph capture failed: {exc}"[:200]
+        torch.cuda.synchronize()
     # the three products alone, operands already in the product layouts (bf16)
     pat = layer.pattern
     vb = layer.values.detach().to(torch.bfloat16).contiguous()
@@ -923,6 +944,9 @@ def run_train_leg(B, args):
     k_ms = sum(kerns.values()) / 1e3
     return {"layer": lay["name"], "shape": {"rows": w.rows, "cols": w.cols, "n": n}, "sparsity": args.sparsity,
             "step_ms": ms_step, "step_tflops": flops * B.world / (ms_step * 1e-3) / 1e12,
+            "graph_step_ms": ms_graph,
+            "graph_step_tflops": None if ms_graph is None else flops * B.world / (ms_graph * 1e-3) / 1e12,
+            "graph_note": graph_note,
             "products_us": kerns, "products_tflops": flops * B.world / (k_ms * 1e-3) / 1e12,
             "what": "SGD step of TrainableSparseLinear(compute='bf16'): bf16 operands, fp32 accumulation / "
                     "gradients / master values; FLOPs = 3 x 2 nnz N (forward, W^T dO, pattern dW)"}
