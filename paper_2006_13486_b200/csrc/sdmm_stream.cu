@@ -1,36 +1,37 @@
-// sdmm_stream.cu -- K5: the RBGP4 SDMM streamed through tcgen05 at the HBM rate.
+// sdmm_stream.cu -- K5: the RBGP4 SDMM and its implicit-im2col convolution streamed through
+// tcgen05, the default compute="bf16" path.
 //
-// Replaces kronsparse.sdmm._tile_worker (reference sdmm.py:148-205) for compute="bf16" on
-// the tensor-core factorisation with 16 x 16 dense element blocks (g_r = (1,1), g_i (8,8) of
-// degree 2, g_b = (16,16): SURVEY §8(d) "TC16"), the shape the VGG19 512-channel layers, the
-// bench headline and the config-4 sweep run.  Same transposed product as K4
-// (sdmm_gather.cu) per output tile (tile-row tbm, 128 batch columns n0..):
-//     D^T (128 x rows) += I^T (128 x 16) * W^T (16 x rows)   per g_i column block,
-// M = 128 batch columns (MN-major I, as TMA lands it), the gather being the A descriptor's
-// start address.  K5 changes everything around the MMAs, from B200 measurements
-// (tools/stream_bench.cu, tools/epi_bench.cu, tools/tma_issue_bench.cu):
+// Replaces kronsparse.sdmm._tile_worker (reference sdmm.py:148-205).  Transposed product per
+// output tile (tile-row tbm, 128 batch columns / pixels n0..):
+//     D^T (128 x rows) += I^T (128 x 16) * W^T (16 x rows)   per K16 slice of a step,
+// M = 128 batch columns (the I slab exactly as TMA lands it: MN-major for the SDMM, the K-major
+// NHWC pixel x channel box for the conv), the gather being the A descriptor's start address,
+// D in TMEM.  Which W rows a slice multiplies is a per-matrix relayout prepared once:
 //
-// * TMA issue is the producer's cost, not bandwidth: one thread spends ~265-310 cycles per
-//   3-D box and ~140-155 per 2-D box whatever its size.  So the loads of a step are spread
-//   over THREE producer warps, and a step is as few boxes as possible (whole tiles: one I
-//   slab + one W tile; row groups: the group's W rows are ONE box of a row-permuted copy).
-// * Setup.  K4 spent ~6k cycles before its first I request.  Here the W producer requests
-//   the W tiles of the first ring's worth of steps before griddepcontrol.wait (weights are
-//   never the previous grid's output); the I producers wait only for the barrier init.
-// * Work units.  Many tiles: whole tiles (the K4 TC16 relayout: 8 MMAs of N = 32 per step)
-//   in a persistent loop.  Few tiles (small N): ROW GROUPS -- a unit owns G row blocks of a
-//   tile and loads only the 16-row pieces of each slab those row blocks read (the union of
-//   their g_i neighbours), so the grid fills the SMs with NO split-K partial exchange (DSMEM
-//   measured 15 B/clk per SM).
-// * Epilogue.  Each epilogue warp owns 32 batch columns: it packs column pairs into 32-bit
-//   words with one shuffle (sub-word shared stores from different lanes measured ~60 cycles
-//   each), and stores its own rows: direct global stores under the next unit's main loop, or
-//   -- for a CTA's last unit, the only exposed one -- staging in the then idle ring and its
-//   own TMA tensor store (no cross-warp barrier).
+// * TC16 (g_r (1,1), g_i (8,8) of degree 2, g_b (16,16): SURVEY §8(d), the bench headline):
+//   K4's column-block relayout -- 8 MMAs of N = 32 per step (two row blocks of 16 per column
+//   block); for small N, ROW GROUPS -- a unit owns G row blocks of a tile and loads only the
+//   16-row pieces of each slab those row blocks read (no split-K exchange).
+// * Slices (any g_b that tiles K16: 8 x 8 / 4 x 4 blocks, g_i degree <= 4): slice kb of a step
+//   times the union of the rows reading it, zero-padded to N = 32 / 64; each row sums <= 4
+//   TMEM partials in the epilogue.
+// * Merged tile-row pairs (g_o complete): one unit = two tile-rows, unions twice as wide, the I
+//   slab loaded once for both; single-buffered 512-column accumulator.
+// * Conv: tap-shifted 4-D NHWC boxes per step, or HALO strips (3x3, stride 1, one channel
+//   block): a 16 x 8 output strip stages its 18 x 10 halo once and the nine taps are
+//   descriptor row offsets; ReLU and the following 2x2 max pool fused into the epilogue.
 //
-// Warps (384 threads): 0-3 epilogue (TMEM lane = batch column), 4 and 7-11 I producers (steps
-// round-robin), 6 W producer, 5 TMEM allocation + MMA issue.  Deterministic: every unit owns its
-// output rows; fixed step order.
+// Measured design rules (tools/stream_bench.cu, tma_par_bench.cu, umma_bench3.cu, epi_bench.cu;
+// DESIGN.md "What bounds the kernels"): a TMA box costs its issuing THREAD ~450 cycles whatever
+// its size, so up to six I producer warps take the steps round-robin; an M128 K16 MMA costs ~82
+// cycles up to N = 64, so a step is as few, as wide MMAs as the pattern allows; the W producer
+// requests the first ring's W before griddepcontrol.wait (weights never depend on the previous
+// grid); epilogue warps pack column pairs with one shuffle and store directly under the next
+// unit's main loop, the CTA's last unit staged in the idle ring and TMA-stored.
+//
+// Warps (384 threads): 0-3 epilogue (TMEM lane = batch column), 4 and 7-11 I producers, 6 W
+// producer, 5 TMEM allocation + MMA issue (heavy epilogues: warps 8-11 a second epilogue group).
+// Deterministic: every unit owns its output rows; fixed step and partial-sum order.
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
