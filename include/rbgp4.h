@@ -207,10 +207,14 @@ int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t
  * Plan overrides (A/B switches for tests and tuning; the defaults are the production plan).
  * Thread-local: a value set on one host thread affects only launches planned on that thread.
  * Names: relayout, dense, persistent, msplit, ksplit, stages, multicast, sym, pdl, simt_ct,
- * tc_tn, tc_na, tc_nb, tc_nw, wswz, ostore, sched, i3d, promo, conv_wide, debug (include the
- * kernels' trace/ablation hooks only in a debug build, see rbgp4_debug_build).  Unknown names
- * and out-of-range values return RBGP4_EINVAL.  None of them changes results beyond the fp32
- * summation order of the tensor-core modes.  ABI v3.
+ * tc_tn, tc_na, tc_nb, tc_nw, wswz, ostore, sched, i3d, promo, conv_wide, stream, stream_g,
+ * halo, simt_wide, merge, debug (include the kernels' trace/ablation hooks only in a debug
+ * build, see rbgp4_debug_build).  Unknown names and out-of-range values return RBGP4_EINVAL.
+ * None of them changes results beyond the fp32 summation order of the tensor-core modes.
+ * `relayout`, `merge` and `sched` change the layout of a prepared buffer: a buffer must be used
+ * under the values they had at rbgp4_prepare (rbgp4_prepare_size differs between the layouts,
+ * so a cache keyed by the size -- as paper_2006_13486_b200.sdmm.prepared() does -- is safe).
+ * ABI v3.
  */
 int rbgp4_set_option(const char *name, int64_t value);
 int rbgp4_get_option(const char *name, int64_t *value);
