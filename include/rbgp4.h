@@ -211,9 +211,10 @@ int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t
  * halo, simt_wide, merge, debug (include the kernels' trace/ablation hooks only in a debug
  * build, see rbgp4_debug_build).  Unknown names and out-of-range values return RBGP4_EINVAL.
  * None of them changes results beyond the fp32 summation order of the tensor-core modes.
- * `relayout`, `merge` and `sched` change the layout of a prepared buffer: a buffer must be used
- * under the values they had at rbgp4_prepare (rbgp4_prepare_size differs between the layouts,
- * so a cache keyed by the size -- as paper_2006_13486_b200.sdmm.prepared() does -- is safe).
+ * `relayout` and `merge` change the layout of a prepared buffer: a buffer must be used under the
+ * values they had at rbgp4_prepare (rbgp4_prepare_size differs between the layouts, so a cache
+ * keyed by the size -- as paper_2006_13486_b200.sdmm.prepared() does -- is safe; `sched` only
+ * reorders the steps the buffer records).
  * ABI v3.
  */
 int rbgp4_set_option(const char *name, int64_t value);
