@@ -138,3 +138,36 @@ def test_worker_count_and_gpu_count_invariance(recorded):
         parts = [ks.rbgp4mm(w, np.ascontiguousarray(inp[:, i * step:(i + 1) * step]), p)[0]
                  for i in range(shards)]
         assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+REF_OBJECTS = r'''
+import sys
+import numpy as np
+sys.path.insert(0, "/root/reference/pkg/src")
+import kronsparse as kr                     # the reference itself
+import paper_2006_13486_b200 as ks          # this package (its own modules, no alias)
+from paper_2006_13486_b200.errors import DeviceError
+g = [kr.complete_graph(2, 4), kr.complete_graph(1, 1),
+     kr.generate_ramanujan(kr.LiftChainSpec(8, 8, 0.75, rng_seed=3)).graph, kr.complete_graph(16, 16)]
+chain = kr.RbgpChain(tuple(g))
+w = kr.init_random(chain, kr.make_rng(5), precision="f32")
+params = ks.tiling_for_chain(w.chain)                       # our tiling on the reference's chain
+assert params == ks.TilingParams(**{f: getattr(kr.tiling_for_chain(w.chain), f)
+                                    for f in ks.TilingParams.__dataclass_fields__})
+inp = np.ones((w.cols, 256), dtype=np.float32)
+try:
+    ks.rbgp4mm(w, inp, params)                              # validation accepts it; no GPU here
+except DeviceError:
+    print("DEVICE-ONLY")
+'''
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_TESTS), reason="reference not present (GPU box)")
+def test_reference_built_objects_reach_the_device(tmp_path):
+    """Route 1's claim (INTEGRATION.md): an RcubsMatrix / RbgpChain built by the reference itself
+    goes through this package's tiling and rbgp4mm validation unchanged (duck-typed on
+    .chain / .values) -- on this GPU-less host the call ends in DeviceError, i.e. at the device."""
+    env = dict(os.environ, PYTHONPATH=ROOT, CUDA_VISIBLE_DEVICES="")
+    res = subprocess.run([sys.executable, "-c", REF_OBJECTS], env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert "DEVICE-ONLY" in res.stdout
