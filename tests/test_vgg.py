@@ -3,7 +3,7 @@
 CPU: every sparse layer gets a certified factorisation at the paper's sparsities.
 GPU: the NHWC max-pool is bit-exact against torch, and the whole network (dense conv1,
 15 RBGP4 convs with fused ReLU, 5 pools, dense classifier) matches a torch fp32 forward
-with the same (bf16-rounded) dense weights to rel-L2 <= 2e-2 -- bf16 activations are
+with the same (bf16-rounded) dense weights to rel-L2 <= 1e-2 -- bf16 activations are
 re-rounded at every layer on the product path, so the error compounds over 16 layers.
 """
 
@@ -50,4 +50,4 @@ def test_vgg19_forward_matches_dense(sparsity):
     ref = net.reference_forward(x)
     rel = float((y - ref).norm() / ref.norm())
     assert y.shape == (6, 100)
-    assert rel <= 2e-2, rel
+    assert rel <= 1e-2, rel  # measured 4.0e-3 .. 6.9e-3 over seeds 3-5 at 87.5 / 50 %

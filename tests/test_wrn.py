@@ -41,7 +41,7 @@ def test_wrn_forward_bf16_and_ffma():
     y16 = net(x, compute="bf16").float()
     ref16 = net.reference_forward(x, round_bf16=True)
     assert y16.shape == (4, 10)
-    assert float((y16 - ref16).norm() / ref16.norm()) < 3e-2
+    assert float((y16 - ref16).norm() / ref16.norm()) < 3e-3  # measured 4.0e-4 / 6.3e-4 (seeds 2, 3)
     y32 = net(x, compute="ffma")
     tf32 = torch.backends.cudnn.allow_tf32
     torch.backends.cudnn.allow_tf32 = False  # the fp32 reference must not round to tf32
