@@ -49,6 +49,8 @@ SDMM_CASES = [
     ((2, 18), 0.0, (16, 16), 0.875, (8, 8), 65536, "K5 stream", "persistent, merged tile-row pairs (g_o complete)"),
     ((4, 18), 0.0, (8, 8), 0.75, (16, 16), 8192, "K5 stream", "TC16 with g_o complete: merged pairs, N = 64"),
     ((2, 9), 0.0, (16, 16), 0.875, (8, 8), 1024, "K5 stream", "merged pairs, one unit per CTA"),
+    ((2, 9), 0.0, (16, 16), 0.875, (8, 8), 4160, "K5 stream", "merged pairs, ragged last column tile (N % 128 = 64)"),
+    ((4, 36), 0.5, (16, 16), 0.875, (8, 8), 4160, "K5 stream", "8x8 slices, ragged last column tile"),
     ((4, 36), 0.5, (16, 16), 0.75, (8, 8), 4096, "K5 stream", "g_i degree 4 (8x8 blocks): four partials, N = 64"),
     ((2, 18), 0.0, (8, 8), 0.5, (16, 16), 8192, "K5 stream", "TC16 blocks, g_i degree 4 (50 %): four partials"),
     ((4, 36), 0.5, (16, 16), 0.5, (8, 8), 1024, "K2 tc", "g_i degree 8: too many partials -> densify K2"),

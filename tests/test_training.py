@@ -90,7 +90,9 @@ def test_trainable_layer_rejects_mixed_dtypes():
 TC_CHAINS = [
     wl.SweepConfig("tc16", (4, 8), 0.5, (1, 1), (8, 8), 0.75, (16, 16), n_cols=1, seed=4),        # K5 TC16
     wl.SweepConfig("slice8", (4, 8), 0.5, (1, 1), (16, 16), 0.875, (8, 8), n_cols=1, seed=5),     # K5 slices
-    wl.SweepConfig("tc", (4, 6), 0.5, (1, 1), (16, 16), 0.75, (8, 8), n_cols=1, seed=3),          # K2
+    wl.SweepConfig("tc", (4, 6), 0.5, (1, 1), (16, 16), 0.75, (8, 8), n_cols=1, seed=3),          # K5, 4 partials
+    wl.SweepConfig("merged", (2, 6), 0.0, (1, 1), (8, 8), 0.75, (16, 16), n_cols=1, seed=6),      # merged pairs
+    wl.SweepConfig("tc16-d4", (4, 8), 0.5, (1, 1), (8, 8), 0.5, (16, 16), n_cols=1, seed=7),      # TC16, 4 partials
 ]
 
 
