@@ -63,7 +63,7 @@ def parse_args(argv=None):
                     help="base-graph factorisation of every layer")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--quick", action="store_true", help="headline, roofline and e2e only")
-    for leg in ("cpu-baseline", "e2e", "alt", "conv", "sweep", "precision", "l2", "train"):
+    for leg in ("cpu-baseline", "e2e", "alt", "conv", "sweep", "precision", "l2", "train", "config1"):
         ap.add_argument(f"--no-{leg}", action="store_true")
     ap.add_argument("--wrn-batch", type=int, default=512,
                     help="WRN-40-4 leg (config 3): batch per rank; 0 = skip")
@@ -74,6 +74,7 @@ def parse_args(argv=None):
     args = ap.parse_args(argv)
     if args.quick:
         args.no_alt = args.no_conv = args.no_sweep = args.no_precision = args.no_l2 = args.no_train = True
+        args.no_config1 = True
         args.wrn_batch = args.vgg_batch = 0
     return args
 
@@ -700,6 +701,8 @@ def run_ours(args):
         legs["vgg19"] = run_vgg_leg(B, args)
     if not args.no_train:
         legs["train_bf16"] = run_train_leg(B, args)
+    if not args.no_config1 and rank == 0:
+        legs["config1"] = run_config1_leg(B, args)
     if args.wrn_batch > 0:
         legs["wrn40_4"] = run_wrn_leg(B, args)
 
@@ -853,6 +856,64 @@ def run_vgg_leg(B, args):
                                    "ok": err < 1e-2}
         B.barrier()
     del y
+    return res
+
+
+def run_config1_leg(B, args):
+    """BASELINE configs[0]: the single RBGP4 SDMM the reference benchmarks on its CPU path --
+    W 512 x 512 fp32 at 75 % (C1a: G_o (8,16) @ .5, G_r (2,1), G_i (32,32) @ .5, G_b (1,1)) x I
+    512 x 1024 -- on the GPU in every compute mode (each a CUDA graph of 20 launches, inputs
+    resident) next to the pinned C port of _tile_worker on the host cores (same metric)."""
+    torch = B.torch
+    import oracle
+    import paper_2006_13486_b200 as ks
+    from paper_2006_13486_b200 import _native
+    from paper_2006_13486_b200 import workloads as wl
+    from paper_2006_13486_b200.device import device_format
+    from paper_2006_13486_b200.sdmm import launch_sdmm
+    chain, w, inp = wl.make_operands(wl.C1A)
+    n = inp.shape[1]
+    g_o, _, g_i, _ = chain.graphs
+    lay = dict(flops=2 * w.nnz * n, nnz=w.nnz, m=w.rows, k=w.cols, n=n,
+               adj_ints=g_o.num_left * len(g_o.adjacency[0]) + g_i.num_left * len(g_i.adjacency[0]))
+    res = {"what": "C1a: W 512x512 fp32 @75% (G_b (1,1), G_r (2,1)) x I 512x1024; GPU CUDA graphs of 20 "
+                   "launches vs the C port of _tile_worker", "gpu": {}}
+    reps = 20
+    for compute in ("exact", "ffma", "tf32", "bf16"):
+        dt = torch.bfloat16 if compute == "bf16" else torch.float32
+        fmt = device_format(w, B.dev, dt)
+        x = torch.from_numpy(inp).to(B.dev).to(dt)
+        o = torch.empty((w.rows, n), device=B.dev, dtype=dt)
+        with torch.cuda.stream(B.stream):
+            launch_sdmm(fmt, compute, x, o, B.dev)
+            B.stream.synchronize()
+            kern = _native.last_kernel()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=B.stream):
+                for _ in range(reps):
+                    launch_sdmm(fmt, compute, x, o, B.dev)
+            g.replay()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(B.stream)
+            g.replay()
+            b.record(B.stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        s_el = 2 if compute == "bf16" else 4
+        res["gpu"][compute] = {"us": ms * 1e3, "tflops_eff": lay["flops"] / (ms * 1e-3) / 1e12, "kernel": kern,
+                               "roofline": roofline(lay, ms, s_el, s_el, compute, B.peaks)}
+        del g
+    threads = len(os.sched_getaffinity(0))
+    params = ks.tiling_for_chain(chain, workers=threads)
+    oracle.tiled(w, inp, params, threads=threads)
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < 2.0 or k < 3:
+        oracle.tiled(w, inp, params, threads=threads)
+        k += 1
+    cpu_s = (time.perf_counter() - t0) / k
+    res["cpu_port"] = {"ms": cpu_s * 1e3, "tflops_eff": lay["flops"] / cpu_s / 1e12, "threads": threads,
+                       "kind": "port (oracle/ C restatement of kronsparse._tile_worker, f32 exact order)"}
     return res
 
 
