@@ -18,6 +18,9 @@
 // never contracted) and is bit-identical to the reference for any tiling;
 // EXACT=false uses FFMA in the same order (rel. error ~1e-7, 2x issue rate).
 #include "common.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
 
 namespace rbgp4 {
 namespace {
@@ -27,6 +30,7 @@ struct SimtParams {
     int32_t d_o, tm, tk, rm, rk, bm, bk, u_i, v_i, d_i, d_t, g;
     int32_t tnc, cthreads, wstride, istride;
     int32_t vec_in, vec_out;  // 16-byte paths legal for I loads / O stores
+    int32_t nbuf;             // wide variant: TMA ring slots
 };
 
 constexpr int kThreads = 256;
@@ -232,126 +236,164 @@ simt_kernel(const SimtParams p, const T *__restrict__ values, const int32_t *__r
 // each thread owns 16 rows of one group x 4 columns, so an I vector (LDS.128) feeds 64 FMAs
 // and the W values of 4 consecutive j are one broadcast LDS.128 per row -- about one shared
 // wavefront per 8 FFMA instead of one per 2 (the generic kernel is shared-memory bound at
-// ~0.22 of the FFMA peak).  W is staged with 16-byte cp.async.  Same per-element order as the
-// reference (sdmm.py:178-204): c = 0; c += w*x over j ascending; acc += c per step.
-constexpr int kWideRows = 16;
+// ~0.22 of the FFMA peak).  Both operands of a step arrive by TMA (one W box of the compressed
+// tile-row, tm x d_t, and one I box, tk x tnc, zero-filled past n_cols) into a 2-slot ring
+// completed on mbarriers: one thread issues two copies per step, where per-thread cp.async
+// address arithmetic was ~40 % of the kernel's instructions and stall samples
+// (profiles/r02f_k1wide_conv10_ncu_*).  Same per-element order as the reference
+// (sdmm.py:178-204): c = 0; c += w*x over j ascending; acc += c per step.
+constexpr int kWideBox = 256;  // TMA box rows per copy
 
-template <bool EXACT>
+// ROWS rows of one repetition group x COLV float4 column chunks per thread (ROWS * COLV = 16,
+// 64 outputs): (16, 1) for groups of >= 16 rows, (8, 2) and (4, 4) for the 8- and 4-row groups
+// of the WRN factorisations (G_b (8,8) / (4,4)).  Per 4 consecutive j a thread reads 4 * COLV
+// I vectors and ROWS W vectors (LDS.128) for 256 FFMA.  Column chunk k of thread tc sits at
+// column 4 * (tc + k * cthreads), so every LDS.128 of a half-warp is one contiguous 256 B row.
+template <bool EXACT, int ROWS, int COLV>
 __global__ void __launch_bounds__(kThreads)
-simt_wide_kernel(const SimtParams p, const float *__restrict__ values, const int32_t *__restrict__ adj_o,
-                 const int32_t *__restrict__ adj_i, const float *__restrict__ inp, float *__restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+simt_wide_kernel(const SimtParams p, const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap imap,
+                 const int32_t *__restrict__ adj_o, const int32_t *__restrict__ adj_i, float *__restrict__ out) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int64_t n0 = int64_t(blockIdx.x) * p.tnc;
     const int64_t tbm = blockIdx.y;
     const int tid = threadIdx.x;
-    float *wring = reinterpret_cast<float *>(smem_raw);
-    float *iring = wring + 2 * p.tm * p.wstride;
-    int32_t *rowidx = reinterpret_cast<int32_t *>(iring + 2 * p.tk * p.istride);
-    const int wslot = p.tm * p.wstride, islot = p.tk * p.istride;
+    const int nbuf = p.nbuf;
+    float *ring = reinterpret_cast<float *>(smem_raw);
+    const int wslot = p.tm * p.d_t, slot = wslot + p.tk * p.tnc;  // floats per ring slot
+    int32_t *rowidx = reinterpret_cast<int32_t *>(ring + nbuf * slot);
+    uint64_t *full = reinterpret_cast<uint64_t *>(rowidx + ((p.u_i * p.d_t + 1) & ~1));
+    const int32_t *orow = adj_o + tbm * p.d_o;
+    const uint32_t step_bytes = uint32_t(slot) * 4u;
+    auto issue = [&](int s) {  // thread 0: both boxes of step s into slot s % nbuf
+        const int b = s % nbuf;
+        float *ws = ring + b * slot, *is = ws + wslot;
+        uint64_t *bar = &full[b];
+        mbar_expect_tx(bar, step_bytes);
+        const int32_t oind = orow[s];
+        for (int r = 0; r < p.tm; r += kWideBox)
+            tma_load_2d(ws + r * p.d_t, &wmap, bar, s * p.d_t, int32_t(tbm * p.tm + r));
+        for (int r = 0; r < p.tk; r += kWideBox)
+            tma_load_2d(is + r * p.tnc, &imap, bar, int32_t(n0), oind * p.tk + r);
+    };
+    if (tid == 0) {
+        for (int b = 0; b < nbuf; ++b) mbar_init(&full[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < nbuf && s < p.d_o; ++s) issue(s);
+    }
+    // row table pre-multiplied by the I row stride (the wanted I row of W column j of group ui)
     for (int e = tid; e < p.u_i * p.d_t; e += int(blockDim.x)) {
         int ui = e / p.d_t, j = e - ui * p.d_t;
         int k = j % p.bk, q = j / p.bk, ink = q % p.d_i, rk = q / p.d_i;
-        rowidx[e] = (rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k;
+        rowidx[e] = ((rk * p.v_i + adj_i[ui * p.d_i + ink]) * p.bk + k) * p.tnc;
     }
     const int tc = tid % p.cthreads;
-    const int slot0 = (tid / p.cthreads) * kWideRows;  // this thread's 16 group slots
+    const int slot0 = (tid / p.cthreads) * ROWS;  // this thread's group slots
     const int ui = slot0 / p.g;
-    int urow[kWideRows];
+    int urow[ROWS];  // W row offsets (floats) inside a slot
 #pragma unroll
-    for (int i = 0; i < kWideRows; ++i) {
+    for (int i = 0; i < ROWS; ++i) {
         const int w = slot0 - ui * p.g + i, rm = w / p.bm, m = w - rm * p.bm;
-        urow[i] = (rm * p.u_i + ui) * p.bm + m;
+        urow[i] = ((rm * p.u_i + ui) * p.bm + m) * p.d_t;
     }
-    float acc[kWideRows][4];
+    float acc[ROWS][COLV * 4];
 #pragma unroll
-    for (int i = 0; i < kWideRows; ++i)
+    for (int i = 0; i < ROWS; ++i)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[i][e] = 0.0f;
-    const int32_t *orow = adj_o + tbm * p.d_o;
-    auto stage_w = [&](int s, float *ws, const float *is_unused) {
-        (void)is_unused;
-        const float *wsrc = values + tbm * p.tm * p.row_nnz + int64_t(s) * p.d_t;
-        const int chunks = p.d_t / 4;
-        for (int e = tid; e < p.tm * chunks; e += int(blockDim.x)) {
-            const int r = e / chunks, c4 = (e - r * chunks) * 4;
-            cp_async16(ws + r * p.wstride + c4, wsrc + r * p.row_nnz + c4, true);
-        }
-    };
-    auto stage_i = [&](int64_t oind, float *is) {
-        const float *isrc = inp + oind * p.tk * p.ld_in + n0;
-        const int chunks = p.tnc / 4;
-        for (int e = tid; e < p.tk * chunks; e += int(blockDim.x)) {
-            const int r = e / chunks, c = (e - r * chunks) * 4;
-            const bool ok = n0 + c < p.n_cols;
-            cp_async16(is + r * p.istride + c, ok ? isrc + r * p.ld_in + c : isrc, ok);
-        }
-    };
-    stage_w(0, wring, nullptr);
-    stage_i(orow[0], iring);
-    cp_async_commit();
+        for (int e = 0; e < COLV * 4; ++e) acc[i][e] = 0.0f;
+    __syncthreads();  // row table and barrier init visible
     const int32_t *ridx = rowidx + ui * p.d_t;
+    const int cstep = 4 * p.cthreads;  // floats between a thread's column chunks
     for (int s = 0; s < p.d_o; ++s) {
-        if (s + 1 < p.d_o) {
-            const int b = (s + 1) & 1;
-            stage_w(s + 1, wring + b * wslot, nullptr);
-            stage_i(orow[s + 1], iring + b * islot);
-            cp_async_commit();
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-        const float *ws = wring + (s & 1) * wslot;
-        const float *is = iring + (s & 1) * islot + tc * 4;
-        float c[kWideRows][4];
+        const int b = s % nbuf;
+        mbar_wait(&full[b], uint32_t(s / nbuf) & 1u);
+        const float *ws = ring + b * slot;
+        const float *is = ws + wslot + tc * 4;
+        float c[ROWS][COLV * 4];
 #pragma unroll
-        for (int i = 0; i < kWideRows; ++i)
+        for (int i = 0; i < ROWS; ++i)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) c[i][e] = 0.0f;
+            for (int e = 0; e < COLV * 4; ++e) c[i][e] = 0.0f;
 #pragma unroll 1
         for (int j = 0; j < p.d_t; j += 4) {
-            float x[4][4];
+            if constexpr (COLV == 1) {
+                float x[4][4];
 #pragma unroll
-            for (int jj = 0; jj < 4; ++jj) load4<float>(is + ridx[j + jj] * p.istride, x[jj]);
+                for (int jj = 0; jj < 4; ++jj) load4<float>(is + ridx[j + jj], x[jj]);
 #pragma unroll
-            for (int i = 0; i < kWideRows; ++i) {
-                const float4 w4 = *reinterpret_cast<const float4 *>(ws + urow[i] * p.wstride + j);
-                const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+                for (int i = 0; i < ROWS; ++i) {
+                    const float4 w4 = *reinterpret_cast<const float4 *>(ws + urow[i] + j);
+                    const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
+                    for (int jj = 0; jj < 4; ++jj)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        if constexpr (EXACT) c[i][e] = __fadd_rn(c[i][e], __fmul_rn(w[jj], x[jj][e]));
-                        else c[i][e] = __fmaf_rn(w[jj], x[jj][e], c[i][e]);
+                        for (int e = 0; e < 4; ++e) {
+                            if constexpr (EXACT) c[i][e] = __fadd_rn(c[i][e], __fmul_rn(w[jj], x[jj][e]));
+                            else c[i][e] = __fmaf_rn(w[jj], x[jj][e], c[i][e]);
+                        }
+                }
+            } else {
+                float w[ROWS][4];
+#pragma unroll
+                for (int i = 0; i < ROWS; ++i) {
+                    const float4 w4 = *reinterpret_cast<const float4 *>(ws + urow[i] + j);
+                    w[i][0] = w4.x; w[i][1] = w4.y; w[i][2] = w4.z; w[i][3] = w4.w;
+                }
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const float *xr = is + ridx[j + jj];
+                    float x[COLV * 4];
+#pragma unroll
+                    for (int k = 0; k < COLV; ++k) {
+                        const float4 v = *reinterpret_cast<const float4 *>(xr + k * cstep);
+                        x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
                     }
+#pragma unroll
+                    for (int i = 0; i < ROWS; ++i)
+#pragma unroll
+                        for (int e = 0; e < COLV * 4; ++e) {
+                            if constexpr (EXACT) c[i][e] = __fadd_rn(c[i][e], __fmul_rn(w[i][jj], x[e]));
+                            else c[i][e] = __fmaf_rn(w[i][jj], x[e], c[i][e]);
+                        }
+                }
             }
         }
 #pragma unroll
-        for (int i = 0; i < kWideRows; ++i)
+        for (int i = 0; i < ROWS; ++i)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) acc[i][e] = __fadd_rn(acc[i][e], c[i][e]);
-        __syncthreads();
+            for (int e = 0; e < COLV * 4; ++e) acc[i][e] = __fadd_rn(acc[i][e], c[i][e]);
+        __syncthreads();  // every thread is done with slot b
+        if (tid == 0 && s + nbuf < p.d_o) issue(s + nbuf);
     }
-    const int64_t col = n0 + tc * 4;
 #pragma unroll
-    for (int i = 0; i < kWideRows; ++i) {
-        float *dst = out + (tbm * p.tm + urow[i]) * p.ld_out + col;
-        if (p.vec_out && col + 3 < p.n_cols) {
-            *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-        } else {
+    for (int i = 0; i < ROWS; ++i) {
+        float *drow = out + (tbm * p.tm + urow[i] / p.d_t) * p.ld_out;
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (col + e < p.n_cols) dst[e] = acc[i][e];
+        for (int k = 0; k < COLV; ++k) {
+            const int64_t col = n0 + tc * 4 + k * cstep;
+            float *dst = drow + col;
+            if (p.vec_out && col + 3 < p.n_cols) {
+                *reinterpret_cast<float4 *>(dst) =
+                    make_float4(acc[i][4 * k], acc[i][4 * k + 1], acc[i][4 * k + 2], acc[i][4 * k + 3]);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (col + e < p.n_cols) dst[e] = acc[i][4 * k + e];
+            }
         }
     }
 }
 
-// wide-variant geometry: (tm / 16) row threads x cthreads column threads (<= 256 per CTA)
+// rows per thread of the wide variant for this chain (0: not eligible)
+int wide_rows(const ChainDims &c) {
+    for (int r : {16, 8, 4})
+        if (c.g % r == 0 && c.tm % r == 0) return r;
+    return 0;
+}
+
 bool wide_ok(const ChainDims &c, const void *values, const void *inp) {
     if (opts().simt_wide == 0) return false;
-    return c.g % kWideRows == 0 && c.tm % kWideRows == 0 && c.tm / kWideRows * 8 <= kThreads &&
-           c.d_t % 4 == 0 && c.row_nnz % 4 == 0 &&
-           c.ld_in % 4 == 0 && c.n_cols % 4 == 0 && reinterpret_cast<uintptr_t>(values) % 16 == 0 &&
+    return wide_rows(c) && c.d_t % 4 == 0 && c.d_t <= 256 && c.row_nnz % 4 == 0 &&
+           c.ld_in % 4 == 0 && reinterpret_cast<uintptr_t>(values) % 16 == 0 &&
            reinterpret_cast<uintptr_t>(inp) % 16 == 0;
 }
 
@@ -362,26 +404,70 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
     p.rows = c.rows; p.n_cols = c.n_cols; p.ld_in = c.ld_in; p.ld_out = c.ld_out;
     p.row_nnz = c.row_nnz; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.rm = c.rm; p.rk = c.rk;
     p.bm = c.bm; p.bk = c.bk; p.u_i = c.u_i; p.v_i = c.v_i; p.d_i = c.d_i; p.d_t = c.d_t; p.g = c.g;
-    // 16 column threads (64 columns): with ~255 registers per thread, two 128-thread CTAs share
-    // an SM, each with its own 2-stage ring (conv10 ffma: 104 us against 151 us at 32 column
-    // threads and 148 us on the generic kernel, tools/simt_ab.py); below one CTA per SM the
-    // generic kernel's narrower tiles win (conv13, N = 1024: 62 vs 69 us), so it takes those
-    const int rthreads = c.tm / kWideRows;
+    const int rows = wide_rows(c), colv = 16 / rows;
+    const int rthreads = c.tm / rows;
     const int64_t row_blocks = c.rows / c.tm;
-    int ct = 16;
-    if (opts().simt_ct == 8 || opts().simt_ct == 16 || opts().simt_ct == 32) ct = opts().simt_ct;
-    else if ((c.n_cols + 4 * ct - 1) / (4 * ct) * row_blocks < kNumSMs) return RBGP4_EUNSUPPORTED;
-    if (ct * rthreads > kThreads) return RBGP4_EUNSUPPORTED;
+    // column threads: 16 (64 columns per CTA at 16 rows per thread; ~220 registers, two CTAs
+    // per SM), 8 when 16 would leave SMs without a CTA (conv14, N = 1024: 48 us either way
+    // against 62 us on the generic kernel, tools/simt_ab.py); a warp-multiple CTA of <= 256
+    int ct = 0;
+    if (opts().simt_ct == 8 || opts().simt_ct == 16 || opts().simt_ct == 32) {
+        ct = opts().simt_ct;
+    } else {
+        for (int cand : {16, 8}) {
+            if (cand * rthreads > kThreads || (cand * rthreads) % 32) continue;
+            ct = cand;
+            if ((c.n_cols + 4 * colv * cand - 1) / (4 * colv * cand) * row_blocks >= kNumSMs) break;
+        }
+    }
+    if (ct == 0 || ct * rthreads > kThreads || (ct * rthreads) % 32) return RBGP4_EUNSUPPORTED;
     p.cthreads = ct;
-    p.tnc = 4 * ct;
-    p.wstride = c.d_t + 4;
+    p.tnc = 4 * colv * ct;
+    p.wstride = c.d_t;
     p.istride = p.tnc;
-    p.vec_in = 1;
     p.vec_out = (c.ld_out % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    const size_t smem = (2 * (size_t(c.tm) * p.wstride + size_t(c.tk) * p.tnc) * 4 + 15) / 16 * 16 +
-                        size_t(c.u_i) * c.d_t * 4;
+    // ring depth: as many slots as fit two CTAs per SM (one step in flight is enough when a
+    // step is long, e.g. conv10's 48 KB slots; short steps such as WRN's d_t = 8 need more)
+    const size_t slot_bytes = (size_t(c.tm) * c.d_t + size_t(c.tk) * p.tnc) * 4;
+    const size_t fixed = size_t((c.u_i * c.d_t + 1) & ~1) * 4 + 4 * sizeof(uint64_t);
+    int nbuf = int(std::min<size_t>(4, (110 * 1024 - fixed) / slot_bytes));
+    if (nbuf < 2) nbuf = 2;
+    p.nbuf = nbuf;
+    const size_t smem = nbuf * slot_bytes + fixed;
     if (smem > 227 * 1024) return RBGP4_EUNSUPPORTED;
-    auto kern = simt_wide_kernel<EXACT>;
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return RBGP4_ECUDA;
+    }
+    CUtensorMap wmap, imap;
+    const cuuint32_t estr[2] = {1, 1};
+    {   // RcubsMatrix.values as stored: (row_nnz, rows); box d_t x min(tm, 256)
+        const cuuint64_t dims[2] = {cuuint64_t(c.row_nnz), cuuint64_t(c.rows)};
+        const cuuint64_t strides[1] = {cuuint64_t(c.row_nnz) * 4};
+        const cuuint32_t box[2] = {cuuint32_t(c.d_t), cuuint32_t(std::min(c.tm, kWideBox))};
+        CUresult r = enc(&wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(values), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(simt W) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    {   // I: (n_cols, K) with row stride ld_in; box tnc x min(tk, 256), zero fill past n_cols
+        const cuuint64_t dims[2] = {cuuint64_t(c.n_cols), cuuint64_t(c.cols)};
+        const cuuint64_t strides[1] = {cuuint64_t(c.ld_in) * 4};
+        const cuuint32_t box[2] = {cuuint32_t(p.tnc), cuuint32_t(std::min(c.tk, kWideBox))};
+        CUresult r = enc(&imap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(inp), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(simt I) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    auto kern = rows == 16 ? simt_wide_kernel<EXACT, 16, 1>
+              : rows == 8 ? simt_wide_kernel<EXACT, 8, 2> : simt_wide_kernel<EXACT, 4, 4>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) {
@@ -391,7 +477,7 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
     }
     dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm));
     note_kernel("K1 simt wide");
-    kern<<<grid, unsigned(rthreads * ct), smem, stream>>>(p, values, adj_o, adj_i, inp, out);
+    kern<<<grid, unsigned(rthreads * ct), smem, stream>>>(p, wmap, imap, adj_o, adj_i, out);
     RBGP4_CHECK_LAUNCH("simt_wide_kernel launch");
     return RBGP4_OK;
 }

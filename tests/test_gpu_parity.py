@@ -166,3 +166,30 @@ def test_tensor_core_modes_stage_unaligned_operands(compute, n_cols):
     ref = f64_oracle(w, x.double().numpy())
     assert out.shape == (w.rows, n_cols)
     assert oracle.rel_l2(out.cpu().numpy(), ref) < 1e-2
+
+
+@pytest.mark.parametrize("layer", [(64, 64), (128, 128), (256, 256), (64, 16)])
+@pytest.mark.parametrize("n_cols", [1000, 4096])
+def test_simt_wide_variants(layer, n_cols, plan_options):
+    """K1's TMA-fed wide kernel at 16 / 8 / 4 rows per thread (VGG tc16 and WRN-40-4 G_b (8,8) /
+    (4,4) factorisations), ragged N (zero-filled TMA boxes): exact mode bit-identical to the
+    pinned C port of _tile_worker and to the generic K1 kernel; ffma within 1e-5 of f64."""
+    from paper_2006_13486_b200.wrn import wrn_layer_chain
+    chain = wrn_layer_chain(layer[0], layer[1], 0.875, 3)
+    w = ks.init_random(chain, 5, precision="f32")
+    inp = np.random.default_rng(n_cols).uniform(-1, 1, (w.cols, n_cols)).astype(np.float32)
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    x = torch.from_numpy(inp).cuda()
+    out, _ = ks.rbgp4mm(w, x, p)
+    kern = _native.last_kernel()
+    g = chain.graphs[3].num_left * chain.graphs[1].num_left
+    assert kern == ("K1 simt wide" if g % 4 == 0 else "K1 simt"), (layer, kern)
+    got = out.cpu().numpy()
+    assert np.array_equal(got, oracle.tiled(w, inp, p, threads=8)), layer
+    plan_options("simt_wide", 0)
+    generic, _ = ks.rbgp4mm(w, x, p)
+    assert _native.last_kernel() == "K1 simt"
+    assert torch.equal(generic, out)
+    plan_options("simt_wide", -1)
+    fast, _ = ks.rbgp4mm(w, x, p, compute="ffma")
+    assert oracle.max_rel(fast.cpu().numpy(), f64_oracle(w, inp)) <= 1e-5
