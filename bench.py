@@ -1027,17 +1027,20 @@ def run_wrn_leg(B, args):
     res = {"global_batch": batch * B.world, "sparsity": args.sparsity,
            "model": "WideResNet-40-4 CIFAR-10: dense conv1 + FC, 39 RBGP4 convs (36 3x3 + 3 1x1 shortcuts)",
            "data": "synthetic images, random-init weights", "sparse_gflop_per_forward": flops / 1e9}
-    for compute in ("bf16", "ffma"):
+    def timed(compute, fuse):
         with torch.cuda.stream(B.stream):
-            net(x, compute=compute)  # warm-up: prepared formats, tensor maps
+            net(x, compute=compute, fuse=fuse)  # warm-up: prepared formats, tensor maps
             reps = 3
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(B.stream)
             for _ in range(reps):
-                net(x, compute=compute)
+                net(x, compute=compute, fuse=fuse)
             b.record(B.stream)
         torch.cuda.synchronize()
-        ms = B.max_over_ranks(a.elapsed_time(b) / reps)
+        return B.max_over_ranks(a.elapsed_time(b) / reps)
+
+    for compute in ("bf16", "ffma"):
+        ms = timed(compute, True)
         elt = 2 if compute == "bf16" else 4
         nbytes = net.compulsory_bytes(batch, elt)
         peak = B.peaks["bf16_tflops" if compute == "bf16" else "ffma_tflops"][0]
@@ -1046,7 +1049,10 @@ def run_wrn_leg(B, args):
                         "sparse_tflops": flops * B.world / (ms * 1e-3) / 1e12,
                         "compulsory_bytes": nbytes, "roofline_frac": t_star / (ms * 1e-3),
                         "bound": "hbm" if nbytes / (B.peaks["hbm_gbs"][0] * 1e9) >= flops / (peak * 1e12)
-                        else ("tensor" if compute == "bf16" else "ffma")}
+                        else ("tensor" if compute == "bf16" else "ffma"),
+                        # the block tail (residual add + next ReLU) as separate torch ops instead
+                        # of conv_b's epilogue
+                        "ms_per_forward_unfused_tail": timed(compute, False)}
     return res
 
 

@@ -140,6 +140,20 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
                  const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
                  const void *x, void *out, void *workspace, size_t workspace_bytes, void *stream);
 
+/*
+ * The WRN block tail fused into the convolution's epilogue: O = conv(X) + R, R an NHWC tensor
+ * shaped and typed like O, rounded as the unfused conv-then-add rounds (bf16: round the conv,
+ * add in f32, round again), so the result is bit-identical to rbgp4_conv2d followed by the
+ * add; with out_relu != NULL also relu(O) into out_relu (the next block's input).  conv->relu
+ * must be 0.  Streamed kernel (K5) only: other shapes return RBGP4_EUNSUPPORTED (add separately).
+ * Replaces nothing in the reference (its bench lowers convs to rbgp4mm over im2col); it serves
+ * the WRN-40-4 model of SURVEY §8(f).
+ */
+int rbgp4_conv2d_residual(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dtype,
+                          const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
+                          const void *x, const void *residual, void *out, void *out_relu, void *workspace,
+                          size_t workspace_bytes, void *stream);
+
 /* 2x2 / stride-2 max pooling of a bf16 NHWC tensor (the VGG stage boundary);
  * H, W even, channels % 8 == 0, 16-byte aligned. */
 int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int width, int channels,
@@ -153,6 +167,10 @@ int rbgp4_im2col_nhwc(int dtype, const void *x, void *cols, int batch, int heigh
 
 /* dst (n, rows) = src (rows, n) transposed (the product's O back to NHWC), ReLU fused if relu. */
 int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, void *stream);
+/* The same transpose with the WRN block tail: dst = src^T + residual (residual NHWC like dst,
+ * rounded like the unfused add), and relu(dst) into dst_relu when it is not NULL. */
+int rbgp4_nc_to_nhwc_residual(int dtype, const void *src, const void *residual, void *dst, void *dst_relu,
+                              int rows, int64_t n, void *stream);
 
 /*
  * Training direction: the weight gradient restricted to the pattern,
@@ -208,7 +226,7 @@ int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t
  * Thread-local: a value set on one host thread affects only launches planned on that thread.
  * Names: relayout, dense, persistent, msplit, ksplit, stages, multicast, sym, pdl, simt_ct,
  * tc_tn, tc_na, tc_nb, tc_nw, wswz, ostore, sched, i3d, promo, conv_wide, stream, stream_g,
- * halo, simt_wide, merge, debug (include the kernels' trace/ablation hooks only in a debug
+ * halo, simt_wide, merge, stream_ctas, debug (include the kernels' trace/ablation hooks only in a debug
  * build, see rbgp4_debug_build).  Unknown names and out-of-range values return RBGP4_EINVAL.
  * None of them changes results beyond the fp32 summation order of the tensor-core modes.
  * `relayout` and `merge` change the layout of a prepared buffer: a buffer must be used under the

@@ -26,6 +26,7 @@ EXPORTED = (
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count", "rbgp4_last_kernel", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
     "rbgp4_reset_options", "rbgp4_debug_build", "rbgp4_im2col_nhwc", "rbgp4_nc_to_nhwc",
+    "rbgp4_conv2d_residual", "rbgp4_nc_to_nhwc_residual",
 )
 
 
@@ -100,6 +101,11 @@ def lib():
     h.rbgp4_im2col_nhwc.restype = i32
     h.rbgp4_nc_to_nhwc.argtypes = [i32, vp, vp, i32, ctypes.c_int64, i32, vp]
     h.rbgp4_nc_to_nhwc.restype = i32
+    h.rbgp4_conv2d_residual.argtypes = [ctypes.POINTER(Desc), ctypes.POINTER(ConvDesc), i32, vp, vp, vp, vp,
+                                        vp, vp, vp, vp, vp, sz, vp]
+    h.rbgp4_conv2d_residual.restype = i32
+    h.rbgp4_nc_to_nhwc_residual.argtypes = [i32, vp, vp, vp, vp, i32, ctypes.c_int64, vp]
+    h.rbgp4_nc_to_nhwc_residual.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

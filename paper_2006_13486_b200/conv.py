@@ -43,7 +43,7 @@ def conv_out_hw(height: int, width: int, k: int, stride: int):
 
 
 def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = False, out=None,
-                  out_dtype=None, pool: bool = False):
+                  out_dtype=None, pool: bool = False, residual=None, relu_copy: bool = False):
     """NHWC conv of `x` (batch, H, W, c_in) with chain matrix `w`, 'same' padding, stride 1 or 2.
 
     Returns an NHWC (batch, H', W', c_out) CUDA tensor.  `x` must be a CUDA bf16 tensor
@@ -52,6 +52,11 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
     pool=True also applies the 2x2 / stride-2 max pool (bf16 output (batch, H'/2, W'/2, c_out)):
     fused into the streamed kernel's epilogue where its pixel tiles hold whole windows, else
     the separate NHWC pool kernel.
+    residual=R (an NHWC tensor shaped and typed like the output; relu and pool off) returns
+    conv(x) + R, and relu_copy=True returns (conv(x) + R, relu(conv(x) + R)) -- the WRN block
+    tail, fused into the streamed kernel's epilogue (`rbgp4_conv2d_residual`) and bit-identical to
+    the conv followed by the torch add; shapes the streamed kernel does not take run the add
+    separately.
     """
     t = torch()
     if w.chain.k != 4:
@@ -74,6 +79,15 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
     if res_dt not in (t.bfloat16, t.float32):
         raise InvalidArgumentError(f"conv writes bf16 or f32, got {res_dt}")
     oh, ow = conv_out_hw(height, width, kh, stride)
+    if residual is not None:
+        if relu or pool:
+            raise InvalidArgumentError("residual=... adds before any ReLU / pool (relu and pool must be off)")
+        if (not isinstance(residual, t.Tensor) or residual.device != x.device or residual.dtype != res_dt
+                or tuple(residual.shape) != (batch, oh, ow, w.rows) or not residual.is_contiguous()):
+            raise ShapeError(f"residual must be a contiguous NHWC ({batch}, {oh}, {ow}, {w.rows}) {res_dt} tensor "
+                             f"on {x.device}")
+    elif relu_copy:
+        raise InvalidArgumentError("relu_copy=True needs residual=...")
     if pool:
         if res_dt != t.bfloat16 or oh % 2 or ow % 2:
             raise InvalidArgumentError("pool=True needs a bf16 output with an even output map")
@@ -96,17 +110,29 @@ def sparse_conv2d(w, x, kernel_size: int = 3, *, stride: int = 1, relu: bool = F
                     or tuple(res.shape) != (batch, oh, ow, w.rows) or not res.is_contiguous()):
                 raise ShapeError(f"out must be a contiguous NHWC ({batch}, {oh}, {ow}, {w.rows}) bf16 or "
                                  f"f32 tensor on {dev}")
+        res_relu = t.empty_like(res) if relu_copy else None
         if n_cols == 0:
-            return res
+            return (res, res_relu) if relu_copy else res
         lib = _native.lib()
         prep = prepared(fmt, "bf16", dev, desc)
         need = lib.rbgp4_conv2d_workspace_size(ctypes.byref(desc), ctypes.byref(cv))
         ws = workspace(dev, need, stream_handle(dev)) if need else None
         code = {t.bfloat16: _native.BF16, t.float32: _native.F32}[res.dtype]
-        rc = lib.rbgp4_conv2d(
-            ctypes.byref(desc), ctypes.byref(cv), code, fmt.values.data_ptr(), fmt.adj_o.data_ptr(),
-            fmt.adj_i.data_ptr(), prep.data_ptr() if prep is not None else None, x.data_ptr(),
-            res.data_ptr(), ws.data_ptr() if ws is not None else None, need, stream_handle(dev))
+        args = (fmt.values.data_ptr(), fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(),
+                prep.data_ptr() if prep is not None else None, x.data_ptr())
+        tail = (ws.data_ptr() if ws is not None else None, need, stream_handle(dev))
+        if residual is not None:
+            rc = lib.rbgp4_conv2d_residual(
+                ctypes.byref(desc), ctypes.byref(cv), code, *args, residual.data_ptr(), res.data_ptr(),
+                res_relu.data_ptr() if res_relu is not None else None, *tail)
+            if rc == _native.EUNSUPPORTED:
+                # no streamed plan for this shape: the conv, then the add on the device
+                y = sparse_conv2d(w, x, kernel_size, stride=stride, out=res, out_dtype=res_dt)
+                y.add_(residual)
+                return (y, t.relu(y)) if relu_copy else y
+            _native.check(rc, "rbgp4_conv2d_residual")
+            return (res, res_relu) if relu_copy else res
+        rc = lib.rbgp4_conv2d(ctypes.byref(desc), ctypes.byref(cv), code, *args, res.data_ptr(), *tail)
         if pool and rc == _native.EUNSUPPORTED:
             # no fused window layout for this shape: conv, then the NHWC pool kernel
             from .vgg import maxpool2x2

@@ -76,9 +76,19 @@ struct Options {
     int32_t halo = -1;        // K5 halo-strip conv where admissible: -1 auto, 0 off
     int32_t simt_wide = -1;   // K1 wide f32 kernel (16 rows x 4 columns per thread): -1 auto, 0 off
     int32_t merge = -1;       // K5: two tile-rows per unit when g_o is complete: -1 auto, 0 off
+    int32_t stream_ctas = 0;  // K5 grid cap: 0 auto (one CTA per SM), else at most this many CTAs
     int32_t debug = 0;        // trace / ablation bits (debug builds only)
 };
 Options &opts();
+
+// Residual epilogue of the convolution (rbgp4_conv2d_residual, the WRN block tail): set for the
+// duration of one call on the calling thread; only the streamed conv (K5) honours it, every other
+// conv path refuses a call that sets it.
+struct ConvEpilogue {
+    const void *res = nullptr;  // O = round(conv) + res  (NHWC, the output's dtype)
+    void *out2 = nullptr;       // and relu(O) here
+};
+ConvEpilogue &conv_epilogue();
 
 // Derived sizes of a four-factor chain (SURVEY §8 notation).
 struct ChainDims {

@@ -150,7 +150,8 @@ __global__ void __launch_bounds__(256) im2col_nhwc_kernel(const T *__restrict__ 
 }
 
 template <typename T>
-__global__ void nc_to_nhwc_kernel(const T *__restrict__ src, T *__restrict__ dst, int rows, int64_t n, int relu) {
+__global__ void nc_to_nhwc_kernel(const T *__restrict__ src, T *__restrict__ dst, int rows, int64_t n, int relu,
+                                  const T *__restrict__ res, T *__restrict__ dst_relu) {
     __shared__ T tile[32][33];
     const int64_t n0 = int64_t(blockIdx.x) * 32;
     const int r0 = blockIdx.y * 32;
@@ -168,7 +169,10 @@ __global__ void nc_to_nhwc_kernel(const T *__restrict__ src, T *__restrict__ dst
         if (row < rows && col < n) {
             T v = tile[threadIdx.x][r];
             if (relu && float(v) < 0.0f) v = T(0.0f);
+            // residual (the WRN block tail): v + R rounded like the unfused add; relu copy
+            if (res != nullptr) v = T(float(v) + float(res[col * rows + row]));
             dst[col * rows + row] = v;
+            if (dst_relu != nullptr) dst_relu[col * rows + row] = float(v) < 0.0f ? T(0.0f) : v;
         }
     }
 }
@@ -200,7 +204,9 @@ extern "C" int rbgp4_im2col_nhwc(int dtype, const void *x, void *cols, int batch
     return RBGP4_OK;
 }
 
-extern "C" int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, void *stream) {
+namespace {
+int nc_to_nhwc_impl(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, const void *res,
+                    void *dst_relu, void *stream) {
     using namespace rbgp4;
     RBGP4_REQUIRE(dtype == RBGP4_F32 || dtype == RBGP4_BF16, "nc_to_nhwc: F32 or BF16");
     RBGP4_REQUIRE(rows >= 0 && n >= 0, "nc_to_nhwc: bad sizes");
@@ -210,10 +216,24 @@ extern "C" int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows,
     auto s = static_cast<cudaStream_t>(stream);
     if (dtype == RBGP4_F32)
         nc_to_nhwc_kernel<float><<<grid, block, 0, s>>>(static_cast<const float *>(src), static_cast<float *>(dst),
-                                                        rows, n, relu);
+                                                        rows, n, relu, static_cast<const float *>(res),
+                                                        static_cast<float *>(dst_relu));
     else
-        nc_to_nhwc_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(static_cast<const __nv_bfloat16 *>(src),
-                                                                static_cast<__nv_bfloat16 *>(dst), rows, n, relu);
+        nc_to_nhwc_kernel<__nv_bfloat16><<<grid, block, 0, s>>>(
+            static_cast<const __nv_bfloat16 *>(src), static_cast<__nv_bfloat16 *>(dst), rows, n, relu,
+            static_cast<const __nv_bfloat16 *>(res), static_cast<__nv_bfloat16 *>(dst_relu));
     RBGP4_CHECK_LAUNCH("nc_to_nhwc launch");
     return RBGP4_OK;
+}
+}  // namespace
+
+extern "C" int rbgp4_nc_to_nhwc(int dtype, const void *src, void *dst, int rows, int64_t n, int relu, void *stream) {
+    return nc_to_nhwc_impl(dtype, src, dst, rows, n, relu, nullptr, nullptr, stream);
+}
+
+extern "C" int rbgp4_nc_to_nhwc_residual(int dtype, const void *src, const void *residual, void *dst,
+                                         void *dst_relu, int rows, int64_t n, void *stream) {
+    using namespace rbgp4;
+    RBGP4_REQUIRE(residual != nullptr, "nc_to_nhwc_residual: null residual");
+    return nc_to_nhwc_impl(dtype, src, dst, rows, n, 0, residual, dst_relu, stream);
 }

@@ -35,7 +35,7 @@ constexpr OptionSlot kOptionSlots[] = {
     {"promo", &Options::promo, -1, 256},         {"conv_wide", &Options::conv_wide, 0, 1},
     {"stream", &Options::stream, -1, 0},         {"stream_g", &Options::stream_g, 0, 8},
     {"halo", &Options::halo, -1, 0},             {"simt_wide", &Options::simt_wide, -1, 0},
-    {"merge", &Options::merge, -1, 0},
+    {"merge", &Options::merge, -1, 0},          {"stream_ctas", &Options::stream_ctas, 0, 1024},
     {"debug", &Options::debug, 0, 1 << 30},
 };
 const OptionSlot *find_option(const char *name) {
@@ -47,6 +47,8 @@ const OptionSlot *find_option(const char *name) {
 }  // namespace
 
 Options &opts() { return g_opts; }
+thread_local ConvEpilogue g_conv_epi;
+ConvEpilogue &conv_epilogue() { return g_conv_epi; }
 
 void set_error(const char *fmt, ...) {
     va_list ap;
@@ -263,6 +265,22 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
     RBGP4_REQUIRE(values && adj_o && adj_i && x && out, "null device pointer");
     return launch_conv(c, conv, out_dtype, values, adj_o, adj_i, prep, x, out, workspace,
                        workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+int rbgp4_conv2d_residual(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dtype,
+                          const void *values, const int32_t *adj_o, const int32_t *adj_i, const void *prep,
+                          const void *x, const void *residual, void *out, void *out_relu, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+    RBGP4_REQUIRE(residual != nullptr, "rbgp4_conv2d_residual: null residual");
+    RBGP4_REQUIRE(conv != nullptr && !(conv->relu & (RBGP4_CONV_RELU | RBGP4_CONV_POOL2)),
+                  "rbgp4_conv2d_residual: the residual is added before any ReLU / pool (conv->relu must be 0)");
+    ConvEpilogue &ep = conv_epilogue();
+    ep.res = residual;
+    ep.out2 = out_relu;
+    const int rc = rbgp4_conv2d(desc, conv, out_dtype, values, adj_o, adj_i, prep, x, out, workspace,
+                                workspace_bytes, stream);
+    ep = ConvEpilogue{};
+    return rc;
 }
 
 int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t n, void *stream) {

@@ -107,6 +107,9 @@ struct SParams {
     int32_t halo_atom, strips_y, strips_x, epi2;  // epi2: warps 8-11 are a second epilogue group
     int32_t nbuf;                      // TMEM accumulator buffers (2: epilogue overlapped; 1: 512 columns)
     int32_t debug, slot;
+    // conv residual epilogue (relu bits 2 / 3): O = round(acc) + res; relu(O) also into out2
+    const void *res;
+    void *out2;
 };
 
 __device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t src, int32_t x, int32_t y) {
@@ -225,6 +228,13 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         const int k2 = lane >> 1, odd = lane & 1;  // bf16: lane pair (2k, 2k+1) -> columns 2k, 2k+1
         // warps 0-3 follow acc_full[b] unit by unit; the helpers (warps 4-7) may be many phases
         // behind it, so they wait on the single-phase last_full instead
+        // residual epilogue: pull this lane's pixel row of R into L2 while the MMAs still run
+        const bool resid = CONV && (p.relu & 4) && ok;
+        if (resid) {
+            const char *ra = static_cast<const char *>(p.res) + (pix * p.ld_out + m0) * (OUT_BF16 ? 2 : 4);
+            for (int o = 0; o < nrows * (OUT_BF16 ? 2 : 4); o += 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ra + o));
+        }
         if (helper) mbar_wait_parked(last_full, 0u);
         else mbar_wait_parked(&acc_full[b], bph);
         tc_fence_after();
@@ -237,7 +247,20 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // 16 fp32 rows (row block rb, staging slot rs) of this lane's column -> bf16 pairs packed
         // across the lane pair / f32 as is; staged (last unit) or stored directly.  Kept compact
         // (a loop over row blocks, not unrolled): the epilogue runs cold in the instruction cache.
-        auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two) {
+        // residual row block i (16 output channels of this lane's pixel) into registers, one row
+        // block ahead of its use (the loads would otherwise serialise the row-block loop)
+        auto rload = [&](int i, uint4 (&r)[4]) {
+            if constexpr (CONV) {
+                if (resid) {
+                    const uint4 *src = reinterpret_cast<const uint4 *>(
+                        static_cast<const char *>(p.res) + (pix * p.ld_out + m0 + int64_t(i) * 16) * (OUT_BF16 ? 2 : 4));
+#pragma unroll
+                    for (int h = 0; h < (OUT_BF16 ? 2 : 4); ++h) r[h] = src[h];
+                }
+            }
+        };
+        auto put16 = [&](int rs, int rb, const uint32_t (&va)[16], const uint32_t (&vb)[16], bool two,
+                         const uint4 (&rr)[4]) {
             const int64_t grow0 = m0 + int64_t(rb) * 16;
             if constexpr (CONV) {
                 // NHWC: this lane's pixel c0 + lane holds output channels grow0 .. grow0 + 15
@@ -257,6 +280,28 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     if (!leader) return;
                 }
                 if (!ok) return;
+                const int64_t off = pix * p.ld_out + grow0;
+                if (p.relu & 4) {
+                    // residual (the WRN block tail): O = round(conv) + R, rounded once more on
+                    // the store -- what the unfused conv then bf16 / f32 add computes
+                    if constexpr (OUT_BF16) {
+                        const uint32_t rw[8] = {rr[0].x, rr[0].y, rr[0].z, rr[0].w, rr[1].x, rr[1].y, rr[1].z, rr[1].w};
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) {
+                            const float2 rf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&rw[h]));
+                            const float2 cf = __bfloat1622float2(__floats2bfloat162_rn(x[2 * h], x[2 * h + 1]));
+                            x[2 * h] = cf.x + rf.x;
+                            x[2 * h + 1] = cf.y + rf.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const float4 v = make_float4(__uint_as_float(rr[h].x), __uint_as_float(rr[h].y),
+                                                         __uint_as_float(rr[h].z), __uint_as_float(rr[h].w));
+                            x[4 * h] += v.x; x[4 * h + 1] += v.y; x[4 * h + 2] += v.z; x[4 * h + 3] += v.w;
+                        }
+                    }
+                }
                 if constexpr (OUT_BF16) {
                     uint32_t w[8];
 #pragma unroll
@@ -264,13 +309,31 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         const __nv_bfloat162 v2 = __floats2bfloat162_rn(x[2 * h], x[2 * h + 1]);
                         w[h] = *reinterpret_cast<const uint32_t *>(&v2);
                     }
-                    uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + pix * p.ld_out + grow0);
+                    uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + off);
                     g[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     g[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    if (p.relu & 8) {  // relu(O): max(0, .) of the rounded pair, sign-exact
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) {
+                            const __nv_bfloat162 v2 = __hmax2(*reinterpret_cast<const __nv_bfloat162 *>(&w[h]),
+                                                              __float2bfloat162_rn(0.0f));
+                            w[h] = *reinterpret_cast<const uint32_t *>(&v2);
+                        }
+                        uint4 *g2 = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(p.out2) + off);
+                        g2[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                        g2[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    }
                 } else {
-                    float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + pix * p.ld_out + grow0);
+                    float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + off);
 #pragma unroll
                     for (int h = 0; h < 4; ++h) g[h] = make_float4(x[4 * h], x[4 * h + 1], x[4 * h + 2], x[4 * h + 3]);
+                    if (p.relu & 8) {
+                        float4 *g2 = reinterpret_cast<float4 *>(static_cast<float *>(p.out2) + off);
+#pragma unroll
+                        for (int h = 0; h < 4; ++h)
+                            g2[h] = make_float4(fmaxf(x[4 * h], 0.0f), fmaxf(x[4 * h + 1], 0.0f),
+                                                fmaxf(x[4 * h + 2], 0.0f), fmaxf(x[4 * h + 3], 0.0f));
+                    }
                 }
             } else if constexpr (OUT_BF16) {
                 // all 8 shuffles first, then the stores (plain C++ stores: a volatile asm store with
@@ -357,6 +420,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // software pipeline over row blocks: row block i+1's TMEM loads are in flight while row
         // block i is converted and stored (tcgen05.wait::ld waits for all of them)
         uint32_t a0[16], b0[16], a1[16], b1[16];
+        uint4 rA[4], rB[4];  // residual row blocks (conv residual epilogue only)
         if (nparts > 2) {
             // four partials per row (g_i degree 4): both pairs of a row block, then
             // (p0 + p2) + (p1 + p3) in a fixed order -- not pipelined across row blocks
@@ -364,25 +428,27 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             for (int i = rb0; i < rb1; ++i) {
                 tload(i, a0, b0, 0);
                 tload(i, a1, b1, 1);
+                rload(i, rA);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int m = 0; m < 16; ++m) {
                     a0[m] = __float_as_uint(__uint_as_float(a0[m]) + __uint_as_float(a1[m]));
                     b0[m] = __float_as_uint(__uint_as_float(b0[m]) + __uint_as_float(b1[m]));
                 }
-                put16(i, i, a0, b0, true);
+                put16(i, i, a0, b0, true, rA);
             }
         } else {
         tload(rb0, a0, b0, 0);
+        rload(rb0, rA);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll 1
         for (int i = rb0; i < rb1; i += 2) {
-            if (i + 1 < rb1) tload(i + 1, a1, b1, 0);
-            put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG);
+            if (i + 1 < rb1) { tload(i + 1, a1, b1, 0); rload(i + 1, rB); }
+            put16(i, RG ? rec[kRgRows + i] : i, a0, b0, !RG, rA);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             if (i + 1 >= rb1) break;
-            if (i + 2 < rb1) tload(i + 2, a0, b0, 0);
-            put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG);
+            if (i + 2 < rb1) { tload(i + 2, a0, b0, 0); rload(i + 2, rA); }
+            put16(i + 1, RG ? rec[kRgRows + i + 1] : i + 1, a1, b1, !RG, rB);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         }
         }
@@ -538,6 +604,14 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                             tma_load_4d(ring + size_t(cst) * SB + size_t(a) * p.halo_atom, &imap, &full[cst], 64 * a,
                                         sx * 8 - 1, sy * 16 - 1, int32_t(bimg));
                     }
+                    if ((p.relu & 4) && lane < 16) {
+                        // residual epilogue: the strip's 16 rows of 8 pixels of R into L2, a unit
+                        // ahead of the epilogue that reads them
+                        const int64_t px = (bimg * p.img_h + sy * 16 + lane) * p.img_w + sx * 8;
+                        const uint32_t rb = uint32_t(8 * p.ld_out * (OUT_BF16 ? 2 : 4));
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                         static_cast<const char *>(p.res) + px * rb / 8), "r"(rb) : "memory");
+                    }
                     __syncwarp();
 #if RBGP4_DEBUG
                     if (trace && lane == 0 && gu < 64) g_k5_trace[0][gu] = clock64() - c_entry;
@@ -585,6 +659,17 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 if (++ip == n_ip) ip = 0;
                 const int32_t word = step_word(s);
                 if (wprod) {
+                    if constexpr (CONV) {
+                        if (s == 0 && (p.relu & 4) && elect_one()) {
+                            // residual epilogue: the unit's 128 pixel rows of R into L2 while its
+                            // main loop runs
+                            const int64_t npix = min(int64_t(kSBatch), p.n_cols - n0);
+                            const int64_t pb = p.ld_out * (OUT_BF16 ? 2 : 4);
+                            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                             static_cast<const char *>(p.res) + n0 * pb), "r"(uint32_t(npix * pb)) : "memory");
+                        }
+                        __syncwarp();
+                    }
                     if (g >= NS) mbar_wait(&empty[st], ph ^ 1u);
                     if (g >= pre) issue_w(st, tbm, word);
                 } else if (ipc == iparity) {
@@ -1314,7 +1399,8 @@ int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, cons
         p.wres_bytes = int((size_t(c.d_o) * p.w_rows * 32 + 1023) & ~size_t(1023));
     }
     p.acc_cols = rg ? g * 16 : p.w_rows;
-    const unsigned grid = unsigned(std::min<int64_t>(p.n_units, kNumSMs));
+    const int cap = opts().stream_ctas > 0 ? std::min(opts().stream_ctas, kNumSMs) : kNumSMs;
+    const unsigned grid = unsigned(std::min<int64_t>(p.n_units, cap));
     const bool multi = p.n_units > int64_t(grid);
     // two accumulator buffers when they fit (epilogue of unit i under the MMAs of unit i+1)
     p.nbuf = (multi && p.acc_cols * 2 <= 512) ? 2 : 1;
@@ -1408,7 +1494,7 @@ int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &im
     cfg.attrs = at;
     cfg.numAttrs = opts().pdl ? 1 : 0;
     if (!conv) note_kernel(pl.rg ? "K5 rows" : "K5 stream");
-    else if (pl.halo) note_kernel((pl.p.relu & 2) ? "K5 halo+pool" : "K5 halo");
+    else if (pl.halo) note_kernel((pl.p.relu & 2) ? "K5 halo+pool" : (pl.p.relu & 4) ? "K5 halo+res" : "K5 halo");
     e = cudaLaunchKernelEx(&cfg, kern, imap, wmap, omap, imaps, pl.p, out);
     if (e != cudaSuccess) {
         set_error("stream_kernel launch (%u CTAs, smem %zu): %s", pl.grid, pl.smem, cudaGetErrorString(e));
@@ -1570,6 +1656,17 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     p.relu = cv->relu;
     RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(x) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0,
                   "conv input / output must be 16-byte aligned");
+    const ConvEpilogue &ep = conv_epilogue();
+    if (ep.res != nullptr) {
+        RBGP4_REQUIRE(!(cv->relu & 3), "the residual epilogue adds before any ReLU / pool (conv->relu must be 0)");
+        RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(ep.res) % 16 == 0 &&
+                          reinterpret_cast<uintptr_t>(ep.out2) % 16 == 0,
+                      "residual / relu output must be 16-byte aligned");
+        p.res = ep.res;
+        p.out2 = ep.out2;
+        p.relu |= 4 | (ep.out2 != nullptr ? 8 : 0);
+        note_kernel("K5 conv+res");  // (launch_planned names the halo variant)
+    }
     auto enc = encode_fn();
     if (!enc) {
         set_error("cuTensorMapEncodeTiled unavailable from the driver");

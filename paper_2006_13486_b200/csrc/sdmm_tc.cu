@@ -1348,6 +1348,10 @@ int launch_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dtype, co
         set_error("rbgp4_conv2d: the fused 2x2 pool runs on the streamed kernel only (this shape: pool separately)");
         return RBGP4_EUNSUPPORTED;
     }
+    if (conv_epilogue().res != nullptr) {
+        set_error("rbgp4_conv2d_residual: the residual epilogue runs on the streamed kernel only (this shape: add separately)");
+        return RBGP4_EUNSUPPORTED;
+    }
     {
         const void *k4 = tc_prep_k4(c, pl, RBGP4_COMPUTE_BF16, prep);
         if (gather_conv_supported(c, cv, out_dtype, k4 != nullptr))

@@ -16,7 +16,10 @@ Two compute paths over the same RcubsMatrix weights:
 * ``compute="ffma"`` -- fp32 activations, every sparse layer as im2col + the FFMA SIMT kernel
   (``rbgp4mm(compute="ffma")``), the reference's fp32 arithmetic on the GPU.
 
-Element-wise glue (ReLU on the pre-activation, residual adds, the final pooling) is plain torch.
+The block tail -- the residual add and the next block's pre-activation ReLU -- is written by
+conv_b's epilogue (``sparse_conv2d(residual=..., relu_copy=True)`` on the streamed kernel, or the
+im2col path's transpose ``rbgp4_nc_to_nhwc_residual``), bit-identical to the unfused torch ops
+(``forward(fuse=False)``); the final pooling is plain torch.
 """
 
 from __future__ import annotations
@@ -28,7 +31,7 @@ import numpy as np
 from .conv import columns_to_conv_weight, conv_out_hw, sparse_conv2d
 from . import _native
 from .device import stream_handle, torch
-from .errors import GenerationExhaustedError, InvalidArgumentError
+from .errors import GenerationExhaustedError, InvalidArgumentError, ShapeError
 from .rcubs import init_random
 from .sdmm import rbgp4mm, tiling_for_chain
 from .vgg import _factor
@@ -88,14 +91,26 @@ def im2col(x_nhwc, k: int, stride: int):
     return cols, (b, oh, ow)
 
 
-def to_nhwc(y, b, oh, ow, relu: bool):
-    """The product's (C, B*H'*W') output -> NHWC (B, H', W', C), ReLU fused (`rbgp4_nc_to_nhwc`)."""
+def to_nhwc(y, b, oh, ow, relu: bool, residual=None, relu_copy: bool = False):
+    """The product's (C, B*H'*W') output -> NHWC (B, H', W', C), ReLU fused (`rbgp4_nc_to_nhwc`).
+
+    residual=R: returns y^T + R (the WRN block tail, `rbgp4_nc_to_nhwc_residual`, rounded like the
+    unfused add); with relu_copy=True also relu(y^T + R) as a second tensor.
+    """
     t = torch()
     out = t.empty((b, oh, ow, y.shape[0]), dtype=y.dtype, device=y.device)
     code = {t.float32: _native.F32, t.bfloat16: _native.BF16}[y.dtype]
-    _native.check(_native.lib().rbgp4_nc_to_nhwc(code, y.data_ptr(), out.data_ptr(), y.shape[0], y.shape[1],
-                                                 int(bool(relu)), stream_handle(y.device)), "rbgp4_nc_to_nhwc")
-    return out
+    if residual is None:
+        _native.check(_native.lib().rbgp4_nc_to_nhwc(code, y.data_ptr(), out.data_ptr(), y.shape[0], y.shape[1],
+                                                     int(bool(relu)), stream_handle(y.device)), "rbgp4_nc_to_nhwc")
+        return out
+    if relu or residual.shape != out.shape or residual.dtype != y.dtype or not residual.is_contiguous():
+        raise ShapeError("to_nhwc: residual must match the NHWC output (and relu must be off)")
+    out_relu = t.empty_like(out) if relu_copy else None
+    _native.check(_native.lib().rbgp4_nc_to_nhwc_residual(
+        code, y.data_ptr(), residual.data_ptr(), out.data_ptr(), out_relu.data_ptr() if relu_copy else None,
+        y.shape[0], y.shape[1], stream_handle(y.device)), "rbgp4_nc_to_nhwc_residual")
+    return (out, out_relu) if relu_copy else out
 
 
 @dataclass
@@ -145,30 +160,41 @@ class WRN40_4Sparse:
         return [c for blk in self.blocks for c in blk if c is not None]
 
     # ---------------------------------------------------------------- one sparse layer
-    def _conv(self, layer: _Conv, x, relu: bool, compute: str):
-        t = torch()
+    def _conv(self, layer: _Conv, x, relu: bool, compute: str, residual=None):
+        """One RBGP4 conv; with residual=R it returns (conv(x) + R, relu(conv(x) + R)): the block's
+        sum and the ReLU the next block starts with, both written by the same epilogue."""
         if compute == "bf16" and layer.c_in % 64 == 0:
-            return sparse_conv2d(layer.w, x, layer.k, stride=layer.stride, relu=relu)
+            return sparse_conv2d(layer.w, x, layer.k, stride=layer.stride, relu=relu, residual=residual,
+                                 relu_copy=residual is not None)
         # materialised im2col + the product kernel (tcgen05 bf16 or SIMT fp32 FFMA)
         cols, (b, oh, ow) = im2col(x, layer.k, layer.stride)
         params = tiling_for_chain(layer.w.chain, tn=1, rn=1, bn=1)
         y, _ = rbgp4mm(layer.w, cols, params, compute=compute)
-        return to_nhwc(y, b, oh, ow, relu)
+        return to_nhwc(y, b, oh, ow, relu, residual=residual, relu_copy=residual is not None)
 
-    def forward(self, x_nhwc, compute: str = "bf16"):
-        """x: (batch, 32, 32, 3) CUDA tensor -> (batch, num_classes) logits."""
+    def forward(self, x_nhwc, compute: str = "bf16", fuse: bool = True):
+        """x: (batch, 32, 32, 3) CUDA tensor -> (batch, num_classes) logits.
+
+        fuse=True (default): every block's residual add and the next block's ReLU are written by
+        conv_b's epilogue; fuse=False runs them as separate torch ops (bit-identical results).
+        """
         t = torch()
         if compute not in ("bf16", "ffma"):
             raise InvalidArgumentError(f"compute must be 'bf16' or 'ffma', got {compute!r}")
         act_dt = t.bfloat16 if compute == "bf16" else t.float32
         x = t.nn.functional.conv2d(x_nhwc.permute(0, 3, 1, 2).float(), self.conv1, padding=1)
         x = x.permute(0, 2, 3, 1).contiguous().to(act_dt)
+        o = t.relu(x)
         for conv_a, conv_b, short in self.blocks:
-            o = t.relu(x)
+            if not fuse:
+                o = t.relu(x)
             y = self._conv(conv_a, o, True, compute)
-            y = self._conv(conv_b, y, False, compute)
-            x = y + (self._conv(short, o, False, compute) if short is not None else x)
-        x = t.relu(x).float().mean(dim=(1, 2))
+            r = self._conv(short, o, False, compute) if short is not None else x
+            if fuse:
+                x, o = self._conv(conv_b, y, False, compute, residual=r)
+            else:
+                x = self._conv(conv_b, y, False, compute) + r
+        x = (o if fuse else t.relu(x)).float().mean(dim=(1, 2))
         return x @ self.fc.t()
 
     __call__ = forward

@@ -70,3 +70,56 @@ def test_native_im2col_and_transpose_are_exact(dtype, b, h, w, c, k, stride):
     y = torch.randn(24, bb * oh * ow).to(tdt)
     got = wrn.to_nhwc(y.cuda(), bb, oh, ow, relu=True).cpu()
     assert torch.equal(got, y.t().reshape(bb, oh, ow, 24).relu())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c,hw,k,stride,out_dt,kern", [
+    (64, 32, 3, 1, torch.bfloat16, "K5 halo+res"),    # WRN group 1 conv_b: halo strips
+    (128, 16, 3, 1, torch.bfloat16, "K5 halo+res"),   # group 2
+    (256, 8, 3, 1, torch.bfloat16, "K5 conv+res"),    # group 3: tap-shifted boxes (8x8 maps)
+    (64, 32, 3, 1, torch.float32, "K5 halo+res"),     # f32 output
+    (128, 16, 1, 1, torch.bfloat16, "K5 conv+res"),   # 1x1
+])
+def test_conv_residual_epilogue_bit_identical(c, hw, k, stride, out_dt, kern):
+    """sparse_conv2d(residual=R, relu_copy=True) == (conv + R, relu(conv + R)) computed unfused (the
+    conv, then the torch add), bit for bit: the epilogue rounds the conv, adds in f32 and rounds
+    again exactly as the separate ops do."""
+    from paper_2006_13486_b200 import _native
+    from paper_2006_13486_b200.conv import sparse_conv2d
+    from paper_2006_13486_b200.rcubs import init_random
+    w = init_random(wrn_layer_chain(c, c, 0.875, k, seed=7), 3, precision="f32")
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn(4, hw, hw, c, device="cuda", generator=g).to(torch.bfloat16)
+    r = torch.randn(4, hw // stride, hw // stride, c, device="cuda", generator=g).to(out_dt)
+    y, yr = sparse_conv2d(w, x, k, stride=stride, out_dtype=out_dt, residual=r, relu_copy=True)
+    assert _native.last_kernel() == kern
+    z = sparse_conv2d(w, x, k, stride=stride, out_dtype=out_dt)
+    want = z + r
+    torch.cuda.synchronize()
+    assert torch.equal(y, want) and torch.equal(yr, want.relu())
+    y2 = sparse_conv2d(w, x, k, stride=stride, out_dtype=out_dt, residual=r)  # no relu copy
+    assert torch.equal(y2, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("compute", ["bf16", "ffma"])
+def test_wrn_fused_block_tail_matches_unfused(compute):
+    """The fused WRN forward (residual add + next ReLU in conv_b's epilogue) is bit-identical to the
+    forward with separate torch ops."""
+    from paper_2006_13486_b200.wrn import WRN40_4Sparse
+    net = WRN40_4Sparse(sparsity=0.875, seed=4)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    x = torch.randn(8, 32, 32, 3, device="cuda", generator=g)
+    assert torch.equal(net(x, compute=compute, fuse=True), net(x, compute=compute, fuse=False))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_transpose_residual_is_exact(dtype):
+    """rbgp4_nc_to_nhwc_residual == transpose + torch add (+ relu copy), bit for bit."""
+    from paper_2006_13486_b200 import wrn
+    y = torch.randn(48, 2 * 6 * 5).to(dtype).cuda()
+    r = torch.randn(2, 6, 5, 48).to(dtype).cuda()
+    s, sr = wrn.to_nhwc(y, 2, 6, 5, relu=False, residual=r, relu_copy=True)
+    want = y.t().reshape(2, 6, 5, 48) + r
+    assert torch.equal(s, want) and torch.equal(sr, want.relu())
