@@ -625,14 +625,37 @@ def run_ours(args):
         e2e_mean_s = B.max_over_ranks(statistics.mean(dts))
         h2d = int(sum(x.numel() * x.element_size() for x in st["host_in"]))
         d2h = int(sum(o.numel() * o.element_size() for o in host_out))
+        matches = all(torch.equal(oh, o.cpu()) for oh, o in zip(host_out, st["dev_out"]))
+        # the PCIe ceiling of this leg: the same copies alone (every input H2D on one stream, every
+        # output D2H on another, no kernels), host clock, median -- e2e cannot beat it
+        scratch_in = [torch.empty_like(x, device=B.dev) for x in st["host_in"]]
+        s_in, s_out = torch.cuda.Stream(B.dev), torch.cuda.Stream(B.dev)
+        cts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(s_in):
+                for d, xh in zip(scratch_in, st["host_in"]):
+                    d.copy_(xh, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for oh, o in zip(host_out, st["dev_out"]):
+                    oh.copy_(o, non_blocking=True)
+            torch.cuda.synchronize()
+            cts.append(time.perf_counter() - t0)
+        copy_s = B.max_over_ranks(statistics.median(cts))
+        del scratch_in
         e2e = {"value": st["flops"] * world / e2e_s / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                "pcie_gbs": (h2d + d2h) / e2e_s / 1e9, "steps_timed": reps, "timing": "median of per-step host-clock times",
                "mean_ms_per_step": e2e_mean_s * 1e3,
+               "copy_ceiling": {"ms_per_step": copy_s * 1e3, "value": st["flops"] * world / copy_s / 1e12,
+                                "frac": copy_s / e2e_s,
+                                "how": "the step's H2D and D2H copies alone on two streams (no kernels), "
+                                       "host clock, median"},
                "path": ("paper_2006_13486_b200.rbgp4mm(w, pinned host bf16 tensor, params, compute=, "
                         "out=pinned host tensor, non_blocking=True) per layer: H2D on a copy-in stream, "
                         "kernel on the compute stream, D2H on a copy-out stream, one sync per step"),
-               "matches_device_path": all(torch.equal(oh, o.cpu()) for oh, o in zip(host_out, st["dev_out"]))}
+               "matches_device_path": matches}
 
     # ---- multi-GPU: one NCCL all-gather of conv10's output shards vs the single-GPU product
     multi = None
@@ -1039,6 +1062,29 @@ def run_wrn_leg(B, args):
         torch.cuda.synchronize()
         return B.max_over_ranks(a.elapsed_time(b) / reps)
 
+    def graphed(compute, fuse):
+        # the whole forward as one CUDA graph (no host launch overhead: the eager forward at this
+        # batch is partly host-bound on the per-layer Python calls)
+        try:
+            with torch.cuda.stream(B.stream):
+                net(x, compute=compute, fuse=fuse)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=B.stream):
+                net(x, compute=compute, fuse=fuse)
+            with torch.cuda.stream(B.stream):
+                g.replay()
+                reps = 5
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(B.stream)
+                for _ in range(reps):
+                    g.replay()
+                b.record(B.stream)
+            torch.cuda.synchronize()
+            return B.max_over_ranks(a.elapsed_time(b) / reps)
+        except Exception as exc:  # report, do not hide: the eager number stands
+            return f"graph capture failed: {exc}"
+
     for compute in ("bf16", "ffma"):
         ms = timed(compute, True)
         elt = 2 if compute == "bf16" else 4
@@ -1052,7 +1098,10 @@ def run_wrn_leg(B, args):
                         else ("tensor" if compute == "bf16" else "ffma"),
                         # the block tail (residual add + next ReLU) as separate torch ops instead
                         # of conv_b's epilogue
-                        "ms_per_forward_unfused_tail": timed(compute, False)}
+                        "ms_per_forward_unfused_tail": timed(compute, False),
+                        "graph": {"ms_per_forward": graphed(compute, True),
+                                  "ms_per_forward_unfused_tail": graphed(compute, False),
+                                  "how": "the forward captured once as a CUDA graph, 5 replays between events"}}
     return res
 
 

@@ -31,6 +31,7 @@ struct SimtParams {
     int32_t tnc, cthreads, wstride, istride;
     int32_t vec_in, vec_out;  // 16-byte paths legal for I loads / O stores
     int32_t nbuf;             // wide variant: TMA ring slots
+    int32_t ksplit;           // wide ffma variant: 2 = the steps halved over a (1,1,2) cluster
 };
 
 constexpr int kThreads = 256;
@@ -264,8 +265,12 @@ simt_wide_kernel(const SimtParams p, const __grid_constant__ CUtensorMap wmap, c
     uint64_t *full = reinterpret_cast<uint64_t *>(rowidx + ((p.u_i * p.d_t + 1) & ~1));
     const int32_t *orow = adj_o + tbm * p.d_o;
     const uint32_t step_bytes = uint32_t(slot) * 4u;
-    auto issue = [&](int s) {  // thread 0: both boxes of step s into slot s % nbuf
-        const int b = s % nbuf;
+    // split steps (ffma only, never EXACT): CTA z of the cluster pair runs steps [s_lo, s_hi)
+    const int half = (p.d_o + 1) / 2;
+    const int kz = (!EXACT && p.ksplit > 1) ? int(blockIdx.z) : 0;
+    const int s_lo = kz ? half : 0, s_hi = (!EXACT && p.ksplit > 1 && kz == 0) ? half : p.d_o;
+    auto issue = [&](int s) {  // thread 0: both boxes of step s into slot (s - s_lo) % nbuf
+        const int b = (s - s_lo) % nbuf;
         float *ws = ring + b * slot, *is = ws + wslot;
         uint64_t *bar = &full[b];
         mbar_expect_tx(bar, step_bytes);
@@ -278,7 +283,7 @@ simt_wide_kernel(const SimtParams p, const __grid_constant__ CUtensorMap wmap, c
     if (tid == 0) {
         for (int b = 0; b < nbuf; ++b) mbar_init(&full[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < nbuf && s < p.d_o; ++s) issue(s);
+        for (int s = s_lo; s < s_lo + nbuf && s < s_hi; ++s) issue(s);
     }
     // row table pre-multiplied by the I row stride (the wanted I row of W column j of group ui)
     for (int e = tid; e < p.u_i * p.d_t; e += int(blockDim.x)) {
@@ -303,9 +308,9 @@ simt_wide_kernel(const SimtParams p, const __grid_constant__ CUtensorMap wmap, c
     __syncthreads();  // row table and barrier init visible
     const int32_t *ridx = rowidx + ui * p.d_t;
     const int cstep = 4 * p.cthreads;  // floats between a thread's column chunks
-    for (int s = 0; s < p.d_o; ++s) {
-        const int b = s % nbuf;
-        mbar_wait(&full[b], uint32_t(s / nbuf) & 1u);
+    for (int s = s_lo; s < s_hi; ++s) {
+        const int b = (s - s_lo) % nbuf;
+        mbar_wait(&full[b], uint32_t((s - s_lo) / nbuf) & 1u);
         const float *ws = ring + b * slot;
         const float *is = ws + wslot + tc * 4;
         float c[ROWS][COLV * 4];
@@ -362,7 +367,33 @@ simt_wide_kernel(const SimtParams p, const __grid_constant__ CUtensorMap wmap, c
 #pragma unroll
             for (int e = 0; e < COLV * 4; ++e) acc[i][e] = __fadd_rn(acc[i][e], c[i][e]);
         __syncthreads();  // every thread is done with slot b
-        if (tid == 0 && s + nbuf < p.d_o) issue(s + nbuf);
+        if (tid == 0 && s + nbuf < s_hi) issue(s + nbuf);
+    }
+    if constexpr (!EXACT) {
+        if (p.ksplit > 1) {
+            // the second half's partial joins the first in CTA 0 of the pair (fixed order: first
+            // half + second half, deterministic): its rings are idle after both main loops
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            float *xch = ring + tid * (ROWS * COLV * 4);
+            if (kz == 1) {
+                uint32_t dst;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(dst) : "r"(smem_u32(xch)));
+#pragma unroll
+                for (int i = 0; i < ROWS; ++i)
+#pragma unroll
+                    for (int e = 0; e < COLV * 4; e += 4)
+                        asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                         dst + uint32_t((i * COLV * 4 + e) * 4)),
+                                     "f"(acc[i][e]), "f"(acc[i][e + 1]), "f"(acc[i][e + 2]), "f"(acc[i][e + 3])
+                                     : "memory");
+            }
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+            if (kz == 1) return;
+#pragma unroll
+            for (int i = 0; i < ROWS; ++i)
+#pragma unroll
+                for (int e = 0; e < COLV * 4; ++e) acc[i][e] = __fadd_rn(acc[i][e], xch[i * COLV * 4 + e]);
+        }
     }
 #pragma unroll
     for (int i = 0; i < ROWS; ++i) {
@@ -410,6 +441,14 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
     // column threads: 16 (64 columns per CTA at 16 rows per thread; ~220 registers, two CTAs
     // per SM), 8 when 16 would leave SMs without a CTA (conv14, N = 1024: 48 us either way
     // against 62 us on the generic kernel, tools/simt_ab.py); a warp-multiple CTA of <= 256
+    // ffma only: a grid short of the SMs halves the steps over (1,1,2) clusters (never EXACT,
+    // whose per-element order is the reference's sequential sum over the steps)
+    int ksplit = 1;
+    if (!EXACT && c.d_o >= 4 && opts().simt_ksplit != 1) {
+        const int64_t g16 = (c.n_cols + 4 * colv * 16 - 1) / (4 * colv * 16) * row_blocks;
+        const int64_t g8 = (c.n_cols + 4 * colv * 8 - 1) / (4 * colv * 8) * row_blocks;
+        if (opts().simt_ksplit == 2 || std::max(g16, g8) < kNumSMs) ksplit = 2;
+    }
     int ct = 0;
     if (opts().simt_ct == 8 || opts().simt_ct == 16 || opts().simt_ct == 32) {
         ct = opts().simt_ct;
@@ -417,7 +456,7 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
         for (int cand : {16, 8}) {
             if (cand * rthreads > kThreads || (cand * rthreads) % 32) continue;
             ct = cand;
-            if ((c.n_cols + 4 * colv * cand - 1) / (4 * colv * cand) * row_blocks >= kNumSMs) break;
+            if ((c.n_cols + 4 * colv * cand - 1) / (4 * colv * cand) * row_blocks * ksplit >= kNumSMs) break;
         }
     }
     if (ct == 0 || ct * rthreads > kThreads || (ct * rthreads) % 32) return RBGP4_EUNSUPPORTED;
@@ -433,6 +472,9 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
     int nbuf = int(std::min<size_t>(4, (110 * 1024 - fixed) / slot_bytes));
     if (nbuf < 2) nbuf = 2;
     p.nbuf = nbuf;
+    // the pair's exchange reuses CTA 0's ring: 64 floats per thread
+    if (size_t(nbuf) * slot_bytes < size_t(rthreads) * ct * 64 * 4) ksplit = 1;
+    p.ksplit = ksplit;
     const size_t smem = nbuf * slot_bytes + fixed;
     if (smem > 227 * 1024) return RBGP4_EUNSUPPORTED;
     auto enc = encode_fn();
@@ -475,9 +517,29 @@ int launch_wide(const ChainDims &c, const float *values, const int32_t *adj_o, c
             return RBGP4_ECUDA;
         }
     }
-    dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm));
-    note_kernel("K1 simt wide");
-    kern<<<grid, unsigned(rthreads * ct), smem, stream>>>(p, wmap, imap, adj_o, adj_i, out);
+    dim3 grid(unsigned((c.n_cols + p.tnc - 1) / p.tnc), unsigned(c.rows / c.tm), unsigned(ksplit));
+    note_kernel(ksplit > 1 ? "K1 simt wide split" : "K1 simt wide");
+    if (ksplit > 1) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(unsigned(rthreads * ct));
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 1;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 2;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, wmap, imap, adj_o, adj_i, out);
+        if (e != cudaSuccess) {
+            set_error("simt_wide_kernel (split pair) launch: %s", cudaGetErrorString(e));
+            return RBGP4_ECUDA;
+        }
+    } else {
+        kern<<<grid, unsigned(rthreads * ct), smem, stream>>>(p, wmap, imap, adj_o, adj_i, out);
+    }
     RBGP4_CHECK_LAUNCH("simt_wide_kernel launch");
     return RBGP4_OK;
 }

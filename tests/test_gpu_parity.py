@@ -193,3 +193,29 @@ def test_simt_wide_variants(layer, n_cols, plan_options):
     plan_options("simt_wide", -1)
     fast, _ = ks.rbgp4mm(w, x, p, compute="ffma")
     assert oracle.max_rel(fast.cpu().numpy(), f64_oracle(w, inp)) <= 1e-5
+
+
+@pytest.mark.parametrize("layer,n_cols", [((512, 512), 1024), ((64, 64), 256), ((256, 256), 1000)])
+def test_simt_wide_ffma_split_pair(layer, n_cols, plan_options):
+    """K1 wide ffma with the steps halved over a (1,1,2) cluster (grids short of the SMs): within
+    1e-5 of the f64 oracle, deterministic (two runs bit-identical), and the unsplit plan agrees to
+    fp32 reassociation; EXACT never splits."""
+    from paper_2006_13486_b200.wrn import wrn_layer_chain
+    chain = wrn_layer_chain(layer[0], layer[1], 0.875, 3)
+    w = ks.init_random(chain, 9, precision="f32")
+    inp = np.random.default_rng(n_cols + 1).uniform(-1, 1, (w.cols, n_cols)).astype(np.float32)
+    p = ks.tiling_for_chain(chain, tn=1, rn=1, bn=1)
+    x = torch.from_numpy(inp).cuda()
+    plan_options("simt_ksplit", 2)
+    a, _ = ks.rbgp4mm(w, x, p, compute="ffma")
+    assert _native.last_kernel() == "K1 simt wide split"
+    b, _ = ks.rbgp4mm(w, x, p, compute="ffma")
+    assert torch.equal(a, b)
+    assert oracle.max_rel(a.cpu().numpy(), f64_oracle(w, inp)) <= 1e-5
+    e, _ = ks.rbgp4mm(w, x, p)  # exact: never split
+    assert _native.last_kernel() == "K1 simt wide"
+    assert np.array_equal(e.cpu().numpy(), oracle.tiled(w, inp, p, threads=8))
+    plan_options("simt_ksplit", 1)
+    c, _ = ks.rbgp4mm(w, x, p, compute="ffma")
+    assert _native.last_kernel() == "K1 simt wide"
+    assert float((a - c).norm() / c.norm()) < 1e-6
