@@ -219,3 +219,32 @@ def test_simt_wide_ffma_split_pair(layer, n_cols, plan_options):
     c, _ = ks.rbgp4mm(w, x, p, compute="ffma")
     assert _native.last_kernel() == "K1 simt wide"
     assert float((a - c).norm() / c.norm()) < 1e-6
+
+
+def test_acceptance_criteria_6_and_7_on_device(golden):
+    """The reference's acceptance criteria 6 and 7 (test_acceptance.py:283-356) over the same
+    108-config corpus, with the products on the B200: exact mode within 1e-12 (f64) / 1e-5 (f32) of
+    the f64 oracle, bit-identical for workers 1, 2 and 8 (the GPU analogue of the reference's
+    worker-count invariance, sdmm.py:18-20), and WorkReport's fma / skip counts equal to their
+    closed forms."""
+    worst = {"f64": 0.0, "f32": 0.0}
+    n = 0
+    for rec in golden["corpus"]:
+        chain = corpus_chain(rec)
+        for precision, tol in (("f64", 1e-12), ("f32", 1e-5)):
+            w, inp = corpus_inputs(rec, chain, precision)
+            p = ks.tiling_for_chain(chain, tn=rec["tn"], rn=rec["rn"], bn=rec["bn"], workers=1)
+            outs = {nw: ks.rbgp4mm(w, inp, ks.with_workers(p, nw)) for nw in (1, 2, 8)}
+            ref = f64_oracle(w, inp)
+            rel = float(np.abs(outs[1][0] - ref).max() / np.abs(ref).max())
+            worst[precision] = max(worst[precision], rel)
+            assert rel <= tol, (rec, precision, rel)
+            assert np.array_equal(outs[1][0], outs[2][0]) and np.array_equal(outs[1][0], outs[8][0])
+            rep = outs[1][1]
+            assert rep.fma_count == w.nnz * inp.shape[1]
+            tiles_per_row = w.cols // p.tk
+            g_o = chain.graphs[0]
+            assert rep.steps_skipped_per_tile == tiles_per_row - len(g_o.adjacency[0])
+            assert rep.steps_skipped_per_tile == g_o.sparsity * tiles_per_row
+            n += 1
+    assert n >= 200, n
