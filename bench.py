@@ -629,15 +629,15 @@ def run_ours(args):
         # the PCIe ceiling of this leg: the same copies alone (every input H2D on one stream, every
         # output D2H on another, no kernels), host clock, median -- e2e cannot beat it
         scratch_in = [torch.empty_like(x, device=B.dev) for x in st["host_in"]]
-        s_in, s_out = torch.cuda.Stream(B.dev), torch.cuda.Stream(B.dev)
+        cp_in, cp_out = torch.cuda.Stream(B.dev), torch.cuda.Stream(B.dev)
         cts = []
         for _ in range(reps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            with torch.cuda.stream(s_in):
+            with torch.cuda.stream(cp_in):
                 for d, xh in zip(scratch_in, st["host_in"]):
                     d.copy_(xh, non_blocking=True)
-            with torch.cuda.stream(s_out):
+            with torch.cuda.stream(cp_out):
                 for oh, o in zip(host_out, st["dev_out"]):
                     oh.copy_(o, non_blocking=True)
             torch.cuda.synchronize()
@@ -865,6 +865,39 @@ def run_vgg_leg(B, args):
            "sparse_tflops": net.sparse_flops_per_image * batch * B.world / (ms * 1e-3) / 1e12,
            "model": "VGG19-CIFAR-100, RBGP4 convs 2-16 (bf16, NHWC), dense conv1 + classifier",
            "data": "synthetic images, random-init weights"}
+    # per layer (eager, events around each call, as the forward runs them: pools fused into the
+    # conv that precedes them); the kernel each RBGP4 conv took
+    from paper_2006_13486_b200.vgg import _dense_conv_relu, maxpool2x2
+    from paper_2006_13486_b200 import _native
+    per = []
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(B.stream)
+        return e
+
+    for _pass in range(2):  # the first pass warms the eager path (cuDNN plans, allocator); keep the second
+        evs = []
+        with torch.cuda.stream(B.stream):
+            e0 = ev()
+            h = _dense_conv_relu(x.permute(0, 3, 1, 2), net.conv1).permute(0, 2, 3, 1).contiguous()
+            evs.append(("conv1 (dense, cuDNN)", e0, ev(), None))
+            i = 0
+            while i < len(net.layers):
+                kind, layer = net.layers[i]
+                e0 = ev()
+                if kind == "conv" and i + 1 < len(net.layers) and net.layers[i + 1][0] == "pool":
+                    h = layer(h, pool=True)
+                    name, i = f"conv{i}+pool", i + 2
+                else:
+                    h = maxpool2x2(h) if kind == "pool" else layer(h)
+                    name, i = f"{kind}{i}", i + 1
+                evs.append((f"{name} -> {tuple(h.shape[1:])}", e0, ev(),
+                            _native.last_kernel() if kind == "conv" else None))
+    torch.cuda.synchronize()
+    for name, e0, e1, kern in evs:
+        per.append({"layer": name, "us": round(e0.elapsed_time(e1) * 1e3, 1), **({"kernel": kern} if kern else {})})
+    res["layers"] = per
+    del h
     if B.world > 1:
         logits = y.float().contiguous()
         parts = [torch.empty_like(logits) for _ in range(B.world)]

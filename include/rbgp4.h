@@ -145,7 +145,8 @@ int rbgp4_conv2d(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, int out_dt
  * shaped and typed like O, rounded as the unfused conv-then-add rounds (bf16: round the conv,
  * add in f32, round again), so the result is bit-identical to rbgp4_conv2d followed by the
  * add; with out_relu != NULL also relu(O) into out_relu (the next block's input).  conv->relu
- * must be 0.  Streamed kernel (K5) only: other shapes return RBGP4_EUNSUPPORTED (add separately).
+ * must be 0.  Streamed kernel (K5), bf16 output only: other shapes / an f32 output return
+ * RBGP4_EUNSUPPORTED (add separately).
  * Replaces nothing in the reference (its bench lowers convs to rbgp4mm over im2col); it serves
  * the WRN-40-4 model of SURVEY §8(f).
  */

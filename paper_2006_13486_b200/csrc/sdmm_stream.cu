@@ -124,7 +124,7 @@ __device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t 
 // taps) stays resident -- the taps no longer re-read the input from L2 (9x -> 1.4x);
 // BM: element-block rows of the chain (16 / 8 / 4) -- the granularity of the epilogue's
 // TMEM partial loads
-template <bool OUT_BF16, bool RG, bool CONV, int BM, bool HALO = false>
+template <bool OUT_BF16, bool RG, bool CONV, int BM, bool HALO = false, bool RES = false>
 __global__ void __launch_bounds__(kSThreads, 1)
 stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ CUtensorMap wmap,
               const __grid_constant__ CUtensorMap omap, const __grid_constant__ IMaps imaps, const SParams p,
@@ -229,7 +229,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // warps 0-3 follow acc_full[b] unit by unit; the helpers (warps 4-7) may be many phases
         // behind it, so they wait on the single-phase last_full instead
         // residual epilogue: pull this lane's pixel row of R into L2 while the MMAs still run
-        const bool resid = CONV && (p.relu & 4) && ok;
+        const bool resid = CONV && RES && ok;
         if (resid) {
             const char *ra = static_cast<const char *>(p.res) + (pix * p.ld_out + m0) * (OUT_BF16 ? 2 : 4);
             for (int o = 0; o < nrows * (OUT_BF16 ? 2 : 4); o += 128)
@@ -250,7 +250,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // residual row block i (16 output channels of this lane's pixel) into registers, one row
         // block ahead of its use (the loads would otherwise serialise the row-block loop)
         auto rload = [&](int i, uint4 (&r)[4]) {
-            if constexpr (CONV) {
+            if constexpr (CONV && RES) {
                 if (resid) {
                     const uint4 *src = reinterpret_cast<const uint4 *>(
                         static_cast<const char *>(p.res) + (pix * p.ld_out + m0 + int64_t(i) * 16) * (OUT_BF16 ? 2 : 4));
@@ -281,7 +281,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 }
                 if (!ok) return;
                 const int64_t off = pix * p.ld_out + grow0;
-                if (p.relu & 4) {
+                if constexpr (RES) {
                     // residual (the WRN block tail): O = round(conv) + R, rounded once more on
                     // the store -- what the unfused conv then bf16 / f32 add computes
                     if constexpr (OUT_BF16) {
@@ -312,7 +312,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + off);
                     g[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     g[1] = make_uint4(w[4], w[5], w[6], w[7]);
-                    if (p.relu & 8) {  // relu(O): max(0, .) of the rounded pair, sign-exact
+                    if (RES && (p.relu & 8)) {  // relu(O): max(0, .) of the rounded pair, sign-exact
 #pragma unroll
                         for (int h = 0; h < 8; ++h) {
                             const __nv_bfloat162 v2 = __hmax2(*reinterpret_cast<const __nv_bfloat162 *>(&w[h]),
@@ -327,7 +327,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     float4 *g = reinterpret_cast<float4 *>(static_cast<float *>(out) + off);
 #pragma unroll
                     for (int h = 0; h < 4; ++h) g[h] = make_float4(x[4 * h], x[4 * h + 1], x[4 * h + 2], x[4 * h + 3]);
-                    if (p.relu & 8) {
+                    if (RES && (p.relu & 8)) {
                         float4 *g2 = reinterpret_cast<float4 *>(static_cast<float *>(p.out2) + off);
 #pragma unroll
                         for (int h = 0; h < 4; ++h)
@@ -604,7 +604,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                             tma_load_4d(ring + size_t(cst) * SB + size_t(a) * p.halo_atom, &imap, &full[cst], 64 * a,
                                         sx * 8 - 1, sy * 16 - 1, int32_t(bimg));
                     }
-                    if ((p.relu & 4) && lane < 16) {
+                    if (RES && lane < 16) {
                         // residual epilogue: the strip's 16 rows of 8 pixels of R into L2, a unit
                         // ahead of the epilogue that reads them
                         const int64_t px = (bimg * p.img_h + sy * 16 + lane) * p.img_w + sx * 8;
@@ -660,7 +660,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 const int32_t word = step_word(s);
                 if (wprod) {
                     if constexpr (CONV) {
-                        if (s == 0 && (p.relu & 4) && elect_one()) {
+                        if (RES && s == 0 && elect_one()) {
                             // residual epilogue: the unit's 128 pixel rows of R into L2 while its
                             // main loop runs
                             const int64_t npix = min(int64_t(kSBatch), p.n_cols - n0);
@@ -1444,6 +1444,16 @@ StreamKernel pick_kernel(bool rg, bool conv, int bm, bool halo) {
                                                                     : stream_kernel<OB, false, false, 4>;
 }
 
+// the residual epilogue (bf16 conv only): its own instantiations, so the other convs keep their
+// register allocation (the runtime-flag version spilled and cost VGG19 19.3 -> 25.3 ms)
+StreamKernel pick_res_kernel(int bm, bool halo) {
+    if (halo) return bm == 16 ? stream_kernel<true, false, true, 16, true, true>
+                              : bm == 8 ? stream_kernel<true, false, true, 8, true, true>
+                                        : stream_kernel<true, false, true, 4, true, true>;
+    return bm == 16 ? stream_kernel<true, false, true, 16, false, true>
+                    : bm == 8 ? stream_kernel<true, false, true, 8, false, true> : stream_kernel<true, false, true, 4, false, true>;
+}
+
 // the whole-tile W map: slice-relayout rows of 16 k (32 B), box = one step's nsl x mma_n rows
 int encode_slice_w(CUtensorMap *wmap, const ChainDims &c, const SParams &p, const void *vals) {
     auto enc = encode_fn();
@@ -1476,7 +1486,8 @@ void whole_tile_views(const ChainDims &c, const void *k4, const void *k5, const 
 
 int launch_planned(SPlan &pl, int oelt, bool conv, int bm, const CUtensorMap &imap, const CUtensorMap &wmap,
                    const CUtensorMap &omap, const IMaps &imaps, void *out, cudaStream_t stream) {
-    StreamKernel kern = oelt == 2 ? pick_kernel<true>(pl.rg, conv, bm, pl.halo) : pick_kernel<false>(pl.rg, conv, bm, pl.halo);
+    StreamKernel kern = (conv && (pl.p.relu & 4)) ? pick_res_kernel(bm, pl.halo)
+                      : oelt == 2 ? pick_kernel<true>(pl.rg, conv, bm, pl.halo) : pick_kernel<false>(pl.rg, conv, bm, pl.halo);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem));
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(K5): %s", cudaGetErrorString(e));
@@ -1659,6 +1670,10 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     const ConvEpilogue &ep = conv_epilogue();
     if (ep.res != nullptr) {
         RBGP4_REQUIRE(!(cv->relu & 3), "the residual epilogue adds before any ReLU / pool (conv->relu must be 0)");
+        if (out_dtype != RBGP4_BF16) {
+            set_error("rbgp4_conv2d_residual: the residual epilogue writes bf16 (this output: add separately)");
+            return RBGP4_EUNSUPPORTED;
+        }
         RBGP4_REQUIRE(reinterpret_cast<uintptr_t>(ep.res) % 16 == 0 &&
                           reinterpret_cast<uintptr_t>(ep.out2) % 16 == 0,
                       "residual / relu output must be 16-byte aligned");
