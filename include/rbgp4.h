@@ -155,6 +155,13 @@ int rbgp4_conv2d_residual(const rbgp4_desc *desc, const rbgp4_conv_desc *conv, i
                           const void *x, const void *residual, void *out, void *out_relu, void *workspace,
                           size_t workspace_bytes, void *stream);
 
+/* The dense first convolution of the VGG19 model (kept dense as in PAPER.md:195-196): 3x3 'same',
+ * stride 1, 3 input channels -> c_out = 64, ReLU fused, NHWC bf16 in (batch, height, width, 3) and
+ * out (batch, height, width, 64), fp32 accumulation on tcgen05.  w: bf16 [64][32], column
+ * k = (i*3 + j)*3 + c for weight[c_out][c][i][j], columns 27..31 zero; 16-byte aligned w / out. */
+int rbgp4_dense_conv3x3_c3(const void *x, const void *w, void *out, int batch, int height, int width,
+                           int c_out, void *stream);
+
 /* 2x2 / stride-2 max pooling of a bf16 NHWC tensor (the VGG stage boundary);
  * H, W even, channels % 8 == 0, 16-byte aligned. */
 int rbgp4_maxpool2x2_nhwc(const void *x, void *y, int batch, int height, int width, int channels,

@@ -26,7 +26,7 @@ EXPORTED = (
     "rbgp4_csr_sdmm", "rbgp4_cast", "rbgp4_last_error", "rbgp4_abi_version", "rbgp4_launch_count",
     "rbgp4_reset_launch_count", "rbgp4_last_kernel", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
     "rbgp4_reset_options", "rbgp4_debug_build", "rbgp4_im2col_nhwc", "rbgp4_nc_to_nhwc",
-    "rbgp4_conv2d_residual", "rbgp4_nc_to_nhwc_residual",
+    "rbgp4_conv2d_residual", "rbgp4_nc_to_nhwc_residual", "rbgp4_dense_conv3x3_c3",
 )
 
 
@@ -106,6 +106,8 @@ def lib():
     h.rbgp4_conv2d_residual.restype = i32
     h.rbgp4_nc_to_nhwc_residual.argtypes = [i32, vp, vp, vp, vp, i32, ctypes.c_int64, vp]
     h.rbgp4_nc_to_nhwc_residual.restype = i32
+    h.rbgp4_dense_conv3x3_c3.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    h.rbgp4_dense_conv3x3_c3.restype = i32
     h.rbgp4_workspace_size.argtypes = [ctypes.POINTER(Desc), i32, i32]
     h.rbgp4_workspace_size.restype = sz
     h.rbgp4_sdmm_supported.argtypes = [ctypes.POINTER(Desc), i32, i32, i32]

@@ -77,6 +77,33 @@ def _dense_conv_relu(x, w):
     return t.nn.functional.conv2d(x, w, padding=1).relu_()
 
 
+def dense_conv1_relu(x_nhwc, w_cols):
+    """The dense first conv (3 -> 64, 3x3 'same') with its ReLU on the library's own tcgen05 kernel
+    (`rbgp4_dense_conv3x3_c3`, K8): NHWC bf16 in and out, w_cols the bf16 (64, 32) weight matrix
+    from `conv1_columns`.  HBM-write-bound (4.3 GB out at batch 32768); cuDNN's fused conv + ReLU
+    took 2.6-3.6 ms there."""
+    t = torch()
+    if not (x_nhwc.is_cuda and x_nhwc.dtype == t.bfloat16 and x_nhwc.dim() == 4 and x_nhwc.shape[3] == 3):
+        raise InvalidArgumentError("dense_conv1_relu: x must be a CUDA bf16 NHWC tensor with 3 channels")
+    x_nhwc = x_nhwc.contiguous()
+    b, h, w, _ = x_nhwc.shape
+    out = t.empty((b, h, w, w_cols.shape[0]), dtype=t.bfloat16, device=x_nhwc.device)
+    _native.check(_native.lib().rbgp4_dense_conv3x3_c3(x_nhwc.data_ptr(), w_cols.data_ptr(), out.data_ptr(), b, h, w,
+                                                       w_cols.shape[0], stream_handle(x_nhwc.device)),
+                  "rbgp4_dense_conv3x3_c3")
+    return out
+
+
+def conv1_columns(weight):
+    """(64, 3, 3, 3) conv weight -> the bf16 (64, 32) matrix K8 reads: column (i*3 + j)*3 + c, zeros
+    past 27."""
+    t = torch()
+    c_out = weight.shape[0]
+    cols = t.zeros((c_out, 32), dtype=t.bfloat16, device=weight.device)
+    cols[:, :27] = weight.permute(0, 2, 3, 1).reshape(c_out, 27).to(t.bfloat16)
+    return cols.contiguous()
+
+
 def maxpool2x2(x):
     t = torch()
     b, h, w, c = x.shape
@@ -101,6 +128,7 @@ class VGG19Sparse:
         # dense first conv (3 -> 64), channels-last bf16
         self.conv1 = (t.randn(64, 3, 3, 3, generator=gen) * (2.0 / 27) ** 0.5).to(
             self.device, t.bfloat16).to(memory_format=t.channels_last)
+        self.conv1_cols = conv1_columns(self.conv1)
         self.layers = []   # ("conv", SparseConv2d) | ("pool", None)
         self.chains = []
         c_in, idx = 64, 0
@@ -115,12 +143,17 @@ class VGG19Sparse:
             c_in, idx = v, idx + 1
         self.fc = (t.randn(self.num_classes, 512, generator=gen) / 512 ** 0.5).to(self.device, t.bfloat16)
 
-    def forward(self, x_nhwc):
-        """x: (batch, 32, 32, 3) bf16 CUDA tensor -> (batch, num_classes) logits."""
+    def forward(self, x_nhwc, dense: str = "native"):
+        """x: (batch, 32, 32, 3) bf16 CUDA tensor -> (batch, num_classes) logits.
+
+        dense: the first (dense) conv on the library's K8 kernel ("native") or cuDNN ("cudnn")."""
         t = torch()
-        x = x_nhwc.permute(0, 3, 1, 2)  # NCHW view of channels-last memory
-        x = _dense_conv_relu(x, self.conv1)
-        x = x.permute(0, 2, 3, 1).contiguous()  # NHWC (a view: cuDNN wrote channels-last)
+        if dense == "native":
+            x = dense_conv1_relu(x_nhwc, self.conv1_cols)
+        else:
+            x = x_nhwc.permute(0, 3, 1, 2)  # NCHW view of channels-last memory
+            x = _dense_conv_relu(x, self.conv1)
+            x = x.permute(0, 2, 3, 1).contiguous()  # NHWC (a view: cuDNN wrote channels-last)
         i = 0
         while i < len(self.layers):
             kind, layer = self.layers[i]

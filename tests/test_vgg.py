@@ -51,3 +51,34 @@ def test_vgg19_forward_matches_dense(sparsity):
     rel = float((y - ref).norm() / ref.norm())
     assert y.shape == (6, 100)
     assert rel <= 1e-2, rel  # measured 4.0e-3 .. 6.9e-3 over seeds 3-5 at 87.5 / 50 %
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("b,h,w", [(3, 32, 32), (2, 7, 5), (1, 1, 1), (5, 16, 24)])
+def test_dense_conv1_native_matches_torch(b, h, w):
+    """K8 (the dense 3 -> 64 first conv on tcgen05, ReLU fused) against torch's fp32 conv of the same
+    bf16 operands: within the bf16 output rounding; ragged pixel counts (tiles of 128 pixels) and
+    borders (zero padding) included."""
+    import torch
+    from paper_2006_13486_b200 import _native
+    from paper_2006_13486_b200.vgg import conv1_columns, dense_conv1_relu
+    g = torch.Generator(device="cuda").manual_seed(b * 100 + h)
+    wt = torch.randn(64, 3, 3, 3, device="cuda", generator=g).to(torch.bfloat16)
+    x = torch.randn(b, h, w, 3, device="cuda", generator=g).to(torch.bfloat16)
+    y = dense_conv1_relu(x, conv1_columns(wt))
+    assert _native.last_kernel() == "K8 dense c3"
+    ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), wt.float(), padding=1).relu().permute(0, 2, 3, 1)
+    assert y.shape == ref.shape
+    err = (y.float() - ref).abs()
+    assert float(err.max()) <= float(ref.abs().max()) * 2 ** -7, float(err.max())
+    assert float(err.norm() / ref.norm()) < 5e-3
+
+
+@pytest.mark.gpu
+def test_vgg19_native_dense_conv1_matches_cudnn():
+    import torch
+    from paper_2006_13486_b200.vgg import VGG19Sparse
+    net = VGG19Sparse(sparsity=0.875, seed=4)
+    x = torch.randn(4, 32, 32, 3, device="cuda").to(torch.bfloat16)
+    a, b = net(x).float(), net(x, dense="cudnn").float()
+    assert float((a - b).norm() / b.norm()) < 1e-2
