@@ -280,6 +280,9 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     if (!leader) return;
                 }
                 if (!ok) return;
+#if RBGP4_DEBUG
+                if (p.debug & 4096) return;  // ablation: no conv output stores (tools/conv_store_ab.py)
+#endif
                 const int64_t off = pix * p.ld_out + grow0;
                 if constexpr (RES) {
                     // residual (the WRN block tail): O = round(conv) + R, rounded once more on
