@@ -234,7 +234,7 @@ int rbgp4_cast(int src_dtype, int dst_dtype, const void *src, void *dst, int64_t
  * Thread-local: a value set on one host thread affects only launches planned on that thread.
  * Names: relayout, dense, persistent, msplit, ksplit, stages, multicast, sym, pdl, simt_ct,
  * tc_tn, tc_na, tc_nb, tc_nw, wswz, ostore, sched, i3d, promo, conv_wide, stream, stream_g,
- * halo, simt_wide, merge, stream_ctas, simt_ksplit, debug (include the kernels' trace/ablation hooks only in a debug
+ * halo, simt_wide, merge, stream_ctas, simt_ksplit, conv_ostage, debug (include the kernels' trace/ablation hooks only in a debug
  * build, see rbgp4_debug_build).  Unknown names and out-of-range values return RBGP4_EINVAL.
  * None of them changes results beyond the fp32 summation order of the tensor-core modes.
  * `relayout` and `merge` change the layout of a prepared buffer: a buffer must be used under the

@@ -76,6 +76,7 @@ struct Options {
     int32_t halo = -1;        // K5 halo-strip conv where admissible: -1 auto, 0 off
     int32_t simt_wide = -1;   // K1 wide f32 kernel (16 rows x 4 columns per thread): -1 auto, 0 off
     int32_t merge = -1;       // K5: two tile-rows per unit when g_o is complete: -1 auto, 0 off
+    int32_t conv_ostage = 1;  // K5 conv: staged TMA-store epilogue (bf16, no pool / residual): 1 on, 0 off
     int32_t simt_ksplit = 0;  // K1 wide ffma step halving over a cluster pair: 0 auto, 1 off, 2 on
     int32_t stream_ctas = 0;  // K5 grid cap: 0 auto (one CTA per SM), else at most this many CTAs
     int32_t debug = 0;        // trace / ablation bits (debug builds only)

@@ -36,7 +36,7 @@ constexpr OptionSlot kOptionSlots[] = {
     {"stream", &Options::stream, -1, 0},         {"stream_g", &Options::stream_g, 0, 8},
     {"halo", &Options::halo, -1, 0},             {"simt_wide", &Options::simt_wide, -1, 0},
     {"merge", &Options::merge, -1, 0},          {"stream_ctas", &Options::stream_ctas, 0, 1024},
-    {"simt_ksplit", &Options::simt_ksplit, 0, 2},
+    {"simt_ksplit", &Options::simt_ksplit, 0, 2},    {"conv_ostage", &Options::conv_ostage, 0, 1},
     {"debug", &Options::debug, 0, 1 << 30},
 };
 const OptionSlot *find_option(const char *name) {

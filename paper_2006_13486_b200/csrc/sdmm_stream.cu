@@ -107,11 +107,18 @@ struct SParams {
     int32_t halo_atom, strips_y, strips_x, epi2;  // epi2: warps 8-11 are a second epilogue group
     int32_t nbuf;                      // TMEM accumulator buffers (2: epilogue overlapped; 1: 512 columns)
     int32_t debug, slot;
+    // conv (bf16, no pool / residual): each epilogue warp stages 64 channels x its 32 pixels
+    // (4 KB, 128B swizzle) at ostage_off + 4 KB * slot and writes them with one TMA store
+    int32_t ostage, ostage_off;
     // conv residual epilogue (relu bits 2 / 3): O = round(acc) + res; relu(O) also into out2
     const void *res;
     void *out2;
 };
 
+__device__ __forceinline__ void tma_store_3d_g(const CUtensorMap *map, uint32_t src, int32_t x, int32_t y, int32_t z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(src) : "memory");
+}
 __device__ __forceinline__ void tma_store_2d_g(const CUtensorMap *map, uint32_t src, int32_t x, int32_t y) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                      reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(src) : "memory");
@@ -198,6 +205,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
         // conv: this lane's output pixel (NHWC row); halo strips: (r, c) = (m / 8, m % 8) of the
         // unit's 16 x 8 strip, m = TMEM lane
         int64_t pix = c0 + lane;
+        int32_t st_x = int32_t(c0), st_y = 0;  // staged conv store: the warp's box coordinates
         // fused 2x2 max pool (conv flag bit 1): window partners are lanes ^1 (x) and ^ystr (y);
         // the (even x, even y) lane stores the pooled pixel `pix` of the (H/2, W/2) map
         const bool pool = CONV && (p.relu & 2);
@@ -209,6 +217,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int sy = int((u - bimg * per_img) / p.strips_x), sx = int(u % p.strips_x);
             const int m = q * 32 + lane;
             pix = (bimg * p.img_h + sy * 16 + (m >> 3)) * p.img_w + sx * 8 + (m & 7);
+            st_x = sx * 8;  // the warp's 4 strip rows x 8 pixels
+            st_y = int32_t(bimg * p.img_h + sy * 16 + q * 4);
             if (pool) {
                 ystr = 8;
                 leader = !(m & 1) && !(m & 8);
@@ -223,6 +233,10 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             pix = (bimg * (p.img_h / 2) + y / 2) * (p.img_w / 2) + x / 2;
         }
         const int nrows = RG ? p.g * 16 : p.tm;
+        // staged conv stores: whole 64-channel groups only (a range of 4k row blocks from 4k)
+        const bool ost = CONV && !RES && OUT_BF16 && !pool && p.ostage && !helper && (rb0 % 4) == 0 &&
+                         ((rb1 - rb0) % 4) == 0;
+        const uint32_t ostg = smem_u32(base) + uint32_t(p.ostage_off) + uint32_t(((warp & 3) + (warp >= 8 ? 4 : 0)) * 4096);
         unsigned char *wstage_p = ring + q * nrows * kRowBytes;  // [row][kRowBytes] for columns c0..
         const uint32_t wstage = smem_u32(wstage_p);
         const int k2 = lane >> 1, odd = lane & 1;  // bf16: lane pair (2k, 2k+1) -> columns 2k, 2k+1
@@ -311,6 +325,29 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                     for (int h = 0; h < 8; ++h) {
                         const __nv_bfloat162 v2 = __floats2bfloat162_rn(x[2 * h], x[2 * h + 1]);
                         w[h] = *reinterpret_cast<const uint32_t *>(&v2);
+                    }
+                    if (ost) {
+                        // row block rb = channels 16 (rb % 4) .. of the warp's 64-channel group:
+                        // chunks 2 (rb % 4), +1 of this lane's 128-byte row, 128B swizzle
+                        const int g4 = rb & 3;
+                        if (g4 == 0) {  // the previous group's TMA store has read the staging
+                            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                            __syncwarp();
+                        }
+                        const uint32_t row = ostg + uint32_t(lane) * 128u;
+                        sts128(row + ((uint32_t(2 * g4) ^ uint32_t(lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+                        sts128(row + ((uint32_t(2 * g4 + 1) ^ uint32_t(lane & 7)) << 4), w[4], w[5], w[6], w[7]);
+                        if (g4 == 3) {
+                            fence_async_smem();
+                            __syncwarp();
+                            if (lane == 0) {
+                                const int32_t ch0 = int32_t(grow0 - 48);
+                                if constexpr (HALO) tma_store_3d_g(&omap, ostg, ch0, st_x, st_y);
+                                else tma_store_2d_g(&omap, ostg, ch0, st_x);
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                        }
+                        return;
                     }
                     uint4 *g = reinterpret_cast<uint4 *>(static_cast<__nv_bfloat16 *>(out) + off);
                     g[0] = make_uint4(w[0], w[1], w[2], w[3]);
@@ -928,6 +965,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             const int split = (last && nrb >= 2) ? nrb / 2 : nrb;
             drain(u, it, 0, split, s_cols, RG ? s_rg + int(u % p.n_rg) * kRgWords : nullptr, false);
         }
+        // staged conv stores: all of this warp's TMA stores done before the CTA retires
+        if (CONV && p.ostage && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     if (!kEpiB && warp >= 4 && warp < 8) {
         // warps 4-7 after their roles: the second half of the last unit's row blocks (tables
@@ -1416,8 +1455,14 @@ int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, cons
     const size_t staging = conv ? 0 : size_t(rg ? g * 16 : c.tm) * kSBatch * oelt;
     const size_t statics = (rg ? size_t(kMaxRg) * kRgWords * 4 : 512) + 64;
     const size_t fixed = 1024 + 1024;  // alignment slack + barrier block
-    if (fixed + statics + p.wres_bytes + 2 * size_t(p.stage_bytes) > kSSmemCap) return 0;
-    int ns = int(std::min<size_t>(16, (kSSmemCap - fixed - statics - p.wres_bytes) / p.stage_bytes));
+    // conv (bf16, no pool / residual): 4 KB of output staging per epilogue warp (TMA stores).
+    // Not for halo strips: their stages are 23-46 KB and the staging would cost one (128 ch @16x16
+    // 1.37 -> 1.46 ms), while the tap-shifted convs gain 11-17 % (tools/conv_store_ab.py)
+    const bool ost = conv && !halo && opts().conv_ostage != 0 && out_dtype == RBGP4_BF16 && cv != nullptr &&
+                     !(cv->relu & 2) && conv_epilogue().res == nullptr && c.tm % 64 == 0;
+    const size_t ost_bytes = ost ? size_t(p.epi2 ? 8 : 4) * 4096 : 0;
+    if (fixed + statics + p.wres_bytes + ost_bytes + 2 * size_t(p.stage_bytes) > kSSmemCap) return 0;
+    int ns = int(std::min<size_t>(16, (kSSmemCap - fixed - statics - p.wres_bytes - ost_bytes) / p.stage_bytes));
     // row groups: the kernel re-cuts the ring into stages of the longest range actually used
     p.ring_bytes = int(kSSmemCap - fixed - statics - p.wres_bytes) & ~1023;
     if (opts().stages > 0) ns = std::max(2, std::min(ns, int(opts().stages)));
@@ -1427,6 +1472,13 @@ int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, cons
     p.slot = -1;
     pl->p = p;
     pl->smem = (rg ? fixed + size_t(p.ring_bytes) : fixed + size_t(ns) * p.stage_bytes) + p.wres_bytes;
+    if (ost) {  // after the ring (1024-aligned: stages and the W block are multiples of 1 KB)
+        p.ostage = 1;
+        p.ostage_off = int(1024 + p.wres_bytes + size_t(ns) * p.stage_bytes);
+        pl->p.ostage = 1;
+        pl->p.ostage_off = p.ostage_off;
+        pl->smem += ost_bytes;
+    }
     pl->grid = grid;
     pl->rg = rg;
     pl->halo = halo;
@@ -1720,6 +1772,31 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
         }
     }
     if (int rc = encode_slice_w(&wmap, pl.eff, p, rvals)) return rc;
+    if (p.ostage) {
+        // the output for the staged epilogue: NHWC as (channels, pixels) -- box 64 x 32 -- or, for
+        // halo strips, (channels, x, batch * rows) -- box 64 x 8 x 4; 128B swizzle like the staging
+        const cuuint64_t cb = cuuint64_t(c.rows) * 2;
+        cuuint64_t dims[3] = {cuuint64_t(c.rows), cuuint64_t(c.n_cols), 1};
+        cuuint64_t strides[2] = {cb, 0};
+        cuuint32_t box[3] = {64, 32, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        cuuint32_t rank = 2;
+        if (pl.halo) {
+            dims[1] = cuuint64_t(ow);
+            dims[2] = cuuint64_t(cv->batch) * oh;
+            strides[1] = cuuint64_t(ow) * cb;
+            box[1] = 8;
+            box[2] = 4;
+            rank = 3;
+        }
+        CUresult r = enc(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, out, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K5 conv output) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
     return launch_planned(pl, oelt, true, c.bm, imap, wmap, omap, imaps, out, stream);
 }
 

@@ -1,5 +1,6 @@
 """What the K5 conv epilogue's per-lane NHWC stores cost: VGG19 / WRN conv layers on the debug
-library with and without them (option debug bit 4096 drops the conv output stores; ablation only).
+library with and without them (option debug bit 4096 drops the conv output stores; ablation only),
+and the staged TMA-store epilogue (default) against per-lane stores (option conv_ostage=0).
 
     python tools/conv_store_ab.py [batch]
 """
@@ -39,6 +40,9 @@ for c_out, c_in, hw, pool in ((64, 64, 32, True), (128, 128, 16, False), (256, 2
     kern = _native.last_kernel()
     with _native.options(debug=4096):
         nost = timed(lambda: sparse_conv2d(w, x, 3, relu=True, pool=pool))
+    with _native.options(conv_ostage=0):
+        direct = timed(lambda: sparse_conv2d(w, x, 3, relu=True, pool=pool))
     out_mb = batch * (hw // (2 if pool else 1)) ** 2 * c_out * 2 / 1e6
     print(f"{c_out}x{c_in} @{hw}x{hw}{' +pool' if pool else ''} [{kern}]: {base:.3f} ms with stores, "
-          f"{nost:.3f} ms without ({out_mb:.0f} MB out)", flush=True)
+          f"{nost:.3f} ms without, {direct:.3f} ms with per-lane stores (conv_ostage=0) ({out_mb:.0f} MB out)",
+          flush=True)
