@@ -223,6 +223,8 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                 ystr = 8;
                 leader = !(m & 1) && !(m & 8);
                 pix = (bimg * (p.img_h / 2) + (sy * 16 + (m >> 3)) / 2) * (p.img_w / 2) + (sx * 8 + (m & 7)) / 2;
+                st_x = sx * 4;  // pooled: the warp's 2 rows x 4 pixels
+                st_y = int32_t((bimg * p.img_h + sy * 16 + q * 4) / 2);
             }
         } else if (pool) {
             const int64_t hw = int64_t(p.img_h) * p.img_w;
@@ -231,12 +233,18 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
             ystr = p.img_w;
             leader = !(x & 1) && !(y & 1);
             pix = (bimg * (p.img_h / 2) + y / 2) * (p.img_w / 2) + x / 2;
+            // maps up to 16 wide: a warp's leaders are 8 consecutive pooled pixels from lane 0's
+            st_x = int32_t(__shfl_sync(0xffffffffu, pix, 0));
         }
         const int nrows = RG ? p.g * 16 : p.tm;
         // staged conv stores: whole 64-channel groups only (a range of 4k row blocks from 4k)
-        const bool ost = CONV && !RES && OUT_BF16 && !pool && p.ostage && !helper && (rb0 % 4) == 0 &&
+        // (pooled: the warp's 8 pooled pixels, 1 KB; the staging row of a leader lane is its pooled
+        // pixel's index among them)
+        const bool ost = CONV && !RES && OUT_BF16 && p.ostage && !helper && (rb0 % 4) == 0 &&
                          ((rb1 - rb0) % 4) == 0;
-        const uint32_t ostg = smem_u32(base) + uint32_t(p.ostage_off) + uint32_t(((warp & 3) + (warp >= 8 ? 4 : 0)) * 4096);
+        const uint32_t ostg = smem_u32(base) + uint32_t(p.ostage_off) +
+                              uint32_t(((warp & 3) + (warp >= 8 ? 4 : 0)) * (pool ? 1024 : 4096));
+        const int orow = !pool ? lane : HALO ? ((lane >> 4) * 4 + ((lane & 7) >> 1)) : int(pix - st_x);
         unsigned char *wstage_p = ring + q * nrows * kRowBytes;  // [row][kRowBytes] for columns c0..
         const uint32_t wstage = smem_u32(wstage_p);
         const int k2 = lane >> 1, odd = lane & 1;  // bf16: lane pair (2k, 2k+1) -> columns 2k, 2k+1
@@ -291,7 +299,7 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                         x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], 1));
                         x[m] = fmaxf(x[m], __shfl_xor_sync(0xffffffffu, x[m], ystr));
                     }
-                    if (!leader) return;
+                    if (!leader && !ost) return;
                 }
                 if (!ok) return;
 #if RBGP4_DEBUG
@@ -334,9 +342,11 @@ stream_kernel(const __grid_constant__ CUtensorMap imap, const __grid_constant__ 
                             if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                             __syncwarp();
                         }
-                        const uint32_t row = ostg + uint32_t(lane) * 128u;
-                        sts128(row + ((uint32_t(2 * g4) ^ uint32_t(lane & 7)) << 4), w[0], w[1], w[2], w[3]);
-                        sts128(row + ((uint32_t(2 * g4 + 1) ^ uint32_t(lane & 7)) << 4), w[4], w[5], w[6], w[7]);
+                        if (leader) {
+                            const uint32_t row = ostg + uint32_t(orow) * 128u;
+                            sts128(row + ((uint32_t(2 * g4) ^ uint32_t(orow & 7)) << 4), w[0], w[1], w[2], w[3]);
+                            sts128(row + ((uint32_t(2 * g4 + 1) ^ uint32_t(orow & 7)) << 4), w[4], w[5], w[6], w[7]);
+                        }
                         if (g4 == 3) {
                             fence_async_smem();
                             __syncwarp();
@@ -1458,9 +1468,12 @@ int stream_plan(const ChainDims &c_in, int out_dtype, bool conv, SPlan *pl, cons
     // conv (bf16, no pool / residual): 4 KB of output staging per epilogue warp (TMA stores).
     // Not for halo strips: their stages are 23-46 KB and the staging would cost one (128 ch @16x16
     // 1.37 -> 1.46 ms), while the tap-shifted convs gain 11-17 % (tools/conv_store_ab.py)
-    const bool ost = conv && !halo && opts().conv_ostage != 0 && out_dtype == RBGP4_BF16 && cv != nullptr &&
-                     !(cv->relu & 2) && conv_epilogue().res == nullptr && c.tm % 64 == 0;
-    const size_t ost_bytes = ost ? size_t(p.epi2 ? 8 : 4) * 4096 : 0;
+    // Pooled epilogues stage only the warp's 8 pooled pixels (1 KB); not for halo strips either
+    // (64 ch @32x32 + pool: 4.67 -> 4.87 ms staged).
+    const bool pooled = cv != nullptr && (cv->relu & 2);
+    const bool ost = conv && !halo && opts().conv_ostage != 0 && out_dtype == RBGP4_BF16 &&
+                     cv != nullptr && conv_epilogue().res == nullptr && c.tm % 64 == 0;
+    const size_t ost_bytes = ost ? size_t(p.epi2 ? 8 : 4) * (pooled ? 1024 : 4096) : 0;
     if (fixed + statics + p.wres_bytes + ost_bytes + 2 * size_t(p.stage_bytes) > kSSmemCap) return 0;
     int ns = int(std::min<size_t>(16, (kSSmemCap - fixed - statics - p.wres_bytes - ost_bytes) / p.stage_bytes));
     // row groups: the kernel re-cuts the ring into stages of the longest range actually used
@@ -1775,18 +1788,20 @@ int launch_stream_conv(const ChainDims &c, const rbgp4_conv_desc *cv, int out_dt
     if (p.ostage) {
         // the output for the staged epilogue: NHWC as (channels, pixels) -- box 64 x 32 -- or, for
         // halo strips, (channels, x, batch * rows) -- box 64 x 8 x 4; 128B swizzle like the staging
+        // (pooled: the (H/2, W/2) output -- box 64 x 8 pooled pixels, or 64 x 4 x 2 for halo strips)
+        const bool pooled = (cv->relu & 2) != 0;
         const cuuint64_t cb = cuuint64_t(c.rows) * 2;
-        cuuint64_t dims[3] = {cuuint64_t(c.rows), cuuint64_t(c.n_cols), 1};
+        cuuint64_t dims[3] = {cuuint64_t(c.rows), cuuint64_t(pooled ? c.n_cols / 4 : c.n_cols), 1};
         cuuint64_t strides[2] = {cb, 0};
-        cuuint32_t box[3] = {64, 32, 1};
+        cuuint32_t box[3] = {64, pooled ? 8u : 32u, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         cuuint32_t rank = 2;
         if (pl.halo) {
-            dims[1] = cuuint64_t(ow);
-            dims[2] = cuuint64_t(cv->batch) * oh;
-            strides[1] = cuuint64_t(ow) * cb;
-            box[1] = 8;
-            box[2] = 4;
+            dims[1] = cuuint64_t(pooled ? ow / 2 : ow);
+            dims[2] = cuuint64_t(cv->batch) * (pooled ? oh / 2 : oh);
+            strides[1] = cuuint64_t(pooled ? ow / 2 : ow) * cb;
+            box[1] = pooled ? 4 : 8;
+            box[2] = pooled ? 2 : 4;
             rank = 3;
         }
         CUresult r = enc(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, out, dims, strides, box, estr,

@@ -33,7 +33,8 @@ def timed(fn, reps=5):
     return a.elapsed_time(b) / reps
 
 
-for c_out, c_in, hw, pool in ((64, 64, 32, True), (128, 128, 16, False), (256, 256, 8, False), (512, 512, 4, False)):
+for c_out, c_in, hw, pool in ((64, 64, 32, True), (128, 128, 16, False), (256, 256, 8, False), (512, 512, 4, False),
+                              (256, 256, 8, True), (512, 512, 4, True)):
     w = init_random(layer_chain(c_out, c_in, 0.875, seed=11), 1, precision="f32")
     x = torch.randn(batch, hw, hw, c_in, device="cuda").to(torch.bfloat16)
     base = timed(lambda: sparse_conv2d(w, x, 3, relu=True, pool=pool))
