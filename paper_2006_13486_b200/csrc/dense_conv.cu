@@ -196,7 +196,16 @@ extern "C" int rbgp4_dense_conv3x3_c3(const void *x, const void *w, void *out, i
     const int64_t ntiles = (npix + kC3Pix - 1) / kC3Pix;
     const unsigned grid = unsigned(std::min<int64_t>(ntiles, int64_t(kNumSMs) * 4));
     note_kernel("K8 dense c3");
-    const int smem = 2 * kC3Pix * kC3OutRow;  // output staging (dynamic: 32 KB, under the 48 KB default)
+    // output staging, dynamic 32 KB: with the 20 KB static A / W buffers above the 48 KB default,
+    // so the opt-in is set on every call (per device, cheap).  (Rotating the chunk order over all 8
+    // chunks of a row instead of 4 removes the 2-way store conflicts but its register selects made
+    // K8 slower: 1.06 -> 1.35 ms.)
+    const int smem = 2 * kC3Pix * kC3OutRow;
+    cudaError_t e = cudaFuncSetAttribute(dense_c3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(dense_c3): %s", cudaGetErrorString(e));
+        return RBGP4_ECUDA;
+    }
     dense_c3_kernel<<<grid, kC3Pix, smem, static_cast<cudaStream_t>(stream)>>>(
         static_cast<const __nv_bfloat16 *>(x), static_cast<const __nv_bfloat16 *>(w),
         static_cast<__nv_bfloat16 *>(out), height, width, npix);
