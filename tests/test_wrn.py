@@ -123,3 +123,23 @@ def test_transpose_residual_is_exact(dtype):
     s, sr = wrn.to_nhwc(y, 2, 6, 5, relu=False, residual=r, relu_copy=True)
     want = y.t().reshape(2, 6, 5, 48) + r
     assert torch.equal(s, want) and torch.equal(sr, want.relu())
+
+
+@pytest.mark.gpu
+def test_conv_residual_argument_errors():
+    """residual= with relu / pool, a mismatched residual, or relu_copy without a residual: the
+    reference-style errors, before any device work."""
+    from paper_2006_13486_b200.conv import sparse_conv2d
+    from paper_2006_13486_b200.errors import InvalidArgumentError, ShapeError
+    from paper_2006_13486_b200.rcubs import init_random
+    w = init_random(wrn_layer_chain(64, 64, 0.875, 3, seed=1), 2, precision="f32")
+    x = torch.randn(2, 8, 8, 64, device="cuda").to(torch.bfloat16)
+    r = torch.randn(2, 8, 8, 64, device="cuda").to(torch.bfloat16)
+    with pytest.raises(InvalidArgumentError):
+        sparse_conv2d(w, x, 3, relu=True, residual=r)
+    with pytest.raises(InvalidArgumentError):
+        sparse_conv2d(w, x, 3, relu_copy=True)
+    with pytest.raises(ShapeError):
+        sparse_conv2d(w, x, 3, residual=r[:, :4])
+    with pytest.raises(ShapeError):
+        sparse_conv2d(w, x, 3, residual=r.float())
