@@ -10,10 +10,11 @@
 // NHWC input, packed into one 64-byte K-major row, 64B swizzle), W resident in shared memory,
 // D double-buffered in TMEM (the MMA of tile i+1 runs under the epilogue of tile i), the
 // epilogue reading one pixel's 64 channels per lane (tcgen05.ld) and storing them as one
-// contiguous 128-byte NHWC row with the ReLU fused -- into a shared-memory staging buffer (chunk
-// order rotated per lane: conflict-free), from which each warp's 32 pixels (4 KB, contiguous in
-// NHWC) leave as ONE bulk copy: 16-byte stores straight from the lanes touched 32 lines per
-// instruction and held the kernel at 1.94 ms.  The next tile's input loads are issued before the
+// contiguous 128-byte NHWC row with the ReLU fused -- into a 128B-swizzled shared-memory staging
+// tile (conflict-free), from which each warp's 32 pixels (4 KB, contiguous in NHWC) leave as ONE
+// TMA store: 16-byte stores straight from the lanes touched 32 lines per instruction (1.94 ms), a
+// linear staging tile with a lane-rotated chunk order and a plain bulk copy still had 2-way bank
+// conflicts (1.06 ms); swizzled + TMA store: 0.83 ms, 0.82 of the HBM floor.  The next tile's input loads are issued before the
 // epilogue, so their latency hides under it.  Four CTAs per SM.
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -27,13 +28,16 @@ constexpr int kC3Row = 64;                // bytes per K-major row (32 bf16: 27 
 constexpr int kC3OutRow = kC3Out * 2;     // bytes of one output pixel (NHWC)
 
 __global__ void __launch_bounds__(kC3Pix, 4)
-dense_c3_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__restrict__ w,
+dense_c3_kernel(const __grid_constant__ CUtensorMap omap, const __nv_bfloat16 *__restrict__ x,
+                const __nv_bfloat16 *__restrict__ w,
                 __nv_bfloat16 *__restrict__ out, int height, int width, int64_t npix) {
     __shared__ __align__(1024) unsigned char s_a[2][kC3Pix * kC3Row];
     __shared__ __align__(1024) unsigned char s_b[kC3Out * kC3Row];
     __shared__ uint64_t done[2];
     __shared__ uint32_t tmem_slot;
     extern __shared__ __align__(128) unsigned char s_out[];  // [2][128 pixels][128 B] output staging
+    // 1024-aligned (the 128B swizzle pattern repeats every 8 rows of 128 B)
+    unsigned char *s_out1k = s_out + ((1024u - (smem_u32(s_out) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid / 32;
     // W: [64 rows][32 bf16] as given (k = (ti * 3 + tj) * 3 + c, zero-padded), 64B swizzle
     for (int i = tid; i < kC3Out * 4; i += kC3Pix) {
@@ -95,7 +99,7 @@ dense_c3_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__rest
         const int64_t wpix0 = tile * kC3Pix + warp * 32;  // this warp's first pixel
         // staging buffer b of this warp: 32 pixel rows of 128 B; its previous bulk store (tile
         // it_e - 2) must have finished reading it
-        unsigned char *stg = s_out + size_t(b) * kC3Pix * kC3OutRow + size_t(warp) * 32 * kC3OutRow;
+        unsigned char *stg = s_out1k + size_t(b) * kC3Pix * kC3OutRow + size_t(warp) * 32 * kC3OutRow;
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
         const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(b * kC3Out);
@@ -112,25 +116,20 @@ dense_c3_kernel(const __nv_bfloat16 *__restrict__ x, const __nv_bfloat16 *__rest
                                                                  fmaxf(__uint_as_float(r[2 * k + 1]), 0.0f));
                 o[k] = *reinterpret_cast<const uint32_t *>(&p2);
             }
-            // chunk (h * 4 + k) of this pixel's row; the chunk order rotates with the lane so the
-            // 8 lanes of a wavefront hit 8 different bank quads
-            const uint4 q[4] = {make_uint4(o[0], o[1], o[2], o[3]), make_uint4(o[4], o[5], o[6], o[7]),
-                                make_uint4(o[8], o[9], o[10], o[11]), make_uint4(o[12], o[13], o[14], o[15])};
+            // chunk (h * 4 + k) of this pixel's 128-byte row, 128B swizzle (chunk ^ row % 8): the 8
+            // lanes of a wavefront hit 8 different bank quads; the TMA store undoes the swizzle
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const int k = (kk + lane) & 3;
-                // register select, not a dynamically indexed (local-memory) array
-                const uint4 val = k == 0 ? q[0] : k == 1 ? q[1] : k == 2 ? q[2] : q[3];
-                sts128(srow + uint32_t((h * 4 + k) * 16), val.x, val.y, val.z, val.w);
-            }
+            for (int k = 0; k < 4; ++k)
+                sts128(srow + (uint32_t((h * 4 + k) ^ (lane & 7)) << 4), o[4 * k], o[4 * k + 1], o[4 * k + 2],
+                       o[4 * k + 3]);
         }
         tc_fence_before();
         fence_async_smem();
         __syncwarp();
-        if (lane == 0 && wpix0 < npix) {
-            const int64_t np = min(int64_t(32), npix - wpix0);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + wpix0 * kC3Out),
-                         "r"(smem_u32(stg)), "r"(uint32_t(np * kC3OutRow)) : "memory");
+        if (lane == 0 && wpix0 < npix) {  // box 64 channels x 32 pixels, clipped at npix
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                             reinterpret_cast<uint64_t>(&omap)), "r"(0), "r"(int32_t(wpix0)), "r"(smem_u32(stg))
+                         : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
     };
@@ -196,17 +195,35 @@ extern "C" int rbgp4_dense_conv3x3_c3(const void *x, const void *w, void *out, i
     const int64_t ntiles = (npix + kC3Pix - 1) / kC3Pix;
     const unsigned grid = unsigned(std::min<int64_t>(ntiles, int64_t(kNumSMs) * 4));
     note_kernel("K8 dense c3");
-    // output staging, dynamic 32 KB: with the 20 KB static A / W buffers above the 48 KB default,
-    // so the opt-in is set on every call (per device, cheap).  (Rotating the chunk order over all 8
-    // chunks of a row instead of 4 removes the 2-way store conflicts but its register selects made
-    // K8 slower: 1.06 -> 1.35 ms.)
-    const int smem = 2 * kC3Pix * kC3OutRow;
+    // output staging, dynamic 33 KB: with the 20 KB static A / W buffers above the 48 KB default,
+    // so the opt-in is set on every call (per device, cheap)
+    const int smem = 2 * kC3Pix * kC3OutRow + 1024;
     cudaError_t e = cudaFuncSetAttribute(dense_c3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) {
         set_error("cudaFuncSetAttribute(dense_c3): %s", cudaGetErrorString(e));
         return RBGP4_ECUDA;
     }
-    dense_c3_kernel<<<grid, kC3Pix, smem, static_cast<cudaStream_t>(stream)>>>(
+    // the output as (64 channels, npix pixels): box 64 x 32 (a warp's pixels), 128B swizzle
+    auto enc = encode_fn();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return RBGP4_ECUDA;
+    }
+    CUtensorMap omap;
+    {
+        const cuuint64_t dims[2] = {cuuint64_t(kC3Out), cuuint64_t(npix)};
+        const cuuint64_t strides[1] = {cuuint64_t(kC3OutRow)};
+        const cuuint32_t box[2] = {cuuint32_t(kC3Out), 32};
+        const cuuint32_t estr[2] = {1, 1};
+        CUresult r = enc(&omap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled(K8 output) failed (%d)", int(r));
+            return RBGP4_ECUDA;
+        }
+    }
+    dense_c3_kernel<<<grid, kC3Pix, smem, static_cast<cudaStream_t>(stream)>>>(omap, 
         static_cast<const __nv_bfloat16 *>(x), static_cast<const __nv_bfloat16 *>(w),
         static_cast<__nv_bfloat16 *>(out), height, width, npix);
     RBGP4_CHECK_LAUNCH("dense_c3_kernel launch");
