@@ -867,7 +867,7 @@ def run_vgg_leg(B, args):
            "data": "synthetic images, random-init weights"}
     # per layer (eager, events around each call, as the forward runs them: pools fused into the
     # conv that precedes them); the kernel each RBGP4 conv took
-    from paper_2006_13486_b200.vgg import _dense_conv_relu, maxpool2x2
+    from paper_2006_13486_b200.vgg import dense_conv1_relu, maxpool2x2
     from paper_2006_13486_b200 import _native
     per = []
     def ev():
@@ -879,8 +879,8 @@ def run_vgg_leg(B, args):
         evs = []
         with torch.cuda.stream(B.stream):
             e0 = ev()
-            h = _dense_conv_relu(x.permute(0, 3, 1, 2), net.conv1).permute(0, 2, 3, 1).contiguous()
-            evs.append(("conv1 (dense, cuDNN)", e0, ev(), None))
+            h = dense_conv1_relu(x, net.conv1_cols)  # as the forward runs it (K8)
+            evs.append(("conv1 (dense)", e0, ev(), _native.last_kernel()))
             i = 0
             while i < len(net.layers):
                 kind, layer = net.layers[i]
