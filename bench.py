@@ -978,7 +978,7 @@ def run_train_leg(B, args):
     layer as a TrainableSparseLinear(compute="bf16") on the headline operands (N = 16 * batch
     pixels x K = 4608 inputs): forward O = W x I (K5), input gradient W^T x dO (K5 on the
     transposed chain), weight gradient restricted to the pattern (K7), fp32 master values.
-    Reports the autograd step (eager, incl. the torch layout casts / transposes of the
+    Reports the autograd step (eager, incl. the bf16 casts and K7's operand transposes of the
     nn.Linear-style API and the Python launch overhead) and the three products alone on
     pre-laid-out bf16 operands, each a CUDA graph; FLOPs = 3 x 2 nnz N."""
     torch = B.torch

@@ -14,6 +14,10 @@ compute="bf16" runs all three products on the tensor cores: the forward and W^T 
 streamed / gathered kernels (K5 / K4) of the bf16 values (fp32 master values cast per step; the
 layer owns its prepared buffers and refreshes only their value copies, `rbgp4_prepare_values`),
 and dW on K7 (`rbgp4_sddmm` with bf16 operands, fp32 gradient), fp32 accumulation throughout.
+The forward and W^T x dO take the nn.Linear layout as it is: x (N x in) is an NHWC tensor of N
+one-pixel images, so the product is a 1 x 1 streamed convolution whose NHWC output is y (N x out)
+-- no transposes (`_PatternBF16.product_nk`; shapes the streamed conv does not take fall back to
+the product on transposed operands).
 """
 
 from __future__ import annotations
@@ -132,6 +136,56 @@ class _PatternBF16:
         self.fmt_t = device_format(self.wt, device, t.bfloat16)
         self._prep = {}
 
+    def _prepared(self, fmt, values, desc, device, stream):
+        """The layer's prepared buffer for `fmt` (built once; its value copies refreshed from
+        `values` on every later call -- they follow the trainable values)."""
+        t = torch()
+        lib = _native.lib()
+        code = _native.COMPUTE["bf16"]
+        nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
+        prep = None
+        if nbytes:
+            key = (id(fmt), nbytes)
+            prep = self._prep.get(key)
+            if prep is None:
+                prep = t.empty(nbytes, dtype=t.uint8, device=device)
+                _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, values.data_ptr(), fmt.adj_o.data_ptr(),
+                                                fmt.adj_i.data_ptr(), prep.data_ptr(), nbytes, stream),
+                              "rbgp4_prepare")
+                self._prep[key] = prep
+            else:
+                _native.check(lib.rbgp4_prepare_values(ctypes.byref(desc), code, values.data_ptr(),
+                                                       prep.data_ptr(), nbytes, stream), "rbgp4_prepare_values")
+        return prep
+
+    def product_nk(self, fmt, values, inp_nk, out_dtype):
+        """The same product with both operands in the nn.Linear layout: inp_nk (N x cols) bf16 in,
+        (N x rows) out -- the chain as a 1 x 1 convolution over N one-pixel images (NHWC = row
+        major), so neither the input nor the output is transposed.  None when the streamed conv
+        does not take the shape (the caller then uses `product` on transposed operands)."""
+        t = torch()
+        lib = _native.lib()
+        n, cols = inp_nk.shape
+        rows = fmt.desc_fields["rows"]
+        if n == 0 or cols % 64 or inp_nk.data_ptr() % 16:
+            return None
+        out = t.empty((n, rows), dtype=out_dtype, device=inp_nk.device)
+        desc = make_desc(fmt.desc_fields, n, n, n)
+        cv = _native.ConvDesc(n, 1, 1, cols, 1, 1, 0, 1, 0)
+        stream = stream_handle(inp_nk.device)
+        prep = self._prepared(fmt, values, desc, inp_nk.device, stream)
+        need = lib.rbgp4_conv2d_workspace_size(ctypes.byref(desc), ctypes.byref(cv))
+        from .sdmm import workspace
+        ws = workspace(inp_nk.device, need, stream) if need else None
+        rc = lib.rbgp4_conv2d(ctypes.byref(desc), ctypes.byref(cv), dtype_code(out_dtype), values.data_ptr(),
+                              fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(), prep.data_ptr() if prep is not None else None,
+                              inp_nk.data_ptr(), out.data_ptr(), ws.data_ptr() if ws is not None else None, need,
+                              stream)
+        if rc == _native.EUNSUPPORTED:
+            return None
+        _native.check(rc, "rbgp4_conv2d (1 x 1, trainable layer)")
+        return out
+
     def product(self, fmt, values, inp, out_dtype):
         """O = W x I on the tensor cores with the given bf16 values (the layer's own prep)."""
         t = torch()
@@ -142,20 +196,7 @@ class _PatternBF16:
         desc = make_desc(fmt.desc_fields, inp.shape[1], inp.stride(0), out.stride(0))
         code = _native.COMPUTE["bf16"]
         stream = stream_handle(inp.device)
-        nbytes = lib.rbgp4_prepare_size(ctypes.byref(desc), code)
-        prep = None
-        if nbytes:
-            key = (id(fmt), nbytes)
-            prep = self._prep.get(key)
-            if prep is None:
-                prep = t.empty(nbytes, dtype=t.uint8, device=inp.device)
-                _native.check(lib.rbgp4_prepare(ctypes.byref(desc), code, values.data_ptr(), fmt.adj_o.data_ptr(),
-                                                fmt.adj_i.data_ptr(), prep.data_ptr(), nbytes, stream),
-                              "rbgp4_prepare")
-                self._prep[key] = prep
-            else:
-                _native.check(lib.rbgp4_prepare_values(ctypes.byref(desc), code, values.data_ptr(),
-                                                       prep.data_ptr(), nbytes, stream), "rbgp4_prepare_values")
+        prep = self._prepared(fmt, values, desc, inp.device, stream)
         need = lib.rbgp4_workspace_size(ctypes.byref(desc), code, _native.BF16)
         from .sdmm import workspace
         ws = workspace(inp.device, need, stream) if need else None
@@ -176,22 +217,28 @@ def make_sparse_linear_function_bf16():
         @staticmethod
         def forward(ctx, x, values, pattern):
             vb = values.detach().to(t.bfloat16).contiguous()
-            xt = x.detach().t().to(t.bfloat16).contiguous()
-            ctx.save_for_backward(xt, vb)
+            xb = x.detach().to(t.bfloat16).contiguous()           # (N x in), no transpose
+            ctx.save_for_backward(xb, vb)
             ctx.pattern = pattern
-            return pattern.product(pattern.fmt, vb, xt, t.float32).t()
+            # y (N x out) straight from the N-major operand (the 1 x 1 conv view); else the
+            # product on transposed operands
+            y = pattern.product_nk(pattern.fmt, vb, xb, t.float32)
+            return y if y is not None else pattern.product(pattern.fmt, vb, xb.t().contiguous(), t.float32).t()
 
         @staticmethod
         def backward(ctx, dy):
-            xt, vb = ctx.saved_tensors
+            xb, vb = ctx.saved_tensors
             pat = ctx.pattern
-            d_out = dy.t().to(t.bfloat16).contiguous()        # dO (rows x N), bf16
+            dyb = dy.to(t.bfloat16).contiguous()                  # dO^T (N x out), bf16
             grad_x = grad_v = None
             if ctx.needs_input_grad[0]:
                 vt = vb.reshape(-1)[pat.perm].reshape(pat.wt.rows, pat.wt.row_nnz).contiguous()
-                grad_x = pat.product(pat.fmt_t, vt, d_out, t.float32).t()   # (W^T dO)^T
+                grad_x = pat.product_nk(pat.fmt_t, vt, dyb, t.float32)    # (W^T dO)^T, N x in
+                if grad_x is None:
+                    grad_x = pat.product(pat.fmt_t, vt, dyb.t().contiguous(), t.float32).t()
             if ctx.needs_input_grad[1]:
-                grad_v = sddmm(pat.w, d_out, xt)                              # K7, f32
+                # K7 reads both operands batch-contiguous: dO (out x N), I (in x N)
+                grad_v = sddmm(pat.w, dyb.t().contiguous(), xb.t().contiguous())   # f32
             return grad_x, grad_v, None
 
     return SparseLinearBF16
