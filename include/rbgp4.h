@@ -195,6 +195,13 @@ int rbgp4_sddmm(const rbgp4_desc *desc, int dtype, const int32_t *adj_o, const i
                 const void *d_out, int64_t ld_do, const void *inp, int64_t ld_in, void *grad_values,
                 void *stream);
 
+/* The same weight gradient with batch-major operands (the nn.Linear layout of a training step):
+ * d_out_nk is n_cols x rows (= dO^T, row stride ld_do), inp_nk is n_cols x cols (= I^T, row
+ * stride ld_in), bf16 on the tensor cores (K7 with MN-major operands; the rbgp4_sddmm BF16
+ * constraints), F32 grad_values.  Bit-identical to rbgp4_sddmm on the transposed operands. */
+int rbgp4_sddmm_nk(const rbgp4_desc *desc, const int32_t *adj_o, const int32_t *adj_i, const void *d_out_nk,
+                   int64_t ld_do, const void *inp_nk, int64_t ld_in, void *grad_values, void *stream);
+
 /* Bytes of device workspace rbgp4_sdmm needs for (desc, compute, in_dtype). */
 size_t rbgp4_workspace_size(const rbgp4_desc *desc, int compute, int in_dtype);
 

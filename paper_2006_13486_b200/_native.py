@@ -27,6 +27,7 @@ EXPORTED = (
     "rbgp4_reset_launch_count", "rbgp4_last_kernel", "rbgp4_sddmm", "rbgp4_set_option", "rbgp4_get_option",
     "rbgp4_reset_options", "rbgp4_debug_build", "rbgp4_im2col_nhwc", "rbgp4_nc_to_nhwc",
     "rbgp4_conv2d_residual", "rbgp4_nc_to_nhwc_residual", "rbgp4_dense_conv3x3_c3",
+    "rbgp4_sddmm_nk",
 )
 
 
@@ -87,6 +88,8 @@ def lib():
     h.rbgp4_prepare.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, vp, sz, vp]
     h.rbgp4_sddmm.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
     h.rbgp4_sddmm.restype = i32
+    h.rbgp4_sddmm_nk.argtypes = [ctypes.POINTER(Desc), vp, vp, vp, ctypes.c_int64, vp, ctypes.c_int64, vp, vp]
+    h.rbgp4_sddmm_nk.restype = i32
     h.rbgp4_prepare.restype = i32
     h.rbgp4_prepare_values.argtypes = [ctypes.POINTER(Desc), i32, vp, vp, sz, vp]
     h.rbgp4_prepare_values.restype = i32

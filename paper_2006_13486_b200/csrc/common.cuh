@@ -158,6 +158,7 @@ int gather_prepare(const ChainDims &c, const void *values, const int32_t *adj_i_
 // K7: tensor-core weight gradient (sddmm_tc.cu): bf16 dO / I, f32 gradient in the values layout
 int sddmm_tc_supported(const ChainDims &c);
 int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj_i, const void *d_out,
-                    int64_t ld_do, const void *inp, int64_t ld_in, float *grad, cudaStream_t stream);
+                    int64_t ld_do, const void *inp, int64_t ld_in, float *grad, cudaStream_t stream,
+                    bool nmajor = false);
 
 }  // namespace rbgp4

@@ -97,3 +97,22 @@ extern "C" int rbgp4_sddmm(const rbgp4_desc *desc, int dtype, const int32_t *adj
     RBGP4_CHECK_LAUNCH("sddmm_kernel launch");
     return RBGP4_OK;
 }
+
+// the nn.Linear layout: d_out_nk (n_cols x rows, row stride ld_do) = dO^T, inp_nk (n_cols x cols,
+// row stride ld_in) = I^T, bf16 only (K7 with MN-major operands): no transposed copies
+extern "C" int rbgp4_sddmm_nk(const rbgp4_desc *desc, const int32_t *adj_o, const int32_t *adj_i,
+                              const void *d_out_nk, int64_t ld_do, const void *inp_nk, int64_t ld_in,
+                              void *grad_values, void *stream) {
+    using namespace rbgp4;
+    ChainDims c;
+    rbgp4_desc d = *desc;
+    d.ld_in = d.ld_out = d.n_cols;
+    int rc = validate_desc(&d, &c);
+    if (rc != RBGP4_OK) return rc;
+    RBGP4_REQUIRE(ld_do >= c.rows && ld_in >= c.cols, "rbgp4_sddmm_nk: leading dimensions < rows / cols");
+    RBGP4_REQUIRE(adj_o && adj_i && grad_values && (c.n_cols == 0 || (d_out_nk && inp_nk)),
+                  "rbgp4_sddmm_nk: null pointer");
+    if (c.rows == 0) return RBGP4_OK;
+    return launch_sddmm_tc(c, adj_o, adj_i, d_out_nk, ld_do, inp_nk, ld_in, static_cast<float *>(grad_values),
+                           static_cast<cudaStream_t>(stream), true);
+}

@@ -30,6 +30,7 @@ struct TParams {
     int64_t n_cols, row_nnz;
     int32_t d_o, tm, tk, u_i, d_i, bm, bk, d_t, ns, n_chunks;
     int32_t split;  // 2: two CTAs per tile, each half of the batch chunks, added into a zeroed grad
+    int32_t nmajor; // operands batch-major, dO^T (N x rows) and I^T (N x cols): MN-major MMA operands
 };
 
 template <int BK>
@@ -65,8 +66,16 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
             if (c >= p.ns) mbar_wait(&empty[st], uint32_t((c / p.ns - 1) & 1));
             if (elect_one()) {
                 mbar_expect_tx(&full[st], uint32_t(kStage));
-                tma_load_2d(ring + size_t(st) * kStage, &dmap, &full[st], (c_lo + c) * kChunk, tbm * p.tm);
-                tma_load_2d(ring + size_t(st) * kStage + kHalf, &imap, &full[st], (c_lo + c) * kChunk, kblk * p.tk);
+                if (p.nmajor) {
+                    // [64-row atom][64 batch rows][64 rows x 2 B]: 3-D boxes (64, 64 batch, 2 atoms)
+                    tma_load_3d(ring + size_t(st) * kStage, &dmap, &full[st], 0, (c_lo + c) * kChunk, tbm * p.tm / 64);
+                    tma_load_3d(ring + size_t(st) * kStage + kHalf, &imap, &full[st], 0, (c_lo + c) * kChunk,
+                                kblk * p.tk / 64);
+                } else {
+                    tma_load_2d(ring + size_t(st) * kStage, &dmap, &full[st], (c_lo + c) * kChunk, tbm * p.tm);
+                    tma_load_2d(ring + size_t(st) * kStage + kHalf, &imap, &full[st], (c_lo + c) * kChunk,
+                                kblk * p.tk);
+                }
             }
             __syncwarp();
         }
@@ -78,11 +87,17 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
         asm volatile("barrier.sync 1, %0;" ::"n"(kTThreads) : "memory");
         tc_fence_after();
         const uint32_t tmem_d = *tmem_slot;
-        // D f32, A / B bf16, both K-major, N = 128, M = 128
-        constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (0u << 16) |
-                                   ((128u >> 3) << 17) | ((128u >> 4) << 24);
-        const uint64_t a0 = smem_desc(smem_u32(ring), 0, 1024, 2u);
-        const uint64_t b0 = smem_desc(smem_u32(ring) + kHalf, 0, 1024, 2u);
+        // D f32, A / B bf16, both K-major (rows contiguous along the batch) or both MN-major
+        // (batch-major operands: 64-row atoms 8 KB apart = LBO, 8-batch-row groups 1 KB apart),
+        // N = 128, M = 128
+        const uint32_t mn = p.nmajor ? 1u : 0u;
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (mn << 15) | (mn << 16) |
+                               ((128u >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t lbo = p.nmajor ? uint32_t(kChunk * 128) : 0u;
+        const uint64_t a0 = smem_desc(smem_u32(ring), lbo, 1024, 2u);
+        const uint64_t b0 = smem_desc(smem_u32(ring) + kHalf, lbo, 1024, 2u);
+        // the next K16 of the batch: 32 bytes along K-major rows, 16 rows of 128 B in MN-major atoms
+        const uint32_t kstep = p.nmajor ? uint32_t(16 * 128) >> 4 : 2u;
         for (int c = 0; c < n_my; ++c) {
             const int st = c % p.ns;
             mbar_wait(&full[st], uint32_t((c / p.ns) & 1));
@@ -91,7 +106,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant_
                 const uint32_t off = uint32_t(st * kStage) >> 4;
 #pragma unroll
                 for (int k = 0; k < kChunk / 16; ++k)  // 32 bytes of the 128-byte rows per K16
-                    tc_mma<false>(tmem_d, a0 + off + uint32_t(k * 2), b0 + off + uint32_t(k * 2), idesc,
+                    tc_mma<false>(tmem_d, a0 + off + uint32_t(k) * kstep, b0 + off + uint32_t(k) * kstep, idesc,
                                   (c > 0 || k > 0) ? 1u : 0u);
                 tc_commit(&empty[st]);
                 if (c == n_my - 1) tc_commit(acc_full);
@@ -148,7 +163,7 @@ int sddmm_tc_supported(const ChainDims &c) {
 }
 
 int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj_i, const void *d_out,
-                    int64_t ld_do, const void *inp, int64_t ld_in, float *grad, cudaStream_t stream) {
+                    int64_t ld_do, const void *inp, int64_t ld_in, float *grad, cudaStream_t stream, bool nmajor) {
     if (!sddmm_tc_supported(c)) {
         set_error("rbgp4_sddmm(bf16): the tensor-core gradient needs 128 x 128 tiles, g_r = (1,1), "
                   "bk in {4, 8, 16}, bm | 32");
@@ -164,6 +179,15 @@ int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj
     }
     CUtensorMap dmap, imap;
     auto make = [&](CUtensorMap *m, const void *ptr, int64_t rows, int64_t ld) {
+        if (nmajor) {  // (N x rows), row stride ld: (64 rows, N batch rows, rows / 64 atoms)
+            cuuint64_t d3[3] = {64, cuuint64_t(c.n_cols), cuuint64_t(rows / 64)};
+            cuuint64_t s3[2] = {cuuint64_t(ld) * 2, 128};
+            cuuint32_t b3[3] = {64, kChunk, 2};
+            cuuint32_t e3[3] = {1, 1, 1};
+            return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), d3, s3, b3, e3,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
         cuuint64_t dims[2] = {cuuint64_t(c.n_cols), cuuint64_t(rows)};
         cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
         cuuint32_t box[2] = {kChunk, 128};
@@ -179,6 +203,7 @@ int launch_sddmm_tc(const ChainDims &c, const int32_t *adj_o, const int32_t *adj
     TParams p{};
     p.n_cols = c.n_cols; p.row_nnz = c.row_nnz; p.d_o = c.d_o; p.tm = c.tm; p.tk = c.tk; p.u_i = c.u_i;
     p.d_i = c.d_i; p.bm = c.bm; p.bk = c.bk; p.d_t = c.d_t;
+    p.nmajor = nmajor ? 1 : 0;
     p.n_chunks = int((c.n_cols + kChunk - 1) / kChunk);
     p.ns = 6;
     // fewer tiles than SMs: split each tile's batch over two CTAs (deterministic, see the epilogue)

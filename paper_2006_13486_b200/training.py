@@ -17,7 +17,7 @@ and dW on K7 (`rbgp4_sddmm` with bf16 operands, fp32 gradient), fp32 accumulatio
 The forward and W^T x dO take the nn.Linear layout as it is: x (N x in) is an NHWC tensor of N
 one-pixel images, so the product is a 1 x 1 streamed convolution whose NHWC output is y (N x out)
 -- no transposes (`_PatternBF16.product_nk`; shapes the streamed conv does not take fall back to
-the product on transposed operands).
+the product on transposed operands); dW reads dO^T and I^T as MN-major operands (`sddmm_nk`).
 """
 
 from __future__ import annotations
@@ -56,6 +56,33 @@ def transpose(w) -> RcubsMatrix:
     chain_t = RbgpChain(tuple(transpose_graph(g) for g in w.chain.graphs))
     vals = np.asarray(w.values).reshape(-1)[transpose_permutation(w)]
     return RcubsMatrix(chain_t, vals.reshape(chain_t.num_left, chain_t.row_nnz))
+
+
+def sddmm_nk(w, d_out_nk, inp_nk):
+    """The bf16 pattern gradient from batch-major operands (the nn.Linear layout): d_out_nk
+    (N, rows) = dO^T and inp_nk (N, cols) = I^T, bf16 CUDA tensors with unit column stride; K7
+    reads them as MN-major MMA operands (`rbgp4_sddmm_nk`) -- bit-identical to
+    sddmm(w, d_out_nk.t(), inp_nk.t()) without the transposed copies.  Returns (rows, row_nnz) f32."""
+    t = torch()
+    if w.chain.k != 4:
+        raise InvalidArgumentError("sddmm needs a four-factor chain")
+    if d_out_nk.dim() != 2 or inp_nk.dim() != 2 or d_out_nk.shape[1] != w.rows or inp_nk.shape[1] != w.cols \
+            or d_out_nk.shape[0] != inp_nk.shape[0]:
+        raise ShapeError(f"sddmm_nk: d_out {tuple(d_out_nk.shape)} / inp {tuple(inp_nk.shape)} do not match "
+                         f"W^T ({w.cols} x {w.rows})")
+    if d_out_nk.dtype != t.bfloat16 or inp_nk.dtype != t.bfloat16:
+        raise ShapeError("sddmm_nk: bf16 operands")
+    dev = resolve_device(d_out_nk.device)
+    d_out_nk = d_out_nk if d_out_nk.stride(1) == 1 else d_out_nk.contiguous()
+    inp_nk = inp_nk if inp_nk.stride(1) == 1 else inp_nk.contiguous()
+    fmt = device_format(w, dev, t.bfloat16)
+    res = t.empty((w.rows, w.row_nnz), dtype=t.float32, device=dev)
+    n = d_out_nk.shape[0]
+    desc = make_desc(fmt.desc_fields, n, n, n)
+    _native.check(_native.lib().rbgp4_sddmm_nk(
+        ctypes.byref(desc), fmt.adj_o.data_ptr(), fmt.adj_i.data_ptr(), d_out_nk.data_ptr(), d_out_nk.stride(0),
+        inp_nk.data_ptr(), inp_nk.stride(0), res.data_ptr(), stream_handle(dev)), "rbgp4_sddmm_nk")
+    return res
 
 
 def sddmm(w, d_out, inp, values_out=None):
@@ -237,8 +264,8 @@ def make_sparse_linear_function_bf16():
                 if grad_x is None:
                     grad_x = pat.product(pat.fmt_t, vt, dyb.t().contiguous(), t.float32).t()
             if ctx.needs_input_grad[1]:
-                # K7 reads both operands batch-contiguous: dO (out x N), I (in x N)
-                grad_v = sddmm(pat.w, dyb.t().contiguous(), xb.t().contiguous())   # f32
+                # K7 on the batch-major operands as they are (MN-major MMA operands), f32
+                grad_v = sddmm_nk(pat.w, dyb, xb)
             return grad_x, grad_v, None
 
     return SparseLinearBF16

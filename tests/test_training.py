@@ -152,3 +152,23 @@ def test_autograd_trainable_layer_bf16(cfg):
         assert rel(layer.values.grad.cpu().numpy(), want) < 1e-5, step
         with torch.no_grad():
             layer.values -= 0.05 * layer.values.grad
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", TC_CHAINS, ids=[c.config_id for c in TC_CHAINS])
+@pytest.mark.parametrize("n", [256, 200])
+def test_sddmm_nk_bit_identical(cfg, n):
+    """K7 on batch-major operands (dO^T, I^T as MN-major MMA operands) == K7 on the transposed
+    copies, bit for bit (same MMAs, same batch order); ragged N included."""
+    import torch
+    from paper_2006_13486_b200 import _native
+    chain = wl.build_chain(cfg)
+    w = ks.init_random(chain, 3, precision="f32")
+    g = torch.Generator(device="cuda").manual_seed(n)
+    dnk = torch.randn(n, w.rows, device="cuda", generator=g).to(torch.bfloat16)
+    xnk = torch.randn(n, w.cols, device="cuda", generator=g).to(torch.bfloat16)
+    got = training.sddmm_nk(w, dnk, xnk)
+    assert _native.last_kernel() == "K7 sddmm"
+    want = training.sddmm(w, dnk.t().contiguous(), xnk.t().contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
